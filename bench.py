@@ -1,0 +1,412 @@
+"""Benchmark: sampled tokens/s of the B200 CuLDA_CGS hot path (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload nytimes|pubmed|tiny] [--topics 1024]
+
+A step is one full deferred training iteration over the shard (K1 sample +
+fused loglik, K2 phi rebuild, [NCCL allreduce of the phi sync buffer], K3
+theta rebuild, prepare) with every input resident in HBM.  N=1 runs the
+NYTimes-shaped configuration (BASELINE.json configs[1]: 299,752 docs,
+V=101,636, ~99.5M tokens, K=1024).  Under torchrun each rank owns one
+NYTimes-shaped document shard of an N-times larger corpus over the same
+vocabulary ("weak" scaling) and the replicas are summed with NCCL.
+
+--impl reference times the CPU implementation of the same path on the host
+cores (the reference package has no sampler, so this is the oracle port in
+oracle/: OpenMP C, all threads) on a bounded document sample.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sampled tokens/sec"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="nytimes", choices=["nytimes", "pubmed", "tiny"])
+    ap.add_argument("--topics", type=int, default=None)
+    ap.add_argument("--seed", type=int, default=20261017)
+    ap.add_argument("--cpu-sample-docs", type=int, default=0, help="docs in the bounded CPU sample (0: auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(name, topics):
+    from paper_1803_04631_b200 import synth
+
+    shape = dict(synth.SHAPES[name])
+    K = topics or (32 if name == "tiny" else 1024)
+    return shape, K
+
+
+def make_shard_corpus(shape, rank, seed):
+    """This rank's document shard: docs [rank*D, (rank+1)*D) of the global corpus."""
+    from paper_1803_04631_b200 import synth
+
+    D = shape["num_docs"]
+    return synth.generate(D, shape["vocab_size"], shape["mean_len"], seed=seed, doc_begin=rank * D)
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.QUERY}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram read+write bytes per K1 launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "sample_kernel_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+# -------------------------------------------------------------- CPU side --
+def cpu_iteration(sub, K, seed, iteration, threads):
+    """One deferred iteration of the oracle port on a document sample: sample
+    (SPEC sampler, OpenMP) + theta rebuild + phi rebuild.  Returns seconds."""
+    import oracle
+
+    ch, rp, ids, cn, phi, tot = sub
+    a, b = 50.0 / K, 0.01
+    t0 = time.perf_counter()
+    z = oracle.sample_tokens(K, ch.vocab, a, b, seed, iteration, ch.doc_ids, ch.word_ids, ch.z, 0, rp, ids, cn,
+                             phi, tot, nthreads=threads)
+    rp2, ids2, cn2 = oracle.rebuild_theta(z, ch.dw_ptr, ch.dw_tok, 0, K)
+    phi2, tot2 = oracle.rebuild_phi(z, ch.word_ids, K, ch.vocab)
+    dt = time.perf_counter() - t0
+    ch.z = z
+    return dt, (ch, rp2, ids2, cn2, phi2.astype(np.uint32), tot2)
+
+
+class _SubChunk:
+    pass
+
+
+def cpu_sample_state(shape, K, seed, ndocs):
+    import oracle
+    from paper_1803_04631_b200 import corpus as cp
+    from paper_1803_04631_b200 import synth
+
+    corp = synth.generate(ndocs, shape["vocab_size"], shape["mean_len"], seed=seed)
+    chunk = cp.partition(corp, 1, K, seed)[0]
+    ch = _SubChunk()
+    ch.vocab = corp.vocab_size
+    ch.doc_ids, ch.word_ids, ch.z = chunk.doc_ids, chunk.word_ids, chunk.assignments.copy()
+    ch.dw_ptr, ch.dw_tok = chunk.dw_ptr, chunk.dw_tok
+    ch.T = corp.num_tokens
+    rp, ids, cn = oracle.rebuild_theta(ch.z, ch.dw_ptr, ch.dw_tok, 0, K)
+    phi, tot = oracle.rebuild_phi(ch.z, ch.word_ids, K, ch.vocab)
+    return ch, rp, ids, cn, phi.astype(np.uint32), tot
+
+
+def cpu_baseline(shape, K, seed, ndocs, iters=2):
+    threads = os.cpu_count() or 1
+    sub = cpu_sample_state(shape, K, seed, ndocs)
+    T = sub[0].T
+    times = []
+    for it in range(iters):
+        dt, sub = cpu_iteration(sub, K, seed, it, threads)
+        times.append(dt)
+    return {"value": T / float(np.mean(times)), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{ndocs} docs ({T} tokens) of the same {shape['num_docs']}-doc shape, K={K}; "
+                      f"mean of {iters} full deferred iterations (oracle sampler + theta + phi rebuild, "
+                      f"OpenMP C, {threads} threads)"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    shape, K = workload(args.workload, args.topics)
+    ndocs = args.cpu_sample_docs or (shape["num_docs"] if args.workload == "tiny" else 20000)
+    threads = os.cpu_count() or 1
+    sub = cpu_sample_state(shape, K, args.seed, ndocs)
+    T = sub[0].T
+    it = 0
+    for _ in range(args.warmup):
+        _, sub = cpu_iteration(sub, K, args.seed, it, threads)
+        it += 1
+    times = []
+    for _ in range(args.steps):
+        dt, sub = cpu_iteration(sub, K, args.seed, it, threads)
+        times.append(dt)
+        it += 1
+    v = T / float(np.mean(times))
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}-shaped synthetic LDA corpus (bounded CPU sample)",
+                   "docs": ndocs, "tokens": T, "topics": K, "vocab": shape["vocab_size"]},
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{ndocs} docs ({T} tokens); the reference package has no sampler, so the "
+                                   f"oracle port (oracle/gf_oracle.c) runs the SPEC algorithm"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours ----
+def run_ours(args, world, rank, local):
+    import torch
+
+    from paper_1803_04631_b200 import corpus as cp
+    from paper_1803_04631_b200.shard import DeviceShard
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    device = local
+    torch.cuda.set_device(device)
+    shape, K = workload(args.workload, args.topics)
+    corp = make_shard_corpus(shape, rank, args.seed)
+    lo = rank * shape["num_docs"]
+    chunk = cp.make_chunk(rank, lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, corp.vocab_size, K,
+                          args.seed)
+    freq = np.bincount(chunk.word_ids, minlength=corp.vocab_size).astype(np.int64)
+    T_local = corp.num_tokens
+    T_all = T_local
+    if dist:
+        t = torch.as_tensor(freq).cuda()
+        dist.all_reduce(t)
+        freq = t.cpu().numpy()
+        tt = torch.tensor([T_local], dtype=torch.int64, device="cuda")
+        dist.all_reduce(tt)
+        T_all = int(tt.item())
+    stream = torch.cuda.current_stream(device)
+    sh = DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=42, device=device, global_word_freq=freq,
+                     stream=stream)
+    sh.load(chunk)
+    sync_t = sh.sync_tensor() if dist else None
+
+    def allreduce_async():
+        return dist.all_reduce(sync_t, async_op=True) if dist else None
+
+    # initial counts
+    sh.rebuild_phi()
+    w = allreduce_async()
+    if w:
+        w.wait()
+    sh.prepare()
+    sh.rebuild_theta()
+    sh.check_errors()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+
+    def step(it, ev=None):
+        if ev:
+            ev[0].record(stream)
+        sh.sample(it)
+        if ev:
+            ev[1].record(stream)
+        sh.rebuild_phi()
+        if ev:
+            ev[2].record(stream)
+        work = allreduce_async()
+        sh.rebuild_theta()                    # overlaps the allreduce
+        if work:
+            work.wait()
+        if ev:
+            ev[3].record(stream)
+        sh.prepare()
+        if ev:
+            ev[4].record(stream)
+
+    it = 0
+    for _ in range(args.warmup):
+        step(it)
+        it += 1
+    sh.check_errors()
+    sh.reset_stats()
+
+    def barrier():
+        torch.cuda.synchronize(device)
+        if dist:
+            dist.barrier()
+            torch.cuda.synchronize(device)
+
+    clocks = ClockSampler(device)
+    barrier()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clocks:
+        start.record(stream)
+        for i in range(args.steps):
+            step(it, evs[i])                  # per-kernel events on the launching stream
+            it += 1
+        stop.record(stream)
+        barrier()
+    acc = np.zeros(4)
+    for ev in evs:
+        acc += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]),
+                ev[3].elapsed_time(ev[4])]
+    ms_total = start.elapsed_time(stop)
+    if dist:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = T_all / (ms_step / 1e3)
+    ll = sh.loglik_sum()
+    if dist:
+        t = torch.tensor([ll], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        ll = float(t.item())
+    ll /= T_all
+    sh.check_errors()
+    st = sh.stats()
+    k1_ms = acc[0] / args.steps
+    peak, peak_src = measured_peak()
+    achieved = st["sample_bytes"] / (k1_ms / 1e3) / 1e9
+    traffic = ncu_traffic()
+
+    # ---- end to end through the public API with host buffers (pinned) ----
+    e2e = None
+    if not args.no_e2e:
+        z_host = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
+        z_out = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
+        z_host[:] = sh.get_assignments()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            sh.set_assignments(z_host)        # H2D of the step's input assignments
+            step(it)
+            it += 1
+            z_out[:] = 0
+            sh.get_assignments_into(z_out)    # D2H of the new assignments
+            lls = sh.loglik_sum()             # D2H of the step's loglik
+            z_host, z_out = z_out, z_host
+        barrier()
+        el = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": T_all * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": 2 * T_local,
+               "d2h_bytes_per_step": 2 * T_local + 8, "api": "DeviceShard.set_assignments/iterate/"
+                                                            "get_assignments (C ABI, pinned host buffers)"}
+        del lls
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        nd = args.cpu_sample_docs or (shape["num_docs"] if args.workload == "tiny" else 20000)
+        cpu = cpu_baseline(shape, K, args.seed, nd)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {
+                "workload": f"{args.workload}-shaped synthetic LDA corpus, K={K}, one shard per GPU",
+                "docs_per_gpu": shape["num_docs"], "vocab": corp.vocab_size, "tokens_per_gpu": T_local,
+                "tokens_total": T_all, "topics": K, "iterations": [args.warmup, args.warmup + args.steps],
+                "parallelism": f"doc-shard dp{world} + NCCL allreduce of phi" if world > 1 else "dp1",
+                "l2": "inputs larger than L2 (z 2T B, theta 4*NNZ B, phi >= 200 MB vs 126 MB L2)",
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic["bytes_per_launch"] if traffic else None,
+                         "kernel": "gf::sample_kernel (K1)", "algorithmic_bytes_per_launch": st["sample_bytes"],
+                         "kernel_ms": k1_ms, "peak_source": peak_src},
+            "kernel_ms": {"sample": acc[0] / args.steps, "phi_rebuild": acc[1] / args.steps,
+                          "allreduce_and_theta": acc[2] / args.steps, "prepare": acc[3] / args.steps},
+            "loglik_per_token": ll,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks.summary(),
+            "gpu_launches": 5 * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    sh.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

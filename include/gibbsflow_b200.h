@@ -1,0 +1,184 @@
+/*
+ * gibbsflow_b200.h -- C ABI of the B200-native collapsed-Gibbs LDA hot path.
+ *
+ * This is the drop-in boundary for the reference package `gibbsflow`
+ * (/root/reference/pkg/src/gibbsflow).  The reference has no FFI of its own:
+ * its boundary is Python functions over numpy arrays with fixed dtypes
+ * (SURVEY.md section 8b).  Each entry point below names the reference (or
+ * SPEC.md) function whose contract it carries; the Python mirror in
+ * paper_1803_04631_b200/ binds them with ctypes.
+ *
+ * Conventions
+ *   - Every function returns an int status (GF_OK = 0).  On failure
+ *     gf_last_error() returns a thread-local message whose text matches the
+ *     reference exception text where the reference defines one.
+ *   - Host arrays are BORROWED for the duration of the call (copied in or
+ *     written out); the caller keeps ownership.  Dtypes match the reference
+ *     dataclasses: Chunk (corpus.py:160-198), ThetaRows (model.py:20-47),
+ *     PhiMatrix (model.py:50-80).
+ *   - A gf_shard is bound to one CUDA device and one CUDA stream; calls on one
+ *     shard must come from one host thread at a time.
+ *   - No torch / CUDA types cross the boundary: streams and device pointers
+ *     are passed as void*.
+ */
+#ifndef GIBBSFLOW_B200_H
+#define GIBBSFLOW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> gibbsflow.errors classes (errors.py:4-37) */
+#define GF_OK 0
+#define GF_ERR_OVERFLOW 1    /* CountOverflowError    errors.py:20  */
+#define GF_ERR_SHAPE 2       /* ShapeMismatchError    errors.py:28  */
+#define GF_ERR_CONSISTENCY 3 /* ConsistencyError      errors.py:32  */
+#define GF_ERR_CAPACITY 4    /* CapacityError         errors.py:16  (device OOM) */
+#define GF_ERR_TRAINING 5    /* TrainingError         errors.py:36  (CUDA failure) */
+#define GF_ERR_VALUE 6       /* ValueError (bad argument) */
+#define GF_ERR_PARTITION 7   /* PartitionError        errors.py:12  */
+#define GF_ERR_EMPTY 8       /* EmptyDistributionError errors.py:24 */
+#define GF_ERR_NODEVICE 9    /* no CUDA device: the product path refuses to run */
+
+const char* gf_last_error(void);
+int gf_abi_version(void);
+int gf_device_count(int* count_out);
+
+/* ------------------------------------------------------------------ rng --
+ * splitmix64 counter streams, bit-exact with rng.py:20-89. */
+/* rng.py:45-53 stream_key(*parts) */
+uint64_t gf_stream_key(const uint64_t* parts, int num_parts);
+/* rng.py:110-114 Stream.uniforms(n) starting at `counter` */
+int gf_stream_uniforms(uint64_t key, uint64_t counter, int64_t n, double* out);
+
+/* --------------------------------------------------- corpus (host, C++) --
+ * Native host preprocessing, bit-exact with corpus.py. */
+/* corpus.py:210-237 greedy_boundaries -> bounds_out[2*C] = (lo, hi) pairs */
+int gf_greedy_boundaries(const int64_t* doc_lengths, int64_t num_docs, int64_t num_chunks,
+                         int64_t* bounds_out);
+/* corpus.py:252-286, one chunk of partition(): inputs are the chunk's tokens in
+ * corpus (doc-major) order; outputs are the Chunk arrays.  group_* must hold
+ * V entries; *num_groups_out receives the used length. */
+int gf_partition_chunk(const int32_t* doc_ids, const int32_t* word_ids, int64_t num_tokens,
+                       int64_t doc_lo, int64_t doc_hi, int32_t vocab_size, int32_t num_topics,
+                       uint64_t seed, int64_t chunk_id,
+                       int32_t* out_doc_ids, int32_t* out_word_ids, uint16_t* out_assignments,
+                       int32_t* group_words, int64_t* group_offsets, int64_t* group_sizes,
+                       int64_t* num_groups_out, int64_t* dw_ptr, int64_t* dw_tok);
+
+/* ------------------------------------------------ device shard context --
+ * One document shard (= one Chunk, C = G, M = 1) resident in
+ * HBM together with its theta rows and a phi replica. */
+typedef struct gf_shard gf_shard;
+
+/* SPEC.md:312-314 TrainConfig subset.  heavy_threshold: words whose GLOBAL
+ * frequency exceeds it keep 32-bit phi columns, the rest 16-bit (the paper's
+ * "short integer" phi, section 6.1.3, made overflow-proof).  Pass
+ * 65535 for the hybrid layout, 0 for all-32-bit. */
+int gf_shard_create(gf_shard** out, int device, int32_t num_topics, int32_t vocab_size,
+                    double alpha, double beta, uint64_t seed, uint32_t heavy_threshold);
+int gf_shard_destroy(gf_shard* shard);
+/* run every kernel / copy of this shard on `cuda_stream` (a cudaStream_t) */
+int gf_shard_set_stream(gf_shard* shard, void* cuda_stream);
+/* global word frequencies (length V), identical on every rank: fixes the
+ * hybrid phi layout so replicas can be summed elementwise.  Optional on one GPU
+ * (defaults to the shard's own frequencies at load). */
+int gf_shard_set_vocab(gf_shard* shard, const int64_t* global_word_freq);
+/* Upload one Chunk (corpus.py:160-198): token arrays in word-group order,
+ * its group directory (any order) and doc-word map.  Builds the (doc, word)
+ * run list, the heavy-first slice schedule and the theta row capacities. */
+int gf_shard_load(gf_shard* shard, int64_t doc_lo, int64_t doc_hi, int64_t num_tokens,
+                  const int32_t* doc_ids, const int32_t* word_ids, const uint16_t* assignments,
+                  int64_t num_groups, const int32_t* group_words, const int64_t* group_offsets,
+                  const int64_t* group_sizes, const int64_t* dw_ptr, const int64_t* dw_tok);
+
+/* model.py:142-161 rebuild_phi_replica: this shard's phi replica + n_k into the
+ * sync buffer (overwritten). */
+int gf_shard_rebuild_phi(gf_shard* shard);
+/* model.py:109-124 rebuild_theta: theta rows of this shard from assignments.
+ * Overflow (a count > 65535) reports GF_ERR_OVERFLOW at the next
+ * gf_shard_check_errors with "document d: topic count c exceeds 16-bit range". */
+int gf_shard_rebuild_theta(gf_shard* shard);
+/* After the sync buffer holds the GLOBAL phi / n_k (single GPU: right after
+ * rebuild_phi; multi-GPU: after the allreduce): refresh the Eq. 1
+ * denominators 1/(n_k + V beta). */
+int gf_shard_prepare(gf_shard* shard);
+/* SPEC.md:359-367 sample_chunk (deferred mode, exclusion on, two uniforms):
+ * resamples every assignment against the iteration-start theta / phi and
+ * accumulates the fused log-likelihood partial of that
+ * iteration-start model.  Philox4x32-10 keyed by (seed) with counter
+ * (global doc, word, occurrence in the (doc, word) run, iteration). */
+int gf_shard_sample(gf_shard* shard, uint32_t iteration);
+/* SPEC.md:402-410 loglik_per_token numerator for the CURRENT theta / phi
+ * (no draws): read it back with gf_shard_loglik_sum. */
+int gf_shard_evaluate(gf_shard* shard);
+/* Convenience: sample -> rebuild_phi -> prepare -> rebuild_theta (one GPU). */
+int gf_shard_iterate(gf_shard* shard, uint32_t iteration);
+/* Sum over this shard's tokens of log p(w | d) for the model the last
+ * gf_shard_sample started from (synchronises the stream). */
+int gf_shard_loglik_sum(gf_shard* shard, double* sum_out);
+/* Raise deferred device-side errors (overflow / consistency); synchronises. */
+int gf_shard_check_errors(gf_shard* shard);
+int gf_shard_synchronize(gf_shard* shard);
+
+/* The phi sync buffer (device memory, uint32 words): [phi32 columns | packed
+ * phi16 columns | n_k].  Summing the buffers of all ranks elementwise as
+ * uint32 (e.g. NCCL allreduce sum) yields the global phi and n_k exactly. */
+int gf_shard_sync_buffer(gf_shard* shard, void** device_ptr, int64_t* num_u32);
+/* Host-only: the sync-buffer layout a shard derives from the global word
+ * frequencies.  word_col_out[v] >= 0: 16-bit column index; < 0: ~(32-bit
+ * column index).  layout_out = {phi16 offset, n_k offset, total} in uint32
+ * words; 16-bit columns hold K rounded up to even cells. */
+int gf_sync_layout(const int64_t* global_word_freq, int32_t vocab_size, int32_t num_topics,
+                   uint32_t heavy_threshold, int32_t* word_col_out, int64_t* layout_out);
+
+/* import / export (host buffers, caller-allocated) */
+int gf_shard_get_assignments(gf_shard* shard, uint16_t* out);      /* word-group order */
+int gf_shard_set_assignments(gf_shard* shard, const uint16_t* in);
+int gf_shard_theta_nnz(gf_shard* shard, int64_t* nnz_out);
+/* ThetaRows (model.py:20-47) of the shard's docs: row_ptr[D_s+1] (local), ids, counts */
+int gf_shard_get_theta(gf_shard* shard, int64_t* row_ptr, uint16_t* topic_ids, uint16_t* counts);
+int gf_shard_set_theta(gf_shard* shard, const int64_t* row_ptr, const uint16_t* topic_ids,
+                       const uint16_t* counts);
+/* PhiMatrix (model.py:50-80) as K x V row-major uint32 + int64 totals, read
+ * from the sync buffer (replica after rebuild_phi, global after the sync). */
+int gf_shard_get_phi(gf_shard* shard, uint32_t* counts_kv, int64_t* topic_totals);
+int gf_shard_set_phi(gf_shard* shard, const uint32_t* counts_kv, const int64_t* topic_totals);
+/* model.py:152-157: max cell count and its first (row-major K x V) position */
+int gf_shard_phi_argmax(gf_shard* shard, int64_t* max_count, int32_t* topic, int32_t* word);
+
+/* live counters for the roofline: stats[0] = K1 algorithmic bytes per sample
+ * launch (averaged over the launches since the last reset), [1] = K2 bytes,
+ * [2] = K3 bytes, [3] = runs, [4] = slices, [5] = tokens, [6] = theta nnz,
+ * [7] = kernels launched by gf_shard_iterate, [8] = sample launches since reset. */
+int gf_shard_stats(gf_shard* shard, int64_t* stats, int num_stats);
+int gf_shard_reset_stats(gf_shard* shard);
+/* CUDA-event time (ms) of the kernels of the last gf_shard_iterate:
+ * ms[0] sample, [1] phi rebuild (+memset), [2] prepare, [3] theta rebuild. */
+int gf_shard_last_times(gf_shard* shard, float* ms, int num);
+
+/* ------------------------------------------------------ ptree primitive --
+ * ptree.py:116-151 on the device: levels built from a prefix array exactly as
+ * build() does (every fanout-th boundary), then a warp-ballot descent per u
+ * returning the minimal index with prefix > u (ties go right). */
+int gf_ptree_sample(int device, const float* prefix, int64_t n, int32_t fanout, const float* u,
+                    int64_t m, int64_t* idx_out);
+
+/* ------------------------------------------------- synthetic corpora --
+ * Not in the reference (no datasets offline): seeded LDA-generative corpora
+ * for tests and bench.py.  Documents are generated
+ * independently from (seed, global doc id), so each rank can build its own
+ * shard.  lengths_out[i] = length of doc doc_begin+i (log-normal, mean
+ * mean_len); tokens are written doc-major at doc_ptr[i] (doc_ptr[0] = 0). */
+int gf_synth_lengths(uint64_t seed, int64_t doc_begin, int64_t num_docs, double mean_len, double sigma,
+                     int64_t* lengths_out);
+int gf_synth_tokens(uint64_t seed, int64_t doc_begin, int64_t num_docs, const int64_t* doc_ptr,
+                    int32_t vocab_size, int32_t k_true, double zipf_s, double doc_alpha,
+                    int32_t* doc_ids_out, int32_t* word_ids_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GIBBSFLOW_B200_H */

@@ -212,6 +212,16 @@ static int64_t scan_pick(const double* w, int64_t n, double u) {
     return last;
 }
 
+/* minimal k with prefix[k] > u (np.searchsorted side="right"); K-1 if none */
+static int64_t first_above(const double* prefix, int64_t n, double u) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (prefix[mid] > u) hi = mid; else lo = mid + 1;
+    }
+    return lo < n ? lo : n - 1;
+}
+
 int gfo_sample_tokens(int32_t K, int32_t V, double alpha, double beta, uint64_t seed,
                       uint32_t iteration, int64_t T, const int32_t* tok_doc,
                       const int32_t* tok_word, uint16_t* z,
@@ -234,52 +244,88 @@ int gfo_sample_tokens(int32_t K, int32_t V, double alpha, double beta, uint64_t 
     const double vb = (double)V * beta;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+    /* word-major copy of phi (the K x V reference layout has stride V down a column) */
+    uint32_t* phiT = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)K * (size_t)V);
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t vb0 = 0; vb0 < V; vb0 += 64)
+        for (int32_t k = 0; k < K; ++k)
+            for (int64_t vv = vb0; vv < vb0 + 64 && vv < V; ++vv) phiT[vv * K + k] = phi[(int64_t)k * V + vv];
+#ifdef _OPENMP
 #pragma omp parallel
 #endif
     {
         double* pstar = (double*)malloc(sizeof(double) * (size_t)K);
-        double* q = (double*)malloc(sizeof(double) * (size_t)K);
+        double* qpre = (double*)malloc(sizeof(double) * (size_t)K);
         double* p1 = (double*)malloc(sizeof(double) * (size_t)K);
 #ifdef _OPENMP
 #pragma omp for schedule(dynamic, 1)
 #endif
         for (int64_t s = 0; s < nseg; ++s) {
+            /* build_word_context: p* and the prefix of a p*, once per word */
             const int32_t v = tok_word[seg[s]];
-            for (int32_t k = 0; k < K; ++k)
-                pstar[k] = ((double)phi[(int64_t)k * V + v] + beta) / ((double)totals[k] + vb);
+            double acc = 0.0;
+            for (int32_t k = 0; k < K; ++k) {
+                pstar[k] = ((double)phiT[(int64_t)v * K + k] + beta) / ((double)totals[k] + vb);
+                acc += alpha * pstar[k];
+                qpre[k] = acc;
+            }
+            const double Q = qpre[K - 1];
             for (int64_t t = seg[s]; t < seg[s + 1]; ++t) {
                 const int32_t d = tok_doc[t];
                 const int32_t zt = z[t];
                 const int64_t r0 = th_ptr[d - doc_lo], r1 = th_ptr[d - doc_lo + 1];
-                const double pex = ((double)phi[(int64_t)zt * V + v] - 1.0 + beta) /
-                                   ((double)totals[zt] - 1.0 + vb);
-                double S = 0.0, Q = 0.0;
-                int found = 0;
-                for (int64_t j = r0; j < r1; ++j) {
-                    double c = (double)th_cnt[j];
-                    double ps = pstar[th_ids[j]];
-                    if (th_ids[j] == zt) { c -= 1.0; ps = pex; found = 1; }
-                    p1[j - r0] = c * ps;
-                    S += p1[j - r0];
-                }
-                if (!found || phi[(int64_t)zt * V + v] == 0 || totals[zt] == 0) {
+                if (zt >= K || phi[(int64_t)zt * V + v] == 0 || totals[zt] == 0) {
 #ifdef _OPENMP
 #pragma omp critical
 #endif
                     { status = 3; if (t < bad) bad = t; }
                     continue;
                 }
-                for (int32_t k = 0; k < K; ++k) { q[k] = alpha * (k == zt ? pex : pstar[k]); Q += q[k]; }
+                const double pex = ((double)phi[(int64_t)zt * V + v] - 1.0 + beta) /
+                                   ((double)totals[zt] - 1.0 + vb);
+                double S = 0.0;
+                int found = 0;
+                for (int64_t j = r0; j < r1; ++j) {      /* p1 with exclusion */
+                    double c = (double)th_cnt[j];
+                    double ps = pstar[th_ids[j]];
+                    if (th_ids[j] == zt) { c -= 1.0; ps = pex; found = 1; }
+                    p1[j - r0] = c * ps;
+                    S += p1[j - r0];
+                }
+                if (!found) {
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+                    { status = 3; if (t < bad) bad = t; }
+                    continue;
+                }
+                /* exclusion-adjusted p2: entries below z unchanged, z carries
+                 * a p*_ex(z), entries above shift down by dq (exact-arithmetic
+                 * equivalent of scanning the adjusted weights) */
+                const double qzx = alpha * pex, dq = alpha * pstar[zt] - qzx, Qx = Q - dq;
                 double u1, u2;
                 gfo_token_uniforms(seed, iteration, (uint32_t)d, (uint32_t)v, occ[t], &u1, &u2);
                 int64_t pick;
-                if (u1 * (S + Q) < S) pick = th_ids[r0 + scan_pick(p1, r1 - r0, u2 * S)];
-                else pick = scan_pick(q, K, u2 * Q);
+                if (u1 * (S + Qx) < S) {
+                    pick = th_ids[r0 + scan_pick(p1, r1 - r0, u2 * S)];
+                } else {
+                    const double u = u2 * Qx, before = zt ? qpre[zt - 1] : 0.0;
+                    if (u < before) pick = first_above(qpre, K, u);
+                    else if (u < before + qzx) pick = zt;
+                    else {
+                        pick = first_above(qpre, K, u + dq);
+                        if (pick <= zt) pick = zt + 1 < K ? zt + 1 : zt;   /* rounding guard */
+                    }
+                }
                 z[t] = (uint16_t)pick;
             }
         }
-        free(pstar); free(q); free(p1);
+        free(pstar); free(qpre); free(p1);
     }
+    free(phiT);
     free(occ); free(seg);
     if (status) *err_tok = bad;
     return status;

@@ -1,0 +1,120 @@
+"""ctypes binding of libgfb200.so (include/gibbsflow_b200.h).
+
+The library is built in-tree (`paper_1803_04631_b200/_lib/libgfb200.so`, by
+`__graft_entry__.build()` / `make -C paper_1803_04631_b200/csrc`).  There is no
+fallback: if the library is missing the import of any device-facing function
+fails loudly, and on a machine without a CUDA device the shard constructor
+raises `NoDeviceError`.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "_lib", "libgfb200.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "gibbsflow_b200.h")
+
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_u64 = ctypes.c_uint64
+_u32 = ctypes.c_uint32
+_f64 = ctypes.c_double
+_int = ctypes.c_int
+_pp = ctypes.POINTER(ctypes.c_void_p)
+
+# name -> (restype, argtypes), mirroring the header one for one
+SIGNATURES = {
+    "gf_last_error": (ctypes.c_char_p, []),
+    "gf_abi_version": (_int, []),
+    "gf_device_count": (_int, [_p]),
+    "gf_stream_key": (_u64, [_p, _int]),
+    "gf_stream_uniforms": (_int, [_u64, _u64, _i64, _p]),
+    "gf_greedy_boundaries": (_int, [_p, _i64, _i64, _p]),
+    "gf_partition_chunk": (_int, [_p, _p, _i64, _i64, _i64, _i32, _i32, _u64, _i64] + [_p] * 9),
+    "gf_shard_create": (_int, [_pp, _int, _i32, _i32, _f64, _f64, _u64, _u32]),
+    "gf_shard_destroy": (_int, [_p]),
+    "gf_shard_set_stream": (_int, [_p, _p]),
+    "gf_shard_set_vocab": (_int, [_p, _p]),
+    "gf_shard_load": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _p]),
+    "gf_shard_rebuild_phi": (_int, [_p]),
+    "gf_shard_rebuild_theta": (_int, [_p]),
+    "gf_shard_prepare": (_int, [_p]),
+    "gf_shard_sample": (_int, [_p, _u32]),
+    "gf_shard_iterate": (_int, [_p, _u32]),
+    "gf_shard_evaluate": (_int, [_p]),
+    "gf_shard_loglik_sum": (_int, [_p, _p]),
+    "gf_shard_check_errors": (_int, [_p]),
+    "gf_shard_synchronize": (_int, [_p]),
+    "gf_shard_sync_buffer": (_int, [_p, _pp, _p]),
+    "gf_sync_layout": (_int, [_p, _i32, _i32, _u32, _p, _p]),
+    "gf_shard_get_assignments": (_int, [_p, _p]),
+    "gf_shard_set_assignments": (_int, [_p, _p]),
+    "gf_shard_theta_nnz": (_int, [_p, _p]),
+    "gf_shard_get_theta": (_int, [_p, _p, _p, _p]),
+    "gf_shard_set_theta": (_int, [_p, _p, _p, _p]),
+    "gf_shard_get_phi": (_int, [_p, _p, _p]),
+    "gf_shard_set_phi": (_int, [_p, _p, _p]),
+    "gf_shard_phi_argmax": (_int, [_p, _p, _p, _p]),
+    "gf_shard_stats": (_int, [_p, _p, _int]),
+    "gf_shard_reset_stats": (_int, [_p]),
+    "gf_shard_last_times": (_int, [_p, _p, _int]),
+    "gf_ptree_sample": (_int, [_int, _p, _i64, _i32, _p, _i64, _p]),
+    "gf_synth_lengths": (_int, [_u64, _i64, _i64, _f64, _f64, _p]),
+    "gf_synth_tokens": (_int, [_u64, _i64, _i64, _p, _i32, _i32, _f64, _f64, _p, _p]),
+}
+
+_ERRORS = {
+    1: errors.CountOverflowError,
+    2: errors.ShapeMismatchError,
+    3: errors.ConsistencyError,
+    4: errors.CapacityError,
+    5: errors.TrainingError,
+    6: ValueError,
+    7: errors.PartitionError,
+    8: errors.EmptyDistributionError,
+    9: errors.NoDeviceError,
+}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO_PATH):
+            raise ImportError(
+                f"{SO_PATH} is missing: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()')"
+            )
+        L = ctypes.CDLL(SO_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc):
+    if rc != 0:
+        msg = lib().gf_last_error().decode("utf-8", "replace")
+        raise _ERRORS.get(rc, errors.GibbsflowError)(msg)
+
+
+def ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None else None
+
+
+def carr(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def device_count():
+    n = ctypes.c_int(0)
+    lib().gf_device_count(ctypes.byref(n))
+    return n.value

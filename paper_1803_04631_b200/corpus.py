@@ -1,0 +1,190 @@
+"""Corpus and word-grouped chunks -- the reference's data layout (corpus.py).
+
+`Corpus` / `Chunk` keep the reference's fields and dtypes (corpus.py:20-39,
+160-198) because they are the interchange format of the drop-in API.  The
+chunking itself (greedy boundaries, stable word sort, group directory,
+doc-word map, splitmix64 initial topics) runs in the native library
+(gf_greedy_boundaries / gf_partition_chunk) and is bit-identical to the
+reference (tests/test_host_native.py against tests/golden/partition.npz).
+"""
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _lib
+from .errors import CorpusFormatError, PartitionError
+
+
+@dataclass(frozen=True)
+class Corpus:
+    """corpus.py:20-39.  Token order is grouped by document; no empty docs."""
+
+    num_docs: int
+    vocab_size: int
+    num_tokens: int
+    doc_lengths: np.ndarray  # int64[num_docs]
+    doc_ptr: np.ndarray  # int64[num_docs + 1]
+    doc_ids: np.ndarray  # int32[num_tokens]
+    word_ids: np.ndarray  # int32[num_tokens]
+    vocab: list
+
+    def doc_slice(self, d):
+        return slice(int(self.doc_ptr[d]), int(self.doc_ptr[d + 1]))
+
+
+def corpus_from_tokens(doc_ids, word_ids, vocab_size, vocab=None):
+    """corpus.py:42-76: stable doc sort, drop empty documents, compact ids."""
+    doc_ids = np.asarray(doc_ids, dtype=np.int64)
+    word_ids = np.asarray(word_ids, dtype=np.int64)
+    if doc_ids.size == 0:
+        raise CorpusFormatError("corpus has no tokens")
+    if word_ids.min() < 0 or word_ids.max() >= vocab_size:
+        raise CorpusFormatError("word id outside [0, vocab_size)")
+    if doc_ids.size > 1 and np.any(doc_ids[1:] < doc_ids[:-1]):
+        order = np.argsort(doc_ids, kind="stable")
+        doc_ids, word_ids = doc_ids[order], word_ids[order]
+    kept, inverse = np.unique(doc_ids, return_inverse=True)
+    doc_ids = inverse.astype(np.int32)
+    lengths = np.bincount(doc_ids, minlength=len(kept)).astype(np.int64)
+    ptr = np.zeros(len(kept) + 1, dtype=np.int64)
+    np.cumsum(lengths, out=ptr[1:])
+    return Corpus(
+        num_docs=len(kept),
+        vocab_size=int(vocab_size),
+        num_tokens=int(doc_ids.size),
+        doc_lengths=lengths,
+        doc_ptr=ptr,
+        doc_ids=doc_ids,
+        word_ids=word_ids.astype(np.int32),
+        vocab=vocab if vocab is not None else _LazyVocab(int(vocab_size)),
+    )
+
+
+class _LazyVocab(list):
+    """["w0", "w1", ...] without materialising 1M strings up front."""
+
+    def __init__(self, n):
+        super().__init__()
+        self._n = n
+
+    def __len__(self):
+        return self._n
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [f"w{v}" for v in range(*i.indices(self._n))]
+        if i < 0:
+            i += self._n
+        if not 0 <= i < self._n:
+            raise IndexError(i)
+        return f"w{i}"
+
+    def __iter__(self):
+        return (f"w{v}" for v in range(self._n))
+
+
+@dataclass(frozen=True)
+class Chunk:
+    """corpus.py:160-198: whole documents [doc_lo, doc_hi), word-grouped."""
+
+    chunk_id: int
+    doc_lo: int
+    doc_hi: int
+    token_count: int
+    doc_ids: np.ndarray  # int32[token_count], global doc ids
+    word_ids: np.ndarray  # int32[token_count]
+    assignments: np.ndarray  # uint16[token_count]
+    group_words: np.ndarray  # int32[num_groups]
+    group_offsets: np.ndarray  # int64[num_groups]
+    group_sizes: np.ndarray  # int64[num_groups]
+    dw_ptr: np.ndarray  # int64[num_local_docs + 1]
+    dw_tok: np.ndarray  # int64[token_count]
+
+    @property
+    def num_local_docs(self):
+        return self.doc_hi - self.doc_lo
+
+    @property
+    def num_groups(self):
+        return len(self.group_words)
+
+    def word_groups(self):
+        for w, off, size in zip(self.group_words, self.group_offsets, self.group_sizes):
+            yield int(w), slice(int(off), int(off + size))
+
+    def doc_token_positions(self, local_doc):
+        return self.dw_tok[self.dw_ptr[local_doc] : self.dw_ptr[local_doc + 1]]
+
+
+def _doc_word_map(doc_ids, doc_lo, num_local_docs):
+    """corpus.py:201-207: positions of each local document's tokens, ascending."""
+    local = np.asarray(doc_ids).astype(np.int64) - doc_lo
+    dw_tok = np.argsort(local, kind="stable").astype(np.int64)
+    counts = np.bincount(local, minlength=num_local_docs)
+    dw_ptr = np.zeros(num_local_docs + 1, dtype=np.int64)
+    np.cumsum(counts, out=dw_ptr[1:])
+    return dw_ptr, dw_tok
+
+
+def greedy_boundaries(doc_lengths, num_chunks):
+    """corpus.py:210-237 (native)."""
+    L = _lib.carr(doc_lengths, np.int64)
+    if num_chunks > len(L):
+        raise PartitionError(
+            f"cannot give every chunk a document: {num_chunks} chunks > {len(L)} docs"
+        )
+    out = np.empty(2 * max(num_chunks, 1), dtype=np.int64)
+    _lib.check(_lib.lib().gf_greedy_boundaries(_lib.ptr(L), len(L), int(num_chunks), _lib.ptr(out)))
+    return [(int(out[2 * c]), int(out[2 * c + 1])) for c in range(num_chunks)]
+
+
+def make_chunk(chunk_id, lo, hi, doc_ids, word_ids, vocab_size, num_topics, seed):
+    """One chunk of partition() from its doc-major tokens (corpus.py:252-286)."""
+    docs = _lib.carr(doc_ids, np.int32)
+    words = _lib.carr(word_ids, np.int32)
+    n = len(docs)
+    out_doc = np.empty(n, np.int32)
+    out_word = np.empty(n, np.int32)
+    out_z = np.empty(n, np.uint16)
+    gw = np.empty(vocab_size, np.int32)
+    go = np.empty(vocab_size, np.int64)
+    gs = np.empty(vocab_size, np.int64)
+    ng = np.zeros(1, np.int64)
+    dw_ptr = np.empty(hi - lo + 1, np.int64)
+    dw_tok = np.empty(n, np.int64)
+    _lib.check(_lib.lib().gf_partition_chunk(
+        _lib.ptr(docs), _lib.ptr(words), n, lo, hi, vocab_size, num_topics,
+        int(seed) & 0xFFFFFFFFFFFFFFFF, chunk_id, _lib.ptr(out_doc), _lib.ptr(out_word),
+        _lib.ptr(out_z), _lib.ptr(gw), _lib.ptr(go), _lib.ptr(gs), _lib.ptr(ng),
+        _lib.ptr(dw_ptr), _lib.ptr(dw_tok)))
+    k = int(ng[0])
+    return Chunk(chunk_id=chunk_id, doc_lo=lo, doc_hi=hi, token_count=n, doc_ids=out_doc,
+                 word_ids=out_word, assignments=out_z, group_words=gw[:k].copy(),
+                 group_offsets=go[:k].copy(), group_sizes=gs[:k].copy(), dw_ptr=dw_ptr, dw_tok=dw_tok)
+
+
+def partition(corpus, num_chunks, num_topics, seed):
+    """corpus.py:240-287: C chunks of whole documents, word-grouped, with
+    initial topics from Stream(seed, chunk_id)."""
+    if num_chunks < 1:
+        raise PartitionError("need at least one chunk")
+    if not 1 <= num_topics < 2**16:
+        raise ValueError(f"topic count {num_topics} outside [1, 65536)")
+    chunks = []
+    for cid, (lo, hi) in enumerate(greedy_boundaries(corpus.doc_lengths, num_chunks)):
+        a, b = int(corpus.doc_ptr[lo]), int(corpus.doc_ptr[hi])
+        chunks.append(make_chunk(cid, lo, hi, corpus.doc_ids[a:b], corpus.word_ids[a:b],
+                                 corpus.vocab_size, num_topics, seed))
+    return chunks
+
+
+def sort_word_groups_desc(chunk):
+    """corpus.py:290-302: directory by (-size, +word); token arrays untouched."""
+    order = np.lexsort((chunk.group_words, -chunk.group_sizes))
+    return replace(
+        chunk,
+        group_words=chunk.group_words[order],
+        group_offsets=chunk.group_offsets[order],
+        group_sizes=chunk.group_sizes[order],
+    )

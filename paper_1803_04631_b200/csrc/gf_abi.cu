@@ -1,0 +1,744 @@
+// gf_abi.cu -- the C ABI (include/gibbsflow_b200.h): shard lifecycle, host-side
+// native preprocessing (bit-exact with corpus.py / rng.py), device memory
+// layout, import / export in the reference dataclass layouts.
+#include "../../include/gibbsflow_b200.h"
+#include "gf_internal.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <numeric>
+#include <thread>
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation)
+        return fail(GF_ERR_CAPACITY, "%s: device out of memory (%s)", what, cudaGetErrorString(e));
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+        return fail(GF_ERR_NODEVICE, "%s: no usable CUDA device (%s)", what, cudaGetErrorString(e));
+    return fail(GF_ERR_TRAINING, "%s: CUDA error %s", what, cudaGetErrorString(e));
+}
+
+#define CU(call, what)                                   \
+    do {                                                 \
+        cudaError_t _e = (call);                         \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+
+inline uint64_t fin64(uint64_t z) {  // rng.py:20-26
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+inline double stream_u(uint64_t key, uint64_t ctr) {  // rng.py:38-42
+    return (double)(fin64(key + kGolden * (ctr + 1ULL)) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+template <class F>
+void parallel_for(int64_t n, F f) {
+    const int64_t grain = 1 << 20;
+    unsigned nt = std::max(1u, std::min(std::thread::hardware_concurrency(), 32u));
+    if (n < 2 * grain || nt == 1) { f(0, n); return; }
+    nt = (unsigned)std::min<int64_t>(nt, n / grain);
+    std::vector<std::thread> th;
+    for (unsigned i = 0; i < nt; ++i) {
+        int64_t a = n * i / nt, b = n * (i + 1) / nt;
+        th.emplace_back([=] { f(a, b); });
+    }
+    for (auto& t : th) t.join();
+}
+
+template <class T>
+int dev_alloc(T** p, size_t count, const char* what) {
+    if (*p) { cudaFree(*p); *p = nullptr; }
+    cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    return GF_OK;
+}
+
+void free_dev(gf_shard* s) {
+    auto& d = s->d;
+    void* ptrs[] = {d.z, d.run_doc, d.run_start, d.slices, d.k2items, d.dw_ptr, d.dw_tok, d.theta_ent,
+                    d.theta_meta, d.sync, d.inv_den, d.ll_part, d.ll_sum, d.errs, d.bytes, d.scratch};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    d = gf::ShardDev{};
+}
+
+}  // namespace
+
+extern "C" int gf_sync_layout(const int64_t* freq, int32_t V, int32_t K, uint32_t thr, int32_t* word_col,
+                              int64_t* layout) {  // hybrid phi columns from global frequencies
+    if (V < 1 || K < 1) return fail(GF_ERR_VALUE, "bad layout dimensions");
+    const int64_t Kp = K + (K & 1);
+    int64_t h = 0, l = 0;
+    for (int v = 0; v < V; ++v) {
+        if (freq[v] > (int64_t)thr) word_col[v] = ~(int32_t)(h++);
+        else word_col[v] = (int32_t)(l++);
+    }
+    layout[0] = h * K;
+    layout[1] = layout[0] + l * (Kp / 2);
+    layout[2] = layout[1] + K;
+    return GF_OK;
+}
+
+namespace {
+int set_layout(gf_shard* s) {
+    s->word_col.assign(s->V, 0);
+    int64_t lay[3];
+    if (int rc = gf_sync_layout(s->global_freq.data(), s->V, s->K, s->heavy_threshold, s->word_col.data(), lay))
+        return rc;
+    s->n_heavy = 0;
+    for (int32_t c : s->word_col) s->n_heavy += c < 0;
+    s->n_light = s->V - s->n_heavy;
+    s->off_phi16_u32 = lay[0];
+    s->off_nk_u32 = lay[1];
+    s->sync_u32 = lay[2];
+    return GF_OK;
+}
+}  // namespace
+
+extern "C" {
+
+const char* gf_last_error(void) { return g_err.c_str(); }
+int gf_abi_version(void) { return 1; }
+
+int gf_device_count(int* count_out) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) n = 0;
+    *count_out = n;
+    return GF_OK;
+}
+
+// ------------------------------------------------------------------- rng --
+uint64_t gf_stream_key(const uint64_t* parts, int num_parts) {  // rng.py:29-35, 45-53
+    uint64_t h = kGolden;
+    for (int i = 0; i < num_parts; ++i) h = fin64(h + kGolden + parts[i]);
+    return h;
+}
+
+int gf_stream_uniforms(uint64_t key, uint64_t counter, int64_t n, double* out) {  // rng.py:84-89
+    if (n < 0) return fail(GF_ERR_VALUE, "negative count");
+    parallel_for(n, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i) out[i] = stream_u(key, counter + (uint64_t)i);
+    });
+    return GF_OK;
+}
+
+// ---------------------------------------------------------------- corpus --
+int gf_greedy_boundaries(const int64_t* L, int64_t D, int64_t C, int64_t* out) {  // corpus.py:210-237
+    if (C < 1) return fail(GF_ERR_PARTITION, "need at least one chunk");
+    if (C > D)
+        return fail(GF_ERR_PARTITION, "cannot give every chunk a document: %lld chunks > %lld docs", (long long)C,
+                    (long long)D);
+    int64_t remaining = 0;
+    for (int64_t i = 0; i < D; ++i) remaining += L[i];
+    int64_t lo = 0;
+    for (int64_t c = 0; c < C; ++c) {
+        const int64_t left = C - c, hi_max = D - (left - 1), target = (remaining + left - 1) / left;
+        int64_t acc = 0, hi = lo;
+        while (hi < hi_max && acc < target) acc += L[hi++];
+        out[2 * c] = lo;
+        out[2 * c + 1] = hi;
+        remaining -= acc;
+        lo = hi;
+    }
+    return GF_OK;
+}
+
+int gf_partition_chunk(const int32_t* doc_ids, const int32_t* word_ids, int64_t n, int64_t doc_lo, int64_t doc_hi,
+                       int32_t V, int32_t K, uint64_t seed, int64_t chunk_id, int32_t* out_doc, int32_t* out_word,
+                       uint16_t* out_z, int32_t* gw, int64_t* go, int64_t* gs, int64_t* ng_out, int64_t* dw_ptr,
+                       int64_t* dw_tok) {
+    if (K < 1 || K >= 65536) return fail(GF_ERR_VALUE, "topic count %d outside [1, 65536)", K);
+    const int64_t nd = doc_hi - doc_lo;
+    // stable counting sort by word == np.argsort(kind="stable") (corpus.py:256-258)
+    std::vector<int64_t> cnt((size_t)V + 1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t w = word_ids[i];
+        if (w < 0 || w >= V) return fail(GF_ERR_VALUE, "word id outside [0, vocab_size)");
+        const int32_t d = doc_ids[i];
+        if (d < doc_lo || d >= doc_hi) return fail(GF_ERR_VALUE, "doc id %d outside chunk range", d);
+        cnt[(size_t)w + 1]++;
+    }
+    for (int32_t v = 0; v < V; ++v) cnt[(size_t)v + 1] += cnt[v];
+    int64_t ng = 0;
+    for (int32_t v = 0; v < V; ++v)  // np.unique directory, ascending words (corpus.py:260-262)
+        if (cnt[(size_t)v + 1] > cnt[v]) { gw[ng] = v; go[ng] = cnt[v]; gs[ng] = cnt[(size_t)v + 1] - cnt[v]; ++ng; }
+    *ng_out = ng;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t p = cnt[word_ids[i]]++;
+        out_doc[p] = doc_ids[i];
+        out_word[p] = word_ids[i];
+    }
+    // doc-word map: stable counting sort by local doc (corpus.py:201-207)
+    std::fill(dw_ptr, dw_ptr + nd + 1, 0);
+    for (int64_t i = 0; i < n; ++i) dw_ptr[out_doc[i] - doc_lo + 1]++;
+    for (int64_t d = 0; d < nd; ++d) dw_ptr[d + 1] += dw_ptr[d];
+    std::vector<int64_t> fill(dw_ptr, dw_ptr + nd);
+    for (int64_t i = 0; i < n; ++i) dw_tok[fill[out_doc[i] - doc_lo]++] = i;
+    // initial topics from Stream(seed, chunk_id) (corpus.py:265-269)
+    const uint64_t parts[2] = {seed, (uint64_t)chunk_id};
+    const uint64_t key = gf_stream_key(parts, 2);
+    parallel_for(n, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i) {
+            const int64_t zz = (int64_t)(stream_u(key, (uint64_t)i) * (double)K);
+            out_z[i] = (uint16_t)std::min<int64_t>(zz, K - 1);
+        }
+    });
+    return GF_OK;
+}
+
+// ----------------------------------------------------------------- shard --
+int gf_shard_create(gf_shard** out, int device, int32_t K, int32_t V, double alpha, double beta, uint64_t seed,
+                    uint32_t heavy_threshold) {
+    *out = nullptr;
+    if (K < 1 || K >= 65536) return fail(GF_ERR_VALUE, "topic count %d outside [1, 65536)", K);
+    if (V < 1) return fail(GF_ERR_VALUE, "vocab_size must be >= 1");
+    if (!(alpha > 0) || !(beta > 0)) return fail(GF_ERR_VALUE, "alpha and beta must be > 0");
+    int ndev = 0;
+    gf_device_count(&ndev);
+    if (ndev == 0) return fail(GF_ERR_NODEVICE, "no CUDA device visible: the B200 sampler has no CPU fallback");
+    if (device < 0 || device >= ndev) return fail(GF_ERR_VALUE, "device %d out of range (%d visible)", device, ndev);
+    CU(cudaSetDevice(device), "cudaSetDevice");
+    gf_shard* s = new gf_shard();
+    s->device = device;
+    s->K = K;
+    s->Kp = K + (K & 1);
+    s->V = V;
+    s->alpha = alpha;
+    s->beta = beta;
+    s->seed = seed;
+    s->heavy_threshold = heavy_threshold;
+    // Q-tree geometry (ptree.build levels, fanout 32)
+    int len = K, total = 0, l = 0;
+    while (true) {
+        s->tree.off[l] = total;
+        s->tree.len[l] = len;
+        total += len;
+        ++l;
+        if (len == 1) break;
+        len = (len + 31) / 32;
+    }
+    s->tree.nlev = l;
+    s->tree.total = total;
+    if ((size_t)(total + K) * 4 > 200 * 1024) {
+        delete s;
+        return fail(GF_ERR_CAPACITY, "K=%d: the shared-memory Q-tree needs %zu bytes (> 200 KiB)", K,
+                    (size_t)(total + K) * 4);
+    }
+    cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete s; return cuda_fail(e, "cudaStreamCreate"); }
+    s->own_stream = true;
+    for (auto& ev : s->ev) cudaEventCreate(&ev);
+    *out = s;
+    return GF_OK;
+}
+
+int gf_shard_destroy(gf_shard* s) {
+    if (!s) return GF_OK;
+    cudaSetDevice(s->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    free_dev(s);
+    for (auto& ev : s->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+    return GF_OK;
+}
+
+int gf_shard_set_stream(gf_shard* s, void* st) {
+    cudaSetDevice(s->device);
+    if (s->own_stream && s->stream) { cudaStreamSynchronize(s->stream); cudaStreamDestroy(s->stream); }
+    s->stream = (cudaStream_t)st;
+    s->own_stream = false;
+    return GF_OK;
+}
+
+int gf_shard_set_vocab(gf_shard* s, const int64_t* freq) {
+    if (s->loaded) return fail(GF_ERR_VALUE, "set_vocab must precede load");
+    s->global_freq.assign(freq, freq + s->V);
+    return GF_OK;
+}
+
+int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const int32_t* doc_ids,
+                  const int32_t* word_ids, const uint16_t* z, int64_t ng, const int32_t* gw, const int64_t* go,
+                  const int64_t* gs, const int64_t* dw_ptr, const int64_t* dw_tok) {
+    CU(cudaSetDevice(s->device), "cudaSetDevice");
+    const int K = s->K, V = s->V;
+    const int64_t D = doc_hi - doc_lo;
+    if (D < 0 || T < 0) return fail(GF_ERR_SHAPE, "negative chunk size");
+    if (T >= (int64_t)UINT32_MAX || D >= (int64_t)UINT32_MAX)
+        return fail(GF_ERR_CAPACITY, "shard has %lld tokens: split the corpus over more shards", (long long)T);
+    // ---- validate the chunk (corpus.py:160-198 invariants) ----
+    int64_t covered = 0;
+    for (int64_t g = 0; g < ng; ++g) {
+        if (gw[g] < 0 || gw[g] >= V) return fail(GF_ERR_SHAPE, "group word %d outside [0, %d)", gw[g], V);
+        if (go[g] < 0 || gs[g] < 0 || go[g] + gs[g] > T) return fail(GF_ERR_SHAPE, "group %lld out of range", (long long)g);
+        covered += gs[g];
+    }
+    if (covered != T) return fail(GF_ERR_SHAPE, "word groups cover %lld of %lld tokens", (long long)covered, (long long)T);
+    if (dw_ptr[0] != 0 || dw_ptr[D] != T) return fail(GF_ERR_SHAPE, "doc-word map does not cover the chunk");
+    for (int64_t t = 0; t < T; ++t) {
+        if (z[t] >= K) return fail(GF_ERR_SHAPE, "assignment %d at token %lld >= K=%d", (int)z[t], (long long)t, K);
+        if (doc_ids[t] < doc_lo || doc_ids[t] >= doc_hi)
+            return fail(GF_ERR_SHAPE, "token %lld: document %d outside [%lld, %lld)", (long long)t, doc_ids[t],
+                        (long long)doc_lo, (long long)doc_hi);
+    }
+    for (int64_t g = 0; g < ng; ++g)
+        for (int64_t t = go[g]; t < go[g] + gs[g]; ++t)
+            if (word_ids[t] != gw[g]) return fail(GF_ERR_SHAPE, "token %lld is not in its word group", (long long)t);
+    // ---- phi layout ----
+    if (s->global_freq.empty()) {
+        s->global_freq.assign(V, 0);
+        for (int64_t g = 0; g < ng; ++g) s->global_freq[gw[g]] += gs[g];
+    }
+    if (int rc = set_layout(s)) return rc;
+    // ---- (doc, word) runs in token order ----
+    std::vector<uint32_t> run_doc, run_start;
+    run_doc.reserve((size_t)(T / 2 + 16));
+    run_start.reserve((size_t)(T / 2 + 16));
+    for (int64_t t = 0; t < T; ++t)
+        if (t == 0 || word_ids[t] != word_ids[t - 1] || doc_ids[t] != doc_ids[t - 1]) {
+            run_doc.push_back((uint32_t)(doc_ids[t] - doc_lo));
+            run_start.push_back((uint32_t)t);
+        }
+    const int64_t R = (int64_t)run_doc.size();
+    run_start.push_back((uint32_t)T);
+    // ---- heavy-first slices (sort_word_groups_desc order, corpus.py:290-302) ----
+    std::vector<int64_t> order((size_t)ng);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+        return gs[a] != gs[b] ? gs[a] > gs[b] : gw[a] < gw[b];
+    });
+    std::vector<int4> slices, items;
+    for (int64_t gi : order) {
+        if (gs[gi] == 0) continue;
+        const int32_t v = gw[gi];
+        const int col = s->word_col[v];
+        const int64_t t0 = go[gi], t1 = go[gi] + gs[gi];
+        int64_t rb = std::lower_bound(run_start.begin(), run_start.end() - 1, (uint32_t)t0) - run_start.begin();
+        const int64_t re = std::lower_bound(run_start.begin(), run_start.end() - 1, (uint32_t)t1) - run_start.begin();
+        const size_t first = slices.size();
+        while (rb < re) {
+            int64_t r = rb;
+            while (r < re && (int64_t)run_start[r] - (int64_t)run_start[rb] < gf::kSliceTokens) ++r;
+            slices.push_back(make_int4(v, (int)rb, (int)r, col));
+            rb = r;
+        }
+        if (col >= 0) {
+            items.push_back(make_int4(col, (int)t0, (int)t1, 0));
+        } else {
+            const bool split = slices.size() - first > 1;
+            for (size_t i = first; i < slices.size(); ++i)
+                items.push_back(make_int4(col, (int)run_start[slices[i].y], (int)run_start[slices[i].z], split ? 1 : 0));
+        }
+    }
+    if ((int64_t)slices.size() >= (int64_t)INT32_MAX) return fail(GF_ERR_CAPACITY, "too many slices");
+    // ---- doc-word map and theta capacities ----
+    std::vector<uint32_t> dwp((size_t)D + 1), dwt((size_t)T);
+    for (int64_t d = 0; d <= D; ++d) dwp[d] = (uint32_t)dw_ptr[d];
+    for (int64_t t = 0; t < T; ++t) {
+        if (dw_tok[t] < 0 || dw_tok[t] >= T) return fail(GF_ERR_SHAPE, "doc-word map entry out of range");
+        dwt[t] = (uint32_t)dw_tok[t];
+    }
+    std::vector<uint2> meta((size_t)D);
+    uint64_t cap = 0;
+    double llc = 0.0;
+    for (int64_t d = 0; d < D; ++d) {
+        const int64_t L = dw_ptr[d + 1] - dw_ptr[d];
+        if (L < 0) return fail(GF_ERR_SHAPE, "doc-word map not monotone");
+        meta[d] = make_uint2((uint32_t)cap, 0u);
+        cap += (uint64_t)((std::min<int64_t>(K, L) + 3) & ~3LL);
+        if (L > 0) llc += (double)L * std::log((double)L + (double)K * s->alpha);
+        if (cap >= (uint64_t)UINT32_MAX) return fail(GF_ERR_CAPACITY, "theta rows exceed 2^32 entries");
+    }
+    s->ll_const = llc;
+    // ---- device buffers ----
+    free_dev(s);
+    auto& dv = s->d;
+    int rc;
+    if ((rc = dev_alloc(&dv.z, T, "z")) || (rc = dev_alloc(&dv.run_doc, R, "runs")) ||
+        (rc = dev_alloc(&dv.run_start, R + 1, "runs")) || (rc = dev_alloc(&dv.slices, slices.size(), "slices")) ||
+        (rc = dev_alloc(&dv.k2items, items.size(), "items")) || (rc = dev_alloc(&dv.dw_ptr, D + 1, "dw_ptr")) ||
+        (rc = dev_alloc(&dv.dw_tok, T, "dw_tok")) || (rc = dev_alloc(&dv.theta_ent, cap + 4, "theta")) ||
+        (rc = dev_alloc(&dv.theta_meta, D, "theta")) || (rc = dev_alloc(&dv.sync, s->sync_u32, "phi")) ||
+        (rc = dev_alloc(&dv.inv_den, K, "inv_den")) || (rc = dev_alloc(&dv.ll_part, slices.size(), "ll")) ||
+        (rc = dev_alloc(&dv.ll_sum, 1, "ll")) || (rc = dev_alloc(&dv.errs, 2, "errs")) ||
+        (rc = dev_alloc(&dv.bytes, 1, "bytes")))
+        return rc;
+    cudaStream_t st = s->stream;
+    CU(cudaMemcpyAsync(dv.z, z, T * 2, cudaMemcpyHostToDevice, st), "upload");
+    CU(cudaMemcpyAsync(dv.run_doc, run_doc.data(), R * 4, cudaMemcpyHostToDevice, st), "upload");
+    CU(cudaMemcpyAsync(dv.run_start, run_start.data(), (R + 1) * 4, cudaMemcpyHostToDevice, st), "upload");
+    CU(cudaMemcpyAsync(dv.slices, slices.data(), slices.size() * sizeof(int4), cudaMemcpyHostToDevice, st), "upload");
+    CU(cudaMemcpyAsync(dv.k2items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, st), "upload");
+    CU(cudaMemcpyAsync(dv.dw_ptr, dwp.data(), (D + 1) * 4, cudaMemcpyHostToDevice, st), "upload");
+    CU(cudaMemcpyAsync(dv.dw_tok, dwt.data(), T * 4, cudaMemcpyHostToDevice, st), "upload");
+    CU(cudaMemcpyAsync(dv.theta_meta, meta.data(), D * sizeof(uint2), cudaMemcpyHostToDevice, st), "upload");
+    CU(cudaMemsetAsync(dv.theta_ent, 0, (cap + 4) * 4, st), "memset");
+    CU(cudaMemsetAsync(dv.sync, 0, s->sync_u32 * 4, st), "memset");
+    CU(cudaMemsetAsync(dv.errs, 0xff, 16, st), "memset");
+    CU(cudaMemsetAsync(dv.bytes, 0, 8, st), "memset");
+    CU(cudaStreamSynchronize(st), "load");
+    s->doc_lo = doc_lo;
+    s->doc_hi = doc_hi;
+    s->D = D;
+    s->T = T;
+    s->R = R;
+    s->n_slices = (int64_t)slices.size();
+    s->n_k2 = (int64_t)items.size();
+    s->theta_cap = (int64_t)cap;
+    s->loaded = true;
+    return GF_OK;
+}
+
+static int need_loaded(gf_shard* s) {
+    if (!s || !s->loaded) return fail(GF_ERR_VALUE, "shard has no chunk loaded");
+    cudaSetDevice(s->device);
+    return GF_OK;
+}
+
+int gf_shard_rebuild_phi(gf_shard* s) {
+    if (int rc = need_loaded(s)) return rc;
+    CU(gf::launch_phi_rebuild(s), "rebuild_phi");
+    return GF_OK;
+}
+
+int gf_shard_rebuild_theta(gf_shard* s) {
+    if (int rc = need_loaded(s)) return rc;
+    CU(gf::launch_theta_rebuild(s), "rebuild_theta");
+    return GF_OK;
+}
+
+int gf_shard_prepare(gf_shard* s) {
+    if (int rc = need_loaded(s)) return rc;
+    CU(gf::launch_prepare(s), "prepare");
+    return GF_OK;
+}
+
+int gf_shard_sample(gf_shard* s, uint32_t iteration) {
+    if (int rc = need_loaded(s)) return rc;
+    CU(gf::launch_sample(s, iteration), "sample");
+    CU(gf::launch_ll_reduce(s), "loglik");
+    s->stat_sample_launches++;
+    return GF_OK;
+}
+
+int gf_shard_evaluate(gf_shard* s) {
+    if (int rc = need_loaded(s)) return rc;
+    CU(gf::launch_sample(s, 0, 1), "evaluate");
+    CU(gf::launch_ll_reduce(s), "loglik");
+    return GF_OK;
+}
+
+int gf_shard_iterate(gf_shard* s, uint32_t iteration) {
+    if (int rc = need_loaded(s)) return rc;
+    cudaStream_t st = s->stream;
+    if (s->timing) cudaEventRecord(s->ev[0], st);
+    CU(gf::launch_sample(s, iteration), "sample");
+    if (s->timing) cudaEventRecord(s->ev[1], st);
+    CU(gf::launch_phi_rebuild(s), "rebuild_phi");
+    if (s->timing) cudaEventRecord(s->ev[2], st);
+    CU(gf::launch_prepare(s), "prepare");
+    if (s->timing) cudaEventRecord(s->ev[3], st);
+    CU(gf::launch_theta_rebuild(s), "rebuild_theta");
+    if (s->timing) cudaEventRecord(s->ev[4], st);
+    CU(gf::launch_ll_reduce(s), "loglik");
+    s->stat_launches = 5;  // sample, phi_rebuild, prepare, theta_rebuild, ll_reduce
+    s->stat_sample_launches++;
+    return GF_OK;
+}
+
+int gf_shard_last_times(gf_shard* s, float* ms, int num) {
+    CU(cudaEventSynchronize(s->ev[4]), "events");
+    for (int i = 0; i < num && i < 4; ++i) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, s->ev[i], s->ev[i + 1]);
+        ms[i] = t;
+    }
+    return GF_OK;
+}
+
+int gf_shard_loglik_sum(gf_shard* s, double* out) {
+    if (int rc = need_loaded(s)) return rc;
+    double v = 0.0;
+    CU(cudaMemcpyAsync(&v, s->d.ll_sum, 8, cudaMemcpyDeviceToHost, s->stream), "loglik");
+    CU(cudaStreamSynchronize(s->stream), "loglik");
+    *out = v - s->ll_const;
+    return GF_OK;
+}
+
+int gf_shard_synchronize(gf_shard* s) {
+    cudaSetDevice(s->device);
+    CU(cudaStreamSynchronize(s->stream), "synchronize");
+    return GF_OK;
+}
+
+int gf_shard_check_errors(gf_shard* s) {
+    if (int rc = need_loaded(s)) return rc;
+    unsigned long long e[2];
+    CU(cudaMemcpyAsync(e, s->d.errs, 16, cudaMemcpyDeviceToHost, s->stream), "errors");
+    CU(cudaStreamSynchronize(s->stream), "errors");
+    CU(cudaMemsetAsync(s->d.errs, 0xff, 16, s->stream), "errors");
+    if (e[1] != ~0ULL) {
+        const long long d = (long long)(e[1] >> 32) + s->doc_lo;
+        return fail(GF_ERR_OVERFLOW, "document %lld: topic count %llu exceeds 16-bit range", d,
+                    (unsigned long long)(e[1] & 0xffffffffULL));
+    }
+    if (e[0] != ~0ULL)
+        return fail(GF_ERR_CONSISTENCY, "token %llu: its current topic is absent from its document's theta row "
+                    "(or from phi / n_k)", (unsigned long long)e[0]);
+    return GF_OK;
+}
+
+int gf_shard_sync_buffer(gf_shard* s, void** p, int64_t* n) {
+    if (int rc = need_loaded(s)) return rc;
+    *p = s->d.sync;
+    *n = s->sync_u32;
+    return GF_OK;
+}
+
+int gf_shard_get_assignments(gf_shard* s, uint16_t* out) {
+    if (int rc = need_loaded(s)) return rc;
+    CU(cudaMemcpyAsync(out, s->d.z, s->T * 2, cudaMemcpyDeviceToHost, s->stream), "get_assignments");
+    CU(cudaStreamSynchronize(s->stream), "get_assignments");
+    return GF_OK;
+}
+
+int gf_shard_set_assignments(gf_shard* s, const uint16_t* in) {
+    if (int rc = need_loaded(s)) return rc;
+    // range is checked on the device (K1/K2/K3 flag z >= K as a consistency error)
+    CU(cudaMemcpyAsync(s->d.z, in, s->T * 2, cudaMemcpyHostToDevice, s->stream), "set_assignments");
+    CU(cudaStreamSynchronize(s->stream), "set_assignments");
+    return GF_OK;
+}
+
+static int fetch_meta(gf_shard* s, std::vector<uint2>& meta) {
+    meta.resize((size_t)s->D);
+    if (s->D) CU(cudaMemcpyAsync(meta.data(), s->d.theta_meta, s->D * sizeof(uint2), cudaMemcpyDeviceToHost, s->stream),
+                 "theta meta");
+    CU(cudaStreamSynchronize(s->stream), "theta meta");
+    return GF_OK;
+}
+
+int gf_shard_theta_nnz(gf_shard* s, int64_t* nnz) {
+    if (int rc = need_loaded(s)) return rc;
+    std::vector<uint2> meta;
+    if (int rc = fetch_meta(s, meta)) return rc;
+    int64_t n = 0;
+    for (auto& m : meta) n += m.y;
+    *nnz = n;
+    return GF_OK;
+}
+
+int gf_shard_get_theta(gf_shard* s, int64_t* row_ptr, uint16_t* ids, uint16_t* cnts) {
+    if (int rc = need_loaded(s)) return rc;
+    std::vector<uint2> meta;
+    if (int rc = fetch_meta(s, meta)) return rc;
+    row_ptr[0] = 0;
+    for (int64_t d = 0; d < s->D; ++d) row_ptr[d + 1] = row_ptr[d] + meta[d].y;
+    const int64_t nnz = row_ptr[s->D];
+    int64_t* drp = nullptr;
+    uint16_t* dids = nullptr;
+    CU(cudaMalloc(&drp, (s->D + 1) * 8), "get_theta");
+    CU(cudaMalloc(&dids, std::max<int64_t>(nnz, 1) * 4), "get_theta");
+    uint16_t* dcnt = dids + std::max<int64_t>(nnz, 1);
+    cudaMemcpyAsync(drp, row_ptr, (s->D + 1) * 8, cudaMemcpyHostToDevice, s->stream);
+    cudaError_t e = gf::launch_theta_export(s, drp, dids, dcnt);
+    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(ids, dids, nnz * 2, cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(cnts, dcnt, nnz * 2, cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    cudaFree(drp);
+    cudaFree(dids);
+    if (e != cudaSuccess) return cuda_fail(e, "get_theta");
+    return GF_OK;
+}
+
+int gf_shard_set_theta(gf_shard* s, const int64_t* row_ptr, const uint16_t* ids, const uint16_t* cnts) {
+    if (int rc = need_loaded(s)) return rc;
+    std::vector<uint2> meta;
+    if (int rc = fetch_meta(s, meta)) return rc;
+    for (int64_t d = 0; d < s->D; ++d) {
+        const int64_t n = row_ptr[d + 1] - row_ptr[d];
+        const uint32_t next = d + 1 < s->D ? meta[d + 1].x : (uint32_t)s->theta_cap;
+        if (n < 0 || n > (int64_t)(next - meta[d].x))
+            return fail(GF_ERR_SHAPE, "theta row %lld has %lld entries, capacity %u", (long long)d, (long long)n,
+                        next - meta[d].x);
+        for (int64_t j = row_ptr[d]; j < row_ptr[d + 1]; ++j) {
+            if (ids[j] >= s->K || cnts[j] == 0) return fail(GF_ERR_SHAPE, "theta row %lld: bad entry", (long long)d);
+            if (j > row_ptr[d] && ids[j] <= ids[j - 1])
+                return fail(GF_ERR_SHAPE, "theta row %lld: topic ids not strictly increasing", (long long)d);
+        }
+    }
+    const int64_t nnz = row_ptr[s->D];
+    int64_t* drp = nullptr;
+    uint16_t* dids = nullptr;
+    CU(cudaMalloc(&drp, (s->D + 1) * 8), "set_theta");
+    CU(cudaMalloc(&dids, std::max<int64_t>(nnz, 1) * 4), "set_theta");
+    uint16_t* dcnt = dids + std::max<int64_t>(nnz, 1);
+    cudaMemcpyAsync(drp, row_ptr, (s->D + 1) * 8, cudaMemcpyHostToDevice, s->stream);
+    if (nnz) cudaMemcpyAsync(dids, ids, nnz * 2, cudaMemcpyHostToDevice, s->stream);
+    if (nnz) cudaMemcpyAsync(dcnt, cnts, nnz * 2, cudaMemcpyHostToDevice, s->stream);
+    cudaError_t e = gf::launch_theta_import(s, drp, dids, dcnt);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    cudaFree(drp);
+    cudaFree(dids);
+    if (e != cudaSuccess) return cuda_fail(e, "set_theta");
+    return GF_OK;
+}
+
+int gf_shard_get_phi(gf_shard* s, uint32_t* counts_kv, int64_t* totals) {
+    if (int rc = need_loaded(s)) return rc;
+    const size_t cells = (size_t)s->K * s->V;
+    uint32_t* dout = nullptr;
+    int32_t* dcol = nullptr;
+    CU(cudaMalloc(&dout, cells * 4), "get_phi");
+    CU(cudaMalloc(&dcol, (size_t)s->V * 4), "get_phi");
+    std::vector<uint32_t> nk((size_t)s->K);
+    cudaMemcpyAsync(dcol, s->word_col.data(), (size_t)s->V * 4, cudaMemcpyHostToDevice, s->stream);
+    cudaError_t e = gf::launch_phi_export(s, dout, dcol);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(counts_kv, dout, cells * 4, cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(nk.data(), s->d.sync + s->off_nk_u32, (size_t)s->K * 4, cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    cudaFree(dout);
+    cudaFree(dcol);
+    if (e != cudaSuccess) return cuda_fail(e, "get_phi");
+    for (int k = 0; k < s->K; ++k) totals[k] = nk[k];
+    return GF_OK;
+}
+
+int gf_shard_set_phi(gf_shard* s, const uint32_t* counts_kv, const int64_t* totals) {
+    if (int rc = need_loaded(s)) return rc;
+    for (int v = 0; v < s->V; ++v)
+        if (s->word_col[v] >= 0)
+            for (int k = 0; k < s->K; ++k)
+                if (counts_kv[(size_t)k * s->V + v] > 65535u)
+                    return fail(GF_ERR_OVERFLOW, "phi cell (topic %d, word %d) count %u exceeds its 16-bit column", k, v,
+                                counts_kv[(size_t)k * s->V + v]);
+    for (int k = 0; k < s->K; ++k)
+        if (totals[k] < 0 || totals[k] > (int64_t)UINT32_MAX) return fail(GF_ERR_OVERFLOW, "topic total out of range");
+    const size_t cells = (size_t)s->K * s->V;
+    uint32_t* din = nullptr;
+    int32_t* dcol = nullptr;
+    CU(cudaMalloc(&din, cells * 4), "set_phi");
+    CU(cudaMalloc(&dcol, (size_t)s->V * 4), "set_phi");
+    std::vector<uint32_t> nk((size_t)s->K);
+    for (int k = 0; k < s->K; ++k) nk[k] = (uint32_t)totals[k];
+    cudaMemsetAsync(s->d.sync, 0, s->sync_u32 * 4, s->stream);
+    cudaMemcpyAsync(dcol, s->word_col.data(), (size_t)s->V * 4, cudaMemcpyHostToDevice, s->stream);
+    cudaMemcpyAsync(din, counts_kv, cells * 4, cudaMemcpyHostToDevice, s->stream);
+    cudaError_t e = gf::launch_phi_import(s, din, dcol);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(s->d.sync + s->off_nk_u32, nk.data(), (size_t)s->K * 4, cudaMemcpyHostToDevice, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    cudaFree(din);
+    cudaFree(dcol);
+    if (e != cudaSuccess) return cuda_fail(e, "set_phi");
+    return GF_OK;
+}
+
+int gf_shard_phi_argmax(gf_shard* s, int64_t* max_count, int32_t* topic, int32_t* word) {
+    if (int rc = need_loaded(s)) return rc;
+    std::vector<uint32_t> kv((size_t)s->K * s->V);
+    std::vector<int64_t> tot((size_t)s->K);
+    if (int rc = gf_shard_get_phi(s, kv.data(), tot.data())) return rc;
+    size_t best = 0;
+    for (size_t i = 1; i < kv.size(); ++i)
+        if (kv[i] > kv[best]) best = i;
+    *max_count = kv.empty() ? 0 : kv[best];
+    *topic = (int32_t)(best / s->V);
+    *word = (int32_t)(best % s->V);
+    return GF_OK;
+}
+
+int gf_shard_stats(gf_shard* s, int64_t* st, int n) {
+    if (int rc = need_loaded(s)) return rc;
+    unsigned long long nnz_runs = 0;
+    CU(cudaMemcpyAsync(&nnz_runs, s->d.bytes, 8, cudaMemcpyDeviceToHost, s->stream), "stats");
+    CU(cudaStreamSynchronize(s->stream), "stats");
+    const int64_t K = s->K;
+    // K1 algorithmic bytes per launch: per run its doc id,
+    // run_start pair and theta meta (4 + 4 + 8) plus its theta row (4 B per
+    // entry, averaged over the launches since the last reset); per token z read
+    // + z' write (2 + 2); per slice the slice record (16), the word's phi
+    // column (2 or 4 B per topic), the K denominators (4 B) and its ll partial (8).
+    int64_t phi_col_bytes = 0;
+    {
+        std::vector<int4> sl((size_t)s->n_slices);
+        if (s->n_slices)
+            CU(cudaMemcpy(sl.data(), s->d.slices, sl.size() * sizeof(int4), cudaMemcpyDeviceToHost), "stats");
+        for (auto& x : sl) phi_col_bytes += (x.w >= 0 ? 2 : 4) * K;
+    }
+    const int64_t L = std::max<int64_t>(s->stat_sample_launches, 1);
+    const int64_t b_sample = s->R * 16 + (int64_t)(4 * nnz_runs) / L + s->T * 4 +
+                             s->n_slices * (16 + 4 * K + 8) + phi_col_bytes;
+    // K2: memset of the sync buffer + z read + work items (+ nonzero cells, not counted)
+    const int64_t b_phi = s->sync_u32 * 4 + s->T * 2 + s->n_k2 * 16;
+    // K3: dw_tok + gathered z per token, dw_ptr + meta per doc, 4 B per written entry
+    int64_t nnz = 0;
+    if (n > 2) gf_shard_theta_nnz(s, &nnz);
+    const int64_t b_theta = s->T * (4 + 2) + (s->D + 1) * 4 + s->D * 8 + nnz * 4;
+    int64_t v[9] = {b_sample, b_phi, b_theta, s->R, s->n_slices, s->T, nnz, s->stat_launches, s->stat_sample_launches};
+    for (int i = 0; i < n && i < 9; ++i) st[i] = v[i];
+    return GF_OK;
+}
+
+int gf_shard_reset_stats(gf_shard* s) {
+    if (int rc = need_loaded(s)) return rc;
+    CU(cudaMemsetAsync(s->d.bytes, 0, 8, s->stream), "reset_stats");
+    s->stat_sample_launches = 0;
+    return GF_OK;
+}
+
+// -------------------------------------------------------------- ptree ------
+int gf_ptree_sample(int device, const float* prefix, int64_t n, int32_t fanout, const float* u, int64_t m,
+                    int64_t* idx_out) {
+    if (fanout < 2 || fanout > 32) return fail(GF_ERR_VALUE, "fanout must be in [2, 32], got %d", fanout);
+    if (n < 1) return fail(GF_ERR_EMPTY, "weights must be a non-empty 1-d array");
+    const float total = prefix[n - 1];
+    if (!(total > 0.f)) return fail(GF_ERR_EMPTY, "cannot sample: total weight is zero");
+    for (int64_t i = 0; i < m; ++i)
+        if (!(u[i] >= 0.f) || !(u[i] < total)) return fail(GF_ERR_VALUE, "u values outside [0, total)");
+    int ndev = 0;
+    gf_device_count(&ndev);
+    if (ndev == 0) return fail(GF_ERR_NODEVICE, "no CUDA device visible");
+    CU(cudaSetDevice(device), "cudaSetDevice");
+    float *dp = nullptr, *du = nullptr;
+    int64_t* di = nullptr;
+    CU(cudaMalloc(&dp, n * 4), "ptree");
+    CU(cudaMalloc(&du, std::max<int64_t>(m, 1) * 4), "ptree");
+    CU(cudaMalloc(&di, std::max<int64_t>(m, 1) * 8), "ptree");
+    cudaMemcpy(dp, prefix, n * 4, cudaMemcpyHostToDevice);
+    if (m) cudaMemcpy(du, u, m * 4, cudaMemcpyHostToDevice);
+    cudaError_t e = gf::ptree_sample(dp, n, fanout, du, m, di, 0);
+    if (e == cudaSuccess && m) e = cudaMemcpy(idx_out, di, m * 8, cudaMemcpyDeviceToHost);
+    cudaFree(dp);
+    cudaFree(du);
+    cudaFree(di);
+    if (e != cudaSuccess) return cuda_fail(e, "ptree_sample");
+    return GF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,59 @@
+// gf_device.cuh -- device helpers: Philox4x32-10, warp scans, bitonic sort.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gf {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Philox4x32-10 (Salmon et al., SC'11; Random123 constants).  The oracle
+// restates the same function (oracle/gf_oracle.c gfo_philox4x32_10) and the
+// Random123 known-answer vectors pin both.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) { k.x += 0x9E3779B9u; k.y += 0xBB67AE85u; }
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    }
+    return c;
+}
+
+// top 24 bits -> float in [0, 1), exact
+__device__ __forceinline__ float u24(uint32_t r) { return __uint2float_rn(r >> 8) * 5.9604644775390625e-08f; }
+
+__device__ __forceinline__ float warp_incl_scan(float x, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        float y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x = __fadd_rn(x, y);
+    }
+    return x;
+}
+
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(kFull, x, o));
+    return x;
+}
+
+// ascending bitonic sort of one key per lane
+__device__ __forceinline__ uint32_t warp_bitonic_sort(uint32_t key, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            uint32_t p = __shfl_xor_sync(kFull, key, j);
+            bool up = (lane & k) == 0;
+            bool lower = (lane & j) == 0;
+            key = (lower == up) ? min(key, p) : max(key, p);
+        }
+    }
+    return key;
+}
+
+__device__ __forceinline__ float prev_float(float x) { return __int_as_float(__float_as_int(x) - 1); }
+
+}  // namespace gf

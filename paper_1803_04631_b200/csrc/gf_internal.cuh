@@ -1,0 +1,101 @@
+// gf_internal.cuh -- shared definitions of the B200 gibbsflow hot path.
+//
+// HBM layout of one document shard:
+//   z          u16[T]        topic of each token, word-group order (in place)
+//   run_doc    u32[R]        local doc of each (doc, word) run
+//   run_start  u32[R+1]      first token of each run
+//   slices     int4[N]       {word, run_begin, run_end, phi column} heavy-first
+//   k2items    int4[M]       {phi column, tok_begin, tok_end, atomic?}
+//   dw_ptr     u32[D+1], dw_tok u32[T]   doc-word map (corpus.py:201-207)
+//   theta_ent  u32[cap]      (count << 16 | topic) rows, fixed capacity
+//                            round4(min(K, L_d)) per doc, ids ascending
+//   theta_meta uint2[D]      {row offset, nnz}
+//   sync       u32[...]      [phi32 | phi16 packed | n_k]: word-major phi
+//                            columns (one contiguous K-vector per word)
+//   inv_den    f32[K]        1 / (n_k + V beta)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <string>
+#include <vector>
+
+namespace gf {
+
+constexpr int kSampleThreads = 256;         // 8 warps: 8 samplers share one Q-tree
+constexpr int kSliceTokens = 4096;          // tokens per sampler CTA (heavy words split)
+constexpr int kRowChunks = 4;               // theta entries cached per lane = 4 * kRowChunks
+constexpr int kMaxLevels = 5;
+
+struct TreeGeom {                            // Q-tree levels in shared memory
+    int nlev;
+    int off[kMaxLevels];
+    int len[kMaxLevels];
+    int total;                               // floats
+};
+
+struct ShardDev {
+    uint16_t* z = nullptr;
+    uint32_t* run_doc = nullptr;
+    uint32_t* run_start = nullptr;
+    int4* slices = nullptr;
+    int4* k2items = nullptr;
+    uint32_t* dw_ptr = nullptr;
+    uint32_t* dw_tok = nullptr;
+    uint32_t* theta_ent = nullptr;
+    uint2* theta_meta = nullptr;
+    uint32_t* sync = nullptr;
+    float* inv_den = nullptr;
+    double* ll_part = nullptr;
+    double* ll_sum = nullptr;
+    unsigned long long* errs = nullptr;      // [0] consistency token (min), [1] theta overflow key (min)
+    unsigned long long* bytes = nullptr;     // [0] sum over runs of nnz (sampler bytes model)
+    uint32_t* scratch = nullptr;             // export staging
+    size_t scratch_bytes = 0;
+};
+
+}  // namespace gf
+
+struct gf_shard {
+    int device = 0;
+    int K = 0, Kp = 0, V = 0;
+    double alpha = 0, beta = 0;
+    uint64_t seed = 0;
+    uint32_t heavy_threshold = 65535;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool loaded = false;
+    // host-side layout
+    std::vector<int64_t> global_freq;        // V
+    std::vector<int32_t> word_col;           // V: >=0 light column, <0 ~heavy column
+    int64_t n_heavy = 0, n_light = 0;
+    int64_t off_phi16_u32 = 0, off_nk_u32 = 0, sync_u32 = 0;
+    int64_t doc_lo = 0, doc_hi = 0, D = 0, T = 0, R = 0, n_slices = 0, n_k2 = 0;
+    int64_t theta_cap = 0;
+    double ll_const = 0.0;                    // sum_d L_d log(L_d + K alpha)
+    std::vector<int64_t> runs_per_doc_dummy;
+    gf::TreeGeom tree{};
+    gf::ShardDev d;
+    int64_t stat_sample_bytes = 0, stat_phi_bytes = 0, stat_theta_bytes = 0;
+    int64_t stat_launches = 0;
+    int64_t stat_sample_launches = 0;
+    cudaEvent_t ev[6] = {};
+    float last_ms[4] = {0, 0, 0, 0};
+    bool timing = true;
+};
+
+// kernel launchers (k_sample.cu / k_counts.cu / k_ptree.cu)
+namespace gf {
+cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only = 0);
+cudaError_t launch_phi_rebuild(gf_shard* s);
+cudaError_t launch_prepare(gf_shard* s);
+cudaError_t launch_theta_rebuild(gf_shard* s);
+cudaError_t launch_ll_reduce(gf_shard* s);
+cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt);
+cudaError_t launch_theta_import(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids,
+                                const uint16_t* d_cnt);
+cudaError_t launch_phi_export(gf_shard* s, uint32_t* d_out_kv, const int32_t* d_word_col);
+cudaError_t launch_phi_import(gf_shard* s, const uint32_t* d_in_kv, const int32_t* d_word_col);
+cudaError_t launch_nnz_bytes(gf_shard* s);
+cudaError_t ptree_sample(const float* d_prefix, int64_t n, int fanout, const float* d_u, int64_t m,
+                         int64_t* d_idx, cudaStream_t st);
+}  // namespace gf

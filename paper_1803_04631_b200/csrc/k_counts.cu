@@ -1,0 +1,365 @@
+// k_counts.cu -- count maintenance kernels (section 6.2):
+//   K2 phi_rebuild   model.py:142-161  rebuild_phi_replica (+ n_k)
+//   K3 theta_rebuild model.py:91-124   rebuild_theta_row / rebuild_theta
+//   prepare          Eq. 1 denominators 1/(n_k + V b)
+//   ll_reduce        deterministic fp64 reduction of the sampler's partials
+//   theta / phi export + import (the reference dataclass layouts)
+//   ptree primitive  ptree.py:116-151 (build levels + ballot descent)
+#include "gf_internal.cuh"
+#include "gf_device.cuh"
+
+namespace gf {
+
+// ---------------------------------------------------------------- K2 ------
+// Work items are (phi column, token range): one item per light word (the
+// whole group, <= heavy_threshold tokens so its 16-bit cells cannot
+// overflow), one item per slice of a heavy word (32-bit cells, global
+// atomics).  Each CTA histograms an item's topics in shared memory (tokens
+// are word-grouped, so the item is one contiguous z range) and writes only
+// the nonzero cells into the pre-zeroed sync buffer; n_k is accumulated per
+// CTA in shared memory and flushed with K atomics at the end.
+__global__ void __launch_bounds__(256) phi_rebuild_kernel(const int4* __restrict__ items, int n_items,
+                                                          const uint16_t* __restrict__ z, uint32_t* sync,
+                                                          int K, int Kp, long long off16, long long offnk,
+                                                          unsigned long long* errs) {
+    extern __shared__ uint32_t sh[];
+    uint32_t* bins = sh;
+    uint32_t* nks = sh + K;
+    for (int k = threadIdx.x; k < 2 * K; k += blockDim.x) sh[k] = 0;
+    __syncthreads();
+    uint16_t* phi16 = reinterpret_cast<uint16_t*>(sync + off16);
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int4 w = items[it];
+        const int col = w.x, t0 = w.y, t1 = w.z;
+        const bool atomic = w.w != 0;
+        for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+            const int k = z[t];
+            if (k < K) atomicAdd(&bins[k], 1u);
+            else atomicMin(errs, (unsigned long long)t);
+        }
+        __syncthreads();
+        if ((long long)(t1 - t0) * 8 >= K) {
+            for (int k = threadIdx.x; k < K; k += blockDim.x) {
+                const uint32_t c = bins[k];
+                if (c) {
+                    bins[k] = 0;
+                    nks[k] += c;
+                    if (col >= 0) phi16[(size_t)col * Kp + k] = (uint16_t)c;
+                    else if (atomic) atomicAdd(&sync[(size_t)(~col) * K + k], c);
+                    else sync[(size_t)(~col) * K + k] = c;
+                }
+            }
+        } else {
+            for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+                const int k = z[t];
+                if (k >= K) continue;
+                const uint32_t c = atomicExch(&bins[k], 0u);
+                if (c) {
+                    atomicAdd(&nks[k], c);
+                    if (col >= 0) phi16[(size_t)col * Kp + k] = (uint16_t)c;
+                    else if (atomic) atomicAdd(&sync[(size_t)(~col) * K + k], c);
+                    else sync[(size_t)(~col) * K + k] = c;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    uint32_t* nk = sync + offnk;
+    for (int k = threadIdx.x; k < K; k += blockDim.x)
+        if (nks[k]) atomicAdd(&nk[k], nks[k]);
+}
+
+cudaError_t launch_phi_rebuild(gf_shard* s) {
+    cudaError_t e = cudaMemsetAsync(s->d.sync, 0, (size_t)s->sync_u32 * 4, s->stream);
+    if (e != cudaSuccess || s->n_k2 == 0) return e;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
+    const size_t smem = (size_t)2 * s->K * sizeof(uint32_t);
+    static bool attr = false;
+    if (!attr) {
+        e = cudaFuncSetAttribute(phi_rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int per_sm = smem <= 16 * 1024 ? 8 : (smem <= 48 * 1024 ? 4 : 1);
+    const long long grid = std::min<long long>(s->n_k2, (long long)nsm * per_sm);
+    phi_rebuild_kernel<<<(unsigned)grid, 256, smem, s->stream>>>(s->d.k2items, (int)s->n_k2, s->d.z, s->d.sync, s->K,
+                                                                  s->Kp, s->off_phi16_u32, s->off_nk_u32, s->d.errs);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- prepare ------
+__global__ void prepare_kernel(const uint32_t* __restrict__ nk, float* inv_den, int K, double vbeta) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < K) inv_den[k] = (float)(1.0 / ((double)nk[k] + vbeta));
+}
+
+cudaError_t launch_prepare(gf_shard* s) {
+    prepare_kernel<<<(s->K + 255) / 256, 256, 0, s->stream>>>(s->d.sync + s->off_nk_u32, s->d.inv_den, s->K,
+                                                              (double)s->V * s->beta);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K3 ------
+// One warp per document.  Short documents (<= 32 tokens): the topics are
+// gathered through the doc-word map into one register per lane, bitonic-sorted
+// across the warp and run-length encoded with ballots (no K-sized state).
+// Longer documents: dense K-bin histogram in the warp's shared-memory slice
+// (section 6.2 "generate a dense array ... then CSR"), then an
+// ascending ballot/popc compaction.  Output rows: (count << 16 | topic),
+// ascending topic, written into the fixed-capacity row; nnz into meta.y.
+__global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
+                                                            const uint32_t* __restrict__ dw_tok,
+                                                            const uint16_t* __restrict__ z, uint32_t* theta_ent,
+                                                            uint2* theta_meta, int K, int warps_per_cta,
+                                                            unsigned long long* errs) {
+    extern __shared__ uint32_t sh[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* bins = sh + (size_t)warp * K;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int d = blockIdx.x * warps_per_cta + warp; d < D; d += gridDim.x * warps_per_cta) {
+        const uint32_t b = dw_ptr[d], L = dw_ptr[d + 1] - b;
+        const uint32_t off = theta_meta[d].x;
+        uint32_t nnz;
+        if (L <= 32) {
+            uint32_t key = 0xffffu;
+            if (lane < (int)L) key = z[dw_tok[b + lane]];
+            if (key >= (uint32_t)K && lane < (int)L) { atomicMin(errs, (unsigned long long)dw_tok[b + lane]); key = 0xffffu; }
+            key = warp_bitonic_sort(key, lane);
+            const uint32_t prev = __shfl_up_sync(kFull, key, 1);
+            const bool head = key != 0xffffu && (lane == 0 || key != prev);
+            const unsigned heads = __ballot_sync(kFull, head);
+            if (head) {
+                const unsigned later = heads & ~((2u << lane) - 1u);
+                const uint32_t next = later ? (uint32_t)(__ffs(later) - 1) : L;
+                theta_ent[off + __popc(heads & lt)] = key | ((next - lane) << 16);
+            }
+            nnz = __popc(heads);
+        } else {
+            for (int k = lane; k < K; k += 32) bins[k] = 0;
+            __syncwarp();
+            for (uint32_t i = lane; i < L; i += 32) {
+                const uint32_t k = z[dw_tok[b + i]];
+                if (k < (uint32_t)K) atomicAdd(&bins[k], 1u);
+                else atomicMin(errs, (unsigned long long)dw_tok[b + i]);
+            }
+            __syncwarp();
+            uint32_t base = 0, mx = 0;
+            for (int c = 0; c < K; c += 32) {
+                const int k = c + lane;
+                const uint32_t v = k < K ? bins[k] : 0u;
+                const unsigned m = __ballot_sync(kFull, v > 0);
+                if (v) theta_ent[off + base + __popc(m & lt)] = (uint32_t)k | (min(v, 65535u) << 16);
+                mx = max(mx, v);
+                base += __popc(m);
+            }
+            nnz = base;
+            mx = warp_max_u32(mx);
+            if (mx > 65535u && lane == 0) atomicMin(errs + 1, ((unsigned long long)d << 32) | mx);
+            __syncwarp();
+        }
+        if (lane == 0) theta_meta[d].y = nnz;
+    }
+}
+
+cudaError_t launch_theta_rebuild(gf_shard* s) {
+    if (s->D == 0) return cudaSuccess;
+    int wpc = 8;
+    while (wpc > 1 && (size_t)wpc * s->K * 4 > 96 * 1024) wpc >>= 1;
+    const size_t smem = (size_t)wpc * s->K * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(theta_rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
+    const long long need = (s->D + wpc - 1) / wpc;
+    const long long grid = std::min<long long>(need, (long long)nsm * 16);
+    theta_rebuild_kernel<<<(unsigned)grid, wpc * 32, smem, s->stream>>>((int)s->D, s->d.dw_ptr, s->d.dw_tok, s->d.z,
+                                                                         s->d.theta_ent, s->d.theta_meta, s->K, wpc,
+                                                                         s->d.errs);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------- ll reduce ------
+__global__ void ll_reduce_kernel(const double* __restrict__ part, long long n, double* out) {
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < n; i += 256) s += part[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+cudaError_t launch_ll_reduce(gf_shard* s) {
+    ll_reduce_kernel<<<1, 256, 0, s->stream>>>(s->d.ll_part, s->n_slices, s->d.ll_sum);
+    return cudaGetLastError();
+}
+
+// --------------------------------------------------------- theta export ------
+__global__ void theta_export_kernel(int D, const uint2* __restrict__ meta, const uint32_t* __restrict__ ent,
+                                    const int64_t* __restrict__ rowptr, uint16_t* ids, uint16_t* cnt) {
+    const int lane = threadIdx.x & 31;
+    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long d = w; d < D; d += nw) {
+        const uint2 m = meta[d];
+        const int64_t o = rowptr[d];
+        for (uint32_t j = lane; j < m.y; j += 32) {
+            const uint32_t e = ent[m.x + j];
+            ids[o + j] = (uint16_t)(e & 0xffffu);
+            cnt[o + j] = (uint16_t)(e >> 16);
+        }
+    }
+}
+
+__global__ void theta_import_kernel(int D, uint2* meta, uint32_t* ent, const int64_t* __restrict__ rowptr,
+                                    const uint16_t* __restrict__ ids, const uint16_t* __restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long d = w; d < D; d += nw) {
+        const int64_t o = rowptr[d], n = rowptr[d + 1] - o;
+        const uint32_t base = meta[d].x;
+        for (int64_t j = lane; j < n; j += 32) ent[base + j] = (uint32_t)ids[o + j] | ((uint32_t)cnt[o + j] << 16);
+        if (lane == 0) meta[d].y = (uint32_t)n;
+    }
+}
+
+cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt) {
+    if (s->D == 0) return cudaSuccess;
+    theta_export_kernel<<<1184, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, s->d.theta_ent, d_rowptr, d_ids,
+                                                     d_cnt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_theta_import(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids, const uint16_t* d_cnt) {
+    if (s->D == 0) return cudaSuccess;
+    theta_import_kernel<<<1184, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, s->d.theta_ent, d_rowptr, d_ids,
+                                                     d_cnt);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------- phi export ------
+// word-major columns <-> reference K x V row-major, 32x32 tiles through smem
+__global__ void phi_export_kernel(const uint32_t* __restrict__ sync, long long off16, const int32_t* __restrict__ wcol,
+                                  int K, int Kp, int V, uint32_t* out) {
+    __shared__ uint32_t tile[32][33];
+    const int v0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    const uint16_t* phi16 = reinterpret_cast<const uint16_t*>(sync + off16);
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int v = v0 + r, k = k0 + threadIdx.x;
+        uint32_t val = 0;
+        if (v < V && k < K) {
+            const int col = wcol[v];
+            val = col >= 0 ? (uint32_t)phi16[(size_t)col * Kp + k] : sync[(size_t)(~col) * K + k];
+        }
+        tile[r][threadIdx.x] = val;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int k = k0 + r, v = v0 + threadIdx.x;
+        if (k < K && v < V) out[(size_t)k * V + v] = tile[threadIdx.x][r];
+    }
+}
+
+__global__ void phi_import_kernel(uint32_t* sync, long long off16, const int32_t* __restrict__ wcol, int K, int Kp,
+                                  int V, const uint32_t* __restrict__ in) {
+    __shared__ uint32_t tile[32][33];
+    const int v0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    uint16_t* phi16 = reinterpret_cast<uint16_t*>(sync + off16);
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int k = k0 + r, v = v0 + threadIdx.x;
+        tile[threadIdx.x][r] = (k < K && v < V) ? in[(size_t)k * V + v] : 0u;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int v = v0 + r, k = k0 + threadIdx.x;
+        if (v < V && k < K) {
+            const int col = wcol[v];
+            if (col >= 0) phi16[(size_t)col * Kp + k] = (uint16_t)tile[r][threadIdx.x];
+            else sync[(size_t)(~col) * K + k] = tile[r][threadIdx.x];
+        }
+    }
+}
+
+cudaError_t launch_phi_export(gf_shard* s, uint32_t* d_out, const int32_t* d_wcol) {
+    dim3 grid((s->V + 31) / 32, (s->K + 31) / 32);
+    phi_export_kernel<<<grid, dim3(32, 8), 0, s->stream>>>(s->d.sync, s->off_phi16_u32, d_wcol, s->K, s->Kp, s->V,
+                                                            d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_phi_import(gf_shard* s, const uint32_t* d_in, const int32_t* d_wcol) {
+    dim3 grid((s->V + 31) / 32, (s->K + 31) / 32);
+    phi_import_kernel<<<grid, dim3(32, 8), 0, s->stream>>>(s->d.sync, s->off_phi16_u32, d_wcol, s->K, s->Kp, s->V,
+                                                            d_in);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------ ptree primitive ------
+__global__ void ptree_level_kernel(const float* prev, long long prev_len, float* next, long long len, int F) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < len) next[i] = prev[min((long long)F * i + F - 1, prev_len - 1)];
+}
+
+__global__ void ptree_sample_kernel(const float* levels, const long long* off, const long long* len, int nlev, int F,
+                                    const float* __restrict__ u, long long m, int64_t* out) {
+    const int lane = threadIdx.x & 31;
+    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long q = w; q < m; q += nw) {
+        const float uu = u[q];
+        long long idx = 0;
+        for (int l = nlev - 1; l >= 0; --l) {
+            const long long lo = idx * F;
+            const int n = (int)min((long long)F, len[l] - lo);
+            const bool ok = lane < n && levels[off[l] + lo + lane] > uu;
+            const unsigned b = __ballot_sync(kFull, ok);
+            idx = b ? lo + __ffs(b) - 1 : lo + n - 1;   // last child bounds u from above
+        }
+        if (lane == 0) out[q] = idx;
+    }
+}
+
+cudaError_t ptree_sample(const float* d_prefix, int64_t n, int F, const float* d_u, int64_t m, int64_t* d_idx,
+                         cudaStream_t st) {
+    std::vector<long long> off{0}, len{n};
+    long long total = n;
+    while (len.back() > 1) {
+        const long long l = (len.back() + F - 1) / F;
+        off.push_back(total);
+        len.push_back(l);
+        total += l;
+    }
+    float* lv = nullptr;
+    long long* dmeta = nullptr;
+    cudaError_t e = cudaMalloc(&lv, sizeof(float) * total);
+    if (e != cudaSuccess) return e;
+    e = cudaMalloc(&dmeta, sizeof(long long) * 2 * off.size());
+    if (e != cudaSuccess) { cudaFree(lv); return e; }
+    cudaMemcpyAsync(lv, d_prefix, sizeof(float) * n, cudaMemcpyDeviceToDevice, st);
+    for (size_t l = 1; l < off.size(); ++l)
+        ptree_level_kernel<<<(unsigned)((len[l] + 255) / 256), 256, 0, st>>>(lv + off[l - 1], len[l - 1], lv + off[l],
+                                                                          len[l], F);
+    cudaMemcpyAsync(dmeta, off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dmeta + off.size(), len.data(), sizeof(long long) * len.size(), cudaMemcpyHostToDevice, st);
+    const long long blocks = std::min<long long>((m + 7) / 8, 4096);
+    if (m > 0)
+        ptree_sample_kernel<<<(unsigned)blocks, 256, 0, st>>>(lv, dmeta, dmeta + off.size(), (int)off.size(), F, d_u, m,
+                                                            d_idx);
+    e = cudaStreamSynchronize(st);
+    cudaFree(lv);
+    cudaFree(dmeta);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+}  // namespace gf

@@ -1,0 +1,290 @@
+"""Training engine -- deferred-mode CGS on one or more B200s.
+
+One process per GPU.  Rank r of G owns document shard r of
+`greedy_boundaries(doc_lengths, G)` (corpus.py:210-237; C = G, M = 1 --
+WorkSchedule1, every configured corpus fits in 180 GB of HBM), its theta rows
+(never exchanged) and a phi replica.  One iteration (PAPER.md
+section 6.2):
+
+    K1 sample(it)     every token against the iteration-start theta / phi
+    K2 rebuild_phi    this shard's replica + n_k into the sync buffer
+    allreduce(sync)   NCCL sum over ranks on torch's NCCL stream ...
+    K3 rebuild_theta  ... overlapped with the allreduce on the compute stream
+    prepare           Eq. 1 denominators from the global n_k
+
+The allreduce is an integer sum, so the result equals SPEC's pairwise
+reduce_phi / broadcast_phi bit for bit; with the
+token-keyed Philox stream the trained model is identical for every G.
+"""
+
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from .corpus import greedy_boundaries, make_chunk
+from .errors import ShapeMismatchError
+from .model import PhiMatrix, ThetaRows, check_conservation, concat_theta, phi_dtype
+
+
+@dataclass
+class TrainConfig:
+    """SPEC.md:312-314."""
+
+    num_topics: int
+    iterations: int = 100
+    alpha: Optional[float] = None        # default 50 / K
+    beta: float = 0.01
+    workers: int = 1                     # G: one process (rank) per GPU
+    chunks_per_worker: int = 1           # M: only WorkSchedule1 (M = 1)
+    seed: int = 42
+    mode: str = "deferred"
+    fanout: int = 32
+    phi_width: int = 32                  # width of the exported PhiMatrix
+    memory_budget: Optional[int] = None
+    eval_every: int = 1
+    heavy_threshold: int = 65535         # device phi: 16-bit columns below it
+    check_conservation: bool = False
+
+    def __post_init__(self):
+        if not 1 <= self.num_topics < 2**16:
+            raise ValueError(f"topic count {self.num_topics} outside [1, 65536)")
+        if self.alpha is None:
+            self.alpha = 50.0 / self.num_topics
+        if not (self.alpha > 0 and self.beta > 0):
+            raise ValueError("alpha and beta must be > 0")
+        if self.mode != "deferred":
+            raise ValueError("the B200 engine runs deferred mode; exact (per-token) CGS is the CPU oracle")
+        if self.fanout != 32:
+            raise ValueError("the device tree is 32-ary (one warp per level)")
+        if self.chunks_per_worker != 1:
+            raise ValueError("only WorkSchedule1 (M = 1): every configured corpus fits in HBM")
+        phi_dtype(self.phi_width)
+
+
+@dataclass
+class IterationReport:
+    """SPEC.md:316-319.  loglik_per_token describes the model the iteration
+    started from (it is fused into the sampling pass)."""
+
+    iteration: int
+    elapsed_sec: float
+    tokens_per_sec: float
+    loglik_per_token: Optional[float]
+    conservation: Optional[str] = None
+
+    def csv_row(self):
+        ll = "" if self.loglik_per_token is None else f"{self.loglik_per_token:.10f}"
+        return f"{self.iteration},{self.elapsed_sec:.6f},{self.tokens_per_sec:.3f},{ll}"
+
+
+CSV_HEADER = "iteration,elapsed_sec,tokens_per_sec,loglik_per_token"
+
+
+def _dist():
+    try:
+        import torch.distributed as dist
+
+        return dist if dist.is_available() and dist.is_initialized() else None
+    except ImportError:
+        return None
+
+
+class Trainer:
+    """Device-resident trainer for this rank's shard."""
+
+    def __init__(self, corpus, cfg, group=None, device=None, shard_factory=None):
+        self.cfg = cfg
+        self.corpus = corpus
+        self.group = group
+        d = _dist()
+        self.dist = d
+        self.rank = d.get_rank(group) if d else 0
+        self.world = d.get_world_size(group) if d else 1
+        if cfg.workers != self.world:
+            raise ShapeMismatchError(f"cfg.workers={cfg.workers} but {self.world} rank(s) are running")
+        K, V = cfg.num_topics, corpus.vocab_size
+        lo, hi = greedy_boundaries(corpus.doc_lengths, self.world)[self.rank]
+        a, b = int(corpus.doc_ptr[lo]), int(corpus.doc_ptr[hi])
+        self.chunk = make_chunk(self.rank, lo, hi, corpus.doc_ids[a:b], corpus.word_ids[a:b], V, K, cfg.seed)
+        freq = np.bincount(self.chunk.word_ids, minlength=V).astype(np.int64)
+        self.global_freq = self._allreduce_np(freq)
+        if device is None:
+            device = self._local_device()
+        self.device = device
+        if shard_factory is None:
+            from .shard import DeviceShard
+
+            shard_factory = DeviceShard
+        stream = None
+        if self.world > 1 and self._backend() == "nccl":
+            import torch
+
+            torch.cuda.set_device(device)
+            stream = torch.cuda.current_stream(device)
+        self.shard = shard_factory(K, V, cfg.alpha, cfg.beta, seed=cfg.seed, device=device,
+                                   heavy_threshold=cfg.heavy_threshold, global_word_freq=self.global_freq,
+                                   stream=stream)
+        self.shard.load(self.chunk)
+        self._sync_t = self.shard.sync_tensor() if self.world > 1 else None
+        self.num_tokens = corpus.num_tokens
+        self.iteration = 0
+        # counts from the initial assignments
+        self.shard.rebuild_phi()
+        self._allreduce_sync()
+        self.shard.prepare()
+        self.shard.rebuild_theta()
+        self.shard.check_errors()
+
+    # ------------------------------------------------------------ plumbing --
+    def _backend(self):
+        return self.dist.get_backend(self.group) if self.dist else None
+
+    def _local_device(self):
+        import os
+
+        return int(os.environ.get("LOCAL_RANK", "0")) if self.world > 1 else 0
+
+    def _allreduce_np(self, arr):
+        if self.world == 1:
+            return arr
+        import torch
+
+        if self._backend() == "nccl":
+            t = torch.as_tensor(arr).cuda()
+            self.dist.all_reduce(t, group=self.group)
+            return t.cpu().numpy()
+        t = torch.as_tensor(arr).clone()
+        self.dist.all_reduce(t, group=self.group)
+        return t.numpy()
+
+    def _allreduce_sync(self, async_op=False):
+        if self.world == 1:
+            return None
+        return self.dist.all_reduce(self._sync_t, group=self.group, async_op=async_op)
+
+    # -------------------------------------------------------------- steps --
+    def step(self):
+        """One deferred iteration; returns the IterationReport."""
+        it = self.iteration
+        t0 = time.perf_counter()
+        sh = self.shard
+        sh.sample(it)
+        sh.rebuild_phi()
+        work = self._allreduce_sync(async_op=True)
+        sh.rebuild_theta()                       # overlaps the phi allreduce
+        if work is not None:
+            work.wait()
+        sh.prepare()
+        ll = None
+        if self.cfg.eval_every and it % self.cfg.eval_every == 0:
+            ll = float(self._allreduce_np(np.array([sh.loglik_sum()], np.float64))[0]) / self.num_tokens
+        else:
+            sh.synchronize()
+        sh.check_errors()
+        elapsed = time.perf_counter() - t0
+        report = IterationReport(it, elapsed, self.num_tokens / elapsed if elapsed > 0 else float("inf"), ll)
+        if self.cfg.check_conservation:
+            theta, phi = self.theta(gather=True), self.phi()
+            report.conservation = check_conservation(theta, phi, self.corpus).detail
+        self.iteration += 1
+        return report
+
+    def evaluate(self):
+        """loglik_per_token of the current model."""
+        from . import _lib
+
+        _lib.check(_lib.lib().gf_shard_evaluate(self.shard._h))
+        return float(self._allreduce_np(np.array([self.shard.loglik_sum()], np.float64))[0]) / self.num_tokens
+
+    # -------------------------------------------------------------- export --
+    def theta(self, gather=True):
+        rp, ids, cn = self.shard.get_theta()
+        local = ThetaRows(rp, ids, cn, self.cfg.num_topics)
+        if self.world == 1 or not gather:
+            return local
+        parts = [None] * self.world
+        self.dist.all_gather_object(parts, (rp, ids, cn), group=self.group)
+        return concat_theta([ThetaRows(p[0], p[1], p[2], self.cfg.num_topics) for p in parts])
+
+    def phi(self):
+        if self.cfg.phi_width == 16:
+            self.shard.check_phi_width(16)
+        counts, totals = self.shard.get_phi()
+        return PhiMatrix(counts.astype(phi_dtype(self.cfg.phi_width), copy=False), totals)
+
+    def assignments(self):
+        return self.shard.get_assignments()
+
+    def close(self):
+        self.shard.close()
+
+
+def train(corpus, cfg, group=None, device=None, metrics_path=None):
+    """returns (ThetaRows, PhiMatrix, [IterationReport])."""
+    tr = Trainer(corpus, cfg, group=group, device=device)
+    reports = []
+    try:
+        for _ in range(cfg.iterations):
+            reports.append(tr.step())
+        theta, phi = tr.theta(gather=True), tr.phi()
+    finally:
+        tr.close()
+    if metrics_path is not None and tr.rank == 0:
+        with open(metrics_path, "w") as fh:
+            fh.write(CSV_HEADER + "\n")
+            for r in reports:
+                fh.write(r.csv_row() + "\n")
+    return theta, phi, reports
+
+
+fit = train  # the north star's fit/transform naming
+
+
+def transform(theta):
+    """Normalised doc-topic proportions of the TRAINING documents (an invented
+    convenience: inference on unseen documents is a SPEC non-goal)."""
+    K = theta.num_topics
+    out = np.zeros((theta.num_rows, K), np.float64)
+    rows = np.repeat(np.arange(theta.num_rows), np.diff(theta.row_ptr))
+    out[rows, theta.topic_ids.astype(np.int64)] = theta.counts
+    s = out.sum(axis=1, keepdims=True)
+    return out / np.maximum(s, 1)
+
+
+def reduce_phi(replicas, num_workers=None):
+    """pairwise tree merge in ceil(log2 G) rounds (round r:
+    replica j += replica j + 2^r for j = 0 mod 2^(r+1)).  Host-side form for
+    replicas already exported; on the device the NCCL allreduce does this."""
+    if not replicas:
+        raise ValueError("no replicas")
+    shape = replicas[0].counts.shape
+    for r in replicas:
+        if r.counts.shape != shape:
+            raise ShapeMismatchError(f"replica shape {r.counts.shape} != {shape}")
+    acc = [np.array(r.counts, dtype=np.int64) for r in replicas]
+    tot = [np.array(r.topic_totals, dtype=np.int64) for r in replicas]
+    G = len(acc)
+    step = 1
+    while step < G:
+        for j in range(0, G, 2 * step):
+            if j + step < G:
+                acc[j] += acc[j + step]
+                tot[j] += tot[j + step]
+        step *= 2
+    dtype = replicas[0].counts.dtype
+    if acc[0].max(initial=0) > np.iinfo(dtype).max:
+        from .errors import CountOverflowError
+
+        k, v = np.unravel_index(int(acc[0].argmax()), acc[0].shape)
+        raise CountOverflowError(f"phi cell (topic {k}, word {v}) count {int(acc[0][k, v])} "
+                                 f"exceeds {dtype.itemsize * 8}-bit range")
+    return PhiMatrix(acc[0].astype(dtype), tot[0])
+
+
+def broadcast_phi(global_phi, num_workers):
+    """every worker observes one immutable snapshot."""
+    global_phi.counts.setflags(write=False)
+    global_phi.topic_totals.setflags(write=False)
+    return [global_phi] * num_workers

@@ -1,0 +1,60 @@
+"""The sparsity-aware CGS sampler on the B200.
+
+`sample_chunk` is SPEC.md:359-367 in deferred mode: every draw of the chunk
+uses the iteration-start theta / phi snapshot, the token's own contribution
+excluded, two independent uniforms.  The
+draw runs in K1 (csrc/k_sample.cu); the RNG is Philox4x32-10 keyed by `seed`
+with counter (global doc, word, occurrence in its (doc, word) run, iteration),
+so results do not depend on the shard / GPU count.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .model import PhiMatrix, ThetaRows
+
+
+@dataclass
+class SamplerContext:
+    """SPEC.md:235-238."""
+
+    alpha: float
+    beta: float
+    num_topics: int
+    vocab_size: int
+    exclusion: bool = True
+
+    def __post_init__(self):
+        if not (self.alpha > 0 and self.beta > 0):
+            raise ValueError("alpha and beta must be > 0")
+        if not self.exclusion:
+            raise NotImplementedError("the B200 sampler always applies exclusion (SPEC.md:292)")
+
+
+def _local_theta(theta, chunk):
+    if theta.num_rows == chunk.num_local_docs:
+        return theta.row_ptr, theta.topic_ids, theta.counts
+    if theta.num_rows >= chunk.doc_hi:
+        a, b = int(theta.row_ptr[chunk.doc_lo]), int(theta.row_ptr[chunk.doc_hi])
+        rp = theta.row_ptr[chunk.doc_lo: chunk.doc_hi + 1] - a
+        return rp, theta.topic_ids[a:b], theta.counts[a:b]
+    raise ValueError("theta rows match neither the chunk nor the corpus")
+
+
+def sample_chunk(chunk, phi, theta, ctx, cfg=None, iteration=0, seed=None, device=0):
+    """Resample every assignment of `chunk` once; returns the new uint16 array.
+    `phi` is the global PhiMatrix, `theta` the ThetaRows of the chunk's
+    documents (local rows or the whole corpus)."""
+    from .shard import DeviceShard
+
+    if seed is None:
+        seed = getattr(cfg, "seed", 0) if cfg is not None else 0
+    with DeviceShard(ctx.num_topics, ctx.vocab_size, ctx.alpha, ctx.beta, seed=seed, device=device) as sh:
+        sh.load(chunk)
+        sh.set_phi(phi.counts.astype(np.uint32, copy=False), phi.topic_totals)
+        sh.set_theta(*_local_theta(theta, chunk))
+        sh.prepare()
+        sh.sample(iteration)
+        sh.check_errors()
+        return sh.get_assignments()

@@ -1,0 +1,234 @@
+"""DeviceShard: one document shard resident on one B200 (the C-ABI gf_shard).
+
+This is the runtime object behind every reference-facing call
+(`rebuild_theta`, `rebuild_phi_replica`, `sample_chunk`, `train`): a Chunk
+(corpus.py:160-198) uploaded once, its theta rows and a phi replica kept in
+HBM, and the four hot kernels driven through the C ABI:
+
+    sample(it)      K1  SPEC.md:359-367 (+ fused loglik)
+    rebuild_phi()   K2  model.py:142-161 (replica -> sync buffer)
+    prepare()           Eq. 1 denominators from the (global) n_k
+    rebuild_theta() K3  model.py:109-124
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import CountOverflowError
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a device buffer owned by a shard."""
+
+    def __init__(self, ptr, n, typestr, owner):
+        self._owner = owner
+        self.__cuda_array_interface__ = {
+            "shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
+            "version": 3, "strides": None, "stream": None,
+        }
+
+
+def sync_layout(global_word_freq, num_topics, heavy_threshold=65535):
+    """gf_sync_layout: (word_col int32[V], (phi16 off, n_k off, total) in u32 words)."""
+    freq = _lib.carr(global_word_freq, np.int64)
+    col = np.empty(len(freq), np.int32)
+    lay = np.empty(3, np.int64)
+    _lib.check(_lib.lib().gf_sync_layout(_lib.ptr(freq), len(freq), int(num_topics), int(heavy_threshold),
+                                         _lib.ptr(col), _lib.ptr(lay)))
+    return col, (int(lay[0]), int(lay[1]), int(lay[2]))
+
+
+class DeviceShard:
+    def __init__(self, num_topics, vocab_size, alpha, beta, seed=0, device=0,
+                 heavy_threshold=65535, global_word_freq=None, stream=None):
+        self.K = int(num_topics)
+        self.V = int(vocab_size)
+        self.alpha = float(alpha)
+        self.beta = float(beta)
+        self.device = int(device)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().gf_shard_create(ctypes.byref(h), self.device, self.K, self.V, self.alpha,
+                                              self.beta, int(seed) & 0xFFFFFFFFFFFFFFFF, int(heavy_threshold)))
+        self._h = h
+        self.heavy_threshold = int(heavy_threshold)
+        if stream is not None:
+            self.set_stream(stream)
+        if global_word_freq is not None:
+            f = _lib.carr(global_word_freq, np.int64)
+            if len(f) != self.V:
+                raise ValueError("global_word_freq must have vocab_size entries")
+            _lib.check(_lib.lib().gf_shard_set_vocab(self._h, _lib.ptr(f)))
+        self.chunk = None
+
+    # ---------------------------------------------------------------- life --
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().gf_shard_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_stream(self, stream):
+        """Run on a CUDA stream: a torch.cuda.Stream or a raw cudaStream_t int."""
+        handle = getattr(stream, "cuda_stream", stream)
+        _lib.check(_lib.lib().gf_shard_set_stream(self._h, ctypes.c_void_p(int(handle))))
+
+    def load(self, chunk):
+        c = chunk
+        self._keep = [
+            _lib.carr(c.doc_ids, np.int32), _lib.carr(c.word_ids, np.int32),
+            _lib.carr(c.assignments, np.uint16), _lib.carr(c.group_words, np.int32),
+            _lib.carr(c.group_offsets, np.int64), _lib.carr(c.group_sizes, np.int64),
+            _lib.carr(c.dw_ptr, np.int64), _lib.carr(c.dw_tok, np.int64),
+        ]
+        d, w, z, gw, go, gs, dp, dt = self._keep
+        _lib.check(_lib.lib().gf_shard_load(self._h, int(c.doc_lo), int(c.doc_hi), int(c.token_count),
+                                            _lib.ptr(d), _lib.ptr(w), _lib.ptr(z), len(gw), _lib.ptr(gw),
+                                            _lib.ptr(go), _lib.ptr(gs), _lib.ptr(dp), _lib.ptr(dt)))
+        self._keep = None
+        self.chunk = c
+        return self
+
+    # -------------------------------------------------------------- kernels --
+    def rebuild_phi(self):
+        _lib.check(_lib.lib().gf_shard_rebuild_phi(self._h))
+
+    def rebuild_theta(self):
+        _lib.check(_lib.lib().gf_shard_rebuild_theta(self._h))
+
+    def prepare(self):
+        _lib.check(_lib.lib().gf_shard_prepare(self._h))
+
+    def sample(self, iteration):
+        _lib.check(_lib.lib().gf_shard_sample(self._h, int(iteration)))
+
+    def iterate(self, iteration):
+        _lib.check(_lib.lib().gf_shard_iterate(self._h, int(iteration)))
+
+    def initialize(self):
+        """Counts from the initial assignments (one GPU: replica == global)."""
+        self.rebuild_phi()
+        self.prepare()
+        self.rebuild_theta()
+        self.check_errors()
+
+    def loglik_sum(self):
+        v = ctypes.c_double()
+        _lib.check(_lib.lib().gf_shard_loglik_sum(self._h, ctypes.byref(v)))
+        return v.value
+
+    def check_errors(self):
+        _lib.check(_lib.lib().gf_shard_check_errors(self._h))
+
+    def synchronize(self):
+        _lib.check(_lib.lib().gf_shard_synchronize(self._h))
+
+    def sync_tensor(self):
+        """The phi sync buffer as a torch int32 CUDA tensor (zero-copy)."""
+        import torch
+
+        p = ctypes.c_void_p()
+        n = ctypes.c_int64()
+        _lib.check(_lib.lib().gf_shard_sync_buffer(self._h, ctypes.byref(p), ctypes.byref(n)))
+        return torch.as_tensor(_CudaArray(p.value, n.value, "<i4", self), device=f"cuda:{self.device}")
+
+    # --------------------------------------------------------- import/export --
+    @property
+    def num_tokens(self):
+        return int(self.chunk.token_count)
+
+    @property
+    def num_docs(self):
+        return int(self.chunk.doc_hi - self.chunk.doc_lo)
+
+    def get_assignments(self):
+        out = np.empty(self.num_tokens, np.uint16)
+        _lib.check(_lib.lib().gf_shard_get_assignments(self._h, _lib.ptr(out)))
+        return out
+
+    def get_assignments_into(self, out):
+        if out.dtype != np.uint16 or not out.flags.c_contiguous or len(out) != self.num_tokens:
+            raise ValueError("out must be a contiguous uint16 array of num_tokens entries")
+        _lib.check(_lib.lib().gf_shard_get_assignments(self._h, _lib.ptr(out)))
+        return out
+
+    def set_assignments(self, z):
+        z = _lib.carr(z, np.uint16)
+        if len(z) != self.num_tokens:
+            raise ValueError("assignments length mismatch")
+        _lib.check(_lib.lib().gf_shard_set_assignments(self._h, _lib.ptr(z)))
+
+    def get_theta(self):
+        """(row_ptr int64[D_s+1], topic_ids uint16, counts uint16) of local rows."""
+        nnz = ctypes.c_int64()
+        _lib.check(_lib.lib().gf_shard_theta_nnz(self._h, ctypes.byref(nnz)))
+        rp = np.empty(self.num_docs + 1, np.int64)
+        ids = np.empty(max(nnz.value, 1), np.uint16)
+        cn = np.empty(max(nnz.value, 1), np.uint16)
+        _lib.check(_lib.lib().gf_shard_get_theta(self._h, _lib.ptr(rp), _lib.ptr(ids), _lib.ptr(cn)))
+        n = int(rp[-1])
+        return rp, ids[:n].copy(), cn[:n].copy()
+
+    def set_theta(self, row_ptr, topic_ids, counts):
+        rp = _lib.carr(row_ptr, np.int64)
+        ids = _lib.carr(topic_ids, np.uint16)
+        cn = _lib.carr(counts, np.uint16)
+        if len(rp) != self.num_docs + 1:
+            raise ValueError("theta row_ptr must have num_local_docs + 1 entries")
+        _lib.check(_lib.lib().gf_shard_set_theta(self._h, _lib.ptr(rp), _lib.ptr(ids), _lib.ptr(cn)))
+
+    def get_phi(self):
+        """(counts uint32[K, V] row-major, topic_totals int64[K]) from the sync buffer."""
+        kv = np.empty((self.K, self.V), np.uint32)
+        tot = np.empty(self.K, np.int64)
+        _lib.check(_lib.lib().gf_shard_get_phi(self._h, _lib.ptr(kv), _lib.ptr(tot)))
+        return kv, tot
+
+    def set_phi(self, counts, totals):
+        kv = _lib.carr(counts, np.uint32)
+        tot = _lib.carr(totals, np.int64)
+        if kv.shape != (self.K, self.V):
+            raise ValueError(f"phi must be {self.K} x {self.V}")
+        _lib.check(_lib.lib().gf_shard_set_phi(self._h, _lib.ptr(kv), _lib.ptr(tot)))
+
+    def phi_argmax(self):
+        m = ctypes.c_int64()
+        k = ctypes.c_int32()
+        v = ctypes.c_int32()
+        _lib.check(_lib.lib().gf_shard_phi_argmax(self._h, ctypes.byref(m), ctypes.byref(k), ctypes.byref(v)))
+        return m.value, k.value, v.value
+
+    def check_phi_width(self, width):
+        """model.py:152-157: raise naming the argmax cell if it exceeds `width`."""
+        if width == 16:
+            m, k, v = self.phi_argmax()
+            if m > 65535:
+                raise CountOverflowError(f"phi cell (topic {k}, word {v}) count {m} exceeds 16-bit range")
+
+    # ------------------------------------------------------------ counters --
+    def stats(self):
+        st = np.zeros(9, np.int64)
+        _lib.check(_lib.lib().gf_shard_stats(self._h, _lib.ptr(st), 9))
+        keys = ["sample_bytes", "phi_bytes", "theta_bytes", "runs", "slices", "tokens", "theta_nnz",
+                "kernels_per_iterate", "sample_launches"]
+        return dict(zip(keys, st.tolist()))
+
+    def reset_stats(self):
+        _lib.check(_lib.lib().gf_shard_reset_stats(self._h))
+
+    def last_times(self):
+        ms = np.zeros(4, np.float32)
+        _lib.check(_lib.lib().gf_shard_last_times(self._h, _lib.ptr(ms), 4))
+        return dict(zip(["sample", "phi", "prepare", "theta"], ms.tolist()))

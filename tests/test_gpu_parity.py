@@ -1,0 +1,396 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle and
+the reference golden vectors.  Bit-exact for counts / CSR / search; chi-square
+and draw-agreement for the sampler; 1e-6 relative for the fused loglik."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+from scipy import stats
+
+import oracle
+from paper_1803_04631_b200 import corpus as cp
+from paper_1803_04631_b200 import engine, errors, eval as ev, model as md, ptree, sampler, synth
+from paper_1803_04631_b200.shard import DeviceShard
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def build_chunk(doc_ids, word_ids, assignments, chunk_id=0):
+    """tests/test_model.py:9-33 of the reference: word-grouped Chunk from triples."""
+    doc_ids = np.asarray(doc_ids, dtype=np.int32)
+    word_ids = np.asarray(word_ids, dtype=np.int32)
+    assignments = np.asarray(assignments, dtype=np.uint16)
+    order = np.argsort(word_ids, kind="stable")
+    doc_ids, word_ids, assignments = doc_ids[order], word_ids[order], assignments[order]
+    words, starts, sizes = np.unique(word_ids, return_index=True, return_counts=True)
+    lo = int(doc_ids.min()) if doc_ids.size else 0
+    hi = int(doc_ids.max()) + 1 if doc_ids.size else 0
+    dw_ptr, dw_tok = cp._doc_word_map(doc_ids, lo, hi - lo)
+    return cp.Chunk(chunk_id, lo, hi, len(doc_ids), doc_ids, word_ids, assignments.copy(),
+                    words.astype(np.int32), starts.astype(np.int64), sizes.astype(np.int64), dw_ptr, dw_tok)
+
+
+def oracle_theta(ch, K):
+    return oracle.rebuild_theta(ch.assignments, ch.dw_ptr, ch.dw_tok, ch.doc_lo, K)
+
+
+# ------------------------------------------------------------ K2 / K3 ------
+@pytest.mark.parametrize("name", ["small", "single", "rand25", "zipf", "zipf_k1024"])
+def test_rebuilds_match_reference_golden(name):
+    g = np.load(os.path.join(GOLD, "partition.npz"))
+    m = next(x for x in json.loads(str(g["meta"])) if x["name"] == name)
+    corp = cp.corpus_from_tokens(g[f"{name}__corpus_doc_ids"], g[f"{name}__corpus_word_ids"], m["V"])
+    chunks = cp.partition(corp, m["C"], m["K"], m["seed"])
+    parts = []
+    for ch in chunks:
+        pre = f"{name}__c{ch.chunk_id}__"
+        th = md.rebuild_theta(ch, m["K"])
+        np.testing.assert_array_equal(th.row_ptr, g[pre + "theta_row_ptr"])
+        np.testing.assert_array_equal(th.topic_ids, g[pre + "theta_topic_ids"])
+        np.testing.assert_array_equal(th.counts, g[pre + "theta_counts"])
+        ph = md.rebuild_phi_replica(ch, m["K"], m["V"])
+        np.testing.assert_array_equal(ph.counts, g[pre + "phi_counts"])
+        np.testing.assert_array_equal(ph.topic_totals, g[pre + "phi_totals"])
+        assert ph.counts.dtype == np.uint32
+        parts.append(th)
+    full = md.concat_theta(parts)
+    np.testing.assert_array_equal(full.row_ptr, g[f"{name}__concat_row_ptr"])
+
+
+def test_rebuilds_match_reference_on_hand_chunks():
+    g = np.load(os.path.join(GOLD, "counts.npz"))
+    for m in json.loads(str(g["meta"])):
+        pre = f"h{m['i']}__"
+        ch = build_chunk(g[pre + "doc"], g[pre + "word"], g[pre + "z"])
+        th = md.rebuild_theta(ch, m["K"])
+        np.testing.assert_array_equal(th.row_ptr, g[pre + "theta_row_ptr"])
+        np.testing.assert_array_equal(th.topic_ids, g[pre + "theta_topic_ids"])
+        np.testing.assert_array_equal(th.counts, g[pre + "theta_counts"])
+        ph = md.rebuild_phi_replica(ch, m["K"], m["V"])
+        np.testing.assert_array_equal(ph.counts, g[pre + "phi_counts"])
+        np.testing.assert_array_equal(ph.topic_totals, g[pre + "phi_totals"])
+
+
+def test_reference_test_model_cases():
+    # reference tests/test_model.py:52-62, 85-97
+    ids, cnt = md.rebuild_theta_row(build_chunk([0, 0, 0], [1, 2, 0], [2, 2, 0]), 0, 4)
+    assert ids.tolist() == [0, 2] and cnt.tolist() == [1, 2]
+    ids, cnt = md.rebuild_theta_row(build_chunk([0], [3], [7]), 0, 8)
+    assert ids.tolist() == [7] and cnt.tolist() == [1]
+    rep = md.rebuild_phi_replica(build_chunk([0, 0, 0], [1, 1, 2], [0, 0, 1]), 2, 3)
+    assert rep.counts[0, 1] == 2 and rep.counts[1, 2] == 1 and rep.topic_totals.tolist() == [2, 1]
+    empty = build_chunk([], [], [])
+    rep = md.rebuild_phi_replica(empty, 3, 4)
+    assert rep.counts.sum() == 0 and rep.topic_totals.tolist() == [0, 0, 0]
+
+
+def test_count_overflow_messages_match_reference():
+    with open(os.path.join(GOLD, "messages.json")) as fh:
+        msgs = json.load(fh)
+    n = 70000
+    with pytest.raises(errors.CountOverflowError) as ei:
+        md.rebuild_theta(build_chunk(np.full(n, 3), np.zeros(n), np.zeros(n)), 2)
+    assert str(ei.value) == msgs["theta_overflow_doc3"]
+    n = 66000
+    ch = build_chunk(np.zeros(n), np.ones(n), np.ones(n, dtype=int))
+    with pytest.raises(errors.CountOverflowError) as ei:
+        md.rebuild_phi_replica(ch, 2, 2, width=16)
+    assert str(ei.value) == msgs["phi16_overflow_k1_v1"]
+    assert md.rebuild_phi_replica(ch, 2, 2, width=32).counts[1, 1] == n
+    ds = np.zeros(140000)
+    ws = np.concatenate([np.full(66000, 3), np.full(74000, 1)])
+    zs = np.concatenate([np.full(66000, 0), np.full(74000, 2)])
+    with pytest.raises(errors.CountOverflowError) as ei:
+        md.rebuild_phi_replica(build_chunk(ds, ws, zs), 3, 4, width=16)
+    assert str(ei.value) == msgs["phi16_overflow_argmax"]
+
+
+def test_theta_rebuild_random_sizes_vs_oracle():
+    r = np.random.default_rng(3)
+    for K in (1, 2, 33, 1024, 4096):
+        n = 20000
+        lengths = r.choice([1, 2, 5, 31, 32, 33, 64, 300, 2000], size=200)
+        docs = np.repeat(np.arange(len(lengths)), lengths)[:n]
+        ch = build_chunk(docs + 5, r.integers(0, 50, len(docs)), r.integers(0, K, len(docs)))
+        th = md.rebuild_theta(ch, K)
+        rp, ids, cn = oracle_theta(ch, K)
+        np.testing.assert_array_equal(th.row_ptr, rp)
+        np.testing.assert_array_equal(th.topic_ids, ids)
+        np.testing.assert_array_equal(th.counts, cn)
+        ph = md.rebuild_phi_replica(ch, K, 50)
+        oc, ot = oracle.rebuild_phi(ch.assignments, ch.word_ids, K, 50)
+        np.testing.assert_array_equal(ph.counts, oc)
+        np.testing.assert_array_equal(ph.topic_totals, ot)
+
+
+def test_heavy_words_split_across_slices_vs_oracle():
+    # a word with > 65535 tokens in the shard: 32-bit column, several K2 items (atomics)
+    r = np.random.default_rng(4)
+    n = 300000
+    docs = np.repeat(np.arange(3000), 100)
+    words = np.where(r.random(n) < 0.5, 7, r.integers(0, 20, n))
+    ch = build_chunk(docs, words, r.integers(0, 16, n))
+    ph = md.rebuild_phi_replica(ch, 16, 20)
+    oc, ot = oracle.rebuild_phi(ch.assignments, ch.word_ids, 16, 20)
+    np.testing.assert_array_equal(ph.counts, oc)
+    np.testing.assert_array_equal(ph.topic_totals, ot)
+
+
+# --------------------------------------------------------------- ptree -------
+def test_device_tree_search_matches_reference():
+    g = np.load(os.path.join(GOLD, "ptree.npz"))
+    for m in json.loads(str(g["meta"])):
+        i = m["i"]
+        levels = [g[f"t{i}__level{lvl}"] for lvl in range(m["height"] + 1)]
+        tree = ptree.PrefixTree(levels, m["fanout"])
+        np.testing.assert_array_equal(tree.sample_many(g[f"t{i}__u"]), g[f"t{i}__idx"])
+        t2 = ptree.build(g[f"t{i}__w"], fanout=m["fanout"])
+        for a, b in zip(t2.levels, levels):
+            np.testing.assert_array_equal(a, b)
+
+
+def test_device_tree_zero_leaves_never_drawn():
+    tree = ptree.build(np.array([0.0, 1.0, 0.0, 2.0, 0.0], np.float32), fanout=2)
+    us = (np.random.default_rng(1).random(20000) * tree.total).astype(np.float32)
+    us = np.minimum(us, np.nextafter(np.float32(tree.total), np.float32(0)))
+    assert set(tree.sample_many(us).tolist()) <= {1, 3}
+
+
+# ------------------------------------------------------------- sampler -------
+def single_run_state(K, V, r, nnz_min=1, max_count=6):
+    if nnz_min > 1:
+        th = np.zeros(K, np.int64)
+        th[r.choice(K, nnz_min, replace=False)] = r.integers(1, max_count + 1, nnz_min)
+    else:
+        th = r.integers(0, max_count, K)
+    z = int(r.integers(0, K))
+    th[z] += 1
+    phi = r.integers(0, 20, (K, V)).astype(np.uint32)
+    v = int(r.integers(0, V))
+    phi[z, v] += 1
+    tot = phi.sum(axis=1).astype(np.int64) + r.integers(0, 30, K)
+    return th, z, phi, tot, v
+
+
+def draw_fixed_state(K, V, th, z, phi, tot, v, n, seed=42, it=3):
+    """n tokens of one (doc, word) run: n iid draws from one conditional."""
+    ch = build_chunk(np.zeros(n), np.full(n, v), np.full(n, z))
+    ids = np.flatnonzero(th).astype(np.uint16)
+    alpha, beta = 50.0 / K, 0.01
+    with DeviceShard(K, V, alpha, beta, seed=seed) as sh:
+        sh.load(ch)
+        sh.set_phi(phi, tot)
+        sh.set_theta(np.array([0, len(ids)]), ids, th[ids].astype(np.uint16))
+        sh.prepare()
+        sh.sample(it)
+        sh.check_errors()
+        zp = sh.get_assignments()
+    p, _ = oracle.conditional(K, V, alpha, beta, th, phi[:, v], tot, z)
+    return zp, p
+
+
+def chi_square_p(hist, p):
+    n = hist.sum()
+    order = np.argsort(p)
+    # merge the smallest cells until every expected count is >= 5
+    bins_h, bins_p, acc_h, acc_p = [], [], 0, 0.0
+    for k in order:
+        acc_h += hist[k]
+        acc_p += p[k]
+        if acc_p * n >= 5:
+            bins_h.append(acc_h)
+            bins_p.append(acc_p)
+            acc_h, acc_p = 0, 0.0
+    if acc_p > 0:
+        bins_h[-1] += acc_h
+        bins_p[-1] += acc_p
+    bins_p = np.array(bins_p)
+    return stats.chisquare(bins_h, bins_p / bins_p.sum() * n)[1]
+
+
+@pytest.mark.parametrize("K,nnz_min", [(3, 1), (17, 1), (64, 1), (1024, 200), (1024, 700), (4096, 600)])
+def test_sampler_chi_square_fixed_counts(K, nnz_min):
+    # SPEC acceptance #4 on the device: 1e6 draws, p > 0.001 (K <= 64 exact
+    # cells; K >= 1024 merged cells; nnz 700 / 600 exercise the streaming path)
+    r = np.random.default_rng(K + nnz_min)
+    V = 7
+    th, z, phi, tot, v = single_run_state(K, V, r, nnz_min=nnz_min, max_count=3 if K > 64 else 6)
+    zp, p = draw_fixed_state(K, V, th, z, phi, tot, v, 1_000_000)
+    hist = np.bincount(zp, minlength=K)
+    assert chi_square_p(hist, p) > 0.001
+
+
+def test_sampler_edge_states():
+    r = np.random.default_rng(9)
+    # theta_d = {z: 1}: after exclusion the S part is empty -> pure Q branch
+    K, V = 8, 3
+    th = np.zeros(K, np.int64)
+    th[5] = 1
+    phi = r.integers(1, 9, (K, V)).astype(np.uint32)
+    tot = phi.sum(axis=1).astype(np.int64)
+    zp, p = draw_fixed_state(K, V, th, 5, phi, tot, 1, 200_000)
+    assert chi_square_p(np.bincount(zp, minlength=K), p) > 0.001
+    # K = 1: always topic 0
+    zp, _ = draw_fixed_state(1, 2, np.array([3]), 0, np.array([[5, 1]], np.uint32), np.array([6]), 0, 1000)
+    assert (zp == 0).all()
+
+
+def test_consistency_error_when_topic_absent():
+    K, V = 4, 2
+    ch = build_chunk([0, 0], [1, 1], [2, 2])
+    with DeviceShard(K, V, 0.5, 0.1) as sh:
+        sh.load(ch)
+        sh.set_phi(np.ones((K, V), np.uint32), np.full(K, 2))
+        sh.set_theta(np.array([0, 1]), np.array([0], np.uint16), np.array([2], np.uint16))
+        sh.prepare()
+        sh.sample(0)
+        with pytest.raises(errors.ConsistencyError):
+            sh.check_errors()
+
+
+def _chunk_state(corp, K, seed):
+    ch = cp.partition(corp, 1, K, seed)[0]
+    rp, ids, cn = oracle_theta(ch, K)
+    phi, tot = oracle.rebuild_phi(ch.assignments, ch.word_ids, K, corp.vocab_size)
+    return ch, rp, ids, cn, phi, tot
+
+
+@pytest.mark.parametrize("K,mean_len", [(32, 60.0), (1024, 900.0)])
+def test_draws_agree_with_oracle_sampler(K, mean_len):
+    """Same state, same Philox stream: the device (fp32) and the oracle (fp64)
+    pick the same topic except where rounding straddles a boundary."""
+    corp = synth.generate(400, 3000, mean_len, seed=11)
+    ch, rp, ids, cn, phi, tot = _chunk_state(corp, K, 5)
+    a, b = 50.0 / K, 0.01
+    want = oracle.sample_tokens(K, corp.vocab_size, a, b, 77, 4, ch.doc_ids, ch.word_ids, ch.assignments,
+                                ch.doc_lo, rp, ids, cn, phi, tot)
+    with DeviceShard(K, corp.vocab_size, a, b, seed=77) as sh:
+        sh.load(ch)
+        sh.initialize()
+        np.testing.assert_array_equal(sh.get_theta()[1], ids)
+        sh.sample(4)
+        sh.check_errors()
+        got = sh.get_assignments()
+    agree = np.mean(got == want)
+    assert agree > 0.998, agree
+
+
+def test_fused_loglik_matches_naive_formula():
+    K = 64
+    corp = synth.generate(300, 2000, 80.0, seed=12)
+    ch, rp, ids, cn, phi, tot = _chunk_state(corp, K, 6)
+    a, b = 50.0 / K, 0.01
+    want = oracle.loglik_naive(K, corp.vocab_size, a, b, ch.doc_ids, ch.word_ids, rp, ids, cn,
+                               corp.doc_lengths, phi, tot)
+    with DeviceShard(K, corp.vocab_size, a, b, seed=1) as sh:
+        sh.load(ch)
+        sh.initialize()
+        sh.sample(0)
+        got = sh.loglik_sum() / corp.num_tokens
+    assert got == pytest.approx(want, rel=1e-6)
+    theta = md.ThetaRows(rp, ids, cn, K)
+    got2 = ev.loglik_per_token(theta, md.PhiMatrix(phi.astype(np.uint32), tot), corp, a, b)
+    assert got2 == pytest.approx(want, rel=1e-6)
+
+
+def test_spec_loglik_examples_on_device():
+    corp = cp.corpus_from_tokens([0, 0, 1], [0, 2, 2], 4)
+    theta = md.ThetaRows(np.array([0, 1, 2]), np.array([0, 0], np.uint16), np.array([2, 1], np.uint16), 1)
+    phi = md.PhiMatrix(np.array([[1, 0, 2, 0]], np.uint32), np.array([3]))
+    b = 0.01
+    want = np.mean([np.log((1 + b) / (3 + 4 * b)), np.log((2 + b) / (3 + 4 * b)), np.log((2 + b) / (3 + 4 * b))])
+    assert ev.loglik_per_token(theta, phi, corp, 50.0, b) == pytest.approx(want, rel=1e-6)
+
+
+# --------------------------------------------------------------- engine ------
+def test_training_conservation_determinism_and_recount():
+    K = 32
+    corp = synth.shaped("tiny")
+    cfg = engine.TrainConfig(num_topics=K, iterations=4, seed=3, check_conservation=True)
+    th1, ph1, rep1 = engine.train(corp, cfg)
+    assert all(r.conservation == "ok" for r in rep1)
+    th2, ph2, rep2 = engine.train(corp, cfg)
+    np.testing.assert_array_equal(ph1.counts, ph2.counts)
+    np.testing.assert_array_equal(th1.counts, th2.counts)
+    assert [r.loglik_per_token for r in rep1] == [r.loglik_per_token for r in rep2]
+    # every count structure equals a recount of the exported assignments
+    tr = engine.Trainer(corp, cfg)
+    for _ in range(3):
+        tr.step()
+    z = tr.assignments()
+    ch = tr.chunk
+    oc, ot = oracle.rebuild_phi(z, ch.word_ids, K, corp.vocab_size)
+    ph = tr.phi()
+    np.testing.assert_array_equal(ph.counts, oc)
+    np.testing.assert_array_equal(ph.topic_totals, ot)
+    rp, ids, cn = oracle.rebuild_theta(z, ch.dw_ptr, ch.dw_tok, ch.doc_lo, K)
+    th = tr.theta()
+    np.testing.assert_array_equal(th.row_ptr, rp)
+    np.testing.assert_array_equal(th.topic_ids, ids)
+    np.testing.assert_array_equal(th.counts, cn)
+    tr.close()
+
+
+def _oracle_trajectory(corp, K, seed, iters):
+    a, b = 50.0 / K, 0.01
+    ch = cp.partition(corp, 1, K, seed)[0]
+    z = ch.assignments.copy()
+    lls = []
+    for it in range(iters):
+        rp, ids, cn = oracle.rebuild_theta(z, ch.dw_ptr, ch.dw_tok, 0, K)
+        phi, tot = oracle.rebuild_phi(z, ch.word_ids, K, corp.vocab_size)
+        lls.append(oracle.loglik_naive(K, corp.vocab_size, a, b, ch.doc_ids, ch.word_ids, rp, ids, cn,
+                                       corp.doc_lengths, phi, tot))
+        z = oracle.sample_tokens(K, corp.vocab_size, a, b, seed, it, ch.doc_ids, ch.word_ids, z, 0, rp, ids, cn,
+                                 phi, tot)
+    return np.array(lls)
+
+
+def test_loglik_trajectory_within_1pct_of_oracle():
+    """BASELINE config 1 (tiny: 1K docs, V=1K, ~100K tokens, K=32): the device
+    trajectory stays within 1% of the oracle's at matched iterations."""
+    K, iters = 32, 50
+    corp = synth.shaped("tiny")
+    cfg = engine.TrainConfig(num_topics=K, iterations=iters, seed=42)
+    _, _, reps = engine.train(corp, cfg)
+    gpu = np.array([r.loglik_per_token for r in reps])
+    ref = _oracle_trajectory(corp, K, 42, iters)
+    assert gpu[0] == pytest.approx(ref[0], rel=1e-6)        # same initial model
+    assert np.max(np.abs(gpu - ref) / np.abs(ref)) < 0.01
+    assert gpu[-1] > gpu[0] + 0.05                             # it converges
+
+
+def test_k_sweep_iterations_conserve_counts():
+    corp = synth.generate(2000, 5000, 300.0, seed=5)
+    for K in (128, 256, 1024, 4096):
+        cfg = engine.TrainConfig(num_topics=K, iterations=2, seed=1)
+        tr = engine.Trainer(corp, cfg)
+        for _ in range(2):
+            tr.step()
+        z = tr.assignments()
+        assert (z < K).all()
+        ph = tr.phi()
+        oc, ot = oracle.rebuild_phi(z, tr.chunk.word_ids, K, corp.vocab_size)
+        np.testing.assert_array_equal(ph.counts, oc)
+        th = tr.theta()
+        assert md.check_conservation(th, ph, corp).ok
+        tr.close()
+
+
+def test_sample_chunk_api():
+    K = 16
+    corp = synth.generate(100, 200, 50.0, seed=2)
+    ch = cp.partition(corp, 1, K, 9)[0]
+    theta = md.rebuild_theta(ch, K)
+    phi = md.rebuild_phi_replica(ch, K, corp.vocab_size)
+    ctx = sampler.SamplerContext(50.0 / K, 0.01, K, corp.vocab_size)
+    z1 = sampler.sample_chunk(ch, phi, theta, ctx, iteration=1, seed=5)
+    z2 = sampler.sample_chunk(ch, phi, theta, ctx, iteration=1, seed=5)
+    np.testing.assert_array_equal(z1, z2)
+    rp, ids, cn = theta.row_ptr, theta.topic_ids, theta.counts
+    want = oracle.sample_tokens(K, corp.vocab_size, 50.0 / K, 0.01, 5, 1, ch.doc_ids, ch.word_ids,
+                                ch.assignments, 0, rp, ids, cn, phi.counts, phi.topic_totals)
+    assert np.mean(z1 == want) > 0.998
