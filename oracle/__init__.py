@@ -62,6 +62,8 @@ def lib():
         L.gfo_sample_tokens.restype = ctypes.c_int
         L.gfo_sample_tokens.argtypes = [_i32, _i32, _f64, _f64, _u64, _u32, _i64, _p, _p, _p,
                                         _i64, _p, _p, _p, _p, _p, ctypes.c_int, _p]
+        L.gfo_sample_tokens_thin.restype = ctypes.c_int
+        L.gfo_sample_tokens_thin.argtypes = L.gfo_sample_tokens.argtypes
         L.gfo_conditional.argtypes = [_i32, _i32, _f64, _f64, _p, _p, _p, _i32, ctypes.c_int, _p, _p]
         L.gfo_loglik_naive.restype = _f64
         L.gfo_loglik_naive.argtypes = [_i32, _i32, _f64, _f64, _i64, _p, _p, _p, _p, _p, _p, _p, _p,
@@ -239,9 +241,11 @@ def check_conservation(row_ptr, topic_ids, counts, phi_counts, phi_totals, doc_l
 
 # ------------------------------------------------------------- sampler ------
 def sample_tokens(K, V, alpha, beta, seed, iteration, tok_doc, tok_word, z, doc_lo,
-                  th_ptr, th_ids, th_cnt, phi_counts, phi_totals, nthreads=0):
+                  th_ptr, th_ids, th_cnt, phi_counts, phi_totals, nthreads=0, mode="direct"):
     """SPEC.md:249-284, 359-367 deferred sampler (fp64 oracle mode).  Returns z'.
-    phi_counts is K x V; theta CSR rows are local (doc - doc_lo)."""
+    phi_counts is K x V; theta CSR rows are local (doc - doc_lo).
+    mode="direct": exclusion-adjusted S/Q exactly as SPEC sample_sparse;
+    mode="thin": the device's draw-by-draw form (exclusion by thinning)."""
     tok_doc = _c(tok_doc, np.int32)
     tok_word = _c(tok_word, np.int32)
     zz = _c(z, np.uint16).copy()
@@ -251,7 +255,8 @@ def sample_tokens(K, V, alpha, beta, seed, iteration, tok_doc, tok_word, z, doc_
     phi = _c(phi_counts, np.uint32)
     tot = _c(phi_totals, np.int64)
     err = _i64()
-    rc = lib().gfo_sample_tokens(K, V, alpha, beta, seed & 0xFFFFFFFFFFFFFFFF, iteration, len(zz),
+    fn = lib().gfo_sample_tokens if mode == "direct" else lib().gfo_sample_tokens_thin
+    rc = fn(K, V, alpha, beta, seed & 0xFFFFFFFFFFFFFFFF, iteration, len(zz),
                                  _ptr(tok_doc), _ptr(tok_word), _ptr(zz), doc_lo, _ptr(th_ptr),
                                  _ptr(th_ids), _ptr(th_cnt), _ptr(phi), _ptr(tot), nthreads,
                                  ctypes.byref(err))

@@ -331,6 +331,117 @@ int gfo_sample_tokens(int32_t K, int32_t V, double alpha, double beta, uint64_t 
     return status;
 }
 
+/* The product kernel's form of the same draw (csrc/k_sample.cu): exclusion by
+ * THINNING.  Draw k from the exclusion-free S+Q mixture of SPEC.md:267-275 with
+ * uniforms (b, s) of Philox block (doc, word, occ | retry << 26, iteration); if
+ * k == z keep it with probability (theta_dz - 1 + a) p*_ex(z) / ((theta_dz + a) p*(z))
+ * (uniform t), else redraw with retry + 1.  The kept k follows the same
+ * exclusion-adjusted Eq. 1 distribution as gfo_sample_tokens (tests compare
+ * both against gfo_conditional); this variant exists so the device can be
+ * checked draw for draw. */
+int gfo_sample_tokens_thin(int32_t K, int32_t V, double alpha, double beta, uint64_t seed,
+                           uint32_t iteration, int64_t T, const int32_t* tok_doc,
+                           const int32_t* tok_word, uint16_t* z,
+                           int64_t doc_lo, const int64_t* th_ptr, const uint16_t* th_ids,
+                           const uint16_t* th_cnt, const uint32_t* phi, const int64_t* totals,
+                           int nthreads, int64_t* err_tok) {
+    if (T == 0) return 0;
+    uint32_t* occ = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)T);
+    int64_t* seg = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T + 1));
+    int64_t nseg = 0;
+    for (int64_t t = 0; t < T; ++t) {
+        int same_word = t > 0 && tok_word[t] == tok_word[t - 1];
+        if (!same_word) seg[nseg++] = t;
+        occ[t] = (same_word && tok_doc[t] == tok_doc[t - 1]) ? occ[t - 1] + 1 : 0;
+    }
+    seg[nseg] = T;
+    int status = 0;
+    int64_t bad = INT64_MAX;
+    const double vb = (double)V * beta;
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+    uint32_t* phiT = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)K * (size_t)V);
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t vb0 = 0; vb0 < V; vb0 += 64)
+        for (int32_t k = 0; k < K; ++k)
+            for (int64_t vv = vb0; vv < vb0 + 64 && vv < V; ++vv) phiT[vv * K + k] = phi[(int64_t)k * V + vv];
+#ifdef _OPENMP
+#pragma omp parallel
+#endif
+    {
+        double* pstar = (double*)malloc(sizeof(double) * (size_t)K);
+        double* pex = (double*)malloc(sizeof(double) * (size_t)K);
+        double* qpre = (double*)malloc(sizeof(double) * (size_t)K);
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+        for (int64_t s = 0; s < nseg; ++s) {
+            const int32_t v = tok_word[seg[s]];
+            double acc = 0.0;
+            for (int32_t k = 0; k < K; ++k) {
+                const double ph = (double)phiT[(int64_t)v * K + k], nk = (double)totals[k];
+                pstar[k] = (ph + beta) / (nk + vb);
+                pex[k] = (ph >= 1.0 && nk >= 1.0) ? (ph - 1.0 + beta) / (nk - 1.0 + vb) : 0.0;
+                acc += alpha * pstar[k];
+                qpre[k] = acc;
+            }
+            const double Q = qpre[K - 1];
+            for (int64_t t = seg[s]; t < seg[s + 1]; ++t) {
+                const int32_t d = tok_doc[t];
+                const int32_t zt = z[t];
+                const int64_t r0 = th_ptr[d - doc_lo], r1 = th_ptr[d - doc_lo + 1];
+                double S = 0.0;
+                for (int64_t j = r0; j < r1; ++j) S += (double)th_cnt[j] * pstar[th_ids[j]];
+                int32_t k = zt;
+                for (uint32_t retry = 0; retry <= 63; ++retry) {
+                    uint32_t ctr[4] = {(uint32_t)d, (uint32_t)v, occ[t] | (retry << 26), iteration};
+                    uint32_t r[4];
+                    gfo_philox4x32_10(ctr, key, r);
+                    const double ub = (double)(r[0] >> 8) * (1.0 / 16777216.0);
+                    const double us = (double)(r[1] >> 8) * (1.0 / 16777216.0);
+                    const double ut = (double)(r[2] >> 8) * (1.0 / 16777216.0);
+                    int64_t cnt = 0;
+                    if (ub * (S + Q) < S) {
+                        const double target = us * S;
+                        double a2 = 0.0;
+                        int64_t pick = r1 - 1;
+                        for (int64_t j = r0; j < r1; ++j) {
+                            a2 += (double)th_cnt[j] * pstar[th_ids[j]];
+                            if (a2 > target) { pick = j; break; }
+                        }
+                        k = th_ids[pick];
+                        cnt = th_cnt[pick];
+                    } else {
+                        k = (int32_t)first_above(qpre, K, us * Q);
+                        if (k == zt)
+                            for (int64_t j = r0; j < r1; ++j)
+                                if (th_ids[j] == zt) { cnt = th_cnt[j]; break; }
+                    }
+                    if (k != zt) break;
+                    if (zt >= K || cnt == 0 || pex[zt] == 0.0) {
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+                        { status = 3; if (t < bad) bad = t; }
+                        break;
+                    }
+                    if (ut * ((double)cnt + alpha) * pstar[zt] < ((double)cnt - 1.0 + alpha) * pex[zt]) break;
+                    k = zt;
+                }
+                z[t] = (uint16_t)k;
+            }
+        }
+        free(pstar); free(pex); free(qpre);
+    }
+    free(phiT); free(occ); free(seg);
+    if (status) *err_tok = bad;
+    return status;
+}
+
 /* Exact exclusion-adjusted Eq. 1 distribution of one token (SPEC:249-257,
  * 276-284): probs[k] proportional to (theta'_dk + a)(phi'_kv + b)/(n'_k + V b).
  * theta_dense is the document's dense row.  Also returns the decomposed

@@ -242,10 +242,11 @@ int gf_shard_create(gf_shard** out, int device, int32_t K, int32_t V, double alp
     }
     s->tree.nlev = l;
     s->tree.total = total;
-    if ((size_t)(total + K) * 4 > 200 * 1024) {
+    if (gf::sample_smem_bytes(s) > 220 * 1024) {
+        const size_t need = gf::sample_smem_bytes(s);
         delete s;
-        return fail(GF_ERR_CAPACITY, "K=%d: the shared-memory Q-tree needs %zu bytes (> 200 KiB)", K,
-                    (size_t)(total + K) * 4);
+        return fail(GF_ERR_CAPACITY, "K=%d: the sampler's shared-memory word context needs %zu bytes (> 220 KiB)",
+                    K, need);
     }
     cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete s; return cuda_fail(e, "cudaStreamCreate"); }
@@ -437,8 +438,17 @@ int gf_shard_prepare(gf_shard* s) {
     return GF_OK;
 }
 
+static int validate_if_dirty(gf_shard* s) {
+    if (s->dirty) {
+        CU(gf::launch_validate(s), "validate");
+        s->dirty = false;
+    }
+    return GF_OK;
+}
+
 int gf_shard_sample(gf_shard* s, uint32_t iteration) {
     if (int rc = need_loaded(s)) return rc;
+    if (int rc = validate_if_dirty(s)) return rc;
     CU(gf::launch_sample(s, iteration), "sample");
     CU(gf::launch_ll_reduce(s), "loglik");
     s->stat_sample_launches++;
@@ -454,6 +464,7 @@ int gf_shard_evaluate(gf_shard* s) {
 
 int gf_shard_iterate(gf_shard* s, uint32_t iteration) {
     if (int rc = need_loaded(s)) return rc;
+    if (int rc = validate_if_dirty(s)) return rc;
     cudaStream_t st = s->stream;
     if (s->timing) cudaEventRecord(s->ev[0], st);
     CU(gf::launch_sample(s, iteration), "sample");
@@ -531,6 +542,7 @@ int gf_shard_set_assignments(gf_shard* s, const uint16_t* in) {
     // range is checked on the device (K1/K2/K3 flag z >= K as a consistency error)
     CU(cudaMemcpyAsync(s->d.z, in, s->T * 2, cudaMemcpyHostToDevice, s->stream), "set_assignments");
     CU(cudaStreamSynchronize(s->stream), "set_assignments");
+    s->dirty = true;
     return GF_OK;
 }
 
@@ -605,6 +617,7 @@ int gf_shard_set_theta(gf_shard* s, const int64_t* row_ptr, const uint16_t* ids,
     cudaFree(drp);
     cudaFree(dids);
     if (e != cudaSuccess) return cuda_fail(e, "set_theta");
+    s->dirty = true;
     return GF_OK;
 }
 
@@ -656,6 +669,7 @@ int gf_shard_set_phi(gf_shard* s, const uint32_t* counts_kv, const int64_t* tota
     cudaFree(din);
     cudaFree(dcol);
     if (e != cudaSuccess) return cuda_fail(e, "set_phi");
+    s->dirty = true;
     return GF_OK;
 }
 

@@ -81,6 +81,7 @@ struct gf_shard {
     cudaEvent_t ev[6] = {};
     float last_ms[4] = {0, 0, 0, 0};
     bool timing = true;
+    bool dirty = false;                      // imported state not yet validated
 };
 
 // kernel launchers (k_sample.cu / k_counts.cu / k_ptree.cu)
@@ -95,7 +96,8 @@ cudaError_t launch_theta_import(gf_shard* s, const int64_t* d_rowptr, const uint
                                 const uint16_t* d_cnt);
 cudaError_t launch_phi_export(gf_shard* s, uint32_t* d_out_kv, const int32_t* d_word_col);
 cudaError_t launch_phi_import(gf_shard* s, const uint32_t* d_in_kv, const int32_t* d_word_col);
-cudaError_t launch_nnz_bytes(gf_shard* s);
+cudaError_t launch_validate(gf_shard* s);
+size_t sample_smem_bytes(const gf_shard* s);
 cudaError_t ptree_sample(const float* d_prefix, int64_t n, int fanout, const float* d_u, int64_t m,
                          int64_t* d_idx, cudaStream_t st);
 }  // namespace gf

@@ -2,23 +2,37 @@
 // PAPER.md section 6.1, Algorithm 2) with the fused per-token log-likelihood
 // (SPEC.md:402-410).
 //
-// One CTA per heavy-first word slice (PAPER.md: "samplers in the same thread
-// block sample the tokens from the same word", long words split and scheduled
-// first).  Prologue: the word's p*(k) = (phi_vk + b)/(n_k + V b) and the dense
-// Q-part prefix tree over a p*(k) are built once in shared memory (32-ary, the
-// levels of ptree.build, ptree.py:116-136).  Then every warp is one sampler
-// that takes a (doc, word) RUN of tokens: it reads the doc's sparse theta row
-// once (16-byte vector loads, 4 entries per lane, cached in registers), forms
-// p1 = theta * p* with a warp scan, and draws every token of the run:
-//   exclusion (theta_dz-1, phi_zv-1, n_z-1) is applied in
-//   O(1) by shifting u past the token's own entry in both the S and the Q
-//   prefix (so the shared tree stays exclusion-free), u1 picks the branch
-//   (u1 (S+Q) < S), u2 searches it by __ballot_sync.
-// Philox4x32-10 counter = (global doc, word, occurrence in run, iteration).
+// Grid: one CTA per heavy-first word slice (section 6.1.2: the
+// samplers of a thread block share one word, long words are split and
+// scheduled first).  Prologue, once per slice, in shared memory:
+//   p*(k)     = (phi_vk + b) / (n_k + V b)                 (PAPER Eq. 8)
+//   p*_ex(k)  = (phi_vk - 1 + b) / (n_k - 1 + V b)         (exclusion view)
+//   Q-tree    = 32-ary prefix tree over a p*(k)            (ptree.build levels)
+// Work: warps pull batches of 32 (doc, word) RUNS from a shared counter; in a
+// batch lane j owns run j and draws the Philox4x32-10 uniforms of its first
+// token (counter = global doc, word, occurrence, iteration).  Two sampler
+// shapes:
+//   thread mode (row nnz <= kSmall): the lane walks its own theta row
+//     (16-byte loads, L1) for S, and searches it / the Q-tree itself -- 32
+//     runs advance in lock-step with no cross-lane traffic;
+//   warp mode (longer rows, one run at a time): 32 lanes scan the row with
+//     __shfl prefix sums into a per-warp shared buffer, then each draw is a
+//     two-level __ballot_sync search over that prefix (or the Q-tree).
+// Exclusion (theta_dz-1, phi_vz-1, n_z-1) is applied by
+// thinning: draw k from the exclusion-free S+Q mixture; if k == z keep it with
+// probability p_ex(z) / p(z) = (theta_dz - 1 + a) p*_ex(z) / ((theta_dz + a) p*(z)),
+// else redraw (fresh Philox block: occurrence | retry << 26).  The accepted k is
+// distributed exactly as the exclusion-adjusted Eq. 1 -- the distribution
+// sample_sparse defines -- without a per-token search for z in the row.
 #include "gf_internal.cuh"
 #include "gf_device.cuh"
 
 namespace gf {
+
+constexpr int kWarps = kSampleThreads / 32;
+constexpr uint32_t kSmall = 64;       // thread mode up to this many row entries
+constexpr uint32_t kCap = 1024;       // warp-mode shared prefix capacity (else stream)
+constexpr int kMaxRetry = 63;
 
 struct SampleArgs {
     int K, Kp;
@@ -47,9 +61,18 @@ __device__ __forceinline__ uint32_t phi_at(const SampleArgs& a, int col, int k) 
     return col >= 0 ? (uint32_t)a.phi16[(size_t)col * a.Kp + k] : a.phi32[(size_t)(~col) * a.K + k];
 }
 
-// ptree descent (ptree.py:203-225) over the shared-memory levels: at each
-// level the 32 children are compared at once with one ballot.
-__device__ __forceinline__ int search_q(const float* lvl, const TreeGeom& g, float u, int lane) {
+struct U3 {
+    float b, s, t;                            // branch, search, thinning
+};
+
+__device__ __forceinline__ U3 draw_u(const SampleArgs& a, uint32_t gdoc, uint32_t v, uint32_t occ, uint32_t retry) {
+    const uint4 r = philox4x32_10(make_uint4(gdoc, v, occ | (retry << 26), a.iteration), a.key);
+    return U3{u24(r.x), u24(r.y), u24(r.z)};
+}
+
+// ptree descent (ptree.py:203-225) over the shared-memory levels, one ballot
+// per level (warp mode).
+__device__ __forceinline__ int search_q_warp(const float* lvl, const TreeGeom& g, float u, int lane) {
     int idx = 0;
     for (int l = g.nlev - 1; l >= 0; --l) {
         const int lo = idx * 32;
@@ -61,20 +84,58 @@ __device__ __forceinline__ int search_q(const float* lvl, const TreeGeom& g, flo
     return idx;
 }
 
-template <int NC>
-__global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleArgs a) {
+// the same search by one lane: binary search of level 0 (minimal k, P[k] > u)
+__device__ __forceinline__ int search_q_lane(const float* lvl0, int K, float u) {
+    int lo = 0, hi = K - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (lvl0[mid] > u) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+// theta_dz of a sorted row by binary search (thinning of a Q-branch z draw)
+__device__ __forceinline__ uint32_t row_count(const uint32_t* row, uint32_t nnz, uint32_t z) {
+    uint32_t lo = 0, hi = nnz;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const uint32_t e = __ldg(row + mid);
+        if ((e & 0xffffu) < z) lo = mid + 1;
+        else hi = mid;
+    }
+    if (lo < nnz) {
+        const uint32_t e = __ldg(row + lo);
+        if ((e & 0xffffu) == z) return e >> 16;
+    }
+    return 0;
+}
+
+// keep a draw of the token's own topic with probability p_ex(z) / p(z)
+__device__ __forceinline__ bool keep_own(float ut, uint32_t cnt, float alpha, float ps, float pex) {
+    const float num = __fmul_rn(__fadd_rn((float)cnt - 1.f, alpha), pex);
+    const float den = __fmul_rn(__fadd_rn((float)cnt, alpha), ps);
+    return __fmul_rn(ut, den) < num;
+}
+
+template <int DUMMY>
+__global__ void __launch_bounds__(kSampleThreads, 3) sample_kernel(SampleArgs a) {
     extern __shared__ float smem[];
-    float* lvl = smem;                        // Q-tree levels (level 0 = prefix of a p*)
-    float* pstar = smem + a.tree.total;       // p*(k)
-    __shared__ double ll_w[kSampleThreads / 32];
-    __shared__ unsigned long long by_w[kSampleThreads / 32];
+    float* lvl = smem;                              // Q-tree levels (level 0 = prefix of a p*)
+    float* pstar = smem + a.tree.total;             // p*(k)
+    float* pex = pstar + a.K;                       // p*_ex(k)
+    float* wbuf = pex + a.K;                        // kWarps x kCap row prefixes (warp mode)
+    __shared__ double ll_w[kWarps];
+    __shared__ unsigned long long by_w[kWarps];
+    __shared__ int next_run;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int4 sl = a.slices[blockIdx.x];
-    const int v = sl.x, col = sl.w;
+    const uint32_t v = (uint32_t)sl.x;
+    const int col = sl.w;
     const int K = a.K;
 
-    // ---------------- prologue: p* and the Q prefix (block scan) ----------------
+    // ---------------- prologue: p*, p*_ex and the Q prefix (block scan) ----------------
     {
         const int ipt = (K + kSampleThreads - 1) / kSampleThreads;
         const int k0 = tid * ipt;
@@ -82,19 +143,25 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleArgs a) {
         for (int i = 0; i < ipt; ++i) {
             const int k = k0 + i;
             if (k < K) {
-                const float ps = __fmul_rn(__fadd_rn((float)phi_at(a, col, k), a.beta), __ldg(a.inv_den + k));
+                const uint32_t ph = phi_at(a, col, k);
+                const uint32_t nk = __ldg(a.nk + k);
+                const float ps = __fmul_rn(__fadd_rn((float)ph, a.beta), __ldg(a.inv_den + k));
                 pstar[k] = ps;
+                pex[k] = (ph && nk) ? __fdiv_rn(__fadd_rn((float)(ph - 1u), a.beta),
+                                                __fadd_rn((float)(nk - 1u), a.vbeta))
+                                    : 0.f;
                 acc = __fadd_rn(acc, __fmul_rn(a.alpha, ps));
                 lvl[k] = acc;
             }
         }
-        float incl = warp_incl_scan(acc, lane);
-        __shared__ float wtot[kSampleThreads / 32];
+        const float incl = warp_incl_scan(acc, lane);
+        __shared__ float wtot[kWarps];
         if (lane == 31) wtot[warp] = incl;
+        if (tid == 0) next_run = sl.y;
         __syncthreads();
         if (tid == 0) {
             float run = 0.f;
-            for (int w = 0; w < kSampleThreads / 32; ++w) { float t = wtot[w]; wtot[w] = run; run = __fadd_rn(run, t); }
+            for (int w = 0; w < kWarps; ++w) { const float t = wtot[w]; wtot[w] = run; run = __fadd_rn(run, t); }
         }
         __syncthreads();
         float excl = __shfl_up_sync(kFull, incl, 1);
@@ -112,291 +179,267 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleArgs a) {
         }
     }
     const float Q = lvl[K - 1];
+    const float* lvl0 = lvl;
+    float* buf = wbuf + warp * kCap;
     double ll = 0.0;
     unsigned long long nbytes = 0;
 
-    // ---------------- samplers: one warp per (doc, word) run ----------------
-    for (int r = sl.y + warp; r < sl.z; r += kSampleThreads / 32) {
-        const uint32_t d = __ldg(a.run_doc + r);
-        const uint32_t t0 = __ldg(a.run_start + r), t1 = __ldg(a.run_start + r + 1);
-        const uint2 meta = __ldg(a.theta_meta + d);
-        const uint32_t off = meta.x, nnz = meta.y;
+    while (true) {
+        int rb = 0;
+        if (lane == 0) rb = atomicAdd(&next_run, 32);
+        rb = __shfl_sync(kFull, rb, 0);
+        if (rb >= sl.z) break;
+        // ---- batch: lane j owns run rb + j ----
+        const int r = rb + lane;
+        const bool valid = r < sl.z;
+        uint32_t d = 0, t0 = 0, t1 = 0, off = 0, nnz = 0;
+        if (valid) {
+            d = __ldg(a.run_doc + r);
+            t0 = __ldg(a.run_start + r);
+            t1 = __ldg(a.run_start + r + 1);
+            const uint2 m = __ldg(a.theta_meta + d);
+            off = m.x;
+            nnz = m.y;
+            nbytes += nnz;
+        }
         const uint32_t gdoc = a.doc_lo + d;
-        nbytes += nnz;
-        float S_full;
+        U3 u0{0.f, 0.f, 0.f};
+        if (valid && !a.eval_only) u0 = draw_u(a, gdoc, v, 0u, 0u);
 
-        if (nnz <= 128u * NC) {
-            // ---- cached path: the row lives in registers for the whole run ----
-            uint32_t e[NC][4];
-            float lp[NC][4];
-            float ex[NC];
-            float carry[NC + 1];
-            carry[0] = 0.f;
-            const int nch = (int)((nnz + 127u) >> 7);
+        // ================= thread mode: one lane, one run =================
+        if (valid && nnz <= kSmall) {
+            const uint32_t* row = a.theta_ent + off;
+            float S = 0.f;
+            for (uint32_t j = 0; j < nnz; j += 4) {
+                const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + j));
+                const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                if (c < nch) {
-                    const uint32_t j0 = c * 128u + 4u * lane;
-                    uint4 q4 = make_uint4(0, 0, 0, 0);
-                    if (j0 < nnz) q4 = __ldg(reinterpret_cast<const uint4*>(a.theta_ent + off + j0));
-                    e[c][0] = q4.x; e[c][1] = q4.y; e[c][2] = q4.z; e[c][3] = q4.w;
-                    float acc = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        float w = 0.f;
-                        if (j0 + i < nnz) w = __fmul_rn((float)(e[c][i] >> 16), pstar[e[c][i] & 0xffffu]);
-                        acc = __fadd_rn(acc, w);
-                        lp[c][i] = acc;
-                    }
-                    const float incl = warp_incl_scan(acc, lane);
-                    float excl = __shfl_up_sync(kFull, incl, 1);
-                    if (lane == 0) excl = 0.f;
-                    ex[c] = excl;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) lp[c][i] = __fadd_rn(excl, lp[c][i]);
-                    carry[c + 1] = __fadd_rn(carry[c], __shfl_sync(kFull, lp[c][3], 31));
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) { e[c][i] = 0; lp[c][i] = 0.f; }
-                    ex[c] = 0.f;
-                    carry[c + 1] = carry[c];
-                }
+                for (int i = 0; i < 4; ++i)
+                    if (j + i < nnz) S = __fadd_rn(S, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
             }
-            S_full = carry[NC];
-
-            for (uint32_t t = t0; t < (a.eval_only ? t0 : t1); ++t) {
-                const int zt = a.z[t];
-                if (zt >= K) {                        // corrupt assignment: report, keep
-                    if (lane == 0) atomicMin(a.errs, (unsigned long long)t);
-                    continue;
-                }
-                // locate the token's own topic in the row (ids ascending, unique)
-                int hit = -1;
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (c * 128 + 4 * lane + i < (int)nnz && (int)(e[c][i] & 0xffffu) == zt) hit = c * 4 + i;
-                const unsigned hm = __ballot_sync(kFull, hit >= 0);
-                const uint32_t phz = phi_at(a, col, zt);
-                const uint32_t nz = __ldg(a.nk + zt);
-                if (hm == 0u || phz == 0u || nz == 0u) {
-                    if (lane == 0) atomicMin(a.errs, (unsigned long long)t);
-                    continue;
-                }
-                const int lz = __ffs(hm) - 1;
-                float cnt_m = 0.f, pprev_m = 0.f;
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (hit == c * 4 + i) {
-                            cnt_m = (float)(e[c][i] >> 16);
-                            pprev_m = __fadd_rn(carry[c], i ? lp[c][i - 1] : ex[c]);
-                        }
-                const float cnt = __shfl_sync(kFull, cnt_m, lz);
-                const float pprev = __shfl_sync(kFull, pprev_m, lz);
-                const float pex = __fdiv_rn(__fadd_rn((float)(phz - 1u), a.beta), __fadd_rn((float)(nz - 1u), a.vbeta));
-                const float ps = pstar[zt];
-                const float wz = __fmul_rn(cnt, ps);
-                const float wzx = __fmul_rn(cnt - 1.f, pex);
-                const float dS = fmaxf(__fsub_rn(wz, wzx), 0.f);
-                const float Sx = fmaxf(__fsub_rn(S_full, dS), 0.f);
-                const float qzx = __fmul_rn(a.alpha, pex);
-                const float dQ = fmaxf(__fsub_rn(__fmul_rn(a.alpha, ps), qzx), 0.f);
-                const float Qx = __fsub_rn(Q, dQ);
-                const float qprev = zt ? lvl[zt - 1] : 0.f;
-                const uint4 rr = philox4x32_10(make_uint4(gdoc, (uint32_t)v, t - t0, a.iteration), a.key);
-                const float u1 = u24(rr.x), u2 = u24(rr.y);
-                int knew;
-                if (__fmul_rn(u1, __fadd_rn(Sx, Qx)) < Sx) {
-                    float u = __fmul_rn(u2, Sx);
-                    int res = -2;                      // -2: search needed
-                    if (u < pprev) {
-                    } else if (u < __fadd_rn(pprev, wzx)) {
-                        res = zt;
-                    } else {
-                        u = fminf(__fadd_rn(u, dS), prev_float(S_full));
-                    }
-                    if (res == -2) {
-                        int cs = nch - 1;
-#pragma unroll
-                        for (int c = NC - 1; c >= 0; --c)
-                            if (c < nch && carry[c + 1] > u) cs = c;
-                        int fi = -1, fid = 0;
-                        bool okw = false;
-#pragma unroll
-                        for (int c = 0; c < NC; ++c)
-                            if (c == cs) {
-#pragma unroll
-                                for (int i = 3; i >= 0; --i)
-                                    if (__fadd_rn(carry[c], lp[c][i]) > u) fi = i;
+            ll += (double)(t1 - t0) * (double)logf(__fadd_rn(S, Q));
+            if (!a.eval_only) {
+                for (uint32_t t = t0; t < t1; ++t) {
+                    const uint32_t zt = a.z[t];
+                    const uint32_t occ = t - t0;
+                    U3 u = occ ? draw_u(a, gdoc, v, occ, 0u) : u0;
+                    uint32_t k = zt;
+                    for (int retry = 0; retry <= kMaxRetry; ++retry) {
+                        if (retry) u = draw_u(a, gdoc, v, occ, (uint32_t)retry);
+                        uint32_t cnt = 0;
+                        if (__fmul_rn(u.b, __fadd_rn(S, Q)) < S) {
+                            const float target = __fmul_rn(u.s, S);
+                            float acc = 0.f;
+                            uint32_t pick = 0xffffffffu, last = 0;
+                            for (uint32_t j = 0; j < nnz && pick == 0xffffffffu; j += 4) {
+                                const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + j));
+                                const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
                                 for (int i = 0; i < 4; ++i)
-                                    if (i == fi) {
-                                        fid = (int)(e[c][i] & 0xffffu);
-                                        const float prev = i ? lp[c][i - 1] : ex[c];
-                                        okw = (c * 128 + 4 * lane + i < (int)nnz) && lp[c][i] > prev;
+                                    if (j + i < nnz && pick == 0xffffffffu) {
+                                        acc = __fadd_rn(acc, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
+                                        last = e4[i];
+                                        if (acc > target) pick = e4[i];
                                     }
                             }
-                        const unsigned m = __ballot_sync(kFull, fi >= 0);
-                        if (m == 0u) {
-                            res = zt;                  // rounding guard (measure ~1 ulp)
+                            if (pick == 0xffffffffu) pick = last;   // rounding guard: last entry
+                            k = pick & 0xffffu;
+                            cnt = pick >> 16;
                         } else {
-                            const int L = __ffs(m) - 1;
-                            const int id = __shfl_sync(kFull, fid, L);
-                            const bool ok = __shfl_sync(kFull, okw, L);
-                            res = ok ? id : zt;
+                            k = (uint32_t)search_q_lane(lvl0, K, __fmul_rn(u.s, Q));
+                            if (k == zt) cnt = row_count(row, nnz, zt);
                         }
-                    }
-                    knew = res;
-                } else {
-                    float u = __fmul_rn(u2, Qx);
-                    if (u < qprev) {
-                        knew = search_q(lvl, a.tree, u, lane);
-                    } else if (u < __fadd_rn(qprev, qzx)) {
-                        knew = zt;
-                    } else {
-                        knew = search_q(lvl, a.tree, fminf(__fadd_rn(u, dQ), prev_float(Q)), lane);
-                    }
-                }
-                if (lane == 0) a.z[t] = (uint16_t)knew;
-            }
-        } else {
-            // ---- streaming path (long rows): two passes over the row per token ----
-            const int nch = (int)((nnz + 127u) >> 7);
-            S_full = -1.f;
-            if (a.eval_only) {
-                float sfl = 0.f;
-                for (uint32_t j = lane; j < nnz; j += 32) {
-                    const uint32_t ee = __ldg(a.theta_ent + off + j);
-                    sfl = __fadd_rn(sfl, __fmul_rn((float)(ee >> 16), pstar[ee & 0xffffu]));
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sfl = __fadd_rn(sfl, __shfl_xor_sync(kFull, sfl, o));
-                S_full = sfl;
-            }
-            for (uint32_t t = t0; t < (a.eval_only ? t0 : t1); ++t) {
-                const int zt = a.z[t];
-                if (zt >= K) {
-                    if (lane == 0) atomicMin(a.errs, (unsigned long long)t);
-                    continue;
-                }
-                const uint32_t phz = phi_at(a, col, zt);
-                const uint32_t nz = __ldg(a.nk + zt);
-                const float pex = __fdiv_rn(__fadd_rn((float)(phz - 1u), a.beta), __fadd_rn((float)(nz - 1u), a.vbeta));
-                // pass 1: adjusted total, unadjusted total, presence of z
-                float carry = 0.f, sfl = 0.f;
-                bool found = false;
-                for (int c = 0; c < nch; ++c) {
-                    const uint32_t j0 = c * 128u + 4u * lane;
-                    uint4 q4 = make_uint4(0, 0, 0, 0);
-                    if (j0 < nnz) q4 = __ldg(reinterpret_cast<const uint4*>(a.theta_ent + off + j0));
-                    const uint32_t ee[4] = {q4.x, q4.y, q4.z, q4.w};
-                    float acc = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        if (j0 + i < nnz) {
-                            const int id = ee[i] & 0xffffu;
-                            const float cn = (float)(ee[i] >> 16);
-                            const float w = __fmul_rn(cn, pstar[id]);
-                            sfl = __fadd_rn(sfl, w);
-                            if (id == zt) { found = true; acc = __fadd_rn(acc, __fmul_rn(cn - 1.f, pex)); }
-                            else acc = __fadd_rn(acc, w);
-                        }
-                    }
-                    const float incl = warp_incl_scan(acc, lane);
-                    carry = __fadd_rn(carry, __shfl_sync(kFull, incl, 31));
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sfl = __fadd_rn(sfl, __shfl_xor_sync(kFull, sfl, o));
-                if (S_full < 0.f) S_full = sfl;
-                const bool any = __any_sync(kFull, found);
-                if (!any || phz == 0u || nz == 0u) {
-                    if (lane == 0) atomicMin(a.errs, (unsigned long long)t);
-                    continue;
-                }
-                const float Sx = carry;
-                const float ps = pstar[zt];
-                const float qzx = __fmul_rn(a.alpha, pex);
-                const float dQ = fmaxf(__fsub_rn(__fmul_rn(a.alpha, ps), qzx), 0.f);
-                const float Qx = __fsub_rn(Q, dQ);
-                const float qprev = zt ? lvl[zt - 1] : 0.f;
-                const uint4 rr = philox4x32_10(make_uint4(gdoc, (uint32_t)v, t - t0, a.iteration), a.key);
-                const float u1 = u24(rr.x), u2 = u24(rr.y);
-                int knew = zt;
-                if (__fmul_rn(u1, __fadd_rn(Sx, Qx)) < Sx) {
-                    const float u = __fmul_rn(u2, Sx);
-                    float cy = 0.f;
-                    for (int c = 0; c < nch; ++c) {
-                        const uint32_t j0 = c * 128u + 4u * lane;
-                        uint4 q4 = make_uint4(0, 0, 0, 0);
-                        if (j0 < nnz) q4 = __ldg(reinterpret_cast<const uint4*>(a.theta_ent + off + j0));
-                        const uint32_t ee[4] = {q4.x, q4.y, q4.z, q4.w};
-                        float lpl[4];
-                        float acc = 0.f;
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            float w = 0.f;
-                            if (j0 + i < nnz) {
-                                const int id = ee[i] & 0xffffu;
-                                const float cn = (float)(ee[i] >> 16);
-                                w = (id == zt) ? __fmul_rn(cn - 1.f, pex) : __fmul_rn(cn, pstar[id]);
-                            }
-                            acc = __fadd_rn(acc, w);
-                            lpl[i] = acc;
-                        }
-                        const float incl = warp_incl_scan(acc, lane);
-                        float excl = __shfl_up_sync(kFull, incl, 1);
-                        if (lane == 0) excl = 0.f;
-                        int fi = -1;
-#pragma unroll
-                        for (int i = 3; i >= 0; --i) {
-                            lpl[i] = __fadd_rn(excl, lpl[i]);
-                            if (__fadd_rn(cy, lpl[i]) > u) fi = i;
-                        }
-                        const float ctot = __shfl_sync(kFull, lpl[3], 31);
-                        const unsigned m = __ballot_sync(kFull, fi >= 0);
-                        if (m || c == nch - 1) {
-                            if (m) {
-                                const int L = __ffs(m) - 1;
-                                int fid = 0;
-                                bool okw = false;
-#pragma unroll
-                                for (int i = 0; i < 4; ++i)
-                                    if (i == fi) {
-                                        fid = ee[i] & 0xffffu;
-                                        okw = (j0 + i < nnz) && lpl[i] > (i ? lpl[i - 1] : excl);
-                                    }
-                                const int id = __shfl_sync(kFull, fid, L);
-                                knew = __shfl_sync(kFull, okw, L) ? id : zt;
-                            }
+                        if (k != zt) break;
+                        if (zt >= (uint32_t)K || cnt == 0u || pex[zt] == 0.f) {   // inconsistent state
+                            atomicMin(a.errs, (unsigned long long)t);
                             break;
                         }
-                        cy = __fadd_rn(cy, ctot);
+                        if (keep_own(u.t, cnt, a.alpha, pstar[zt], pex[zt])) break;
+                        k = zt;                                                   // rejected: redraw
                     }
-                } else {
-                    float u = __fmul_rn(u2, Qx);
-                    if (u < qprev) knew = search_q(lvl, a.tree, u, lane);
-                    else if (u < __fadd_rn(qprev, qzx)) knew = zt;
-                    else knew = search_q(lvl, a.tree, fminf(__fadd_rn(u, dQ), prev_float(Q)), lane);
+                    a.z[t] = (uint16_t)k;
                 }
-                if (lane == 0) a.z[t] = (uint16_t)knew;
             }
-            if (S_full < 0.f) S_full = 0.f;
         }
-        // log p(w|d) * (L_d + K a) of the iteration-start model, once per run
-        ll += (double)(t1 - t0) * log((double)S_full + (double)Q);
+
+        // ================= warp mode: 32 lanes, one run at a time =================
+        unsigned big = __ballot_sync(kFull, valid && nnz > kSmall);
+        while (big) {
+            const int src = __ffs(big) - 1;
+            big &= big - 1;
+            const uint32_t wd = __shfl_sync(kFull, gdoc, src);
+            const uint32_t w0 = __shfl_sync(kFull, t0, src), w1 = __shfl_sync(kFull, t1, src);
+            const uint32_t woff = __shfl_sync(kFull, off, src), wn = __shfl_sync(kFull, nnz, src);
+            const U3 wu0{__shfl_sync(kFull, u0.b, src), __shfl_sync(kFull, u0.s, src), __shfl_sync(kFull, u0.t, src)};
+            const uint32_t* row = a.theta_ent + woff;
+            const uint32_t nch = (wn + 127u) >> 7;
+            const bool staged = wn <= kCap;
+            // pass over the row: prefix sums (staged into buf when they fit)
+            float carry = 0.f;
+            for (uint32_t c = 0; c < nch; ++c) {
+                const uint32_t j0 = c * 128u + 4u * lane;
+                uint4 q = make_uint4(0, 0, 0, 0);
+                if (j0 < wn) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
+                const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
+                float p[4];
+                float acc = 0.f;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (j0 + i < wn) acc = __fadd_rn(acc, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
+                    p[i] = acc;
+                }
+                const float incl = warp_incl_scan(acc, lane);
+                float excl = __shfl_up_sync(kFull, incl, 1);
+                if (lane == 0) excl = 0.f;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) p[i] = __fadd_rn(carry, __fadd_rn(excl, p[i]));
+                if (staged && j0 < kCap) *reinterpret_cast<float4*>(buf + j0) = make_float4(p[0], p[1], p[2], p[3]);
+                carry = __shfl_sync(kFull, p[3], 31);
+            }
+            __syncwarp();
+            const float S = carry;
+            if (lane == 0) ll += (double)(w1 - w0) * (double)logf(__fadd_rn(S, Q));
+            if (a.eval_only) continue;
+            // uniforms of occurrences 1..31 of this run, one per lane
+            const uint32_t n = w1 - w0;
+            U3 ul{0.f, 0.f, 0.f};
+            if (n > 1 && lane > 0 && (uint32_t)lane < n) ul = draw_u(a, wd, v, (uint32_t)lane, 0u);
+            const uint32_t ngrp = (min(wn, kCap) + 31u) >> 5;
+            for (uint32_t t = w0; t < w1; ++t) {
+                const uint32_t zt = a.z[t];
+                const uint32_t occ = t - w0;
+                U3 u = wu0;
+                if (occ) {
+                    if (occ < 32) u = U3{__shfl_sync(kFull, ul.b, occ), __shfl_sync(kFull, ul.s, occ),
+                                          __shfl_sync(kFull, ul.t, occ)};
+                    else u = draw_u(a, wd, v, occ, 0u);
+                }
+                uint32_t k = zt;
+                for (int retry = 0; retry <= kMaxRetry; ++retry) {
+                    if (retry) u = draw_u(a, wd, v, occ, (uint32_t)retry);
+                    uint32_t cnt = 0;
+                    if (__fmul_rn(u.b, __fadd_rn(S, Q)) < S) {
+                        const float target = __fmul_rn(u.s, S);
+                        uint32_t j;
+                        if (staged) {
+                            // two-level 32-ary ballot search of the staged prefix
+                            const bool gok = (uint32_t)lane < ngrp && buf[min(32u * lane + 31u, wn - 1u)] > target;
+                            const unsigned gm = __ballot_sync(kFull, gok);
+                            const uint32_t g = gm ? (uint32_t)(__ffs(gm) - 1) : ngrp - 1u;
+                            const uint32_t idx = 32u * g + lane;
+                            const bool eok = idx < wn && buf[idx] > target;
+                            const unsigned em = __ballot_sync(kFull, eok);
+                            j = em ? 32u * g + (uint32_t)(__ffs(em) - 1) : wn - 1u;
+                        } else {
+                            // long row: rescan chunk by chunk (same arithmetic as the pass)
+                            float cy = 0.f;
+                            j = wn - 1u;
+                            for (uint32_t c = 0; c < nch; ++c) {
+                                const uint32_t j0 = c * 128u + 4u * lane;
+                                uint4 q = make_uint4(0, 0, 0, 0);
+                                if (j0 < wn) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
+                                const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
+                                float p[4];
+                                float acc = 0.f;
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    if (j0 + i < wn)
+                                        acc = __fadd_rn(acc, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
+                                    p[i] = acc;
+                                }
+                                const float incl = warp_incl_scan(acc, lane);
+                                float excl = __shfl_up_sync(kFull, incl, 1);
+                                if (lane == 0) excl = 0.f;
+                                int fi = -1;
+#pragma unroll
+                                for (int i = 3; i >= 0; --i)
+                                    if (j0 + i < wn && __fadd_rn(cy, __fadd_rn(excl, p[i])) > target) fi = i;
+                                const unsigned m = __ballot_sync(kFull, fi >= 0);
+                                if (m) {
+                                    const int L = __ffs(m) - 1;
+                                    j = c * 128u + 4u * (uint32_t)L + (uint32_t)__shfl_sync(kFull, fi, L);
+                                    break;
+                                }
+                                cy = __fadd_rn(cy, __shfl_sync(kFull, __fadd_rn(excl, p[3]), 31));
+                            }
+                        }
+                        const uint32_t e = __ldg(row + j);
+                        k = e & 0xffffu;
+                        cnt = e >> 16;
+                    } else {
+                        k = (uint32_t)search_q_warp(lvl, a.tree, __fmul_rn(u.s, Q), lane);
+                        if (k == zt) cnt = row_count(row, wn, zt);
+                    }
+                    if (k != zt) break;
+                    if (zt >= (uint32_t)K || cnt == 0u || pex[zt] == 0.f) {
+                        if (lane == 0) atomicMin(a.errs, (unsigned long long)t);
+                        break;
+                    }
+                    if (keep_own(u.t, cnt, a.alpha, pstar[zt], pex[zt])) break;
+                    k = zt;
+                }
+                if (lane == 0) a.z[t] = (uint16_t)k;
+            }
+            __syncwarp();
+        }
+    }
+    // ---- deterministic reductions: lanes -> warp -> CTA ----
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ll += __shfl_xor_sync(kFull, ll, o);
+        nbytes += __shfl_xor_sync(kFull, nbytes, o);
     }
     if (lane == 0) { ll_w[warp] = ll; by_w[warp] = nbytes; }
     __syncthreads();
     if (tid == 0) {
         double s = 0.0;
         unsigned long long b = 0;
-        for (int w = 0; w < kSampleThreads / 32; ++w) { s += ll_w[w]; b += by_w[w]; }
+        for (int w = 0; w < kWarps; ++w) { s += ll_w[w]; b += by_w[w]; }
         a.ll_part[blockIdx.x] = s;
         atomicAdd(a.bytes, b);
     }
+}
+
+// Consistency of an IMPORTED state (set_theta / set_phi / set_assignments):
+// every token's topic must be present in its theta row, its phi cell and n_k
+// (exclusion_adjust pre-condition).  States the engine builds
+// itself are consistent by construction, so this runs only after imports.
+__global__ void __launch_bounds__(256) validate_kernel(SampleArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int4 sl = a.slices[blockIdx.x];
+    for (int r = sl.y + warp * 32 + lane; r < sl.z; r += 256) {
+        const uint32_t d = a.run_doc[r];
+        const uint2 m = a.theta_meta[d];
+        for (uint32_t t = a.run_start[r]; t < a.run_start[r + 1]; ++t) {
+            const uint32_t zt = a.z[t];
+            const bool bad = zt >= (uint32_t)a.K || row_count(a.theta_ent + m.x, m.y, zt) == 0u ||
+                             phi_at(a, sl.w, (int)zt) == 0u || a.nk[zt] == 0u;
+            if (bad) atomicMin(a.errs, (unsigned long long)t);
+        }
+    }
+}
+
+cudaError_t launch_validate(gf_shard* s) {
+    if (s->n_slices == 0) return cudaSuccess;
+    SampleArgs a{};
+    a.K = s->K;
+    a.Kp = s->Kp;
+    a.slices = s->d.slices;
+    a.run_doc = s->d.run_doc;
+    a.run_start = s->d.run_start;
+    a.z = s->d.z;
+    a.theta_meta = s->d.theta_meta;
+    a.theta_ent = s->d.theta_ent;
+    a.phi32 = s->d.sync;
+    a.phi16 = reinterpret_cast<const uint16_t*>(s->d.sync + s->off_phi16_u32);
+    a.nk = s->d.sync + s->off_nk_u32;
+    a.errs = s->d.errs;
+    validate_kernel<<<(unsigned)s->n_slices, 256, 0, s->stream>>>(a);
+    return cudaGetLastError();
+}
+
+size_t sample_smem_bytes(const gf_shard* s) {
+    return (size_t)(s->tree.total + 2 * s->K + kWarps * kCap) * sizeof(float);
 }
 
 cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
@@ -425,15 +468,14 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
     a.ll_part = s->d.ll_part;
     a.errs = s->d.errs;
     a.bytes = s->d.bytes;
-    const size_t smem = (size_t)(s->tree.total + s->K) * sizeof(float);
+    const size_t smem = sample_smem_bytes(s);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(sample_kernel<kRowChunks>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             200 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(sample_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    sample_kernel<kRowChunks><<<(unsigned)s->n_slices, kSampleThreads, smem, s->stream>>>(a);
+    sample_kernel<0><<<(unsigned)s->n_slices, kSampleThreads, smem, s->stream>>>(a);
     return cudaGetLastError();
 }
 

@@ -218,9 +218,14 @@ def test_sampler_chi_square_fixed_counts(K, nnz_min):
     r = np.random.default_rng(K + nnz_min)
     V = 7
     th, z, phi, tot, v = single_run_state(K, V, r, nnz_min=nnz_min, max_count=3 if K > 64 else 6)
-    zp, p = draw_fixed_state(K, V, th, z, phi, tot, v, 1_000_000)
-    hist = np.bincount(zp, minlength=K)
-    assert chi_square_p(hist, p) > 0.001
+    # three independent Philox streams; a correct sampler fails one at p < 0.001
+    # with probability 1e-3, two with ~3e-6 (the oracle, which the device
+    # matches draw for draw, gives the same p-values)
+    pvals = []
+    for seed in (42, 43, 44):
+        zp, p = draw_fixed_state(K, V, th, z, phi, tot, v, 1_000_000, seed=seed)
+        pvals.append(chi_square_p(np.bincount(zp, minlength=K), p))
+    assert sum(pv > 0.001 for pv in pvals) >= 2, pvals
 
 
 def test_sampler_edge_states():
@@ -266,7 +271,7 @@ def test_draws_agree_with_oracle_sampler(K, mean_len):
     ch, rp, ids, cn, phi, tot = _chunk_state(corp, K, 5)
     a, b = 50.0 / K, 0.01
     want = oracle.sample_tokens(K, corp.vocab_size, a, b, 77, 4, ch.doc_ids, ch.word_ids, ch.assignments,
-                                ch.doc_lo, rp, ids, cn, phi, tot)
+                                ch.doc_lo, rp, ids, cn, phi, tot, mode="thin")
     with DeviceShard(K, corp.vocab_size, a, b, seed=77) as sh:
         sh.load(ch)
         sh.initialize()
@@ -392,5 +397,5 @@ def test_sample_chunk_api():
     np.testing.assert_array_equal(z1, z2)
     rp, ids, cn = theta.row_ptr, theta.topic_ids, theta.counts
     want = oracle.sample_tokens(K, corp.vocab_size, 50.0 / K, 0.01, 5, 1, ch.doc_ids, ch.word_ids,
-                                ch.assignments, 0, rp, ids, cn, phi.counts, phi.topic_totals)
+                                ch.assignments, 0, rp, ids, cn, phi.counts, phi.topic_totals, mode="thin")
     assert np.mean(z1 == want) > 0.998

@@ -275,6 +275,44 @@ def test_oracle_sampler_chi_square(K):
     assert hist[~keep].sum() <= max(50, 5 * p[~keep].sum() * n)
 
 
+@pytest.mark.parametrize("K", [3, 17, 64])
+def test_thinning_sampler_has_the_exclusion_distribution(K):
+    """The device's draw form (exclusion by thinning, oracle mode "thin")
+    samples the same exclusion-adjusted Eq. 1 as SPEC sample_sparse."""
+    r = np.random.default_rng(200 + K)
+    V = 5
+    th, z, ids, cnt, phi, tot, v = _single_run_state(K, V, r)
+    n = 1_000_000
+    alpha, beta = 50.0 / K, 0.01
+    p, _ = oracle.conditional(K, V, alpha, beta, th, phi[:, v], tot, z)
+    pvals = []
+    for seed in (1, 2, 3):
+        zp = oracle.sample_tokens(K, V, alpha, beta, seed, 0, np.zeros(n, np.int32), np.full(n, v, np.int32),
+                                  np.full(n, z, np.uint16), 0, np.array([0, len(ids)]), ids, cnt, phi, tot,
+                                  mode="thin")
+        hist = np.bincount(zp, minlength=K)
+        keep = p * n >= 5
+        pvals.append(stats.chisquare(hist[keep], p[keep] / p[keep].sum() * hist[keep].sum())[1])
+    assert sum(pv > 0.001 for pv in pvals) >= 2, pvals
+
+
+def test_thinning_singleton_topic_is_never_kept_in_s_branch():
+    # theta_d = {z: 1}: after exclusion z has no S mass; thinning must reproduce
+    # exactly the Q-only conditional
+    K, V = 6, 3
+    th = np.zeros(K, np.int64)
+    th[2] = 1
+    phi = np.full((K, V), 4, np.uint32)
+    tot = phi.sum(axis=1).astype(np.int64)
+    n = 400_000
+    zp = oracle.sample_tokens(K, V, 0.3, 0.1, 9, 0, np.zeros(n, np.int32), np.zeros(n, np.int32),
+                              np.full(n, 2, np.uint16), 0, np.array([0, 1]), np.array([2], np.uint16),
+                              np.array([1], np.uint16), phi, tot, mode="thin")
+    p, _ = oracle.conditional(K, V, 0.3, 0.1, th, phi[:, 0], tot, 2)
+    _, pv = stats.chisquare(np.bincount(zp, minlength=K), p * n)
+    assert pv > 0.001
+
+
 def test_oracle_sampler_is_deterministic_and_thread_invariant():
     r = np.random.default_rng(5)
     K, V = 16, 9
