@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kSampleThreads, 3) sample_kernel(SampleArgs a)
     float* lvl = smem;                              // Q-tree levels (level 0 = prefix of a p*)
     float* pstar = smem + a.tree.total;             // p*(k)
     float* pex = pstar + a.K;                       // p*_ex(k)
-    float* wbuf = pex + a.K;                        // kWarps x kCap row prefixes (warp mode)
+    float* wbuf = smem + ((a.tree.total + 2 * a.K + 3) & ~3);   // kWarps x kCap row prefixes (16 B aligned)
     __shared__ double ll_w[kWarps];
     __shared__ unsigned long long by_w[kWarps];
     __shared__ int next_run;
@@ -439,7 +439,7 @@ cudaError_t launch_validate(gf_shard* s) {
 }
 
 size_t sample_smem_bytes(const gf_shard* s) {
-    return (size_t)(s->tree.total + 2 * s->K + kWarps * kCap) * sizeof(float);
+    return (size_t)(((s->tree.total + 2 * s->K + 3) & ~3) + kWarps * kCap) * sizeof(float);
 }
 
 cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
