@@ -119,7 +119,7 @@ __device__ __forceinline__ bool keep_own(float ut, uint32_t cnt, float alpha, fl
 }
 
 template <int DUMMY>
-__global__ void __launch_bounds__(kSampleThreads, 3) sample_kernel(SampleArgs a) {
+__global__ void __launch_bounds__(kSampleThreads, 4) sample_kernel(SampleArgs a) {
     extern __shared__ float smem[];
     float* lvl = smem;                              // Q-tree levels (level 0 = prefix of a p*)
     float* pstar = smem + a.tree.total;             // p*(k)
@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(kSampleThreads, 3) sample_kernel(SampleArgs a)
         const uint32_t gdoc = a.doc_lo + d;
         U3 u0{0.f, 0.f, 0.f};
         if (valid && !a.eval_only) u0 = draw_u(a, gdoc, v, 0u, 0u);
+        float myS = 0.f;                             // S of this lane's run (either shape)
 
         // ================= thread mode: one lane, one run =================
         if (valid && nnz <= kSmall) {
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(kSampleThreads, 3) sample_kernel(SampleArgs a)
                 for (int i = 0; i < 4; ++i)
                     if (j + i < nnz) S = __fadd_rn(S, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
             }
-            ll += (double)(t1 - t0) * (double)logf(__fadd_rn(S, Q));
+            myS = S;
             if (!a.eval_only) {
                 for (uint32_t t = t0; t < t1; ++t) {
                     const uint32_t zt = a.z[t];
@@ -278,27 +279,36 @@ __global__ void __launch_bounds__(kSampleThreads, 3) sample_kernel(SampleArgs a)
             float carry = 0.f;
             for (uint32_t c = 0; c < nch; ++c) {
                 const uint32_t j0 = c * 128u + 4u * lane;
-                uint4 q = make_uint4(0, 0, 0, 0);
-                if (j0 < wn) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
-                const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
                 float p[4];
-                float acc = 0.f;
+                if ((c + 1u) * 128u <= wn) {            // full chunk: no bounds checks
+                    const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + j0));
+                    p[0] = __fmul_rn((float)(q.x >> 16), pstar[q.x & 0xffffu]);
+                    p[1] = __fadd_rn(p[0], __fmul_rn((float)(q.y >> 16), pstar[q.y & 0xffffu]));
+                    p[2] = __fadd_rn(p[1], __fmul_rn((float)(q.z >> 16), pstar[q.z & 0xffffu]));
+                    p[3] = __fadd_rn(p[2], __fmul_rn((float)(q.w >> 16), pstar[q.w & 0xffffu]));
+                } else {
+                    uint4 q = make_uint4(0, 0, 0, 0);
+                    if (j0 < wn) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
+                    const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
+                    float acc = 0.f;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    if (j0 + i < wn) acc = __fadd_rn(acc, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
-                    p[i] = acc;
+                    for (int i = 0; i < 4; ++i) {
+                        if (j0 + i < wn) acc = __fadd_rn(acc, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
+                        p[i] = acc;
+                    }
                 }
-                const float incl = warp_incl_scan(acc, lane);
+                const float incl = warp_incl_scan(p[3], lane);
                 float excl = __shfl_up_sync(kFull, incl, 1);
                 if (lane == 0) excl = 0.f;
+                const float base = __fadd_rn(carry, excl);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) p[i] = __fadd_rn(carry, __fadd_rn(excl, p[i]));
+                for (int i = 0; i < 4; ++i) p[i] = __fadd_rn(base, p[i]);
                 if (staged && j0 < kCap) *reinterpret_cast<float4*>(buf + j0) = make_float4(p[0], p[1], p[2], p[3]);
                 carry = __shfl_sync(kFull, p[3], 31);
             }
             __syncwarp();
             const float S = carry;
-            if (lane == 0) ll += (double)(w1 - w0) * (double)logf(__fadd_rn(S, Q));
+            if (lane == src) myS = S;                   // its log joins the batch's SIMT logf
             if (a.eval_only) continue;
             // uniforms of occurrences 1..31 of this run, one per lane
             const uint32_t n = w1 - w0;
@@ -382,6 +392,8 @@ __global__ void __launch_bounds__(kSampleThreads, 3) sample_kernel(SampleArgs a)
             }
             __syncwarp();
         }
+        // log p(w|d) (L_d + K a) of the iteration-start model, one SIMT logf per batch
+        if (valid) ll += (double)(t1 - t0) * (double)logf(__fadd_rn(myS, Q));
     }
     // ---- deterministic reductions: lanes -> warp -> CTA ----
 #pragma unroll
@@ -472,6 +484,9 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(sample_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(sample_kernel<0>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
