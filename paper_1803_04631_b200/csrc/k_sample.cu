@@ -181,17 +181,20 @@ __global__ void __launch_bounds__(kSampleThreads, 4) sample_kernel(SampleArgs a)
     const float Q = lvl[K - 1];
     const float* lvl0 = lvl;
     float* buf = wbuf + warp * kCap;
+    // runs per grab: 32 (one per lane) unless the slice is too small to give
+    // every warp at least two grabs -- then smaller grabs keep all 8 warps busy
+    const int batch = min(32, max(1, (sl.z - sl.y + 2 * kWarps - 1) / (2 * kWarps)));
     double ll = 0.0;
     unsigned long long nbytes = 0;
 
     while (true) {
         int rb = 0;
-        if (lane == 0) rb = atomicAdd(&next_run, 32);
+        if (lane == 0) rb = atomicAdd(&next_run, batch);
         rb = __shfl_sync(kFull, rb, 0);
         if (rb >= sl.z) break;
         // ---- batch: lane j owns run rb + j ----
         const int r = rb + lane;
-        const bool valid = r < sl.z;
+        const bool valid = lane < batch && r < sl.z;
         uint32_t d = 0, t0 = 0, t1 = 0, off = 0, nnz = 0;
         if (valid) {
             d = __ldg(a.run_doc + r);
@@ -211,12 +214,12 @@ __global__ void __launch_bounds__(kSampleThreads, 4) sample_kernel(SampleArgs a)
         if (valid && nnz <= kSmall) {
             const uint32_t* row = a.theta_ent + off;
             float S = 0.f;
-            for (uint32_t j = 0; j < nnz; j += 4) {
+            for (uint32_t j = 0; j < nnz; j += 4) {             // zero pads add nothing
                 const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + j));
-                const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (j + i < nnz) S = __fadd_rn(S, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
+                S = __fadd_rn(S, __fmul_rn((float)(q.x >> 16), pstar[q.x & 0xffffu]));
+                S = __fadd_rn(S, __fmul_rn((float)(q.y >> 16), pstar[q.y & 0xffffu]));
+                S = __fadd_rn(S, __fmul_rn((float)(q.z >> 16), pstar[q.z & 0xffffu]));
+                S = __fadd_rn(S, __fmul_rn((float)(q.w >> 16), pstar[q.w & 0xffffu]));
             }
             myS = S;
             if (!a.eval_only) {
@@ -237,9 +240,9 @@ __global__ void __launch_bounds__(kSampleThreads, 4) sample_kernel(SampleArgs a)
                                 const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
                                 for (int i = 0; i < 4; ++i)
-                                    if (j + i < nnz && pick == 0xffffffffu) {
+                                    if (pick == 0xffffffffu) {
                                         acc = __fadd_rn(acc, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
-                                        last = e4[i];
+                                        if (e4[i] >> 16) last = e4[i];       // pads (count 0) never picked
                                         if (acc > target) pick = e4[i];
                                     }
                             }
@@ -265,6 +268,14 @@ __global__ void __launch_bounds__(kSampleThreads, 4) sample_kernel(SampleArgs a)
 
         // ================= warp mode: 32 lanes, one run at a time =================
         unsigned big = __ballot_sync(kFull, valid && nnz > kSmall);
+        // software pipeline: the first 128-entry chunk of the next big row is in
+        // flight while the current run is sampled
+        uint4 qnext = make_uint4(0, 0, 0, 0);
+        if (big) {
+            const int s0 = __ffs(big) - 1;
+            const uint32_t o0 = __shfl_sync(kFull, off, s0), n0 = __shfl_sync(kFull, nnz, s0);
+            if (4u * lane < n0) qnext = __ldg(reinterpret_cast<const uint4*>(a.theta_ent + o0 + 4u * lane));
+        }
         while (big) {
             const int src = __ffs(big) - 1;
             big &= big - 1;
@@ -273,30 +284,28 @@ __global__ void __launch_bounds__(kSampleThreads, 4) sample_kernel(SampleArgs a)
             const uint32_t woff = __shfl_sync(kFull, off, src), wn = __shfl_sync(kFull, nnz, src);
             const U3 wu0{__shfl_sync(kFull, u0.b, src), __shfl_sync(kFull, u0.s, src), __shfl_sync(kFull, u0.t, src)};
             const uint32_t* row = a.theta_ent + woff;
+            const uint4 qcur = qnext;
+            if (big) {
+                const int s1 = __ffs(big) - 1;
+                const uint32_t o1 = __shfl_sync(kFull, off, s1), n1 = __shfl_sync(kFull, nnz, s1);
+                qnext = make_uint4(0, 0, 0, 0);
+                if (4u * lane < n1) qnext = __ldg(reinterpret_cast<const uint4*>(a.theta_ent + o1 + 4u * lane));
+            }
             const uint32_t nch = (wn + 127u) >> 7;
             const bool staged = wn <= kCap;
             // pass over the row: prefix sums (staged into buf when they fit)
             float carry = 0.f;
             for (uint32_t c = 0; c < nch; ++c) {
                 const uint32_t j0 = c * 128u + 4u * lane;
+                // rows are zero-padded to 4 entries (K3), so a (count 0) pad adds nothing
+                uint4 q = make_uint4(0, 0, 0, 0);
+                if (c == 0) q = qcur;
+                else if (j0 < wn) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
                 float p[4];
-                if ((c + 1u) * 128u <= wn) {            // full chunk: no bounds checks
-                    const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + j0));
-                    p[0] = __fmul_rn((float)(q.x >> 16), pstar[q.x & 0xffffu]);
-                    p[1] = __fadd_rn(p[0], __fmul_rn((float)(q.y >> 16), pstar[q.y & 0xffffu]));
-                    p[2] = __fadd_rn(p[1], __fmul_rn((float)(q.z >> 16), pstar[q.z & 0xffffu]));
-                    p[3] = __fadd_rn(p[2], __fmul_rn((float)(q.w >> 16), pstar[q.w & 0xffffu]));
-                } else {
-                    uint4 q = make_uint4(0, 0, 0, 0);
-                    if (j0 < wn) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
-                    const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
-                    float acc = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        if (j0 + i < wn) acc = __fadd_rn(acc, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
-                        p[i] = acc;
-                    }
-                }
+                p[0] = __fmul_rn((float)(q.x >> 16), pstar[q.x & 0xffffu]);
+                p[1] = __fadd_rn(p[0], __fmul_rn((float)(q.y >> 16), pstar[q.y & 0xffffu]));
+                p[2] = __fadd_rn(p[1], __fmul_rn((float)(q.z >> 16), pstar[q.z & 0xffffu]));
+                p[3] = __fadd_rn(p[2], __fmul_rn((float)(q.w >> 16), pstar[q.w & 0xffffu]));
                 const float incl = warp_incl_scan(p[3], lane);
                 float excl = __shfl_up_sync(kFull, incl, 1);
                 if (lane == 0) excl = 0.f;
