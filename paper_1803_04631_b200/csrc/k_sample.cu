@@ -8,30 +8,35 @@
 //   p*(k)     = (phi_vk + b) / (n_k + V b)                 (PAPER Eq. 8)
 //   p*_ex(k)  = (phi_vk - 1 + b) / (n_k - 1 + V b)         (exclusion view)
 //   Q-tree    = 32-ary prefix tree over a p*(k)            (ptree.build levels)
-// Work: warps pull batches of 32 (doc, word) RUNS from a shared counter; in a
-// batch lane j owns run j and draws the Philox4x32-10 uniforms of its first
-// token (counter = global doc, word, occurrence, iteration).  Two sampler
-// shapes:
-//   thread mode (row nnz <= kSmall): the lane walks its own theta row
-//     (16-byte loads, L1) for S, and searches it / the Q-tree itself -- 32
-//     runs advance in lock-step with no cross-lane traffic;
-//   warp mode (longer rows, one run at a time): 32 lanes scan the row with
-//     __shfl prefix sums into a per-warp shared buffer, then each draw is a
-//     two-level __ballot_sync search over that prefix (or the Q-tree).
-// Exclusion (theta_dz-1, phi_vz-1, n_z-1) is applied by
-// thinning: draw k from the exclusion-free S+Q mixture; if k == z keep it with
-// probability p_ex(z) / p(z) = (theta_dz - 1 + a) p*_ex(z) / ((theta_dz + a) p*(z)),
-// else redraw (fresh Philox block: occurrence | retry << 26).  The accepted k is
-// distributed exactly as the exclusion-adjusted Eq. 1 -- the distribution
-// sample_sparse defines -- without a per-token search for z in the row.
+//
+// Work: each warp pulls batches of up to 32 (doc, word) RUNS (lane j owns run
+// j: its doc, token range, theta row and the Philox4x32-10 uniforms of its
+// first token) and handles them as segmented sub-batches:
+//   1. entry-parallel pass: the sub-batch's theta rows (16-byte vectors,
+//      zero-padded to 4 entries) are streamed as one concatenated array, 128
+//      entries per warp step; p1 = theta * p* is prefix-summed by a segmented
+//      __shfl scan (segment heads from one __reduce_or_sync) and staged in the
+//      warp's shared buffer -- S of every run falls out as a segment total;
+//   2. run-parallel draws: lane j samples the tokens of run j -- branch on
+//      u (S+Q) < S, then a binary search of its staged prefix (S part) or of
+//      the Q-tree level 0.
+// Rows longer than the staging buffer (K > 2048 only) take a warp-cooperative
+// streaming path.  Exclusion (theta_dz-1, phi_vz-1, n_z-1)
+// is applied by thinning: draw k from the exclusion-free S+Q mixture; if
+// k == z keep it with probability
+//   p_ex(z) / p(z) = (theta_dz - 1 + a) p*_ex(z) / ((theta_dz + a) p*(z)),
+// else redraw (fresh Philox block: occurrence | retry << 26).  Accepted draws
+// follow exactly the exclusion-adjusted Eq. 1 that sample_sparse defines,
+// without a per-token search for z in the row.
 #include "gf_internal.cuh"
 #include "gf_device.cuh"
+
+#include <cstdlib>
 
 namespace gf {
 
 constexpr int kWarps = kSampleThreads / 32;
-constexpr uint32_t kSmall = 64;       // thread mode up to this many row entries
-constexpr uint32_t kCap = 1024;       // warp-mode shared prefix capacity (else stream)
+constexpr uint32_t kCapMax = 2048;    // largest staging buffer (entries per warp) compiled
 constexpr int kMaxRetry = 63;
 
 struct SampleArgs {
@@ -70,8 +75,12 @@ __device__ __forceinline__ U3 draw_u(const SampleArgs& a, uint32_t gdoc, uint32_
     return U3{u24(r.x), u24(r.y), u24(r.z)};
 }
 
+__device__ __forceinline__ float w_of(uint32_t e, const float* pstar) {
+    return __fmul_rn((float)(e >> 16), pstar[e & 0xffffu]);
+}
+
 // ptree descent (ptree.py:203-225) over the shared-memory levels, one ballot
-// per level (warp mode).
+// per level (warp-cooperative).
 __device__ __forceinline__ int search_q_warp(const float* lvl, const TreeGeom& g, float u, int lane) {
     int idx = 0;
     for (int l = g.nlev - 1; l >= 0; --l) {
@@ -84,12 +93,12 @@ __device__ __forceinline__ int search_q_warp(const float* lvl, const TreeGeom& g
     return idx;
 }
 
-// the same search by one lane: binary search of level 0 (minimal k, P[k] > u)
-__device__ __forceinline__ int search_q_lane(const float* lvl0, int K, float u) {
-    int lo = 0, hi = K - 1;
+// minimal i in [0, n) with P[i] > u (n-1 if none): the same search by one lane
+__device__ __forceinline__ uint32_t first_above(const float* P, uint32_t n, float u) {
+    uint32_t lo = 0, hi = n - 1;
     while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (lvl0[mid] > u) hi = mid;
+        const uint32_t mid = (lo + hi) >> 1;
+        if (P[mid] > u) hi = mid;
         else lo = mid + 1;
     }
     return lo;
@@ -118,13 +127,90 @@ __device__ __forceinline__ bool keep_own(float ut, uint32_t cnt, float alpha, fl
     return __fmul_rn(ut, den) < num;
 }
 
-template <int DUMMY>
-__global__ void __launch_bounds__(kSampleThreads, 4) sample_kernel(SampleArgs a) {
+// Rows longer than the staging buffer: warp-cooperative, one run, the S part
+// re-streamed per S-branch draw.  Returns S (all lanes).
+__device__ __noinline__ float huge_run(const SampleArgs& a, const float* lvl, const float* pstar, const float* pex,
+                                       float Q, uint32_t v, uint32_t gdoc, uint32_t t0, uint32_t t1, uint32_t off,
+                                       uint32_t nnz, U3 u0, int lane) {
+    const uint32_t* row = a.theta_ent + off;
+    const uint32_t nch = (nnz + 127u) >> 7;
+    float S = 0.f;
+    for (uint32_t c = 0; c < nch; ++c) {
+        const uint32_t j0 = c * 128u + 4u * lane;
+        uint4 q = make_uint4(0, 0, 0, 0);
+        if (j0 < nnz) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
+        float s4 = __fadd_rn(__fadd_rn(w_of(q.x, pstar), w_of(q.y, pstar)), __fadd_rn(w_of(q.z, pstar), w_of(q.w, pstar)));
+        const float incl = warp_incl_scan(s4, lane);
+        S = __fadd_rn(S, __shfl_sync(kFull, incl, 31));
+    }
+    if (a.eval_only) return S;
+    for (uint32_t t = t0; t < t1; ++t) {
+        const uint32_t zt = a.z[t];
+        const uint32_t occ = t - t0;
+        U3 u = occ ? draw_u(a, gdoc, v, occ, 0u) : u0;
+        uint32_t k = zt;
+        for (int retry = 0; retry <= kMaxRetry; ++retry) {
+            if (retry) u = draw_u(a, gdoc, v, occ, (uint32_t)retry);
+            uint32_t cnt = 0;
+            if (__fmul_rn(u.b, __fadd_rn(S, Q)) < S) {
+                const float target = __fmul_rn(u.s, S);
+                float cy = 0.f;
+                uint32_t j = nnz - 1u;
+                for (uint32_t c = 0; c < nch; ++c) {
+                    const uint32_t j0 = c * 128u + 4u * lane;
+                    uint4 q = make_uint4(0, 0, 0, 0);
+                    if (j0 < nnz) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
+                    float p[4];
+                    p[0] = w_of(q.x, pstar);
+                    p[1] = __fadd_rn(p[0], w_of(q.y, pstar));
+                    p[2] = __fadd_rn(p[1], w_of(q.z, pstar));
+                    p[3] = __fadd_rn(p[2], w_of(q.w, pstar));
+                    const float incl = warp_incl_scan(p[3], lane);
+                    float excl = __shfl_up_sync(kFull, incl, 1);
+                    if (lane == 0) excl = 0.f;
+                    const float base = __fadd_rn(cy, excl);
+                    int fi = -1;
+#pragma unroll
+                    for (int i = 3; i >= 0; --i)
+                        if (j0 + i < nnz && __fadd_rn(base, p[i]) > target) fi = i;
+                    const unsigned m = __ballot_sync(kFull, fi >= 0);
+                    if (m) {
+                        const int L = __ffs(m) - 1;
+                        j = c * 128u + 4u * (uint32_t)L + (uint32_t)__shfl_sync(kFull, fi, L);
+                        break;
+                    }
+                    cy = __shfl_sync(kFull, __fadd_rn(base, p[3]), 31);
+                }
+                const uint32_t e = __ldg(row + j);
+                k = e & 0xffffu;
+                cnt = e >> 16;
+            } else {
+                k = (uint32_t)search_q_warp(lvl, a.tree, __fmul_rn(u.s, Q), lane);
+                if (k == zt) cnt = row_count(row, nnz, zt);
+            }
+            if (k != zt) break;
+            if (zt >= (uint32_t)a.K || cnt == 0u || pex[zt] == 0.f) {
+                if (lane == 0) atomicMin(a.errs, (unsigned long long)t);
+                break;
+            }
+            if (keep_own(u.t, cnt, a.alpha, pstar[zt], pex[zt])) break;
+            k = zt;
+        }
+        if (lane == 0) a.z[t] = (uint16_t)k;
+    }
+    return S;
+}
+
+// CAPB: staged prefix entries per warp (sub-batch capacity); MINB: CTAs per SM
+template <uint32_t CAPB, int MINB>
+__global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs a) {
+    constexpr uint32_t kCapB = CAPB;
+    constexpr uint32_t kCapU = CAPB / 4;        // ... in 16-byte row vectors
     extern __shared__ float smem[];
     float* lvl = smem;                              // Q-tree levels (level 0 = prefix of a p*)
     float* pstar = smem + a.tree.total;             // p*(k)
     float* pex = pstar + a.K;                       // p*_ex(k)
-    float* wbuf = smem + ((a.tree.total + 2 * a.K + 3) & ~3);   // kWarps x kCap row prefixes (16 B aligned)
+    float* wbuf = smem + ((a.tree.total + 2 * a.K + 3) & ~3);   // kWarps x kCapB staged prefixes
     __shared__ double ll_w[kWarps];
     __shared__ unsigned long long by_w[kWarps];
     __shared__ int next_run;
@@ -134,6 +220,7 @@ __global__ void __launch_bounds__(kSampleThreads, 4) sample_kernel(SampleArgs a)
     const uint32_t v = (uint32_t)sl.x;
     const int col = sl.w;
     const int K = a.K;
+    const unsigned lane_le = (2u << lane) - 1u;     // lanes 0..lane
 
     // ---------------- prologue: p*, p*_ex and the Q prefix (block scan) ----------------
     {
@@ -180,7 +267,7 @@ __global__ void __launch_bounds__(kSampleThreads, 4) sample_kernel(SampleArgs a)
     }
     const float Q = lvl[K - 1];
     const float* lvl0 = lvl;
-    float* buf = wbuf + warp * kCap;
+    float* buf = wbuf + warp * kCapB;
     // runs per grab: 32 (one per lane) unless the slice is too small to give
     // every warp at least two grabs -- then smaller grabs keep all 8 warps busy
     const int batch = min(32, max(1, (sl.z - sl.y + 2 * kWarps - 1) / (2 * kWarps)));
@@ -206,198 +293,114 @@ __global__ void __launch_bounds__(kSampleThreads, 4) sample_kernel(SampleArgs a)
             nbytes += nnz;
         }
         const uint32_t gdoc = a.doc_lo + d;
+        const uint32_t U = max(1u, (nnz + 3u) >> 2);          // row length in 16-byte vectors
+        const bool huge = valid && U > kCapU;
         U3 u0{0.f, 0.f, 0.f};
         if (valid && !a.eval_only) u0 = draw_u(a, gdoc, v, 0u, 0u);
-        float myS = 0.f;                             // S of this lane's run (either shape)
-
-        // ================= thread mode: one lane, one run =================
-        if (valid && nnz <= kSmall) {
-            const uint32_t* row = a.theta_ent + off;
-            float S = 0.f;
-            for (uint32_t j = 0; j < nnz; j += 4) {             // zero pads add nothing
-                const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + j));
-                S = __fadd_rn(S, __fmul_rn((float)(q.x >> 16), pstar[q.x & 0xffffu]));
-                S = __fadd_rn(S, __fmul_rn((float)(q.y >> 16), pstar[q.y & 0xffffu]));
-                S = __fadd_rn(S, __fmul_rn((float)(q.z >> 16), pstar[q.z & 0xffffu]));
-                S = __fadd_rn(S, __fmul_rn((float)(q.w >> 16), pstar[q.w & 0xffffu]));
+        float myS = 0.f;                                       // S of this lane's run
+        unsigned rem = __ballot_sync(kFull, valid);
+        const unsigned hmask = __ballot_sync(kFull, huge);
+        while (rem) {
+            const int first = __ffs(rem) - 1;
+            if ((hmask >> first) & 1u) {                       // rare: row beyond the buffer
+                const U3 hu{__shfl_sync(kFull, u0.b, first), __shfl_sync(kFull, u0.s, first),
+                            __shfl_sync(kFull, u0.t, first)};
+                const float S = huge_run(a, lvl, pstar, pex, Q, v, __shfl_sync(kFull, gdoc, first),
+                                         __shfl_sync(kFull, t0, first), __shfl_sync(kFull, t1, first),
+                                         __shfl_sync(kFull, off, first), __shfl_sync(kFull, nnz, first), hu, lane);
+                if (lane == first) myS = S;
+                rem &= rem - 1u;
+                continue;
             }
-            myS = S;
-            if (!a.eval_only) {
-                for (uint32_t t = t0; t < t1; ++t) {
-                    const uint32_t zt = a.z[t];
-                    const uint32_t occ = t - t0;
-                    U3 u = occ ? draw_u(a, gdoc, v, occ, 0u) : u0;
-                    uint32_t k = zt;
-                    for (int retry = 0; retry <= kMaxRetry; ++retry) {
-                        if (retry) u = draw_u(a, gdoc, v, occ, (uint32_t)retry);
-                        uint32_t cnt = 0;
-                        if (__fmul_rn(u.b, __fadd_rn(S, Q)) < S) {
-                            const float target = __fmul_rn(u.s, S);
-                            float acc = 0.f;
-                            uint32_t pick = 0xffffffffu, last = 0;
-                            for (uint32_t j = 0; j < nnz && pick == 0xffffffffu; j += 4) {
-                                const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + j));
-                                const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
+            // ---- sub-batch: contiguous non-huge lanes [first, ...) whose rows fit kCapB ----
+            const unsigned after = hmask & ~((2u << first) - 1u);
+            const int end = after ? __ffs(after) - 1 : 32;
+            const bool cand = lane >= first && lane < end && ((rem >> lane) & 1u);
+            uint32_t cu = cand ? U : 0u;
 #pragma unroll
-                                for (int i = 0; i < 4; ++i)
-                                    if (pick == 0xffffffffu) {
-                                        acc = __fadd_rn(acc, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
-                                        if (e4[i] >> 16) last = e4[i];       // pads (count 0) never picked
-                                        if (acc > target) pick = e4[i];
-                                    }
-                            }
-                            if (pick == 0xffffffffu) pick = last;   // rounding guard: last entry
-                            k = pick & 0xffffu;
-                            cnt = pick >> 16;
-                        } else {
-                            k = (uint32_t)search_q_lane(lvl0, K, __fmul_rn(u.s, Q));
-                            if (k == zt) cnt = row_count(row, nnz, zt);
-                        }
-                        if (k != zt) break;
-                        if (zt >= (uint32_t)K || cnt == 0u || pex[zt] == 0.f) {   // inconsistent state
-                            atomicMin(a.errs, (unsigned long long)t);
-                            break;
-                        }
-                        if (keep_own(u.t, cnt, a.alpha, pstar[zt], pex[zt])) break;
-                        k = zt;                                                   // rejected: redraw
-                    }
-                    a.z[t] = (uint16_t)k;
-                }
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, cu, o);
+                if (lane >= o) cu += y;
             }
-        }
+            const unsigned selm = __ballot_sync(kFull, cand && cu <= kCapU);   // lane `first` always
+            const bool sel = (selm >> lane) & 1u;
+            const int lastl = 31 - __clz(selm);
+            const uint32_t Utot = __shfl_sync(kFull, cu, lastl);
+            const uint32_t vo = cu - (cand ? U : 0u);                       // first vector of my row
+            rem &= ~selm;
 
-        // ================= warp mode: 32 lanes, one run at a time =================
-        unsigned big = __ballot_sync(kFull, valid && nnz > kSmall);
-        // software pipeline: the first 128-entry chunk of the next big row is in
-        // flight while the current run is sampled
-        uint4 qnext = make_uint4(0, 0, 0, 0);
-        if (big) {
-            const int s0 = __ffs(big) - 1;
-            const uint32_t o0 = __shfl_sync(kFull, off, s0), n0 = __shfl_sync(kFull, nnz, s0);
-            if (4u * lane < n0) qnext = __ldg(reinterpret_cast<const uint4*>(a.theta_ent + o0 + 4u * lane));
-        }
-        while (big) {
-            const int src = __ffs(big) - 1;
-            big &= big - 1;
-            const uint32_t wd = __shfl_sync(kFull, gdoc, src);
-            const uint32_t w0 = __shfl_sync(kFull, t0, src), w1 = __shfl_sync(kFull, t1, src);
-            const uint32_t woff = __shfl_sync(kFull, off, src), wn = __shfl_sync(kFull, nnz, src);
-            const U3 wu0{__shfl_sync(kFull, u0.b, src), __shfl_sync(kFull, u0.s, src), __shfl_sync(kFull, u0.t, src)};
-            const uint32_t* row = a.theta_ent + woff;
-            const uint4 qcur = qnext;
-            if (big) {
-                const int s1 = __ffs(big) - 1;
-                const uint32_t o1 = __shfl_sync(kFull, off, s1), n1 = __shfl_sync(kFull, nnz, s1);
-                qnext = make_uint4(0, 0, 0, 0);
-                if (4u * lane < n1) qnext = __ldg(reinterpret_cast<const uint4*>(a.theta_ent + o1 + 4u * lane));
-            }
-            const uint32_t nch = (wn + 127u) >> 7;
-            const bool staged = wn <= kCap;
-            // pass over the row: prefix sums (staged into buf when they fit)
+            // ---- 1. entry-parallel pass: segmented prefix of p1 over the concatenated rows ----
+            int cprev = first - 1;                                          // run holding vector q0-1
             float carry = 0.f;
-            for (uint32_t c = 0; c < nch; ++c) {
-                const uint32_t j0 = c * 128u + 4u * lane;
-                // rows are zero-padded to 4 entries (K3), so a (count 0) pad adds nothing
-                uint4 q = make_uint4(0, 0, 0, 0);
-                if (c == 0) q = qcur;
-                else if (j0 < wn) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
-                float p[4];
-                p[0] = __fmul_rn((float)(q.x >> 16), pstar[q.x & 0xffffu]);
-                p[1] = __fadd_rn(p[0], __fmul_rn((float)(q.y >> 16), pstar[q.y & 0xffffu]));
-                p[2] = __fadd_rn(p[1], __fmul_rn((float)(q.z >> 16), pstar[q.z & 0xffffu]));
-                p[3] = __fadd_rn(p[2], __fmul_rn((float)(q.w >> 16), pstar[q.w & 0xffffu]));
-                const float incl = warp_incl_scan(p[3], lane);
-                float excl = __shfl_up_sync(kFull, incl, 1);
-                if (lane == 0) excl = 0.f;
-                const float base = __fadd_rn(carry, excl);
+            for (uint32_t q0 = 0; q0 < Utot; q0 += 32) {
+                const uint32_t hb = (sel && vo >= q0 && vo < q0 + 32u) ? (1u << (vo - q0)) : 0u;
+                const unsigned M = __reduce_or_sync(kFull, hb);           // run heads in this step
+                const unsigned mle = M & lane_le;
+                const int ri = min(cprev + __popc(mle), 31);
+                const uint32_t rvo = __shfl_sync(kFull, vo, ri);
+                const uint32_t roff = __shfl_sync(kFull, off, ri);
+                const uint32_t q = q0 + lane;
+                uint4 e = make_uint4(0, 0, 0, 0);
+                if (q < Utot) e = __ldg(reinterpret_cast<const uint4*>(a.theta_ent + roff + 4u * (q - rvo)));
+                float p0 = w_of(e.x, pstar);
+                float p1 = __fadd_rn(p0, w_of(e.y, pstar));
+                float p2 = __fadd_rn(p1, w_of(e.z, pstar));
+                float p3 = __fadd_rn(p2, w_of(e.w, pstar));
+                const int head = mle ? 31 - __clz(mle) : -1;                // my segment's first lane
+                const int lim = max(head, 0);
+                float x = p3;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) p[i] = __fadd_rn(base, p[i]);
-                if (staged && j0 < kCap) *reinterpret_cast<float4*>(buf + j0) = make_float4(p[0], p[1], p[2], p[3]);
-                carry = __shfl_sync(kFull, p[3], 31);
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float y = __shfl_up_sync(kFull, x, o);
+                    if (lane - o >= lim) x = __fadd_rn(x, y);
+                }
+                const float y1 = __shfl_up_sync(kFull, x, 1);
+                float base = (lane - 1 >= lim) ? y1 : 0.f;
+                if (head < 0) base = __fadd_rn(carry, base);               // row continues from q0-1
+                p0 = __fadd_rn(base, p0);
+                p1 = __fadd_rn(base, p1);
+                p2 = __fadd_rn(base, p2);
+                p3 = __fadd_rn(base, p3);
+                if (q < Utot) *reinterpret_cast<float4*>(buf + 4u * q) = make_float4(p0, p1, p2, p3);
+                carry = __shfl_sync(kFull, p3, 31);
+                cprev = __shfl_sync(kFull, ri, 31);
             }
             __syncwarp();
-            const float S = carry;
-            if (lane == src) myS = S;                   // its log joins the batch's SIMT logf
-            if (a.eval_only) continue;
-            // uniforms of occurrences 1..31 of this run, one per lane
-            const uint32_t n = w1 - w0;
-            U3 ul{0.f, 0.f, 0.f};
-            if (n > 1 && lane > 0 && (uint32_t)lane < n) ul = draw_u(a, wd, v, (uint32_t)lane, 0u);
-            const uint32_t ngrp = (min(wn, kCap) + 31u) >> 5;
-            for (uint32_t t = w0; t < w1; ++t) {
-                const uint32_t zt = a.z[t];
-                const uint32_t occ = t - w0;
-                U3 u = wu0;
-                if (occ) {
-                    if (occ < 32) u = U3{__shfl_sync(kFull, ul.b, occ), __shfl_sync(kFull, ul.s, occ),
-                                          __shfl_sync(kFull, ul.t, occ)};
-                    else u = draw_u(a, wd, v, occ, 0u);
-                }
-                uint32_t k = zt;
-                for (int retry = 0; retry <= kMaxRetry; ++retry) {
-                    if (retry) u = draw_u(a, wd, v, occ, (uint32_t)retry);
-                    uint32_t cnt = 0;
-                    if (__fmul_rn(u.b, __fadd_rn(S, Q)) < S) {
-                        const float target = __fmul_rn(u.s, S);
-                        uint32_t j;
-                        if (staged) {
-                            // two-level 32-ary ballot search of the staged prefix
-                            const bool gok = (uint32_t)lane < ngrp && buf[min(32u * lane + 31u, wn - 1u)] > target;
-                            const unsigned gm = __ballot_sync(kFull, gok);
-                            const uint32_t g = gm ? (uint32_t)(__ffs(gm) - 1) : ngrp - 1u;
-                            const uint32_t idx = 32u * g + lane;
-                            const bool eok = idx < wn && buf[idx] > target;
-                            const unsigned em = __ballot_sync(kFull, eok);
-                            j = em ? 32u * g + (uint32_t)(__ffs(em) - 1) : wn - 1u;
-                        } else {
-                            // long row: rescan chunk by chunk (same arithmetic as the pass)
-                            float cy = 0.f;
-                            j = wn - 1u;
-                            for (uint32_t c = 0; c < nch; ++c) {
-                                const uint32_t j0 = c * 128u + 4u * lane;
-                                uint4 q = make_uint4(0, 0, 0, 0);
-                                if (j0 < wn) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
-                                const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
-                                float p[4];
-                                float acc = 0.f;
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    if (j0 + i < wn)
-                                        acc = __fadd_rn(acc, __fmul_rn((float)(e4[i] >> 16), pstar[e4[i] & 0xffffu]));
-                                    p[i] = acc;
-                                }
-                                const float incl = warp_incl_scan(acc, lane);
-                                float excl = __shfl_up_sync(kFull, incl, 1);
-                                if (lane == 0) excl = 0.f;
-                                int fi = -1;
-#pragma unroll
-                                for (int i = 3; i >= 0; --i)
-                                    if (j0 + i < wn && __fadd_rn(cy, __fadd_rn(excl, p[i])) > target) fi = i;
-                                const unsigned m = __ballot_sync(kFull, fi >= 0);
-                                if (m) {
-                                    const int L = __ffs(m) - 1;
-                                    j = c * 128u + 4u * (uint32_t)L + (uint32_t)__shfl_sync(kFull, fi, L);
-                                    break;
-                                }
-                                cy = __fadd_rn(cy, __shfl_sync(kFull, __fadd_rn(excl, p[3]), 31));
+            // ---- 2. run-parallel draws: lane j samples the tokens of run j ----
+            if (sel) {
+                const float* seg = buf + 4u * vo;
+                const float S = seg[4u * U - 1u];                          // segment total (pads add 0)
+                myS = S;
+                if (!a.eval_only) {
+                    const uint32_t* row = a.theta_ent + off;
+                    for (uint32_t t = t0; t < t1; ++t) {
+                        const uint32_t zt = a.z[t];
+                        const uint32_t occ = t - t0;
+                        U3 u = occ ? draw_u(a, gdoc, v, occ, 0u) : u0;
+                        uint32_t k = zt;
+                        for (int retry = 0; retry <= kMaxRetry; ++retry) {
+                            if (retry) u = draw_u(a, gdoc, v, occ, (uint32_t)retry);
+                            uint32_t cnt = 0;
+                            if (__fmul_rn(u.b, __fadd_rn(S, Q)) < S) {
+                                const uint32_t i = min(first_above(seg, 4u * U, __fmul_rn(u.s, S)), nnz - 1u);
+                                const uint32_t e = __ldg(row + i);
+                                k = e & 0xffffu;
+                                cnt = e >> 16;
+                            } else {
+                                k = first_above(lvl0, (uint32_t)K, __fmul_rn(u.s, Q));
+                                if (k == zt) cnt = row_count(row, nnz, zt);
                             }
+                            if (k != zt) break;
+                            if (zt >= (uint32_t)K || cnt == 0u || pex[zt] == 0.f) {   // inconsistent state
+                                atomicMin(a.errs, (unsigned long long)t);
+                                break;
+                            }
+                            if (keep_own(u.t, cnt, a.alpha, pstar[zt], pex[zt])) break;
+                            k = zt;                                                   // rejected: redraw
                         }
-                        const uint32_t e = __ldg(row + j);
-                        k = e & 0xffffu;
-                        cnt = e >> 16;
-                    } else {
-                        k = (uint32_t)search_q_warp(lvl, a.tree, __fmul_rn(u.s, Q), lane);
-                        if (k == zt) cnt = row_count(row, wn, zt);
+                        a.z[t] = (uint16_t)k;
                     }
-                    if (k != zt) break;
-                    if (zt >= (uint32_t)K || cnt == 0u || pex[zt] == 0.f) {
-                        if (lane == 0) atomicMin(a.errs, (unsigned long long)t);
-                        break;
-                    }
-                    if (keep_own(u.t, cnt, a.alpha, pstar[zt], pex[zt])) break;
-                    k = zt;
                 }
-                if (lane == 0) a.z[t] = (uint16_t)k;
             }
             __syncwarp();
         }
@@ -459,8 +462,26 @@ cudaError_t launch_validate(gf_shard* s) {
     return cudaGetLastError();
 }
 
-size_t sample_smem_bytes(const gf_shard* s) {
-    return (size_t)(((s->tree.total + 2 * s->K + 3) & ~3) + kWarps * kCap) * sizeof(float);
+static size_t smem_for(const gf_shard* s, uint32_t capb) {
+    return (size_t)(((s->tree.total + 2 * s->K + 3) & ~3) + kWarps * capb) * sizeof(float);
+}
+
+size_t sample_smem_bytes(const gf_shard* s) { return smem_for(s, kCapMax); }
+
+template <uint32_t CAPB, int MINB>
+static cudaError_t launch_variant(gf_shard* s, const SampleArgs& a) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(sample_kernel<CAPB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             220 * 1024);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(sample_kernel<CAPB, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    sample_kernel<CAPB, MINB><<<(unsigned)s->n_slices, kSampleThreads, smem_for(s, CAPB), s->stream>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
@@ -489,18 +510,14 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
     a.ll_part = s->d.ll_part;
     a.errs = s->d.errs;
     a.bytes = s->d.bytes;
-    const size_t smem = sample_smem_bytes(s);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(sample_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(sample_kernel<0>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
+    // staging-buffer size: 1024 entries (4 CTAs/SM) or 2048 (fewer, larger sub-batches)
+    static int capb = -1;
+    if (capb < 0) {
+        const char* env = getenv("GF_CAPB");
+        capb = env ? atoi(env) : 1024;
     }
-    sample_kernel<0><<<(unsigned)s->n_slices, kSampleThreads, smem, s->stream>>>(a);
-    return cudaGetLastError();
+    if (capb >= 2048) return launch_variant<2048, 2>(s, a);
+    return launch_variant<1024, 4>(s, a);
 }
 
 }  // namespace gf
