@@ -202,7 +202,7 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* lvl, co
 }
 
 // CAPB: staged prefix entries per warp (sub-batch capacity); MINB: CTAs per SM
-template <uint32_t CAPB, int MINB>
+template <uint32_t CAPB, int MINB, uint32_t VEC, bool HUGE>
 __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs a) {
     constexpr uint32_t kCapB = CAPB;
     constexpr uint32_t kCapU = CAPB / 4;        // ... in 16-byte row vectors
@@ -294,7 +294,8 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
         }
         const uint32_t gdoc = a.doc_lo + d;
         const uint32_t U = max(1u, (nnz + 3u) >> 2);          // row length in 16-byte vectors
-        const bool huge = valid && U > kCapU;
+        const uint32_t Up = (U + VEC - 1u) / VEC * VEC;       // ... padded to whole lanes
+        const bool huge = HUGE && valid && Up > kCapU;        // only possible when K > CAPB
         U3 u0{0.f, 0.f, 0.f};
         if (valid && !a.eval_only) u0 = draw_u(a, gdoc, v, 0u, 0u);
         float myS = 0.f;                                       // S of this lane's run
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
         const unsigned hmask = __ballot_sync(kFull, huge);
         while (rem) {
             const int first = __ffs(rem) - 1;
-            if ((hmask >> first) & 1u) {                       // rare: row beyond the buffer
+            if (HUGE && ((hmask >> first) & 1u)) {             // rare: row beyond the buffer
                 const U3 hu{__shfl_sync(kFull, u0.b, first), __shfl_sync(kFull, u0.s, first),
                             __shfl_sync(kFull, u0.t, first)};
                 const float S = huge_run(a, lvl, pstar, pex, Q, v, __shfl_sync(kFull, gdoc, first),
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
             const unsigned after = hmask & ~((2u << first) - 1u);
             const int end = after ? __ffs(after) - 1 : 32;
             const bool cand = lane >= first && lane < end && ((rem >> lane) & 1u);
-            uint32_t cu = cand ? U : 0u;
+            uint32_t cu = cand ? Up : 0u;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(kFull, cu, o);
@@ -326,50 +327,72 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
             const bool sel = (selm >> lane) & 1u;
             const int lastl = 31 - __clz(selm);
             const uint32_t Utot = __shfl_sync(kFull, cu, lastl);
-            const uint32_t vo = cu - (cand ? U : 0u);                       // first vector of my row
+            const uint32_t vo = cu - (cand ? Up : 0u);                      // first vector of my row
             rem &= ~selm;
 
             // ---- 1. entry-parallel pass: segmented prefix of p1 over the concatenated rows ----
+            // each lane owns VEC consecutive vectors (4*VEC entries) of ONE row per step
+            // (rows are laid out VEC-aligned), so 128*VEC entries advance per warp step
             int cprev = first - 1;                                          // run holding vector q0-1
             float carry = 0.f;
-            for (uint32_t q0 = 0; q0 < Utot; q0 += 32) {
-                const uint32_t hb = (sel && vo >= q0 && vo < q0 + 32u) ? (1u << (vo - q0)) : 0u;
+            for (uint32_t q0 = 0; q0 < Utot; q0 += 32u * VEC) {
+                const uint32_t hb = (sel && vo >= q0 && vo < q0 + 32u * VEC) ? (1u << ((vo - q0) / VEC)) : 0u;
                 const unsigned M = __reduce_or_sync(kFull, hb);           // run heads in this step
                 const unsigned mle = M & lane_le;
                 const int ri = min(cprev + __popc(mle), 31);
                 const uint32_t rvo = __shfl_sync(kFull, vo, ri);
                 const uint32_t roff = __shfl_sync(kFull, off, ri);
-                const uint32_t q = q0 + lane;
-                uint4 e = make_uint4(0, 0, 0, 0);
-                if (q < Utot) e = __ldg(reinterpret_cast<const uint4*>(a.theta_ent + roff + 4u * (q - rvo)));
-                float p0 = w_of(e.x, pstar);
-                float p1 = __fadd_rn(p0, w_of(e.y, pstar));
-                float p2 = __fadd_rn(p1, w_of(e.z, pstar));
-                float p3 = __fadd_rn(p2, w_of(e.w, pstar));
+                const uint32_t rU = __shfl_sync(kFull, U, ri);
+                const uint32_t qL = q0 + VEC * (uint32_t)lane;
+                const uint32_t rel = qL - rvo;                              // vector index inside the row
+                uint4 e[VEC];
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) {
+                    e[i] = make_uint4(0, 0, 0, 0);
+                    if (qL + i < Utot && rel + i < rU)
+                        e[i] = __ldg(reinterpret_cast<const uint4*>(a.theta_ent + roff + 4u * (rel + i)));
+                }
+                float p[4 * VEC];
+                float acc = 0.f;
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) {
+                    acc += (float)(e[i].x >> 16) * pstar[e[i].x & 0xffffu];
+                    p[4 * i] = acc;
+                    acc += (float)(e[i].y >> 16) * pstar[e[i].y & 0xffffu];
+                    p[4 * i + 1] = acc;
+                    acc += (float)(e[i].z >> 16) * pstar[e[i].z & 0xffffu];
+                    p[4 * i + 2] = acc;
+                    acc += (float)(e[i].w >> 16) * pstar[e[i].w & 0xffffu];
+                    p[4 * i + 3] = acc;
+                }
                 const int head = mle ? 31 - __clz(mle) : -1;                // my segment's first lane
                 const int lim = max(head, 0);
-                float x = p3;
+                float x = acc;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const float y = __shfl_up_sync(kFull, x, o);
-                    if (lane - o >= lim) x = __fadd_rn(x, y);
+                    if (lane - o >= lim) x += y;
                 }
                 const float y1 = __shfl_up_sync(kFull, x, 1);
                 float base = (lane - 1 >= lim) ? y1 : 0.f;
-                if (head < 0) base = __fadd_rn(carry, base);               // row continues from q0-1
-                p0 = __fadd_rn(base, p0);
-                p1 = __fadd_rn(base, p1);
-                p2 = __fadd_rn(base, p2);
-                p3 = __fadd_rn(base, p3);
-                if (q < Utot) *reinterpret_cast<float4*>(buf + 4u * q) = make_float4(p0, p1, p2, p3);
-                carry = __shfl_sync(kFull, p3, 31);
+                if (head < 0) base += carry;                                // row continues from q0-1
+#pragma unroll
+                for (int i = 0; i < 4 * VEC; ++i) p[i] += base;
+                if (qL < Utot) {
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i)
+                        *reinterpret_cast<float4*>(buf + 4u * (qL + i)) =
+                            make_float4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                }
+                carry = __shfl_sync(kFull, p[4 * VEC - 1], 31);
                 cprev = __shfl_sync(kFull, ri, 31);
             }
             __syncwarp();
             // ---- 2. run-parallel draws: lane j samples the tokens of run j ----
             if (sel) {
                 const float* seg = buf + 4u * vo;
-                const float S = seg[4u * U - 1u];                          // segment total (pads add 0)
+                const uint32_t U = Up;                                      // searched span (pads add 0)
+                const float S = seg[4u * U - 1u];                          // segment total
                 myS = S;
                 if (!a.eval_only) {
                     const uint32_t* row = a.theta_ent + off;
@@ -468,19 +491,19 @@ static size_t smem_for(const gf_shard* s, uint32_t capb) {
 
 size_t sample_smem_bytes(const gf_shard* s) { return smem_for(s, kCapMax); }
 
-template <uint32_t CAPB, int MINB>
+template <uint32_t CAPB, int MINB, uint32_t VEC, bool HUGE>
 static cudaError_t launch_variant(gf_shard* s, const SampleArgs& a) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(sample_kernel<CAPB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(sample_kernel<CAPB, MINB, VEC, HUGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              220 * 1024);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(sample_kernel<CAPB, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        e = cudaFuncSetAttribute(sample_kernel<CAPB, MINB, VEC, HUGE>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    sample_kernel<CAPB, MINB><<<(unsigned)s->n_slices, kSampleThreads, smem_for(s, CAPB), s->stream>>>(a);
+    sample_kernel<CAPB, MINB, VEC, HUGE><<<(unsigned)s->n_slices, kSampleThreads, smem_for(s, CAPB), s->stream>>>(a);
     return cudaGetLastError();
 }
 
@@ -511,13 +534,23 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
     a.errs = s->d.errs;
     a.bytes = s->d.bytes;
     // staging-buffer size: 1024 entries (4 CTAs/SM) or 2048 (fewer, larger sub-batches)
-    static int capb = -1;
+    // and vectors per lane per pass step (tuning knobs GF_CAPB / GF_VEC)
+    static int capb = -1, vec = -1;
     if (capb < 0) {
         const char* env = getenv("GF_CAPB");
         capb = env ? atoi(env) : 1024;
+        env = getenv("GF_VEC");
+        vec = env ? atoi(env) : 2;
     }
-    if (capb >= 2048) return launch_variant<2048, 2>(s, a);
-    return launch_variant<1024, 4>(s, a);
+    // rows can only outgrow the buffer when K > CAPB: otherwise the streaming
+    // path (a register-hungry call) is compiled out
+    if (capb >= 2048 || s->K > 1024) {
+        if (s->K > 2048) return launch_variant<2048, 2, 2, true>(s, a);
+        return vec >= 4 ? launch_variant<2048, 2, 4, false>(s, a) : launch_variant<2048, 2, 2, false>(s, a);
+    }
+    if (vec >= 4) return launch_variant<1024, 4, 4, false>(s, a);
+    if (vec == 1) return launch_variant<1024, 4, 1, false>(s, a);
+    return launch_variant<1024, 4, 2, false>(s, a);
 }
 
 }  // namespace gf
