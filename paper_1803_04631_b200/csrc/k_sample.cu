@@ -38,6 +38,7 @@ namespace gf {
 constexpr int kWarps = kSampleThreads / 32;
 constexpr uint32_t kCapMax = 2048;    // largest staging buffer (entries per warp) compiled
 constexpr int kMaxRetry = 63;
+constexpr int kLaneParallelMin = 12;   // sub-batches with fewer runs draw warp-cooperatively
 
 struct SampleArgs {
     int K, Kp;
@@ -388,12 +389,76 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                 cprev = __shfl_sync(kFull, ri, 31);
             }
             __syncwarp();
-            // ---- 2. run-parallel draws: lane j samples the tokens of run j ----
-            if (sel) {
+            if (sel) myS = buf[4u * (vo + Up) - 1u];                     // segment total (pads add 0)
+            if (!a.eval_only && __popc(selm) < kLaneParallelMin) {
+                // ---- 2a. few long rows: warp-cooperative draws, one token at a time, the
+                //      staged prefix searched by a two-level 32-ary ballot ----
+                unsigned todo = selm;
+                while (todo) {
+                    const int j = __ffs(todo) - 1;
+                    todo &= todo - 1u;
+                    const uint32_t jt0 = __shfl_sync(kFull, t0, j), jt1 = __shfl_sync(kFull, t1, j);
+                    const uint32_t jvo = __shfl_sync(kFull, vo, j), jUp = __shfl_sync(kFull, Up, j);
+                    const uint32_t jn = __shfl_sync(kFull, nnz, j), joff = __shfl_sync(kFull, off, j);
+                    const uint32_t jdoc = __shfl_sync(kFull, gdoc, j);
+                    const float S = __shfl_sync(kFull, myS, j);
+                    const U3 ju0{__shfl_sync(kFull, u0.b, j), __shfl_sync(kFull, u0.s, j), __shfl_sync(kFull, u0.t, j)};
+                    const float* seg = buf + 4u * jvo;
+                    const uint32_t len = 4u * jUp;
+                    const uint32_t gsz = 32u * ((len + 1023u) >> 10);   // 32 groups cover the segment
+                    const uint32_t ngrp = (len + gsz - 1u) / gsz;
+                    const uint32_t* row = a.theta_ent + joff;
+                    const uint32_t n = jt1 - jt0;
+                    U3 ul{0.f, 0.f, 0.f};                                   // occurrences 1..31, one per lane
+                    if (n > 1 && lane > 0 && (uint32_t)lane < n) ul = draw_u(a, jdoc, v, (uint32_t)lane, 0u);
+                    for (uint32_t t = jt0; t < jt1; ++t) {
+                        const uint32_t zt = a.z[t];
+                        const uint32_t occ = t - jt0;
+                        U3 u = ju0;
+                        if (occ) {
+                            if (occ < 32) u = U3{__shfl_sync(kFull, ul.b, occ), __shfl_sync(kFull, ul.s, occ),
+                                                  __shfl_sync(kFull, ul.t, occ)};
+                            else u = draw_u(a, jdoc, v, occ, 0u);
+                        }
+                        uint32_t k = zt;
+                        for (int retry = 0; retry <= kMaxRetry; ++retry) {
+                            if (retry) u = draw_u(a, jdoc, v, occ, (uint32_t)retry);
+                            uint32_t cnt = 0;
+                            if (__fmul_rn(u.b, __fadd_rn(S, Q)) < S) {
+                                const float target = __fmul_rn(u.s, S);
+                                const bool gok = (uint32_t)lane < ngrp && seg[min(gsz * lane + gsz - 1u, len - 1u)] > target;
+                                const unsigned gm = __ballot_sync(kFull, gok);
+                                const uint32_t g = gm ? (uint32_t)(__ffs(gm) - 1) : ngrp - 1u;
+                                uint32_t i = len - 1u;
+                                for (uint32_t c0 = g * gsz; c0 < min(g * gsz + gsz, len); c0 += 32u) {
+                                    const uint32_t idx = c0 + lane;
+                                    const unsigned em = __ballot_sync(kFull, idx < len && seg[idx] > target);
+                                    if (em) { i = c0 + (uint32_t)(__ffs(em) - 1); break; }
+                                }
+                                i = min(i, jn - 1u);
+                                const uint32_t e = __ldg(row + i);
+                                k = e & 0xffffu;
+                                cnt = e >> 16;
+                            } else {
+                                k = (uint32_t)search_q_warp(lvl, a.tree, __fmul_rn(u.s, Q), lane);
+                                if (k == zt) cnt = row_count(row, jn, zt);
+                            }
+                            if (k != zt) break;
+                            if (zt >= (uint32_t)K || cnt == 0u || pex[zt] == 0.f) {
+                                if (lane == 0) atomicMin(a.errs, (unsigned long long)t);
+                                break;
+                            }
+                            if (keep_own(u.t, cnt, a.alpha, pstar[zt], pex[zt])) break;
+                            k = zt;
+                        }
+                        if (lane == 0) a.z[t] = (uint16_t)k;
+                    }
+                }
+            } else if (sel) {
+                // ---- 2b. many short rows: run-parallel draws, lane j samples run j ----
                 const float* seg = buf + 4u * vo;
                 const uint32_t U = Up;                                      // searched span (pads add 0)
-                const float S = seg[4u * U - 1u];                          // segment total
-                myS = S;
+                const float S = myS;
                 if (!a.eval_only) {
                     const uint32_t* row = a.theta_ent + off;
                     for (uint32_t t = t0; t < t1; ++t) {
