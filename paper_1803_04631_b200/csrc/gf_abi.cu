@@ -214,6 +214,8 @@ int gf_shard_create(gf_shard** out, int device, int32_t K, int32_t V, double alp
                     uint32_t heavy_threshold) {
     *out = nullptr;
     if (K < 1 || K >= 65536) return fail(GF_ERR_VALUE, "topic count %d outside [1, 65536)", K);
+    // device theta entries hold the topic as a 16-bit byte offset (topic << 2)
+    if (K > 16384) return fail(GF_ERR_CAPACITY, "K=%d: the device sampler supports K <= 16384", K);
     if (V < 1) return fail(GF_ERR_VALUE, "vocab_size must be >= 1");
     if (!(alpha > 0) || !(beta > 0)) return fail(GF_ERR_VALUE, "alpha and beta must be > 0");
     int ndev = 0;

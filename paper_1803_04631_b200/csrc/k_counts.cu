@@ -106,8 +106,9 @@ cudaError_t launch_prepare(gf_shard* s) {
 // across the warp and run-length encoded with ballots (no K-sized state).
 // Longer documents: dense K-bin histogram in the warp's shared-memory slice
 // (section 6.2 "generate a dense array ... then CSR"), then an
-// ascending ballot/popc compaction.  Output rows: (count << 16 | topic),
-// ascending topic, written into the fixed-capacity row; nnz into meta.y.
+// ascending ballot/popc compaction.  Output rows: (count << 16 | topic << 2)
+// (the topic pre-scaled to a byte offset into K1's shared p* table), ascending
+// topic, written into the fixed-capacity row; nnz into meta.y.
 __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
                                                             const uint32_t* __restrict__ dw_tok,
                                                             const uint16_t* __restrict__ z, uint32_t* theta_ent,
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
             if (head) {
                 const unsigned later = heads & ~((2u << lane) - 1u);
                 const uint32_t next = later ? (uint32_t)(__ffs(later) - 1) : L;
-                theta_ent[off + __popc(heads & lt)] = key | ((next - lane) << 16);
+                theta_ent[off + __popc(heads & lt)] = (key << 2) | ((next - lane) << 16);
             }
             nnz = __popc(heads);
         } else {
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
                 const int k = c + lane;
                 const uint32_t v = k < K ? bins[k] : 0u;
                 const unsigned m = __ballot_sync(kFull, v > 0);
-                if (v) theta_ent[off + base + __popc(m & lt)] = (uint32_t)k | (min(v, 65535u) << 16);
+                if (v) theta_ent[off + base + __popc(m & lt)] = ((uint32_t)k << 2) | (min(v, 65535u) << 16);
                 mx = max(mx, v);
                 base += __popc(m);
             }
@@ -217,7 +218,7 @@ __global__ void theta_export_kernel(int D, const uint2* __restrict__ meta, const
         const int64_t o = rowptr[d];
         for (uint32_t j = lane; j < m.y; j += 32) {
             const uint32_t e = ent[m.x + j];
-            ids[o + j] = (uint16_t)(e & 0xffffu);
+            ids[o + j] = (uint16_t)((e & 0xffffu) >> 2);
             cnt[o + j] = (uint16_t)(e >> 16);
         }
     }
@@ -231,7 +232,7 @@ __global__ void theta_import_kernel(int D, uint2* meta, uint32_t* ent, const int
     for (long long d = w; d < D; d += nw) {
         const int64_t o = rowptr[d], n = rowptr[d + 1] - o;
         const uint32_t base = meta[d].x;
-        for (int64_t j = lane; j < n; j += 32) ent[base + j] = (uint32_t)ids[o + j] | ((uint32_t)cnt[o + j] << 16);
+        for (int64_t j = lane; j < n; j += 32) ent[base + j] = ((uint32_t)ids[o + j] << 2) | ((uint32_t)cnt[o + j] << 16);
         if (lane < ((4 - (n & 3)) & 3)) ent[base + n + lane] = 0u;   // zero pads (see K3)
         if (lane == 0) meta[d].y = (uint32_t)n;
     }

@@ -8,19 +8,23 @@
 //   p*(k)     = (phi_vk + b) / (n_k + V b)                 (PAPER Eq. 8)
 //   p*_ex(k)  = (phi_vk - 1 + b) / (n_k - 1 + V b)         (exclusion view)
 //   Q-tree    = 32-ary prefix tree over a p*(k)            (ptree.build levels)
+// p* sits at shared offset 0 and theta entries carry the topic pre-scaled to a
+// byte offset (count << 16 | topic << 2), so a p1 term is one LOP + LDS + FFMA.
 //
 // Work: each warp pulls batches of up to 32 (doc, word) RUNS (lane j owns run
 // j: its doc, token range, theta row and the Philox4x32-10 uniforms of its
 // first token) and handles them as segmented sub-batches:
 //   1. entry-parallel pass: the sub-batch's theta rows (16-byte vectors,
-//      zero-padded to 4 entries) are streamed as one concatenated array, 128
-//      entries per warp step; p1 = theta * p* is prefix-summed by a segmented
-//      __shfl scan (segment heads from one __reduce_or_sync) and staged in the
+//      zero-padded to 4 entries) are streamed as one concatenated array, VEC
+//      vectors per lane and 128*VEC entries per warp step; p1 = theta * p* is
+//      prefix-summed by a segmented __shfl scan (segment heads from one
+//      __reduce_or_sync) and the prefix at every vector end is staged in the
 //      warp's shared buffer -- S of every run falls out as a segment total;
 //   2. run-parallel draws: lane j samples the tokens of run j -- branch on
-//      u (S+Q) < S, then a binary search of its staged prefix (S part) or of
-//      the Q-tree level 0.
-// Rows longer than the staging buffer (K > 2048 only) take a warp-cooperative
+//      u (S+Q) < S, then a branch-free binary search over its staged vector
+//      ends and a 4-entry walk of the chosen vector (S part), or a binary
+//      search of the Q-tree level 0 (Q part).
+// Rows longer than the staging buffer (K > 4096 only) take a warp-cooperative
 // streaming path.  Exclusion (theta_dz-1, phi_vz-1, n_z-1)
 // is applied by thinning: draw k from the exclusion-free S+Q mixture; if
 // k == z keep it with probability
@@ -36,9 +40,10 @@
 namespace gf {
 
 constexpr int kWarps = kSampleThreads / 32;
-constexpr uint32_t kCapMax = 2048;    // largest staging buffer (entries per warp) compiled
+constexpr uint32_t kCapV = 1024;      // staged vector-end prefixes per warp (4096 entries)
 constexpr int kMaxRetry = 63;
-constexpr int kLaneParallelMin = 12;   // sub-batches with fewer runs draw warp-cooperatively
+
+__device__ const uint4 g_zero16 = {0u, 0u, 0u, 0u};   // load target of idle lanes
 
 struct SampleArgs {
     int K, Kp;
@@ -63,6 +68,10 @@ struct SampleArgs {
     unsigned long long* bytes;
 };
 
+// shared-memory layout (floats): p*[K] at 0 | p*_ex[K] | Q-tree levels | pad | warp buffers
+__host__ __device__ inline int lay_tree(int K) { return 2 * K; }
+__host__ __device__ inline int lay_buf(int K, int tree_total) { return (2 * K + tree_total + 3) & ~3; }
+
 __device__ __forceinline__ uint32_t phi_at(const SampleArgs& a, int col, int k) {
     return col >= 0 ? (uint32_t)a.phi16[(size_t)col * a.Kp + k] : a.phi32[(size_t)(~col) * a.K + k];
 }
@@ -76,9 +85,11 @@ __device__ __forceinline__ U3 draw_u(const SampleArgs& a, uint32_t gdoc, uint32_
     return U3{u24(r.x), u24(r.y), u24(r.z)};
 }
 
-__device__ __forceinline__ float w_of(uint32_t e, const float* pstar) {
-    return __fmul_rn((float)(e >> 16), pstar[e & 0xffffu]);
+// p1 term of one theta entry (count << 16 | topic << 2) against p* at shared offset 0
+__device__ __forceinline__ float w_of(uint32_t e, const float* smem) {
+    return (float)(e >> 16) * smem[(e & 0xfffcu) >> 2];
 }
+__device__ __forceinline__ uint32_t topic_of(uint32_t e) { return (e & 0xffffu) >> 2; }
 
 // ptree descent (ptree.py:203-225) over the shared-memory levels, one ballot
 // per level (warp-cooperative).
@@ -94,29 +105,28 @@ __device__ __forceinline__ int search_q_warp(const float* lvl, const TreeGeom& g
     return idx;
 }
 
-// minimal i in [0, n) with P[i] > u (n-1 if none): the same search by one lane
+// minimal i in [0, n) with P[i] > u (n-1 if none), P non-decreasing: one lane,
+// branch-free (a fixed ladder of power-of-two steps)
 __device__ __forceinline__ uint32_t first_above(const float* P, uint32_t n, float u) {
-    uint32_t lo = 0, hi = n - 1;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (P[mid] > u) hi = mid;
-        else lo = mid + 1;
-    }
-    return lo;
+    uint32_t i = 0;
+    for (uint32_t step = 1u << (31 - __clz(n)); step; step >>= 1)
+        if (i + step <= n && !(P[i + step - 1] > u)) i += step;
+    return min(i, n - 1u);
 }
 
 // theta_dz of a sorted row by binary search (thinning of a Q-branch z draw)
 __device__ __forceinline__ uint32_t row_count(const uint32_t* row, uint32_t nnz, uint32_t z) {
+    const uint32_t key = z << 2;
     uint32_t lo = 0, hi = nnz;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         const uint32_t e = __ldg(row + mid);
-        if ((e & 0xffffu) < z) lo = mid + 1;
+        if ((e & 0xffffu) < key) lo = mid + 1;
         else hi = mid;
     }
     if (lo < nnz) {
         const uint32_t e = __ldg(row + lo);
-        if ((e & 0xffffu) == z) return e >> 16;
+        if ((e & 0xffffu) == key) return e >> 16;
     }
     return 0;
 }
@@ -130,9 +140,11 @@ __device__ __forceinline__ bool keep_own(float ut, uint32_t cnt, float alpha, fl
 
 // Rows longer than the staging buffer: warp-cooperative, one run, the S part
 // re-streamed per S-branch draw.  Returns S (all lanes).
-__device__ __noinline__ float huge_run(const SampleArgs& a, const float* lvl, const float* pstar, const float* pex,
-                                       float Q, uint32_t v, uint32_t gdoc, uint32_t t0, uint32_t t1, uint32_t off,
-                                       uint32_t nnz, U3 u0, int lane) {
+__device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, float Q, uint32_t v, uint32_t gdoc,
+                                       uint32_t t0, uint32_t t1, uint32_t off, uint32_t nnz, U3 u0, int lane) {
+    const float* pstar = smem;
+    const float* pex = smem + a.K;
+    const float* lvl = smem + lay_tree(a.K);
     const uint32_t* row = a.theta_ent + off;
     const uint32_t nch = (nnz + 127u) >> 7;
     float S = 0.f;
@@ -140,9 +152,9 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* lvl, co
         const uint32_t j0 = c * 128u + 4u * lane;
         uint4 q = make_uint4(0, 0, 0, 0);
         if (j0 < nnz) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
-        float s4 = __fadd_rn(__fadd_rn(w_of(q.x, pstar), w_of(q.y, pstar)), __fadd_rn(w_of(q.z, pstar), w_of(q.w, pstar)));
+        const float s4 = (w_of(q.x, smem) + w_of(q.y, smem)) + (w_of(q.z, smem) + w_of(q.w, smem));
         const float incl = warp_incl_scan(s4, lane);
-        S = __fadd_rn(S, __shfl_sync(kFull, incl, 31));
+        S += __shfl_sync(kFull, incl, 31);
     }
     if (a.eval_only) return S;
     for (uint32_t t = t0; t < t1; ++t) {
@@ -162,28 +174,28 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* lvl, co
                     uint4 q = make_uint4(0, 0, 0, 0);
                     if (j0 < nnz) q = __ldg(reinterpret_cast<const uint4*>(row + j0));
                     float p[4];
-                    p[0] = w_of(q.x, pstar);
-                    p[1] = __fadd_rn(p[0], w_of(q.y, pstar));
-                    p[2] = __fadd_rn(p[1], w_of(q.z, pstar));
-                    p[3] = __fadd_rn(p[2], w_of(q.w, pstar));
+                    p[0] = w_of(q.x, smem);
+                    p[1] = p[0] + w_of(q.y, smem);
+                    p[2] = p[1] + w_of(q.z, smem);
+                    p[3] = p[2] + w_of(q.w, smem);
                     const float incl = warp_incl_scan(p[3], lane);
                     float excl = __shfl_up_sync(kFull, incl, 1);
                     if (lane == 0) excl = 0.f;
-                    const float base = __fadd_rn(cy, excl);
+                    const float base = cy + excl;
                     int fi = -1;
 #pragma unroll
                     for (int i = 3; i >= 0; --i)
-                        if (j0 + i < nnz && __fadd_rn(base, p[i]) > target) fi = i;
+                        if (j0 + i < nnz && base + p[i] > target) fi = i;
                     const unsigned m = __ballot_sync(kFull, fi >= 0);
                     if (m) {
                         const int L = __ffs(m) - 1;
                         j = c * 128u + 4u * (uint32_t)L + (uint32_t)__shfl_sync(kFull, fi, L);
                         break;
                     }
-                    cy = __shfl_sync(kFull, __fadd_rn(base, p[3]), 31);
+                    cy = __shfl_sync(kFull, base + p[3], 31);
                 }
                 const uint32_t e = __ldg(row + j);
-                k = e & 0xffffu;
+                k = topic_of(e);
                 cnt = e >> 16;
             } else {
                 k = (uint32_t)search_q_warp(lvl, a.tree, __fmul_rn(u.s, Q), lane);
@@ -202,16 +214,16 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* lvl, co
     return S;
 }
 
-// CAPB: staged prefix entries per warp (sub-batch capacity); MINB: CTAs per SM
-template <uint32_t CAPB, int MINB, uint32_t VEC, bool HUGE>
+// CAPV: staged vector ends per warp; MINB: CTAs per SM; VEC: vectors per lane
+// per pass step; HUGE: compile the streaming path (needed only when K > 4*CAPV)
+template <uint32_t CAPV, int MINB, uint32_t VEC, bool HUGE>
 __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs a) {
-    constexpr uint32_t kCapB = CAPB;
-    constexpr uint32_t kCapU = CAPB / 4;        // ... in 16-byte row vectors
     extern __shared__ float smem[];
-    float* lvl = smem;                              // Q-tree levels (level 0 = prefix of a p*)
-    float* pstar = smem + a.tree.total;             // p*(k)
-    float* pex = pstar + a.K;                       // p*_ex(k)
-    float* wbuf = smem + ((a.tree.total + 2 * a.K + 3) & ~3);   // kWarps x kCapB staged prefixes
+    const int K = a.K;
+    float* pstar = smem;                            // p*(k)        (byte offset = theta topic field)
+    float* pex = smem + K;                          // p*_ex(k)
+    float* lvl = smem + lay_tree(K);                // Q-tree levels (level 0 = prefix of a p*)
+    float* wbuf = smem + lay_buf(K, a.tree.total);  // kWarps x CAPV staged vector-end prefixes
     __shared__ double ll_w[kWarps];
     __shared__ unsigned long long by_w[kWarps];
     __shared__ int next_run;
@@ -220,7 +232,6 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
     const int4 sl = a.slices[blockIdx.x];
     const uint32_t v = (uint32_t)sl.x;
     const int col = sl.w;
-    const int K = a.K;
     const unsigned lane_le = (2u << lane) - 1u;     // lanes 0..lane
 
     // ---------------- prologue: p*, p*_ex and the Q prefix (block scan) ----------------
@@ -268,7 +279,7 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
     }
     const float Q = lvl[K - 1];
     const float* lvl0 = lvl;
-    float* buf = wbuf + warp * kCapB;
+    float* buf = wbuf + warp * CAPV;
     // runs per grab: 32 (one per lane) unless the slice is too small to give
     // every warp at least two grabs -- then smaller grabs keep all 8 warps busy
     const int batch = min(32, max(1, (sl.z - sl.y + 2 * kWarps - 1) / (2 * kWarps)));
@@ -296,7 +307,7 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
         const uint32_t gdoc = a.doc_lo + d;
         const uint32_t U = max(1u, (nnz + 3u) >> 2);          // row length in 16-byte vectors
         const uint32_t Up = (U + VEC - 1u) / VEC * VEC;       // ... padded to whole lanes
-        const bool huge = HUGE && valid && Up > kCapU;        // only possible when K > CAPB
+        const bool huge = HUGE && valid && Up > CAPV;         // only possible when K > 4*CAPV
         U3 u0{0.f, 0.f, 0.f};
         if (valid && !a.eval_only) u0 = draw_u(a, gdoc, v, 0u, 0u);
         float myS = 0.f;                                       // S of this lane's run
@@ -307,14 +318,14 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
             if (HUGE && ((hmask >> first) & 1u)) {             // rare: row beyond the buffer
                 const U3 hu{__shfl_sync(kFull, u0.b, first), __shfl_sync(kFull, u0.s, first),
                             __shfl_sync(kFull, u0.t, first)};
-                const float S = huge_run(a, lvl, pstar, pex, Q, v, __shfl_sync(kFull, gdoc, first),
+                const float S = huge_run(a, smem, Q, v, __shfl_sync(kFull, gdoc, first),
                                          __shfl_sync(kFull, t0, first), __shfl_sync(kFull, t1, first),
                                          __shfl_sync(kFull, off, first), __shfl_sync(kFull, nnz, first), hu, lane);
                 if (lane == first) myS = S;
                 rem &= rem - 1u;
                 continue;
             }
-            // ---- sub-batch: contiguous non-huge lanes [first, ...) whose rows fit kCapB ----
+            // ---- sub-batch: contiguous non-huge lanes [first, ...) whose rows fit CAPV ----
             const unsigned after = hmask & ~((2u << first) - 1u);
             const int end = after ? __ffs(after) - 1 : 32;
             const bool cand = lane >= first && lane < end && ((rem >> lane) & 1u);
@@ -324,7 +335,7 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                 const uint32_t y = __shfl_up_sync(kFull, cu, o);
                 if (lane >= o) cu += y;
             }
-            const unsigned selm = __ballot_sync(kFull, cand && cu <= kCapU);   // lane `first` always
+            const unsigned selm = __ballot_sync(kFull, cand && cu <= CAPV);   // lane `first` always
             const bool sel = (selm >> lane) & 1u;
             const int lastl = 31 - __clz(selm);
             const uint32_t Utot = __shfl_sync(kFull, cu, lastl);
@@ -337,7 +348,7 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
             int cprev = first - 1;                                          // run holding vector q0-1
             float carry = 0.f;
             for (uint32_t q0 = 0; q0 < Utot; q0 += 32u * VEC) {
-                const uint32_t hb = (sel && vo >= q0 && vo < q0 + 32u * VEC) ? (1u << ((vo - q0) / VEC)) : 0u;
+                const uint32_t hb = (sel && vo - q0 < 32u * VEC) ? (1u << ((vo - q0) / VEC)) : 0u;
                 const unsigned M = __reduce_or_sync(kFull, hb);           // run heads in this step
                 const unsigned mle = M & lane_le;
                 const int ri = min(cprev + __popc(mle), 31);
@@ -346,25 +357,24 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                 const uint32_t rU = __shfl_sync(kFull, U, ri);
                 const uint32_t qL = q0 + VEC * (uint32_t)lane;
                 const uint32_t rel = qL - rvo;                              // vector index inside the row
+                const bool act = qL < Utot;
                 uint4 e[VEC];
 #pragma unroll
                 for (int i = 0; i < VEC; ++i) {
-                    e[i] = make_uint4(0, 0, 0, 0);
-                    if (qL + i < Utot && rel + i < rU)
-                        e[i] = __ldg(reinterpret_cast<const uint4*>(a.theta_ent + roff + 4u * (rel + i)));
+                    const uint4* src = (act && rel + i < rU)
+                                           ? reinterpret_cast<const uint4*>(a.theta_ent + roff + 4u * (rel + i))
+                                           : &g_zero16;
+                    e[i] = __ldg(src);
                 }
-                float p[4 * VEC];
+                float p[VEC];                                               // prefix at each vector end
                 float acc = 0.f;
 #pragma unroll
                 for (int i = 0; i < VEC; ++i) {
-                    acc += (float)(e[i].x >> 16) * pstar[e[i].x & 0xffffu];
-                    p[4 * i] = acc;
-                    acc += (float)(e[i].y >> 16) * pstar[e[i].y & 0xffffu];
-                    p[4 * i + 1] = acc;
-                    acc += (float)(e[i].z >> 16) * pstar[e[i].z & 0xffffu];
-                    p[4 * i + 2] = acc;
-                    acc += (float)(e[i].w >> 16) * pstar[e[i].w & 0xffffu];
-                    p[4 * i + 3] = acc;
+                    acc += w_of(e[i].x, smem);
+                    acc += w_of(e[i].y, smem);
+                    acc += w_of(e[i].z, smem);
+                    acc += w_of(e[i].w, smem);
+                    p[i] = acc;
                 }
                 const int head = mle ? 31 - __clz(mle) : -1;                // my segment's first lane
                 const int lim = max(head, 0);
@@ -378,87 +388,24 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                 float base = (lane - 1 >= lim) ? y1 : 0.f;
                 if (head < 0) base += carry;                                // row continues from q0-1
 #pragma unroll
-                for (int i = 0; i < 4 * VEC; ++i) p[i] += base;
-                if (qL < Utot) {
+                for (int i = 0; i < VEC; ++i) p[i] += base;
+                if (act) {
+                    if (VEC == 4) {
+                        *reinterpret_cast<float4*>(buf + qL) = make_float4(p[0], p[1 % VEC], p[2 % VEC], p[3 % VEC]);
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < VEC; ++i)
-                        *reinterpret_cast<float4*>(buf + 4u * (qL + i)) =
-                            make_float4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                        for (int i = 0; i < VEC; ++i) buf[qL + i] = p[i];
+                    }
                 }
-                carry = __shfl_sync(kFull, p[4 * VEC - 1], 31);
+                carry = __shfl_sync(kFull, p[VEC - 1], 31);
                 cprev = __shfl_sync(kFull, ri, 31);
             }
             __syncwarp();
-            if (sel) myS = buf[4u * (vo + Up) - 1u];                     // segment total (pads add 0)
-            if (!a.eval_only && __popc(selm) < kLaneParallelMin) {
-                // ---- 2a. few long rows: warp-cooperative draws, one token at a time, the
-                //      staged prefix searched by a two-level 32-ary ballot ----
-                unsigned todo = selm;
-                while (todo) {
-                    const int j = __ffs(todo) - 1;
-                    todo &= todo - 1u;
-                    const uint32_t jt0 = __shfl_sync(kFull, t0, j), jt1 = __shfl_sync(kFull, t1, j);
-                    const uint32_t jvo = __shfl_sync(kFull, vo, j), jUp = __shfl_sync(kFull, Up, j);
-                    const uint32_t jn = __shfl_sync(kFull, nnz, j), joff = __shfl_sync(kFull, off, j);
-                    const uint32_t jdoc = __shfl_sync(kFull, gdoc, j);
-                    const float S = __shfl_sync(kFull, myS, j);
-                    const U3 ju0{__shfl_sync(kFull, u0.b, j), __shfl_sync(kFull, u0.s, j), __shfl_sync(kFull, u0.t, j)};
-                    const float* seg = buf + 4u * jvo;
-                    const uint32_t len = 4u * jUp;
-                    const uint32_t gsz = 32u * ((len + 1023u) >> 10);   // 32 groups cover the segment
-                    const uint32_t ngrp = (len + gsz - 1u) / gsz;
-                    const uint32_t* row = a.theta_ent + joff;
-                    const uint32_t n = jt1 - jt0;
-                    U3 ul{0.f, 0.f, 0.f};                                   // occurrences 1..31, one per lane
-                    if (n > 1 && lane > 0 && (uint32_t)lane < n) ul = draw_u(a, jdoc, v, (uint32_t)lane, 0u);
-                    for (uint32_t t = jt0; t < jt1; ++t) {
-                        const uint32_t zt = a.z[t];
-                        const uint32_t occ = t - jt0;
-                        U3 u = ju0;
-                        if (occ) {
-                            if (occ < 32) u = U3{__shfl_sync(kFull, ul.b, occ), __shfl_sync(kFull, ul.s, occ),
-                                                  __shfl_sync(kFull, ul.t, occ)};
-                            else u = draw_u(a, jdoc, v, occ, 0u);
-                        }
-                        uint32_t k = zt;
-                        for (int retry = 0; retry <= kMaxRetry; ++retry) {
-                            if (retry) u = draw_u(a, jdoc, v, occ, (uint32_t)retry);
-                            uint32_t cnt = 0;
-                            if (__fmul_rn(u.b, __fadd_rn(S, Q)) < S) {
-                                const float target = __fmul_rn(u.s, S);
-                                const bool gok = (uint32_t)lane < ngrp && seg[min(gsz * lane + gsz - 1u, len - 1u)] > target;
-                                const unsigned gm = __ballot_sync(kFull, gok);
-                                const uint32_t g = gm ? (uint32_t)(__ffs(gm) - 1) : ngrp - 1u;
-                                uint32_t i = len - 1u;
-                                for (uint32_t c0 = g * gsz; c0 < min(g * gsz + gsz, len); c0 += 32u) {
-                                    const uint32_t idx = c0 + lane;
-                                    const unsigned em = __ballot_sync(kFull, idx < len && seg[idx] > target);
-                                    if (em) { i = c0 + (uint32_t)(__ffs(em) - 1); break; }
-                                }
-                                i = min(i, jn - 1u);
-                                const uint32_t e = __ldg(row + i);
-                                k = e & 0xffffu;
-                                cnt = e >> 16;
-                            } else {
-                                k = (uint32_t)search_q_warp(lvl, a.tree, __fmul_rn(u.s, Q), lane);
-                                if (k == zt) cnt = row_count(row, jn, zt);
-                            }
-                            if (k != zt) break;
-                            if (zt >= (uint32_t)K || cnt == 0u || pex[zt] == 0.f) {
-                                if (lane == 0) atomicMin(a.errs, (unsigned long long)t);
-                                break;
-                            }
-                            if (keep_own(u.t, cnt, a.alpha, pstar[zt], pex[zt])) break;
-                            k = zt;
-                        }
-                        if (lane == 0) a.z[t] = (uint16_t)k;
-                    }
-                }
-            } else if (sel) {
-                // ---- 2b. many short rows: run-parallel draws, lane j samples run j ----
-                const float* seg = buf + 4u * vo;
-                const uint32_t U = Up;                                      // searched span (pads add 0)
-                const float S = myS;
+            // ---- 2. run-parallel draws: lane j samples the tokens of run j ----
+            if (sel) {
+                const float* seg = buf + vo;
+                const float S = seg[Up - 1u];                              // segment total (pads add 0)
+                myS = S;
                 if (!a.eval_only) {
                     const uint32_t* row = a.theta_ent + off;
                     for (uint32_t t = t0; t < t1; ++t) {
@@ -470,10 +417,21 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                             if (retry) u = draw_u(a, gdoc, v, occ, (uint32_t)retry);
                             uint32_t cnt = 0;
                             if (__fmul_rn(u.b, __fadd_rn(S, Q)) < S) {
-                                const uint32_t i = min(first_above(seg, 4u * U, __fmul_rn(u.s, S)), nnz - 1u);
-                                const uint32_t e = __ldg(row + i);
-                                k = e & 0xffffu;
-                                cnt = e >> 16;
+                                const float target = __fmul_rn(u.s, S);
+                                const uint32_t g = min(first_above(seg, Up, target), U - 1u);
+                                float cum = g ? seg[g - 1u] : 0.f;
+                                const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + 4u * g));
+                                const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
+                                uint32_t pick = 0u, last = 0u;
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    cum += w_of(e4[i], smem);
+                                    if (e4[i] >> 16) last = e4[i];                  // pads (count 0) never picked
+                                    if (!pick && (e4[i] >> 16) && cum > target) pick = e4[i];
+                                }
+                                if (!pick) pick = last;                             // rounding guard
+                                k = topic_of(pick);
+                                cnt = pick >> 16;
                             } else {
                                 k = first_above(lvl0, (uint32_t)K, __fmul_rn(u.s, Q));
                                 if (k == zt) cnt = row_count(row, nnz, zt);
@@ -550,25 +508,25 @@ cudaError_t launch_validate(gf_shard* s) {
     return cudaGetLastError();
 }
 
-static size_t smem_for(const gf_shard* s, uint32_t capb) {
-    return (size_t)(((s->tree.total + 2 * s->K + 3) & ~3) + kWarps * capb) * sizeof(float);
+static size_t smem_for(const gf_shard* s, uint32_t capv) {
+    return (size_t)(lay_buf(s->K, s->tree.total) + kWarps * capv) * sizeof(float);
 }
 
-size_t sample_smem_bytes(const gf_shard* s) { return smem_for(s, kCapMax); }
+size_t sample_smem_bytes(const gf_shard* s) { return smem_for(s, kCapV); }
 
-template <uint32_t CAPB, int MINB, uint32_t VEC, bool HUGE>
+template <uint32_t CAPV, int MINB, uint32_t VEC, bool HUGE>
 static cudaError_t launch_variant(gf_shard* s, const SampleArgs& a) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(sample_kernel<CAPB, MINB, VEC, HUGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             220 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(sample_kernel<CAPV, MINB, VEC, HUGE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(sample_kernel<CAPB, MINB, VEC, HUGE>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        e = cudaFuncSetAttribute(sample_kernel<CAPV, MINB, VEC, HUGE>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    sample_kernel<CAPB, MINB, VEC, HUGE><<<(unsigned)s->n_slices, kSampleThreads, smem_for(s, CAPB), s->stream>>>(a);
+    sample_kernel<CAPV, MINB, VEC, HUGE><<<(unsigned)s->n_slices, kSampleThreads, smem_for(s, CAPV), s->stream>>>(a);
     return cudaGetLastError();
 }
 
@@ -598,24 +556,18 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
     a.ll_part = s->d.ll_part;
     a.errs = s->d.errs;
     a.bytes = s->d.bytes;
-    // staging-buffer size: 1024 entries (4 CTAs/SM) or 2048 (fewer, larger sub-batches)
-    // and vectors per lane per pass step (tuning knobs GF_CAPB / GF_VEC)
-    static int capb = -1, vec = -1;
-    if (capb < 0) {
-        const char* env = getenv("GF_CAPB");
-        capb = env ? atoi(env) : 1024;
-        env = getenv("GF_VEC");
-        vec = env ? atoi(env) : 2;
-    }
-    // rows can only outgrow the buffer when K > CAPB: otherwise the streaming
+    // tuning knob GF_VEC (vectors per lane per pass step); rows can only
+    // outgrow the staging buffer when K > 4*kCapV -- otherwise the streaming
     // path (a register-hungry call) is compiled out
-    if (capb >= 2048 || s->K > 1024) {
-        if (s->K > 2048) return launch_variant<2048, 2, 2, true>(s, a);
-        return vec >= 4 ? launch_variant<2048, 2, 4, false>(s, a) : launch_variant<2048, 2, 2, false>(s, a);
+    static int vec = -1;
+    if (vec < 0) {
+        const char* env = getenv("GF_VEC");
+        vec = env ? atoi(env) : 4;
     }
-    if (vec >= 4) return launch_variant<1024, 4, 4, false>(s, a);
-    if (vec == 1) return launch_variant<1024, 4, 1, false>(s, a);
-    return launch_variant<1024, 4, 2, false>(s, a);
+    if (s->K > (int)(4 * kCapV)) return launch_variant<kCapV, 3, 2, true>(s, a);
+    if (vec == 2) return launch_variant<kCapV, 4, 2, false>(s, a);
+    if (vec == 1) return launch_variant<kCapV, 4, 1, false>(s, a);
+    return launch_variant<kCapV, 4, 4, false>(s, a);
 }
 
 }  // namespace gf
