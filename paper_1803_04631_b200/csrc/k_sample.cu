@@ -367,15 +367,12 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                     e[i] = __ldg(src);
                 }
                 float p[VEC];                                               // prefix at each vector end
-                float acc = 0.f;
 #pragma unroll
-                for (int i = 0; i < VEC; ++i) {
-                    acc += w_of(e[i].x, smem);
-                    acc += w_of(e[i].y, smem);
-                    acc += w_of(e[i].z, smem);
-                    acc += w_of(e[i].w, smem);
-                    p[i] = acc;
-                }
+                for (int i = 0; i < VEC; ++i)                               // independent pair sums (ILP)
+                    p[i] = (w_of(e[i].x, smem) + w_of(e[i].y, smem)) + (w_of(e[i].z, smem) + w_of(e[i].w, smem));
+#pragma unroll
+                for (int i = 1; i < VEC; ++i) p[i] += p[i - 1];
+                const float acc = p[VEC - 1];
                 const int head = mle ? 31 - __clz(mle) : -1;                // my segment's first lane
                 const int lim = max(head, 0);
                 float x = acc;
@@ -562,12 +559,13 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
     static int vec = -1;
     if (vec < 0) {
         const char* env = getenv("GF_VEC");
-        vec = env ? atoi(env) : 4;
+        vec = env ? atoi(env) : 2;
     }
     if (s->K > (int)(4 * kCapV)) return launch_variant<kCapV, 3, 2, true>(s, a);
-    if (vec == 2) return launch_variant<kCapV, 4, 2, false>(s, a);
+    if (vec == 4) return launch_variant<kCapV, 4, 4, false>(s, a);
+    if (vec == 5) return launch_variant<kCapV, 5, 2, false>(s, a);   // 5 CTAs/SM (51 registers)
     if (vec == 1) return launch_variant<kCapV, 4, 1, false>(s, a);
-    return launch_variant<kCapV, 4, 4, false>(s, a);
+    return launch_variant<kCapV, 4, 2, false>(s, a);
 }
 
 }  // namespace gf
