@@ -18,7 +18,7 @@ token-keyed Philox stream the trained model is identical for every G.
 """
 
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 from typing import Optional
 
 import numpy as np
@@ -94,7 +94,10 @@ def _dist():
 class Trainer:
     """Device-resident trainer for this rank's shard."""
 
-    def __init__(self, corpus, cfg, group=None, device=None, shard_factory=None):
+    def __init__(self, corpus, cfg, group=None, device=None, shard_factory=None, init_assignments=None):
+        """init_assignments: optional uint16 topics for this rank's chunk (word-group
+        order) replacing partition()'s Stream(seed, chunk_id) draw -- e.g. to resume
+        from a chunk store, or to start G ranks from the state of another G."""
         self.cfg = cfg
         self.corpus = corpus
         self.group = group
@@ -108,6 +111,11 @@ class Trainer:
         lo, hi = greedy_boundaries(corpus.doc_lengths, self.world)[self.rank]
         a, b = int(corpus.doc_ptr[lo]), int(corpus.doc_ptr[hi])
         self.chunk = make_chunk(self.rank, lo, hi, corpus.doc_ids[a:b], corpus.word_ids[a:b], V, K, cfg.seed)
+        if init_assignments is not None:
+            z0 = np.ascontiguousarray(init_assignments, dtype=np.uint16)
+            if z0.shape != (self.chunk.token_count,):
+                raise ShapeMismatchError(f"init_assignments has {z0.size} entries, shard has {self.chunk.token_count}")
+            self.chunk = replace(self.chunk, assignments=z0)
         freq = np.bincount(self.chunk.word_ids, minlength=V).astype(np.int64)
         self.global_freq = self._allreduce_np(freq)
         if device is None:

@@ -399,3 +399,68 @@ def test_sample_chunk_api():
     want = oracle.sample_tokens(K, corp.vocab_size, 50.0 / K, 0.01, 5, 1, ch.doc_ids, ch.word_ids,
                                 ch.assignments, 0, rp, ids, cn, phi.counts, phi.topic_totals, mode="thin")
     assert np.mean(z1 == want) > 0.998
+
+
+def test_two_device_shards_with_summed_sync_buffers_match_one_shard():
+    """The multi-GPU protocol on one GPU: two shards (greedy_boundaries, C=2),
+    replicas summed elementwise through their int32 sync-buffer views (what the
+    NCCL allreduce does), K3 after the sum -- the model equals one shard's."""
+    import torch
+
+    K, iters = 32, 3
+    corp = synth.generate(500, 800, 60.0, seed=21)
+    two = cp.partition(corp, 2, K, 11)
+    freq = np.bincount(corp.word_ids, minlength=corp.vocab_size)
+    words = np.concatenate([c.word_ids for c in two])
+    z0 = np.concatenate([c.assignments for c in two])[np.argsort(words, kind="stable")]
+    one = cp.partition(corp, 1, K, 11)[0]
+    from dataclasses import replace
+    one = replace(one, assignments=z0)
+    a, b = 50.0 / K, 0.01
+    shards = [DeviceShard(K, corp.vocab_size, a, b, seed=5, global_word_freq=freq, heavy_threshold=30).load(c)
+              for c in two]
+    single = DeviceShard(K, corp.vocab_size, a, b, seed=5, global_word_freq=freq, heavy_threshold=30).load(one)
+
+    def allreduce():
+        for s in shards:
+            s.synchronize()
+        ts = [s.sync_tensor() for s in shards]
+        tot = ts[0] + ts[1]
+        for t in ts:
+            t.copy_(tot)
+        torch.cuda.synchronize()
+
+    for s in shards:
+        s.rebuild_phi()
+    allreduce()
+    for s in shards:
+        s.prepare()
+        s.rebuild_theta()
+    single.initialize()
+    for it in range(iters):
+        for s in shards:
+            s.sample(it)
+        single.sample(it)
+        ll2 = sum(s.loglik_sum() for s in shards)
+        assert ll2 == pytest.approx(single.loglik_sum(), rel=1e-9)
+        for s in shards:
+            s.rebuild_phi()
+        allreduce()
+        for s in shards:
+            s.rebuild_theta()
+            s.prepare()
+        single.rebuild_phi()
+        single.prepare()
+        single.rebuild_theta()
+    p2, t2 = shards[0].get_phi()
+    p1, t1 = single.get_phi()
+    np.testing.assert_array_equal(p2, p1)
+    np.testing.assert_array_equal(t2, t1)
+    np.testing.assert_array_equal(shards[1].get_phi()[0], p1)
+    th = md.concat_theta([md.ThetaRows(*s.get_theta(), K) for s in shards])
+    rp, ids, cn = single.get_theta()
+    np.testing.assert_array_equal(th.row_ptr, rp)
+    np.testing.assert_array_equal(th.topic_ids, ids)
+    np.testing.assert_array_equal(th.counts, cn)
+    for s in shards + [single]:
+        s.close()
