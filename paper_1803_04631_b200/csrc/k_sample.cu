@@ -345,49 +345,27 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
             // ---- 1. entry-parallel pass: segmented prefix of p1 over the concatenated rows ----
             // each lane owns VEC consecutive vectors (4*VEC entries) of ONE row per step
             // (rows are laid out VEC-aligned), so 128*VEC entries advance per warp step
-            // software pipeline: step s+1's vectors are in flight while step s is
-            // summed, scanned and staged
+            int cprev = first - 1;                                          // run holding vector q0-1
             float carry = 0.f;
-            uint32_t q0 = 0;
-            unsigned mle;
-            int ri;
-            uint4 e[VEC];
-            {
-                const uint32_t hb = (sel && vo < 32u * VEC) ? (1u << (vo / VEC)) : 0u;
-                mle = __reduce_or_sync(kFull, hb) & lane_le;                // run heads up to my lane
-                ri = min(first - 1 + __popc(mle), 31);                      // run owning my vectors
-                const uint32_t rel = VEC * (uint32_t)lane - __shfl_sync(kFull, vo, ri);
-                const uint32_t roff = __shfl_sync(kFull, off, ri), rU = __shfl_sync(kFull, U, ri);
-                const bool act = VEC * (uint32_t)lane < Utot;
-#pragma unroll
-                for (int i = 0; i < VEC; ++i)
-                    e[i] = __ldg((act && rel + i < rU) ? reinterpret_cast<const uint4*>(a.theta_ent + roff + 4u * (rel + i))
-                                                       : &g_zero16);
-            }
-            while (q0 < Utot) {
+            for (uint32_t q0 = 0; q0 < Utot; q0 += 32u * VEC) {
+                const uint32_t hb = (sel && vo - q0 < 32u * VEC) ? (1u << ((vo - q0) / VEC)) : 0u;
+                const unsigned M = __reduce_or_sync(kFull, hb);           // run heads in this step
+                const unsigned mle = M & lane_le;
+                const int ri = min(cprev + __popc(mle), 31);
+                const uint32_t rvo = __shfl_sync(kFull, vo, ri);
+                const uint32_t roff = __shfl_sync(kFull, off, ri);
+                const uint32_t rU = __shfl_sync(kFull, U, ri);
                 const uint32_t qL = q0 + VEC * (uint32_t)lane;
+                const uint32_t rel = qL - rvo;                              // vector index inside the row
                 const bool act = qL < Utot;
-                // ---- issue step s+1 ----
-                const uint32_t q1 = q0 + 32u * VEC;
-                const int cprev1 = __shfl_sync(kFull, ri, 31);
-                unsigned mle1 = 0;
-                int ri1 = cprev1;
-                uint4 e1[VEC];
-                if (q1 < Utot) {
-                    const uint32_t hb = (sel && vo - q1 < 32u * VEC) ? (1u << ((vo - q1) / VEC)) : 0u;
-                    mle1 = __reduce_or_sync(kFull, hb) & lane_le;
-                    ri1 = min(cprev1 + __popc(mle1), 31);
-                    const uint32_t qL1 = q1 + VEC * (uint32_t)lane;
-                    const uint32_t rel = qL1 - __shfl_sync(kFull, vo, ri1);
-                    const uint32_t roff = __shfl_sync(kFull, off, ri1), rU = __shfl_sync(kFull, U, ri1);
-                    const bool act1 = qL1 < Utot;
+                uint4 e[VEC];
 #pragma unroll
-                    for (int i = 0; i < VEC; ++i)
-                        e1[i] = __ldg((act1 && rel + i < rU)
-                                          ? reinterpret_cast<const uint4*>(a.theta_ent + roff + 4u * (rel + i))
-                                          : &g_zero16);
+                for (int i = 0; i < VEC; ++i) {
+                    const uint4* src = (act && rel + i < rU)
+                                           ? reinterpret_cast<const uint4*>(a.theta_ent + roff + 4u * (rel + i))
+                                           : &g_zero16;
+                    e[i] = __ldg(src);
                 }
-                // ---- process step s ----
                 float p[VEC];                                               // prefix at each vector end
 #pragma unroll
                 for (int i = 0; i < VEC; ++i)                               // independent pair sums (ILP)
@@ -417,12 +395,7 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                     }
                 }
                 carry = __shfl_sync(kFull, p[VEC - 1], 31);
-                // ---- rotate ----
-                q0 = q1;
-                mle = mle1;
-                ri = ri1;
-#pragma unroll
-                for (int i = 0; i < VEC; ++i) e[i] = e1[i];
+                cprev = __shfl_sync(kFull, ri, 31);
             }
             __syncwarp();
             // ---- 2. run-parallel draws: lane j samples the tokens of run j ----
