@@ -372,7 +372,8 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
         const int64_t L = dw_ptr[d + 1] - dw_ptr[d];
         if (L < 0) return fail(GF_ERR_SHAPE, "doc-word map not monotone");
         meta[d] = make_uint2((uint32_t)cap, 0u);
-        cap += (uint64_t)((std::min<int64_t>(K, L) + 3) & ~3LL);
+        // 8-entry (32-byte) granules: K1 streams rows with 256-bit loads
+        cap += (uint64_t)((std::min<int64_t>(K, L) + 7) & ~7LL);
         if (L > 0) llc += (double)L * std::log((double)L + (double)K * s->alpha);
         if (cap >= (uint64_t)UINT32_MAX) return fail(GF_ERR_CAPACITY, "theta rows exceed 2^32 entries");
     }

@@ -159,9 +159,9 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
             if (mx > 65535u && lane == 0) atomicMin(errs + 1, ((unsigned long long)d << 32) | mx);
             __syncwarp();
         }
-        // zero the row's padding up to a multiple of 4 entries: K1 reads rows
-        // as 16-byte vectors and relies on (count 0) pads contributing nothing
-        if ((uint32_t)lane < ((4u - (nnz & 3u)) & 3u)) theta_ent[off + nnz + lane] = 0u;
+        // zero the row's padding up to a multiple of 8 entries: K1 reads rows
+        // as 32-byte granules and relies on (count 0) pads contributing nothing
+        if ((uint32_t)lane < ((8u - (nnz & 7u)) & 7u)) theta_ent[off + nnz + lane] = 0u;
         if (lane == 0) theta_meta[d].y = nnz;
     }
 }
@@ -233,7 +233,7 @@ __global__ void theta_import_kernel(int D, uint2* meta, uint32_t* ent, const int
         const int64_t o = rowptr[d], n = rowptr[d + 1] - o;
         const uint32_t base = meta[d].x;
         for (int64_t j = lane; j < n; j += 32) ent[base + j] = ((uint32_t)ids[o + j] << 2) | ((uint32_t)cnt[o + j] << 16);
-        if (lane < ((4 - (n & 3)) & 3)) ent[base + n + lane] = 0u;   // zero pads (see K3)
+        if (lane < ((8 - (n & 7)) & 7)) ent[base + n + lane] = 0u;   // zero pads (see K3)
         if (lane == 0) meta[d].y = (uint32_t)n;
     }
 }

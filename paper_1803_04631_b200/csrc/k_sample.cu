@@ -44,6 +44,14 @@ constexpr uint32_t kCapV = 1024;      // staged vector-end prefixes per warp (40
 constexpr int kMaxRetry = 63;
 
 __device__ const uint4 g_zero16 = {0u, 0u, 0u, 0u};   // load target of idle lanes
+__device__ __align__(32) const uint32_t g_zero32[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+
+// 256-bit read-only global load (sm_100: LDG.E.ENL2.256); p must be 32-byte aligned
+__device__ __forceinline__ void ldg256(const uint32_t* p, uint4& lo, uint4& hi) {
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                 : "l"(p));
+}
 
 struct SampleArgs {
     int K, Kp;
@@ -359,12 +367,19 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                 const uint32_t rel = qL - rvo;                              // vector index inside the row
                 const bool act = qL < Utot;
                 uint4 e[VEC];
+                if (VEC == 2) {
+                    // one 256-bit load per lane: the warp reads 1 KB contiguous per step
+                    // (rows are 32-byte aligned and zero-padded to 8 entries by K3)
+                    const uint32_t* src = act ? a.theta_ent + roff + 4u * rel : &g_zero32[0];
+                    ldg256(src, e[0], e[VEC - 1]);
+                } else {
 #pragma unroll
-                for (int i = 0; i < VEC; ++i) {
-                    const uint4* src = (act && rel + i < rU)
-                                           ? reinterpret_cast<const uint4*>(a.theta_ent + roff + 4u * (rel + i))
-                                           : &g_zero16;
-                    e[i] = __ldg(src);
+                    for (int i = 0; i < VEC; ++i) {
+                        const uint4* src = (act && rel + i < rU)
+                                               ? reinterpret_cast<const uint4*>(a.theta_ent + roff + 4u * (rel + i))
+                                               : &g_zero16;
+                        e[i] = __ldg(src);
+                    }
                 }
                 float p[VEC];                                               // prefix at each vector end
 #pragma unroll
@@ -389,6 +404,8 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                 if (act) {
                     if (VEC == 4) {
                         *reinterpret_cast<float4*>(buf + qL) = make_float4(p[0], p[1 % VEC], p[2 % VEC], p[3 % VEC]);
+                    } else if (VEC == 2) {
+                        *reinterpret_cast<float2*>(buf + qL) = make_float2(p[0], p[1 % VEC]);   // conflict-free
                     } else {
 #pragma unroll
                         for (int i = 0; i < VEC; ++i) buf[qL + i] = p[i];
