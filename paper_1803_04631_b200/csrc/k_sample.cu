@@ -12,18 +12,19 @@
 // byte offset (count << 16 | topic << 2), so a p1 term is one LOP + LDS + FFMA.
 //
 // Work: each warp pulls batches of up to 32 (doc, word) RUNS (lane j owns run
-// j: its doc, token range, theta row and the Philox4x32-10 uniforms of its
-// first token) and handles them as segmented sub-batches:
+// j: its doc, token range and theta row) and handles them as segmented
+// sub-batches:
 //   1. entry-parallel pass: the sub-batch's theta rows (16-byte vectors,
 //      zero-padded to 4 entries) are streamed as one concatenated array, VEC
 //      vectors per lane and 128*VEC entries per warp step; p1 = theta * p* is
 //      prefix-summed by a segmented __shfl scan (segment heads from one
 //      __reduce_or_sync) and the prefix at every vector end is staged in the
 //      warp's shared buffer -- S of every run falls out as a segment total;
-//   2. run-parallel draws: lane j samples the tokens of run j -- branch on
-//      u (S+Q) < S, then a branch-free binary search over its staged vector
-//      ends and a 4-entry walk of the chosen vector (S part), or a binary
-//      search of the Q-tree level 0 (Q part).
+//   2. token-parallel draws: the sub-batch's tokens are one contiguous range;
+//      lane l draws token base + l (its run found from a run-head bitmap),
+//      branch u (S+Q) < S, then ONE branch-free binary search -- over the
+//      run's staged vector ends (S part, followed by a 4-entry walk of the
+//      chosen vector) or over the Q-tree level 0 (Q part).
 // Rows longer than the staging buffer (K > 4096 only) take a warp-cooperative
 // streaming path.  Exclusion (theta_dz-1, phi_vz-1, n_z-1)
 // is applied by thinning: draw k from the exclusion-free S+Q mixture; if
@@ -94,8 +95,13 @@ __device__ __forceinline__ U3 draw_u(const SampleArgs& a, uint32_t gdoc, uint32_
 }
 
 // p1 term of one theta entry (count << 16 | topic << 2) against p* at shared offset 0
+// The count converts without the quarter-rate I2F: one PRMT builds the float
+// 2^23 + count (count in the low mantissa bits), one FADD removes 2^23 (exact).
+__device__ __forceinline__ float count_f(uint32_t e) {
+    return __int_as_float(__byte_perm(e, 0x4B000000u, 0x7432)) - 8388608.f;
+}
 __device__ __forceinline__ float w_of(uint32_t e, const float* smem) {
-    return (float)(e >> 16) * smem[(e & 0xfffcu) >> 2];
+    return count_f(e) * smem[(e & 0xfffcu) >> 2];
 }
 __device__ __forceinline__ uint32_t topic_of(uint32_t e) { return (e & 0xffffu) >> 2; }
 
@@ -149,7 +155,7 @@ __device__ __forceinline__ bool keep_own(float ut, uint32_t cnt, float alpha, fl
 // Rows longer than the staging buffer: warp-cooperative, one run, the S part
 // re-streamed per S-branch draw.  Returns S (all lanes).
 __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, float Q, uint32_t v, uint32_t gdoc,
-                                       uint32_t t0, uint32_t t1, uint32_t off, uint32_t nnz, U3 u0, int lane) {
+                                       uint32_t t0, uint32_t t1, uint32_t off, uint32_t nnz, int lane) {
     const float* pstar = smem;
     const float* pex = smem + a.K;
     const float* lvl = smem + lay_tree(a.K);
@@ -168,10 +174,9 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, f
     for (uint32_t t = t0; t < t1; ++t) {
         const uint32_t zt = a.z[t];
         const uint32_t occ = t - t0;
-        U3 u = occ ? draw_u(a, gdoc, v, occ, 0u) : u0;
         uint32_t k = zt;
         for (int retry = 0; retry <= kMaxRetry; ++retry) {
-            if (retry) u = draw_u(a, gdoc, v, occ, (uint32_t)retry);
+            const U3 u = draw_u(a, gdoc, v, occ, (uint32_t)retry);
             uint32_t cnt = 0;
             if (__fmul_rn(u.b, __fadd_rn(S, Q)) < S) {
                 const float target = __fmul_rn(u.s, S);
@@ -316,19 +321,15 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
         const uint32_t U = max(1u, (nnz + 3u) >> 2);          // row length in 16-byte vectors
         const uint32_t Up = (U + VEC - 1u) / VEC * VEC;       // ... padded to whole lanes
         const bool huge = HUGE && valid && Up > CAPV;         // only possible when K > 4*CAPV
-        U3 u0{0.f, 0.f, 0.f};
-        if (valid && !a.eval_only) u0 = draw_u(a, gdoc, v, 0u, 0u);
         float myS = 0.f;                                       // S of this lane's run
         unsigned rem = __ballot_sync(kFull, valid);
         const unsigned hmask = __ballot_sync(kFull, huge);
         while (rem) {
             const int first = __ffs(rem) - 1;
             if (HUGE && ((hmask >> first) & 1u)) {             // rare: row beyond the buffer
-                const U3 hu{__shfl_sync(kFull, u0.b, first), __shfl_sync(kFull, u0.s, first),
-                            __shfl_sync(kFull, u0.t, first)};
                 const float S = huge_run(a, smem, Q, v, __shfl_sync(kFull, gdoc, first),
                                          __shfl_sync(kFull, t0, first), __shfl_sync(kFull, t1, first),
-                                         __shfl_sync(kFull, off, first), __shfl_sync(kFull, nnz, first), hu, lane);
+                                         __shfl_sync(kFull, off, first), __shfl_sync(kFull, nnz, first), lane);
                 if (lane == first) myS = S;
                 rem &= rem - 1u;
                 continue;
@@ -415,24 +416,44 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                 cprev = __shfl_sync(kFull, ri, 31);
             }
             __syncwarp();
-            // ---- 2. run-parallel draws: lane j samples the tokens of run j ----
-            if (sel) {
-                const float* seg = buf + vo;
-                const float S = seg[Up - 1u];                              // segment total (pads add 0)
-                myS = S;
-                if (!a.eval_only) {
-                    const uint32_t* row = a.theta_ent + off;
-                    for (uint32_t t = t0; t < t1; ++t) {
+            if (sel) myS = buf[vo + Up - 1u];                              // segment total (pads add 0)
+            // ---- 2. token-parallel draws over the sub-batch's tokens ----
+            // The selected runs are consecutive runs of one word, so their tokens
+            // are one contiguous range; lane l takes token base + l and finds its
+            // run (owner lane) from a run-head bitmap, as the pass finds rows.
+            // One search serves both branches (S: the owner's staged vector ends,
+            // Q: the tree's level 0), so S and Q lanes do not diverge.
+            if (!a.eval_only) {
+                const uint32_t tend = __shfl_sync(kFull, t1, lastl);
+                int cown = first - 1;                                       // run holding token base-1
+                for (uint32_t base = __shfl_sync(kFull, t0, first); base < tend; base += 32u) {
+                    const uint32_t th = (sel && t0 - base < 32u) ? (1u << (t0 - base)) : 0u;
+                    const unsigned M = __reduce_or_sync(kFull, th);
+                    const int own = min(cown + __popc(M & lane_le), 31);
+                    const uint32_t ot0 = __shfl_sync(kFull, t0, own);
+                    const uint32_t odoc = __shfl_sync(kFull, gdoc, own);
+                    const uint32_t ooff = __shfl_sync(kFull, off, own);
+                    const uint32_t ovo = __shfl_sync(kFull, vo, own);
+                    const uint32_t onnz = __shfl_sync(kFull, nnz, own);
+                    cown = __shfl_sync(kFull, own, 31);
+                    const uint32_t t = base + (uint32_t)lane;
+                    if (t < tend) {
+                        const uint32_t oU = max(1u, (onnz + 3u) >> 2);
+                        const uint32_t oUp = (oU + VEC - 1u) / VEC * VEC;
+                        const float* seg = buf + ovo;
+                        const float S = seg[oUp - 1u];
+                        const uint32_t* row = a.theta_ent + ooff;
                         const uint32_t zt = a.z[t];
-                        const uint32_t occ = t - t0;
-                        U3 u = occ ? draw_u(a, gdoc, v, occ, 0u) : u0;
+                        const uint32_t occ = t - ot0;
                         uint32_t k = zt;
                         for (int retry = 0; retry <= kMaxRetry; ++retry) {
-                            if (retry) u = draw_u(a, gdoc, v, occ, (uint32_t)retry);
+                            const U3 u = draw_u(a, odoc, v, occ, (uint32_t)retry);
+                            const bool isS = __fmul_rn(u.b, __fadd_rn(S, Q)) < S;
+                            const float target = __fmul_rn(u.s, isS ? S : Q);
+                            uint32_t g = first_above(isS ? seg : lvl0, isS ? oUp : (uint32_t)K, target);
                             uint32_t cnt = 0;
-                            if (__fmul_rn(u.b, __fadd_rn(S, Q)) < S) {
-                                const float target = __fmul_rn(u.s, S);
-                                const uint32_t g = min(first_above(seg, Up, target), U - 1u);
+                            if (isS) {
+                                g = min(g, oU - 1u);
                                 float cum = g ? seg[g - 1u] : 0.f;
                                 const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + 4u * g));
                                 const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
@@ -447,8 +468,8 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                                 k = topic_of(pick);
                                 cnt = pick >> 16;
                             } else {
-                                k = first_above(lvl0, (uint32_t)K, __fmul_rn(u.s, Q));
-                                if (k == zt) cnt = row_count(row, nnz, zt);
+                                k = g;
+                                if (k == zt) cnt = row_count(row, onnz, zt);
                             }
                             if (k != zt) break;
                             if (zt >= (uint32_t)K || cnt == 0u || pex[zt] == 0.f) {   // inconsistent state
