@@ -380,6 +380,8 @@ def run_ours(args, world, rank, local):
                 "tokens_total": T_all, "topics": K, "iterations": [args.warmup, args.warmup + args.steps],
                 "parallelism": f"doc-shard dp{world} + NCCL allreduce of phi" if world > 1 else "dp1",
                 "l2": "inputs larger than L2 (z 2T B, theta 4*NNZ B, phi >= 200 MB vs 126 MB L2)",
+                "runs": st["runs"], "slices": st["slices"], "word_contexts": st["word_contexts"],
+                "doc_blocks": st["doc_blocks"],
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic["bytes_per_launch"] if traffic else None,

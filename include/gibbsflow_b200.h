@@ -152,7 +152,8 @@ int gf_shard_phi_argmax(gf_shard* shard, int64_t* max_count, int32_t* topic, int
 /* live counters for the roofline: stats[0] = K1 algorithmic bytes per sample
  * launch (averaged over the launches since the last reset), [1] = K2 bytes,
  * [2] = K3 bytes, [3] = runs, [4] = slices, [5] = tokens, [6] = theta nnz,
- * [7] = kernels launched by gf_shard_iterate, [8] = sample launches since reset. */
+ * [7] = kernels launched by gf_shard_iterate, [8] = sample launches since reset,
+ * [9] = precomputed word contexts, [10] = document blocks of the slice schedule. */
 int gf_shard_stats(gf_shard* shard, int64_t* stats, int num_stats);
 int gf_shard_reset_stats(gf_shard* shard);
 /* CUDA-event time (ms) of the kernels of the last gf_shard_iterate:

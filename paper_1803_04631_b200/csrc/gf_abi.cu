@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -42,6 +43,11 @@ int cuda_fail(cudaError_t e, const char* what) {
     } while (0)
 
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+
+int64_t env_int(const char* name, int64_t dflt) {  // tuning knobs (A/B runs)
+    const char* e = getenv(name);
+    return e && *e ? atoll(e) : dflt;
+}
 
 inline uint64_t fin64(uint64_t z) {  // rng.py:20-26
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -78,7 +84,8 @@ int dev_alloc(T** p, size_t count, const char* what) {
 void free_dev(gf_shard* s) {
     auto& d = s->d;
     void* ptrs[] = {d.z, d.run_doc, d.run_start, d.slices, d.k2items, d.dw_ptr, d.dw_tok, d.theta_ent,
-                    d.theta_meta, d.sync, d.inv_den, d.ll_part, d.ll_sum, d.errs, d.bytes, d.scratch};
+                    d.theta_meta, d.sync, d.inv_den, d.ctx_tab, d.ctx_cols, d.slice_ctx, d.ll_part, d.ll_sum,
+                    d.errs, d.bytes, d.scratch};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     d = gf::ShardDev{};
@@ -328,13 +335,38 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
         }
     const int64_t R = (int64_t)run_doc.size();
     run_start.push_back((uint32_t)T);
+    // ---- document blocks: contiguous doc ranges whose theta rows fit in L2 ----
+    // K1 reads one theta row per (doc, word) run; scheduling the slices of all
+    // frequent words block by block keeps the rows being read L2-resident, so
+    // each row comes from HBM about once per block instead of once per run.
+    const int64_t blk_bytes = (int64_t)env_int("GF_DOCBLOCK_MB", 64) << 20;
+    const int64_t min_runs = env_int("GF_SLICE_MINRUNS", 1024);
+    std::vector<int32_t> doc_blk((size_t)D);
+    int32_t nblk = 0;
+    {
+        int64_t acc = 0;
+        for (int64_t d = 0; d < D; ++d) {
+            const int64_t L = dw_ptr[d + 1] - dw_ptr[d];
+            const int64_t b = 4 * ((std::min<int64_t>(K, L) + 7) & ~7LL);
+            if (acc > 0 && acc + b > blk_bytes) { ++nblk; acc = 0; }
+            doc_blk[d] = nblk;
+            acc += b;
+        }
+        ++nblk;
+    }
     // ---- heavy-first slices (sort_word_groups_desc order, corpus.py:290-302) ----
+    // A slice is <= kSliceTokens tokens of one word; a frequent word is also cut
+    // at document-block boundaries (pieces of >= min_runs runs).  Slices are then
+    // ordered block-major (stable: heavy-first inside a block); slices spanning
+    // several blocks (rare words: random rows anyway) are spread round-robin.
     std::vector<int64_t> order((size_t)ng);
     std::iota(order.begin(), order.end(), 0);
     std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
         return gs[a] != gs[b] ? gs[a] > gs[b] : gw[a] < gw[b];
     });
     std::vector<int4> slices, items;
+    std::vector<int32_t> slice_key;
+    int64_t rr = 0;
     for (int64_t gi : order) {
         if (gs[gi] == 0) continue;
         const int32_t v = gw[gi];
@@ -343,10 +375,16 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
         int64_t rb = std::lower_bound(run_start.begin(), run_start.end() - 1, (uint32_t)t0) - run_start.begin();
         const int64_t re = std::lower_bound(run_start.begin(), run_start.end() - 1, (uint32_t)t1) - run_start.begin();
         const size_t first = slices.size();
+        const bool blocked = nblk > 1 && re - rb >= 2 * min_runs;
         while (rb < re) {
+            const int32_t b0 = doc_blk[run_doc[rb]];
             int64_t r = rb;
-            while (r < re && (int64_t)run_start[r] - (int64_t)run_start[rb] < gf::kSliceTokens) ++r;
+            while (r < re && (int64_t)run_start[r] - (int64_t)run_start[rb] < gf::kSliceTokens &&
+                   !(blocked && r - rb >= min_runs && doc_blk[run_doc[r]] != b0 && re - r >= min_runs))
+                ++r;
             slices.push_back(make_int4(v, (int)rb, (int)r, col));
+            const bool local = doc_blk[run_doc[r - 1]] - b0 <= 1;
+            slice_key.push_back(local ? b0 : (int32_t)(rr++ % nblk));
             rb = r;
         }
         if (col >= 0) {
@@ -357,6 +395,31 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
                 items.push_back(make_int4(col, (int)run_start[slices[i].y], (int)run_start[slices[i].z], split ? 1 : 0));
         }
     }
+    // word contexts: one per word cut into several slices (built once per iteration)
+    std::vector<int32_t> slice_ctx(slices.size(), -1), ctx_cols;
+    {
+        size_t i = 0;
+        while (i < slices.size()) {
+            size_t j = i;
+            while (j < slices.size() && slices[j].x == slices[i].x) ++j;
+            if (j - i > 1) {
+                for (size_t q = i; q < j; ++q) slice_ctx[q] = (int32_t)ctx_cols.size();
+                ctx_cols.push_back(slices[i].w);
+            }
+            i = j;
+        }
+    }
+    {
+        std::vector<int64_t> so(slices.size());
+        std::iota(so.begin(), so.end(), 0);
+        std::stable_sort(so.begin(), so.end(), [&](int64_t a, int64_t b) { return slice_key[a] < slice_key[b]; });
+        std::vector<int4> sorted(slices.size());
+        std::vector<int32_t> sctx(slices.size());
+        for (size_t i = 0; i < so.size(); ++i) { sorted[i] = slices[so[i]]; sctx[i] = slice_ctx[so[i]]; }
+        slices.swap(sorted);
+        slice_ctx.swap(sctx);
+    }
+    s->n_doc_blocks = nblk;
     if ((int64_t)slices.size() >= (int64_t)INT32_MAX) return fail(GF_ERR_CAPACITY, "too many slices");
     // ---- doc-word map and theta capacities ----
     std::vector<uint32_t> dwp((size_t)D + 1), dwt((size_t)T);
@@ -387,7 +450,10 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
         (rc = dev_alloc(&dv.k2items, items.size(), "items")) || (rc = dev_alloc(&dv.dw_ptr, D + 1, "dw_ptr")) ||
         (rc = dev_alloc(&dv.dw_tok, T, "dw_tok")) || (rc = dev_alloc(&dv.theta_ent, cap + 4, "theta")) ||
         (rc = dev_alloc(&dv.theta_meta, D, "theta")) || (rc = dev_alloc(&dv.sync, s->sync_u32, "phi")) ||
-        (rc = dev_alloc(&dv.inv_den, K, "inv_den")) || (rc = dev_alloc(&dv.ll_part, slices.size(), "ll")) ||
+        (rc = dev_alloc(&dv.inv_den, 2 * K, "inv_den")) ||
+        (rc = dev_alloc(&dv.ctx_tab, ctx_cols.size() * (size_t)gf::context_floats(s), "contexts")) ||
+        (rc = dev_alloc(&dv.ctx_cols, ctx_cols.size(), "contexts")) ||
+        (rc = dev_alloc(&dv.slice_ctx, slices.size(), "contexts")) || (rc = dev_alloc(&dv.ll_part, slices.size(), "ll")) ||
         (rc = dev_alloc(&dv.ll_sum, 1, "ll")) || (rc = dev_alloc(&dv.errs, 2, "errs")) ||
         (rc = dev_alloc(&dv.bytes, 1, "bytes")))
         return rc;
@@ -396,6 +462,9 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
     CU(cudaMemcpyAsync(dv.run_doc, run_doc.data(), R * 4, cudaMemcpyHostToDevice, st), "upload");
     CU(cudaMemcpyAsync(dv.run_start, run_start.data(), (R + 1) * 4, cudaMemcpyHostToDevice, st), "upload");
     CU(cudaMemcpyAsync(dv.slices, slices.data(), slices.size() * sizeof(int4), cudaMemcpyHostToDevice, st), "upload");
+    if (!ctx_cols.empty())
+        CU(cudaMemcpyAsync(dv.ctx_cols, ctx_cols.data(), ctx_cols.size() * 4, cudaMemcpyHostToDevice, st), "upload");
+    CU(cudaMemcpyAsync(dv.slice_ctx, slice_ctx.data(), slice_ctx.size() * 4, cudaMemcpyHostToDevice, st), "upload");
     CU(cudaMemcpyAsync(dv.k2items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, st), "upload");
     CU(cudaMemcpyAsync(dv.dw_ptr, dwp.data(), (D + 1) * 4, cudaMemcpyHostToDevice, st), "upload");
     CU(cudaMemcpyAsync(dv.dw_tok, dwt.data(), T * 4, cudaMemcpyHostToDevice, st), "upload");
@@ -412,6 +481,8 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
     s->R = R;
     s->n_slices = (int64_t)slices.size();
     s->n_k2 = (int64_t)items.size();
+    s->n_ctx = (int64_t)ctx_cols.size();
+    s->ctx_dirty = true;
     s->theta_cap = (int64_t)cap;
     s->loaded = true;
     return GF_OK;
@@ -717,8 +788,9 @@ int gf_shard_stats(gf_shard* s, int64_t* st, int n) {
     int64_t nnz = 0;
     if (n > 2) gf_shard_theta_nnz(s, &nnz);
     const int64_t b_theta = s->T * (4 + 2) + (s->D + 1) * 4 + s->D * 8 + nnz * 4;
-    int64_t v[9] = {b_sample, b_phi, b_theta, s->R, s->n_slices, s->T, nnz, s->stat_launches, s->stat_sample_launches};
-    for (int i = 0; i < n && i < 9; ++i) st[i] = v[i];
+    int64_t v[11] = {b_sample, b_phi,    b_theta, s->R, s->n_slices, s->T, nnz, s->stat_launches, s->stat_sample_launches,
+                     s->n_ctx,  s->n_doc_blocks};
+    for (int i = 0; i < n && i < 11; ++i) st[i] = v[i];
     return GF_OK;
 }
 

@@ -54,6 +54,17 @@ __device__ __forceinline__ uint32_t warp_bitonic_sort(uint32_t key, int lane) {
     return key;
 }
 
+// Transposed topic layout of K1's shared-memory p* table: topic t lives in
+// float slot tpos(t) = (t % m) * 32 + t / m, m = ceil(K / 32), i.e. its bank
+// is t / m (the topic's high bits).  A theta row is sorted by topic, so the
+// lanes of one gather (entries 8 apart in the row) hit distinct banks; with
+// the natural layout (bank = t % 32) they collide like random addresses.
+// Theta entries store tpos(t) << 2 (a byte offset) in their low 16 bits.
+__host__ __device__ inline uint32_t tpos_m(int K) { return (uint32_t)(K + 31) / 32u; }
+__host__ __device__ inline uint32_t tpos_slots(int K) { return 32u * tpos_m(K); }
+__device__ __forceinline__ uint32_t tpos(uint32_t t, uint32_t m) { return (t % m) * 32u + t / m; }
+__device__ __forceinline__ uint32_t tpos_inv(uint32_t p, uint32_t m) { return (p & 31u) * m + (p >> 5); }
+
 __device__ __forceinline__ float prev_float(float x) { return __int_as_float(__float_as_int(x) - 1); }
 
 }  // namespace gf

@@ -44,7 +44,10 @@ struct ShardDev {
     uint32_t* theta_ent = nullptr;
     uint2* theta_meta = nullptr;
     uint32_t* sync = nullptr;
-    float* inv_den = nullptr;
+    float* inv_den = nullptr;                // [2K]: 1/(n_k + V b), 1/(n_k - 1 + V b)
+    float* ctx_tab = nullptr;                // [n_ctx][ctx_stride] word contexts
+    int32_t* ctx_cols = nullptr;             // [n_ctx] phi column of each context's word
+    int32_t* slice_ctx = nullptr;            // [N] context of each slice (-1: built in place)
     double* ll_part = nullptr;
     double* ll_sum = nullptr;
     unsigned long long* errs = nullptr;      // [0] consistency token (min), [1] theta overflow key (min)
@@ -71,6 +74,9 @@ struct gf_shard {
     int64_t off_phi16_u32 = 0, off_nk_u32 = 0, sync_u32 = 0;
     int64_t doc_lo = 0, doc_hi = 0, D = 0, T = 0, R = 0, n_slices = 0, n_k2 = 0;
     int64_t theta_cap = 0;
+    int64_t n_doc_blocks = 1;
+    int64_t n_ctx = 0;
+    bool ctx_dirty = true;                   // phi / n_k changed since the last prepare
     double ll_const = 0.0;                    // sum_d L_d log(L_d + K alpha)
     std::vector<int64_t> runs_per_doc_dummy;
     gf::TreeGeom tree{};
@@ -89,6 +95,7 @@ namespace gf {
 cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only = 0);
 cudaError_t launch_phi_rebuild(gf_shard* s);
 cudaError_t launch_prepare(gf_shard* s);
+cudaError_t launch_contexts(gf_shard* s);
 cudaError_t launch_theta_rebuild(gf_shard* s);
 cudaError_t launch_ll_reduce(gf_shard* s);
 cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt);
@@ -98,6 +105,7 @@ cudaError_t launch_phi_export(gf_shard* s, uint32_t* d_out_kv, const int32_t* d_
 cudaError_t launch_phi_import(gf_shard* s, const uint32_t* d_in_kv, const int32_t* d_word_col);
 cudaError_t launch_validate(gf_shard* s);
 size_t sample_smem_bytes(const gf_shard* s);
+size_t context_floats(const gf_shard* s);
 cudaError_t ptree_sample(const float* d_prefix, int64_t n, int fanout, const float* d_u, int64_t m,
                          int64_t* d_idx, cudaStream_t st);
 }  // namespace gf

@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(256) phi_rebuild_kernel(const int4* __restrict
 }
 
 cudaError_t launch_phi_rebuild(gf_shard* s) {
+    s->ctx_dirty = true;
     cudaError_t e = cudaMemsetAsync(s->d.sync, 0, (size_t)s->sync_u32 * 4, s->stream);
     if (e != cudaSuccess || s->n_k2 == 0) return e;
     int nsm = 148;
@@ -89,26 +90,40 @@ cudaError_t launch_phi_rebuild(gf_shard* s) {
 }
 
 // ------------------------------------------------------------- prepare ------
+// inv_den[k] = 1/(n_k + V b) and inv_den[K + k] = 1/(n_k - 1 + V b) (the
+// exclusion view), once per iteration instead of a division per word and topic
 __global__ void prepare_kernel(const uint32_t* __restrict__ nk, float* inv_den, int K, double vbeta) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < K) inv_den[k] = (float)(1.0 / ((double)nk[k] + vbeta));
+    if (k < K) {
+        inv_den[k] = (float)(1.0 / ((double)nk[k] + vbeta));
+        inv_den[K + k] = nk[k] ? (float)(1.0 / ((double)nk[k] - 1.0 + vbeta)) : 0.f;
+    }
 }
 
 cudaError_t launch_prepare(gf_shard* s) {
     prepare_kernel<<<(s->K + 255) / 256, 256, 0, s->stream>>>(s->d.sync + s->off_nk_u32, s->d.inv_den, s->K,
                                                               (double)s->V * s->beta);
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_contexts(s);                // word contexts of the multi-slice words
 }
 
 // ---------------------------------------------------------------- K3 ------
 // One warp per document.  Short documents (<= 32 tokens): the topics are
 // gathered through the doc-word map into one register per lane, bitonic-sorted
 // across the warp and run-length encoded with ballots (no K-sized state).
-// Longer documents: dense K-bin histogram in the warp's shared-memory slice
-// (section 6.2 "generate a dense array ... then CSR"), then an
-// ascending ballot/popc compaction.  Output rows: (count << 16 | topic << 2)
-// (the topic pre-scaled to a byte offset into K1's shared p* table), ascending
-// topic, written into the fixed-capacity row; nnz into meta.y.
+// Longer documents: K-bin histogram plus a K-bit presence bitmap in the warp's
+// shared-memory slice (section 6.2 "generate a dense array ... then
+// CSR"); the output rank of topic k is popc of the bitmap below k (one warp
+// scan over the K/32 bitmap words), so each lane emits the topics of its
+// bitmap word in ascending order and clears exactly the bins it touched --
+// O(L + K/32) per document instead of O(K).  Bins and bitmap are zeroed once
+// per CTA and kept zero between documents.  Output rows: (count << 16 |
+// topic << 2) (the topic pre-scaled to a byte offset into K1's shared p*
+// table), ascending topic, in the fixed-capacity row; nnz into meta.y.
+__host__ __device__ inline int k3_words(int K) { return (K + 31) >> 5; }
+__host__ __device__ inline int k3_warp_u32(int K) { return K + k3_words(K); }
+
 __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
                                                             const uint32_t* __restrict__ dw_tok,
                                                             const uint16_t* __restrict__ z, uint32_t* theta_ent,
@@ -116,7 +131,12 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
                                                             unsigned long long* errs) {
     extern __shared__ uint32_t sh[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* bins = sh + (size_t)warp * K;
+    const int NW = k3_words(K);
+    const uint32_t tm = tpos_m(K);
+    uint32_t* bins = sh + (size_t)warp * k3_warp_u32(K);
+    uint32_t* bmp = bins + K;
+    for (int i = lane; i < k3_warp_u32(K); i += 32) bins[i] = 0u;
+    __syncwarp();
     const unsigned lt = (1u << lane) - 1u;
     for (int d = blockIdx.x * warps_per_cta + warp; d < D; d += gridDim.x * warps_per_cta) {
         const uint32_t b = dw_ptr[d], L = dw_ptr[d + 1] - b;
@@ -133,26 +153,43 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
             if (head) {
                 const unsigned later = heads & ~((2u << lane) - 1u);
                 const uint32_t next = later ? (uint32_t)(__ffs(later) - 1) : L;
-                theta_ent[off + __popc(heads & lt)] = (key << 2) | ((next - lane) << 16);
+                theta_ent[off + __popc(heads & lt)] = (tpos(key, tm) << 2) | ((next - lane) << 16);
             }
             nnz = __popc(heads);
         } else {
-            for (int k = lane; k < K; k += 32) bins[k] = 0;
-            __syncwarp();
             for (uint32_t i = lane; i < L; i += 32) {
-                const uint32_t k = z[dw_tok[b + i]];
-                if (k < (uint32_t)K) atomicAdd(&bins[k], 1u);
-                else atomicMin(errs, (unsigned long long)dw_tok[b + i]);
+                const uint32_t t = dw_tok[b + i];
+                const uint32_t k = z[t];
+                if (k < (uint32_t)K) {
+                    atomicAdd(&bins[k], 1u);
+                    atomicOr(&bmp[k >> 5], 1u << (k & 31u));
+                } else {
+                    atomicMin(errs, (unsigned long long)t);
+                }
             }
             __syncwarp();
             uint32_t base = 0, mx = 0;
-            for (int c = 0; c < K; c += 32) {
-                const int k = c + lane;
-                const uint32_t v = k < K ? bins[k] : 0u;
-                const unsigned m = __ballot_sync(kFull, v > 0);
-                if (v) theta_ent[off + base + __popc(m & lt)] = ((uint32_t)k << 2) | (min(v, 65535u) << 16);
-                mx = max(mx, v);
-                base += __popc(m);
+            for (int c = 0; c < NW; c += 32) {
+                const int w = c + lane;
+                uint32_t word = w < NW ? bmp[w] : 0u;
+                const uint32_t pc = __popc(word);
+                uint32_t incl = pc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                uint32_t pos = off + base + incl - pc;
+                if (w < NW) bmp[w] = 0u;
+                while (word) {
+                    const uint32_t k = ((uint32_t)w << 5) + (uint32_t)(__ffs(word) - 1);
+                    word &= word - 1u;
+                    const uint32_t v = bins[k];
+                    bins[k] = 0u;
+                    theta_ent[pos++] = (tpos(k, tm) << 2) | (min(v, 65535u) << 16);
+                    mx = max(mx, v);
+                }
+                base += __shfl_sync(kFull, incl, 31);
             }
             nnz = base;
             mx = warp_max_u32(mx);
@@ -168,9 +205,10 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
 
 cudaError_t launch_theta_rebuild(gf_shard* s) {
     if (s->D == 0) return cudaSuccess;
+    const size_t per_warp = (size_t)k3_warp_u32(s->K) * 4;
     int wpc = 8;
-    while (wpc > 1 && (size_t)wpc * s->K * 4 > 96 * 1024) wpc >>= 1;
-    const size_t smem = (size_t)wpc * s->K * 4;
+    while (wpc > 1 && (size_t)wpc * per_warp > 96 * 1024) wpc >>= 1;
+    const size_t smem = (size_t)wpc * per_warp;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(theta_rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -178,10 +216,14 @@ cudaError_t launch_theta_rebuild(gf_shard* s) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    int nsm = 148;
+    // persistent grid (exactly the resident CTAs): the warps sweep the
+    // documents as one contiguous moving window, so the word-major z sectors
+    // they gather are shared by neighbouring documents while still in L2
+    int nsm = 148, per_sm = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, theta_rebuild_kernel, wpc * 32, smem);
     const long long need = (s->D + wpc - 1) / wpc;
-    const long long grid = std::min<long long>(need, (long long)nsm * 16);
+    const long long grid = std::min<long long>(need, (long long)nsm * std::max(per_sm, 1));
     theta_rebuild_kernel<<<(unsigned)grid, wpc * 32, smem, s->stream>>>((int)s->D, s->d.dw_ptr, s->d.dw_tok, s->d.z,
                                                                          s->d.theta_ent, s->d.theta_meta, s->K, wpc,
                                                                          s->d.errs);
@@ -209,7 +251,7 @@ cudaError_t launch_ll_reduce(gf_shard* s) {
 
 // --------------------------------------------------------- theta export ------
 __global__ void theta_export_kernel(int D, const uint2* __restrict__ meta, const uint32_t* __restrict__ ent,
-                                    const int64_t* __restrict__ rowptr, uint16_t* ids, uint16_t* cnt) {
+                                    const int64_t* __restrict__ rowptr, uint16_t* ids, uint16_t* cnt, uint32_t tm) {
     const int lane = threadIdx.x & 31;
     const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -218,21 +260,21 @@ __global__ void theta_export_kernel(int D, const uint2* __restrict__ meta, const
         const int64_t o = rowptr[d];
         for (uint32_t j = lane; j < m.y; j += 32) {
             const uint32_t e = ent[m.x + j];
-            ids[o + j] = (uint16_t)((e & 0xffffu) >> 2);
+            ids[o + j] = (uint16_t)tpos_inv((e & 0xffffu) >> 2, tm);
             cnt[o + j] = (uint16_t)(e >> 16);
         }
     }
 }
 
 __global__ void theta_import_kernel(int D, uint2* meta, uint32_t* ent, const int64_t* __restrict__ rowptr,
-                                    const uint16_t* __restrict__ ids, const uint16_t* __restrict__ cnt) {
+                                    const uint16_t* __restrict__ ids, const uint16_t* __restrict__ cnt, uint32_t tm) {
     const int lane = threadIdx.x & 31;
     const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     for (long long d = w; d < D; d += nw) {
         const int64_t o = rowptr[d], n = rowptr[d + 1] - o;
         const uint32_t base = meta[d].x;
-        for (int64_t j = lane; j < n; j += 32) ent[base + j] = ((uint32_t)ids[o + j] << 2) | ((uint32_t)cnt[o + j] << 16);
+        for (int64_t j = lane; j < n; j += 32) ent[base + j] = (tpos(ids[o + j], tm) << 2) | ((uint32_t)cnt[o + j] << 16);
         if (lane < ((8 - (n & 7)) & 7)) ent[base + n + lane] = 0u;   // zero pads (see K3)
         if (lane == 0) meta[d].y = (uint32_t)n;
     }
@@ -241,14 +283,14 @@ __global__ void theta_import_kernel(int D, uint2* meta, uint32_t* ent, const int
 cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt) {
     if (s->D == 0) return cudaSuccess;
     theta_export_kernel<<<1184, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, s->d.theta_ent, d_rowptr, d_ids,
-                                                     d_cnt);
+                                                     d_cnt, tpos_m(s->K));
     return cudaGetLastError();
 }
 
 cudaError_t launch_theta_import(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids, const uint16_t* d_cnt) {
     if (s->D == 0) return cudaSuccess;
     theta_import_kernel<<<1184, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, s->d.theta_ent, d_rowptr, d_ids,
-                                                     d_cnt);
+                                                     d_cnt, tpos_m(s->K));
     return cudaGetLastError();
 }
 

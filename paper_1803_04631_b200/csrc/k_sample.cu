@@ -54,6 +54,15 @@ __device__ __forceinline__ void ldg256(const uint32_t* p, uint4& lo, uint4& hi) 
                  : "l"(p));
 }
 
+// cp.async (LDGSTS) 16 B global -> shared, L2 only; src_bytes 0 zero-fills
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 struct SampleArgs {
     int K, Kp;
     float alpha, beta, vbeta;
@@ -71,15 +80,21 @@ struct SampleArgs {
     const uint32_t* phi32;
     const uint16_t* phi16;
     const uint32_t* nk;
-    const float* inv_den;
+    const float* inv_den;                     // [K] 1/(n_k + V b), then [K] 1/(n_k - 1 + V b)
+    const float* ctx_tab;                     // precomputed word contexts (multi-slice words)
+    const int32_t* slice_ctx;                 // per slice: context index or -1
+    int ctx_stride;                           // floats per context = lay_buf(K, tree.total)
+    uint32_t tm;                              // transposed p* layout: m = ceil(K / 32) (gf_device.cuh)
     double* ll_part;
     unsigned long long* errs;
     unsigned long long* bytes;
 };
 
-// shared-memory layout (floats): p*[K] at 0 | p*_ex[K] | Q-tree levels | pad | warp buffers
-__host__ __device__ inline int lay_tree(int K) { return 2 * K; }
-__host__ __device__ inline int lay_buf(int K, int tree_total) { return (2 * K + tree_total + 3) & ~3; }
+// shared-memory layout (floats): p*[32m] at 0 in the transposed topic layout |
+// p*_ex[K] (natural) | Q-tree levels (natural) | pad | warp buffers
+__host__ __device__ inline int lay_pex(int K) { return (int)tpos_slots(K); }
+__host__ __device__ inline int lay_tree(int K) { return lay_pex(K) + K; }
+__host__ __device__ inline int lay_buf(int K, int tree_total) { return (lay_tree(K) + tree_total + 3) & ~3; }
 
 __device__ __forceinline__ uint32_t phi_at(const SampleArgs& a, int col, int k) {
     return col >= 0 ? (uint32_t)a.phi16[(size_t)col * a.Kp + k] : a.phi32[(size_t)(~col) * a.K + k];
@@ -103,7 +118,7 @@ __device__ __forceinline__ float count_f(uint32_t e) {
 __device__ __forceinline__ float w_of(uint32_t e, const float* smem) {
     return count_f(e) * smem[(e & 0xfffcu) >> 2];
 }
-__device__ __forceinline__ uint32_t topic_of(uint32_t e) { return (e & 0xffffu) >> 2; }
+__device__ __forceinline__ uint32_t topic_of(uint32_t e, uint32_t tm) { return tpos_inv((e & 0xffffu) >> 2, tm); }
 
 // ptree descent (ptree.py:203-225) over the shared-memory levels, one ballot
 // per level (warp-cooperative).
@@ -129,18 +144,17 @@ __device__ __forceinline__ uint32_t first_above(const float* P, uint32_t n, floa
 }
 
 // theta_dz of a sorted row by binary search (thinning of a Q-branch z draw)
-__device__ __forceinline__ uint32_t row_count(const uint32_t* row, uint32_t nnz, uint32_t z) {
-    const uint32_t key = z << 2;
+__device__ __forceinline__ uint32_t row_count(const uint32_t* row, uint32_t nnz, uint32_t z, uint32_t tm) {
     uint32_t lo = 0, hi = nnz;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         const uint32_t e = __ldg(row + mid);
-        if ((e & 0xffffu) < key) lo = mid + 1;
+        if (topic_of(e, tm) < z) lo = mid + 1;
         else hi = mid;
     }
     if (lo < nnz) {
         const uint32_t e = __ldg(row + lo);
-        if ((e & 0xffffu) == key) return e >> 16;
+        if (topic_of(e, tm) == z) return e >> 16;
     }
     return 0;
 }
@@ -157,7 +171,7 @@ __device__ __forceinline__ bool keep_own(float ut, uint32_t cnt, float alpha, fl
 __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, float Q, uint32_t v, uint32_t gdoc,
                                        uint32_t t0, uint32_t t1, uint32_t off, uint32_t nnz, int lane) {
     const float* pstar = smem;
-    const float* pex = smem + a.K;
+    const float* pex = smem + lay_pex(a.K);
     const float* lvl = smem + lay_tree(a.K);
     const uint32_t* row = a.theta_ent + off;
     const uint32_t nch = (nnz + 127u) >> 7;
@@ -208,18 +222,18 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, f
                     cy = __shfl_sync(kFull, base + p[3], 31);
                 }
                 const uint32_t e = __ldg(row + j);
-                k = topic_of(e);
+                k = topic_of(e, a.tm);
                 cnt = e >> 16;
             } else {
                 k = (uint32_t)search_q_warp(lvl, a.tree, __fmul_rn(u.s, Q), lane);
-                if (k == zt) cnt = row_count(row, nnz, zt);
+                if (k == zt) cnt = row_count(row, nnz, zt, a.tm);
             }
             if (k != zt) break;
             if (zt >= (uint32_t)a.K || cnt == 0u || pex[zt] == 0.f) {
                 if (lane == 0) atomicMin(a.errs, (unsigned long long)t);
                 break;
             }
-            if (keep_own(u.t, cnt, a.alpha, pstar[zt], pex[zt])) break;
+            if (keep_own(u.t, cnt, a.alpha, pstar[tpos(zt, a.tm)], pex[zt])) break;
             k = zt;
         }
         if (lane == 0) a.z[t] = (uint16_t)k;
@@ -227,14 +241,74 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, f
     return S;
 }
 
-// CAPV: staged vector ends per warp; MINB: CTAs per SM; VEC: vectors per lane
-// per pass step; HUGE: compile the streaming path (needed only when K > 4*CAPV)
-template <uint32_t CAPV, int MINB, uint32_t VEC, bool HUGE>
+// The word context of SPEC.md build_word_context in shared
+// memory: p*(k), p*_ex(k) and the 32-ary Q prefix tree over a p*(k) (block
+// scan; ptree.build levels).  Ends with a __syncthreads.
+__device__ __forceinline__ void build_context(const SampleArgs& a, int col, float* smem, int tid) {
+    const int K = a.K, lane = tid & 31, warp = tid >> 5;
+    float* pstar = smem;                             // transposed layout (tpos)
+    float* pex = smem + lay_pex(K);
+    float* lvl = smem + lay_tree(K);
+    __shared__ float wtot[kWarps];
+    const int ipt = (K + kSampleThreads - 1) / kSampleThreads;
+    const int k0 = tid * ipt;
+    float acc = 0.f;
+    for (int i = 0; i < ipt; ++i) {
+        const int k = k0 + i;
+        if (k < K) {
+            const uint32_t ph = phi_at(a, col, k);
+            const float ps = __fmul_rn(__fadd_rn((float)ph, a.beta), __ldg(a.inv_den + k));
+            pstar[tpos((uint32_t)k, a.tm)] = ps;
+            // (phi - 1 + b) / (n_k - 1 + V b), the reciprocal precomputed by prepare
+            pex[k] = ph ? __fmul_rn(__fadd_rn((float)(ph - 1u), a.beta), __ldg(a.inv_den + K + k)) : 0.f;
+            acc = __fadd_rn(acc, __fmul_rn(a.alpha, ps));
+            lvl[k] = acc;
+        }
+    }
+    const float incl = warp_incl_scan(acc, lane);
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();
+    if (tid == 0) {
+        float run = 0.f;
+        for (int w = 0; w < kWarps; ++w) { const float t = wtot[w]; wtot[w] = run; run = __fadd_rn(run, t); }
+    }
+    __syncthreads();
+    float excl = __shfl_up_sync(kFull, incl, 1);
+    if (lane == 0) excl = 0.f;
+    const float off = __fadd_rn(wtot[warp], excl);
+    for (int i = 0; i < ipt; ++i) {
+        const int k = k0 + i;
+        if (k < K) lvl[k] = __fadd_rn(off, lvl[k]);
+    }
+    __syncthreads();
+    for (int l = 1; l < a.tree.nlev; ++l) {
+        for (int i = tid; i < a.tree.len[l]; i += kSampleThreads)
+            lvl[a.tree.off[l] + i] = lvl[a.tree.off[l - 1] + min(32 * i + 31, a.tree.len[l - 1] - 1)];
+        __syncthreads();
+    }
+}
+
+// One CTA per word that the schedule splits into several slices: its context
+// is built once per iteration (same code, so bit-identical) and the slices
+// copy it instead of rebuilding it.
+__global__ void __launch_bounds__(kSampleThreads) context_kernel(SampleArgs a, const int32_t* __restrict__ cols,
+                                                                  float* out) {
+    extern __shared__ float smem[];
+    build_context(a, cols[blockIdx.x], smem, threadIdx.x);
+    float4* dst = reinterpret_cast<float4*>(out + (size_t)blockIdx.x * a.ctx_stride);
+    for (int i = threadIdx.x; i < a.ctx_stride / 4; i += kSampleThreads) dst[i] = reinterpret_cast<const float4*>(smem)[i];
+}
+
+// CAPV: staged vector ends per warp; MINB: CTAs per SM; RING: depth of the
+// per-warp cp.async ring of pass steps (0: direct 256-bit loads); HUGE:
+// compile the streaming path (needed only when K > 4*CAPV)
+constexpr uint32_t VEC = 2;                  // 16-byte vectors per lane per pass step (32 B)
+template <uint32_t CAPV, int MINB, int RING, bool HUGE>
 __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs a) {
     extern __shared__ float smem[];
     const int K = a.K;
-    float* pstar = smem;                            // p*(k)        (byte offset = theta topic field)
-    float* pex = smem + K;                          // p*_ex(k)
+    float* pstar = smem;                            // p*(tpos(k))  (byte offset = theta topic field)
+    float* pex = smem + lay_pex(K);                 // p*_ex(k)
     float* lvl = smem + lay_tree(K);                // Q-tree levels (level 0 = prefix of a p*)
     float* wbuf = smem + lay_buf(K, a.tree.total);  // kWarps x CAPV staged vector-end prefixes
     __shared__ double ll_w[kWarps];
@@ -247,52 +321,21 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
     const int col = sl.w;
     const unsigned lane_le = (2u << lane) - 1u;     // lanes 0..lane
 
-    // ---------------- prologue: p*, p*_ex and the Q prefix (block scan) ----------------
-    {
-        const int ipt = (K + kSampleThreads - 1) / kSampleThreads;
-        const int k0 = tid * ipt;
-        float acc = 0.f;
-        for (int i = 0; i < ipt; ++i) {
-            const int k = k0 + i;
-            if (k < K) {
-                const uint32_t ph = phi_at(a, col, k);
-                const uint32_t nk = __ldg(a.nk + k);
-                const float ps = __fmul_rn(__fadd_rn((float)ph, a.beta), __ldg(a.inv_den + k));
-                pstar[k] = ps;
-                pex[k] = (ph && nk) ? __fdiv_rn(__fadd_rn((float)(ph - 1u), a.beta),
-                                                __fadd_rn((float)(nk - 1u), a.vbeta))
-                                    : 0.f;
-                acc = __fadd_rn(acc, __fmul_rn(a.alpha, ps));
-                lvl[k] = acc;
-            }
-        }
-        const float incl = warp_incl_scan(acc, lane);
-        __shared__ float wtot[kWarps];
-        if (lane == 31) wtot[warp] = incl;
-        if (tid == 0) next_run = sl.y;
+    // ---------------- prologue: the word context (p*, p*_ex, Q-tree) ----------------
+    if (tid == 0) next_run = sl.y;
+    const int ctx = a.slice_ctx[blockIdx.x];
+    if (ctx >= 0) {                                  // word split into several slices: copy (L2)
+        const float4* src = reinterpret_cast<const float4*>(a.ctx_tab + (size_t)ctx * a.ctx_stride);
+        for (int i = tid; i < a.ctx_stride / 4; i += kSampleThreads) reinterpret_cast<float4*>(smem)[i] = __ldg(src + i);
         __syncthreads();
-        if (tid == 0) {
-            float run = 0.f;
-            for (int w = 0; w < kWarps; ++w) { const float t = wtot[w]; wtot[w] = run; run = __fadd_rn(run, t); }
-        }
-        __syncthreads();
-        float excl = __shfl_up_sync(kFull, incl, 1);
-        if (lane == 0) excl = 0.f;
-        const float off = __fadd_rn(wtot[warp], excl);
-        for (int i = 0; i < ipt; ++i) {
-            const int k = k0 + i;
-            if (k < K) lvl[k] = __fadd_rn(off, lvl[k]);
-        }
-        __syncthreads();
-        for (int l = 1; l < a.tree.nlev; ++l) {
-            for (int i = tid; i < a.tree.len[l]; i += kSampleThreads)
-                lvl[a.tree.off[l] + i] = lvl[a.tree.off[l - 1] + min(32 * i + 31, a.tree.len[l - 1] - 1)];
-            __syncthreads();
-        }
+    } else {
+        build_context(a, col, smem, tid);
     }
     const float Q = lvl[K - 1];
     const float* lvl0 = lvl;
     float* buf = wbuf + warp * CAPV;
+    // per-warp ring of RING pass steps (1 KB each: 32 lanes x 32 B) after the staging buffers
+    uint4* ring = reinterpret_cast<uint4*>(wbuf + kWarps * CAPV) + warp * (RING > 0 ? RING : 1) * 64;
     // runs per grab: 32 (one per lane) unless the slice is too small to give
     // every warp at least two grabs -- then smaller grabs keep all 8 warps busy
     const int batch = min(32, max(1, (sl.z - sl.y + 2 * kWarps - 1) / (2 * kWarps)));
@@ -353,45 +396,69 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
 
             // ---- 1. entry-parallel pass: segmented prefix of p1 over the concatenated rows ----
             // each lane owns VEC consecutive vectors (4*VEC entries) of ONE row per step
-            // (rows are laid out VEC-aligned), so 128*VEC entries advance per warp step
+            // (rows are laid out VEC-aligned), so 128*VEC entries advance per warp step.
+            // With RING > 0 the warp's 1 KB steps are fetched RING-1 steps ahead by
+            // cp.async into a shared-memory ring (no registers held by loads in flight).
+            uint32_t qf = 0, sf = 0;
+            int cpf = first - 1;                                            // fetch cursor: run of vector qf-1
+            auto fetch = [&]() {
+                if (qf < Utot) {
+                    const uint32_t hb = (sel && vo - qf < 32u * VEC) ? (1u << ((vo - qf) / VEC)) : 0u;
+                    const unsigned M = __reduce_or_sync(kFull, hb);
+                    const int ri = min(cpf + __popc(M & lane_le), 31);
+                    const uint32_t rvo = __shfl_sync(kFull, vo, ri);
+                    const uint32_t roff = __shfl_sync(kFull, off, ri);
+                    const uint32_t qL = qf + VEC * (uint32_t)lane;
+                    const bool act = qL < Utot;
+                    const uint32_t* src = act ? a.theta_ent + roff + 4u * (qL - rvo) : &g_zero32[0];
+                    uint4* dst = ring + sf * 64u + 2u * (uint32_t)lane;
+                    cp_async16(dst, src, act ? 16u : 0u);
+                    cp_async16(dst + 1, src + 4, act ? 16u : 0u);
+                    cpf = __shfl_sync(kFull, ri, 31);
+                    qf += 32u * VEC;
+                    sf = sf + 1u == (uint32_t)RING ? 0u : sf + 1u;
+                }
+                cp_async_commit();
+            };
+            if (RING > 0) {
+#pragma unroll
+                for (int i = 0; i < RING - 1; ++i) fetch();
+            }
             int cprev = first - 1;                                          // run holding vector q0-1
+            uint32_t sc = 0;
             float carry = 0.f;
             for (uint32_t q0 = 0; q0 < Utot; q0 += 32u * VEC) {
                 const uint32_t hb = (sel && vo - q0 < 32u * VEC) ? (1u << ((vo - q0) / VEC)) : 0u;
                 const unsigned M = __reduce_or_sync(kFull, hb);           // run heads in this step
                 const unsigned mle = M & lane_le;
-                const int ri = min(cprev + __popc(mle), 31);
-                const uint32_t rvo = __shfl_sync(kFull, vo, ri);
-                const uint32_t roff = __shfl_sync(kFull, off, ri);
-                const uint32_t rU = __shfl_sync(kFull, U, ri);
                 const uint32_t qL = q0 + VEC * (uint32_t)lane;
-                const uint32_t rel = qL - rvo;                              // vector index inside the row
                 const bool act = qL < Utot;
                 uint4 e[VEC];
-                if (VEC == 2) {
+                if (RING > 0) {
+                    fetch();
+                    cp_async_wait<(RING > 0 ? RING - 1 : 0)>();
+                    const uint4* src = ring + sc * 64u + 2u * (uint32_t)lane;
+                    e[0] = src[0];
+                    e[1] = src[1];
+                    sc = sc + 1u == (uint32_t)RING ? 0u : sc + 1u;
+                } else {
+                    const int ri = min(cprev + __popc(mle), 31);
+                    const uint32_t rvo = __shfl_sync(kFull, vo, ri);
+                    const uint32_t roff = __shfl_sync(kFull, off, ri);
                     // one 256-bit load per lane: the warp reads 1 KB contiguous per step
                     // (rows are 32-byte aligned and zero-padded to 8 entries by K3)
-                    const uint32_t* src = act ? a.theta_ent + roff + 4u * rel : &g_zero32[0];
-                    ldg256(src, e[0], e[VEC - 1]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < VEC; ++i) {
-                        const uint4* src = (act && rel + i < rU)
-                                               ? reinterpret_cast<const uint4*>(a.theta_ent + roff + 4u * (rel + i))
-                                               : &g_zero16;
-                        e[i] = __ldg(src);
-                    }
+                    const uint32_t* src = act ? a.theta_ent + roff + 4u * (qL - rvo) : &g_zero32[0];
+                    ldg256(src, e[0], e[1]);
+                    cprev = __shfl_sync(kFull, ri, 31);
                 }
                 float p[VEC];                                               // prefix at each vector end
 #pragma unroll
                 for (int i = 0; i < VEC; ++i)                               // independent pair sums (ILP)
                     p[i] = (w_of(e[i].x, smem) + w_of(e[i].y, smem)) + (w_of(e[i].z, smem) + w_of(e[i].w, smem));
-#pragma unroll
-                for (int i = 1; i < VEC; ++i) p[i] += p[i - 1];
-                const float acc = p[VEC - 1];
+                p[1] += p[0];
                 const int head = mle ? 31 - __clz(mle) : -1;                // my segment's first lane
                 const int lim = max(head, 0);
-                float x = acc;
+                float x = p[1];
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const float y = __shfl_up_sync(kFull, x, o);
@@ -400,20 +467,10 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                 const float y1 = __shfl_up_sync(kFull, x, 1);
                 float base = (lane - 1 >= lim) ? y1 : 0.f;
                 if (head < 0) base += carry;                                // row continues from q0-1
-#pragma unroll
-                for (int i = 0; i < VEC; ++i) p[i] += base;
-                if (act) {
-                    if (VEC == 4) {
-                        *reinterpret_cast<float4*>(buf + qL) = make_float4(p[0], p[1 % VEC], p[2 % VEC], p[3 % VEC]);
-                    } else if (VEC == 2) {
-                        *reinterpret_cast<float2*>(buf + qL) = make_float2(p[0], p[1 % VEC]);   // conflict-free
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < VEC; ++i) buf[qL + i] = p[i];
-                    }
-                }
-                carry = __shfl_sync(kFull, p[VEC - 1], 31);
-                cprev = __shfl_sync(kFull, ri, 31);
+                p[0] += base;
+                p[1] += base;
+                if (act) *reinterpret_cast<float2*>(buf + qL) = make_float2(p[0], p[1]);   // conflict-free
+                carry = __shfl_sync(kFull, p[1], 31);
             }
             __syncwarp();
             if (sel) myS = buf[vo + Up - 1u];                              // segment total (pads add 0)
@@ -465,18 +522,18 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                                     if (!pick && (e4[i] >> 16) && cum > target) pick = e4[i];
                                 }
                                 if (!pick) pick = last;                             // rounding guard
-                                k = topic_of(pick);
+                                k = topic_of(pick, a.tm);
                                 cnt = pick >> 16;
                             } else {
                                 k = g;
-                                if (k == zt) cnt = row_count(row, onnz, zt);
+                                if (k == zt) cnt = row_count(row, onnz, zt, a.tm);
                             }
                             if (k != zt) break;
                             if (zt >= (uint32_t)K || cnt == 0u || pex[zt] == 0.f) {   // inconsistent state
                                 atomicMin(a.errs, (unsigned long long)t);
                                 break;
                             }
-                            if (keep_own(u.t, cnt, a.alpha, pstar[zt], pex[zt])) break;
+                            if (keep_own(u.t, cnt, a.alpha, pstar[tpos(zt, a.tm)], pex[zt])) break;
                             k = zt;                                                   // rejected: redraw
                         }
                         a.z[t] = (uint16_t)k;
@@ -517,7 +574,7 @@ __global__ void __launch_bounds__(256) validate_kernel(SampleArgs a) {
         const uint2 m = a.theta_meta[d];
         for (uint32_t t = a.run_start[r]; t < a.run_start[r + 1]; ++t) {
             const uint32_t zt = a.z[t];
-            const bool bad = zt >= (uint32_t)a.K || row_count(a.theta_ent + m.x, m.y, zt) == 0u ||
+            const bool bad = zt >= (uint32_t)a.K || row_count(a.theta_ent + m.x, m.y, zt, a.tm) == 0u ||
                              phi_at(a, sl.w, (int)zt) == 0u || a.nk[zt] == 0u;
             if (bad) atomicMin(a.errs, (unsigned long long)t);
         }
@@ -529,6 +586,7 @@ cudaError_t launch_validate(gf_shard* s) {
     SampleArgs a{};
     a.K = s->K;
     a.Kp = s->Kp;
+    a.tm = tpos_m(s->K);
     a.slices = s->d.slices;
     a.run_doc = s->d.run_doc;
     a.run_start = s->d.run_start;
@@ -543,31 +601,31 @@ cudaError_t launch_validate(gf_shard* s) {
     return cudaGetLastError();
 }
 
-static size_t smem_for(const gf_shard* s, uint32_t capv) {
-    return (size_t)(lay_buf(s->K, s->tree.total) + kWarps * capv) * sizeof(float);
+static size_t smem_for(const gf_shard* s, uint32_t capv, int ring) {
+    return (size_t)(lay_buf(s->K, s->tree.total) + kWarps * capv) * sizeof(float) + (size_t)kWarps * ring * 1024;
 }
 
-size_t sample_smem_bytes(const gf_shard* s) { return smem_for(s, kCapV); }
+size_t sample_smem_bytes(const gf_shard* s) { return smem_for(s, kCapV, 0); }
+size_t context_floats(const gf_shard* s) { return (size_t)lay_buf(s->K, s->tree.total); }
 
-template <uint32_t CAPV, int MINB, uint32_t VEC, bool HUGE>
+template <uint32_t CAPV, int MINB, int RING, bool HUGE>
 static cudaError_t launch_variant(gf_shard* s, const SampleArgs& a) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(sample_kernel<CAPV, MINB, VEC, HUGE>,
+        cudaError_t e = cudaFuncSetAttribute(sample_kernel<CAPV, MINB, RING, HUGE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(sample_kernel<CAPV, MINB, VEC, HUGE>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        e = cudaFuncSetAttribute(sample_kernel<CAPV, MINB, RING, HUGE>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    sample_kernel<CAPV, MINB, VEC, HUGE><<<(unsigned)s->n_slices, kSampleThreads, smem_for(s, CAPV), s->stream>>>(a);
+    sample_kernel<CAPV, MINB, RING, HUGE><<<(unsigned)s->n_slices, kSampleThreads, smem_for(s, CAPV, RING), s->stream>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
-    if (s->n_slices == 0) return cudaSuccess;
-    SampleArgs a;
+static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
+    SampleArgs a{};
     a.K = s->K;
     a.Kp = s->Kp;
     a.alpha = (float)s->alpha;
@@ -588,22 +646,55 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
     a.phi16 = reinterpret_cast<const uint16_t*>(s->d.sync + s->off_phi16_u32);
     a.nk = s->d.sync + s->off_nk_u32;
     a.inv_den = s->d.inv_den;
+    a.ctx_tab = s->d.ctx_tab;
+    a.slice_ctx = s->d.slice_ctx;
+    a.ctx_stride = lay_buf(s->K, s->tree.total);
+    a.tm = tpos_m(s->K);
     a.ll_part = s->d.ll_part;
     a.errs = s->d.errs;
     a.bytes = s->d.bytes;
-    // tuning knob GF_VEC (vectors per lane per pass step); rows can only
-    // outgrow the staging buffer when K > 4*kCapV -- otherwise the streaming
-    // path (a register-hungry call) is compiled out
-    static int vec = -1;
-    if (vec < 0) {
-        const char* env = getenv("GF_VEC");
-        vec = env ? atoi(env) : 2;
+    return a;
+}
+
+cudaError_t launch_contexts(gf_shard* s) {
+    s->ctx_dirty = false;
+    if (s->n_ctx == 0) return cudaSuccess;
+    const SampleArgs a = make_args(s, 0, 0);
+    const size_t smem = (size_t)a.ctx_stride * sizeof(float);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(context_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
     }
-    if (s->K > (int)(4 * kCapV)) return launch_variant<kCapV, 3, 2, true>(s, a);
-    if (vec == 4) return launch_variant<kCapV, 4, 4, false>(s, a);
-    if (vec == 5) return launch_variant<kCapV, 5, 2, false>(s, a);   // 5 CTAs/SM (51 registers)
-    if (vec == 1) return launch_variant<kCapV, 4, 1, false>(s, a);
-    return launch_variant<kCapV, 4, 2, false>(s, a);
+    context_kernel<<<(unsigned)s->n_ctx, kSampleThreads, smem, s->stream>>>(a, s->d.ctx_cols, s->d.ctx_tab);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
+    if (s->n_slices == 0) return cudaSuccess;
+    if (s->ctx_dirty) {                           // phi changed since the last prepare
+        cudaError_t e = launch_prepare(s);
+        if (e != cudaSuccess) return e;
+    }
+    const SampleArgs a = make_args(s, iteration, eval_only);
+    // tuning knob GF_K1 (variant id, A/B runs); rows can only outgrow the
+    // staging buffer when K > 4*CAPV -- otherwise the streaming path (a
+    // register-hungry call) is compiled out
+    static int var = -1;
+    if (var < 0) {
+        const char* env = getenv("GF_K1");
+        var = env ? atoi(env) : 0;
+    }
+    if (s->K > (int)(4 * kCapV)) return launch_variant<kCapV, 3, 0, true>(s, a);
+    if (s->K > 2048 || var == 0) return launch_variant<kCapV, 4, 0, false>(s, a);
+    switch (var) {
+        case 2: return launch_variant<512, 3, 4, false>(s, a);
+        case 3: return launch_variant<1024, 3, 3, false>(s, a);
+        case 4: return launch_variant<256, 4, 4, false>(s, a);
+        case 5: return launch_variant<512, 4, 2, false>(s, a);
+        default: return launch_variant<512, 4, 3, false>(s, a);
+    }
 }
 
 }  // namespace gf

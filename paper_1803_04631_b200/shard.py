@@ -219,10 +219,10 @@ class DeviceShard:
 
     # ------------------------------------------------------------ counters --
     def stats(self):
-        st = np.zeros(9, np.int64)
-        _lib.check(_lib.lib().gf_shard_stats(self._h, _lib.ptr(st), 9))
+        st = np.zeros(11, np.int64)
+        _lib.check(_lib.lib().gf_shard_stats(self._h, _lib.ptr(st), 11))
         keys = ["sample_bytes", "phi_bytes", "theta_bytes", "runs", "slices", "tokens", "theta_nnz",
-                "kernels_per_iterate", "sample_launches"]
+                "kernels_per_iterate", "sample_launches", "word_contexts", "doc_blocks"]
         return dict(zip(keys, st.tolist()))
 
     def reset_stats(self):
