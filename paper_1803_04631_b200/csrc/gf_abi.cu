@@ -83,7 +83,7 @@ int dev_alloc(T** p, size_t count, const char* what) {
 
 void free_dev(gf_shard* s) {
     auto& d = s->d;
-    void* ptrs[] = {d.z, d.run_doc, d.run_start, d.slices, d.k2items, d.dw_ptr, d.dw_tok, d.theta_ent,
+    void* ptrs[] = {d.z, d.run_doc, d.run_start, d.slices, d.k2items, d.dw_ptr, d.zdoc, d.run_dwpos, d.theta_ent,
                     d.theta_meta, d.sync, d.inv_den, d.ctx_tab, d.ctx_cols, d.slice_ctx, d.ll_part, d.ll_sum,
                     d.errs, d.bytes, d.scratch};
     for (void* p : ptrs)
@@ -366,6 +366,7 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
     });
     std::vector<int4> slices, items;
     std::vector<int32_t> slice_key;
+    std::vector<uint8_t> word_blocked((size_t)V, 0);
     int64_t rr = 0;
     for (int64_t gi : order) {
         if (gs[gi] == 0) continue;
@@ -376,6 +377,7 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
         const int64_t re = std::lower_bound(run_start.begin(), run_start.end() - 1, (uint32_t)t1) - run_start.begin();
         const size_t first = slices.size();
         const bool blocked = nblk > 1 && re - rb >= 2 * min_runs;
+        word_blocked[v] = blocked;
         while (rb < re) {
             const int32_t b0 = doc_blk[run_doc[rb]];
             int64_t r = rb;
@@ -422,11 +424,24 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
     s->n_doc_blocks = nblk;
     if ((int64_t)slices.size() >= (int64_t)INT32_MAX) return fail(GF_ERR_CAPACITY, "too many slices");
     // ---- doc-word map and theta capacities ----
-    std::vector<uint32_t> dwp((size_t)D + 1), dwt((size_t)T);
+    std::vector<uint32_t> dwp((size_t)D + 1);
     for (int64_t d = 0; d <= D; ++d) dwp[d] = (uint32_t)dw_ptr[d];
-    for (int64_t t = 0; t < T; ++t) {
+    for (int64_t t = 0; t < T; ++t)
         if (dw_tok[t] < 0 || dw_tok[t] >= T) return fail(GF_ERR_SHAPE, "doc-word map entry out of range");
-        dwt[t] = (uint32_t)dw_tok[t];
+    // doc-major position of every run (zdoc): per doc, the tokens of
+    // block-scheduled words first, then the rest, each in word-sorted order.
+    // K1 writes the heavy part of a block's docs while the block is
+    // L2-resident, so those zdoc sectors are written whole.
+    std::vector<uint32_t> dwpos((size_t)R);
+    {
+        std::vector<uint32_t> heavy_cnt((size_t)D, 0), hcur((size_t)D, 0), lcur((size_t)D, 0);
+        for (int64_t r = 0; r < R; ++r)
+            if (word_blocked[word_ids[run_start[r]]]) heavy_cnt[run_doc[r]] += run_start[r + 1] - run_start[r];
+        for (int64_t r = 0; r < R; ++r) {
+            const uint32_t d = run_doc[r], len = run_start[r + 1] - run_start[r];
+            if (word_blocked[word_ids[run_start[r]]]) { dwpos[r] = dwp[d] + hcur[d]; hcur[d] += len; }
+            else { dwpos[r] = dwp[d] + heavy_cnt[d] + lcur[d]; lcur[d] += len; }
+        }
     }
     std::vector<uint2> meta((size_t)D);
     uint64_t cap = 0;
@@ -448,13 +463,13 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
     if ((rc = dev_alloc(&dv.z, T, "z")) || (rc = dev_alloc(&dv.run_doc, R, "runs")) ||
         (rc = dev_alloc(&dv.run_start, R + 1, "runs")) || (rc = dev_alloc(&dv.slices, slices.size(), "slices")) ||
         (rc = dev_alloc(&dv.k2items, items.size(), "items")) || (rc = dev_alloc(&dv.dw_ptr, D + 1, "dw_ptr")) ||
-        (rc = dev_alloc(&dv.dw_tok, T, "dw_tok")) || (rc = dev_alloc(&dv.theta_ent, cap + 4, "theta")) ||
+        (rc = dev_alloc(&dv.zdoc, T, "zdoc")) || (rc = dev_alloc(&dv.run_dwpos, R, "runs")) || (rc = dev_alloc(&dv.theta_ent, cap + 4, "theta")) ||
         (rc = dev_alloc(&dv.theta_meta, D, "theta")) || (rc = dev_alloc(&dv.sync, s->sync_u32, "phi")) ||
         (rc = dev_alloc(&dv.inv_den, 2 * K, "inv_den")) ||
         (rc = dev_alloc(&dv.ctx_tab, ctx_cols.size() * (size_t)gf::context_floats(s), "contexts")) ||
         (rc = dev_alloc(&dv.ctx_cols, ctx_cols.size(), "contexts")) ||
         (rc = dev_alloc(&dv.slice_ctx, slices.size(), "contexts")) || (rc = dev_alloc(&dv.ll_part, slices.size(), "ll")) ||
-        (rc = dev_alloc(&dv.ll_sum, 1, "ll")) || (rc = dev_alloc(&dv.errs, 2, "errs")) ||
+        (rc = dev_alloc(&dv.ll_sum, 1, "ll")) || (rc = dev_alloc(&dv.errs, 3, "errs")) ||
         (rc = dev_alloc(&dv.bytes, 1, "bytes")))
         return rc;
     cudaStream_t st = s->stream;
@@ -467,12 +482,14 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
     CU(cudaMemcpyAsync(dv.slice_ctx, slice_ctx.data(), slice_ctx.size() * 4, cudaMemcpyHostToDevice, st), "upload");
     CU(cudaMemcpyAsync(dv.k2items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, st), "upload");
     CU(cudaMemcpyAsync(dv.dw_ptr, dwp.data(), (D + 1) * 4, cudaMemcpyHostToDevice, st), "upload");
-    CU(cudaMemcpyAsync(dv.dw_tok, dwt.data(), T * 4, cudaMemcpyHostToDevice, st), "upload");
+    CU(cudaMemcpyAsync(dv.run_dwpos, dwpos.data(), R * 4, cudaMemcpyHostToDevice, st), "upload");
     CU(cudaMemcpyAsync(dv.theta_meta, meta.data(), D * sizeof(uint2), cudaMemcpyHostToDevice, st), "upload");
     CU(cudaMemsetAsync(dv.theta_ent, 0, (cap + 4) * 4, st), "memset");
     CU(cudaMemsetAsync(dv.sync, 0, s->sync_u32 * 4, st), "memset");
-    CU(cudaMemsetAsync(dv.errs, 0xff, 16, st), "memset");
+    CU(cudaMemsetAsync(dv.errs, 0xff, 24, st), "memset");
     CU(cudaMemsetAsync(dv.bytes, 0, 8, st), "memset");
+    s->R = R;
+    CU(gf::launch_zdoc_sync(s), "load");
     CU(cudaStreamSynchronize(st), "load");
     s->doc_lo = doc_lo;
     s->doc_hi = doc_hi;
@@ -582,15 +599,18 @@ int gf_shard_synchronize(gf_shard* s) {
 
 int gf_shard_check_errors(gf_shard* s) {
     if (int rc = need_loaded(s)) return rc;
-    unsigned long long e[2];
-    CU(cudaMemcpyAsync(e, s->d.errs, 16, cudaMemcpyDeviceToHost, s->stream), "errors");
+    unsigned long long e[3];
+    CU(cudaMemcpyAsync(e, s->d.errs, 24, cudaMemcpyDeviceToHost, s->stream), "errors");
     CU(cudaStreamSynchronize(s->stream), "errors");
-    CU(cudaMemsetAsync(s->d.errs, 0xff, 16, s->stream), "errors");
+    CU(cudaMemsetAsync(s->d.errs, 0xff, 24, s->stream), "errors");
     if (e[1] != ~0ULL) {
         const long long d = (long long)(e[1] >> 32) + s->doc_lo;
         return fail(GF_ERR_OVERFLOW, "document %lld: topic count %llu exceeds 16-bit range", d,
                     (unsigned long long)(e[1] & 0xffffffffULL));
     }
+    if (e[2] != ~0ULL)
+        return fail(GF_ERR_CONSISTENCY, "document %lld: a token's topic is outside [0, K=%d)",
+                    (long long)e[2] + s->doc_lo, s->K);
     if (e[0] != ~0ULL)
         return fail(GF_ERR_CONSISTENCY, "token %llu: its current topic is absent from its document's theta row "
                     "(or from phi / n_k)", (unsigned long long)e[0]);
@@ -615,6 +635,7 @@ int gf_shard_set_assignments(gf_shard* s, const uint16_t* in) {
     if (int rc = need_loaded(s)) return rc;
     // range is checked on the device (K1/K2/K3 flag z >= K as a consistency error)
     CU(cudaMemcpyAsync(s->d.z, in, s->T * 2, cudaMemcpyHostToDevice, s->stream), "set_assignments");
+    CU(gf::launch_zdoc_sync(s), "set_assignments");
     CU(cudaStreamSynchronize(s->stream), "set_assignments");
     s->dirty = true;
     return GF_OK;
@@ -767,11 +788,12 @@ int gf_shard_stats(gf_shard* s, int64_t* st, int n) {
     CU(cudaMemcpyAsync(&nnz_runs, s->d.bytes, 8, cudaMemcpyDeviceToHost, s->stream), "stats");
     CU(cudaStreamSynchronize(s->stream), "stats");
     const int64_t K = s->K;
-    // K1 algorithmic bytes per launch (DESIGN.md section 4): per run its doc id,
-    // run_start pair and theta meta (4 + 4 + 8) plus its theta row (4 B per
-    // entry, averaged over the launches since the last reset); per token z read
-    // + z' write (2 + 2); per slice the slice record (16), the word's phi
-    // column (2 or 4 B per topic), the K denominators (4 B) and its ll partial (8).
+    // K1 algorithmic bytes per launch (DESIGN.md section 3): per run its doc id,
+    // run_start pair, zdoc position and theta meta (4 + 4 + 4 + 8) plus its
+    // theta row (4 B per entry, averaged over the launches since the last
+    // reset); per token z read + z' write + zdoc write (2 + 2 + 2); per slice
+    // the slice record (16), its context index (4), the word's phi column (2 or
+    // 4 B per topic), the K denominators (2 x 4 B) and its ll partial (8).
     int64_t phi_col_bytes = 0;
     {
         std::vector<int4> sl((size_t)s->n_slices);
@@ -780,14 +802,14 @@ int gf_shard_stats(gf_shard* s, int64_t* st, int n) {
         for (auto& x : sl) phi_col_bytes += (x.w >= 0 ? 2 : 4) * K;
     }
     const int64_t L = std::max<int64_t>(s->stat_sample_launches, 1);
-    const int64_t b_sample = s->R * 16 + (int64_t)(4 * nnz_runs) / L + s->T * 4 +
-                             s->n_slices * (16 + 4 * K + 8) + phi_col_bytes;
+    const int64_t b_sample = s->R * 20 + (int64_t)(4 * nnz_runs) / L + s->T * 6 +
+                             s->n_slices * (16 + 4 + 8 * K + 8) + phi_col_bytes;
     // K2: memset of the sync buffer + z read + work items (+ nonzero cells, not counted)
     const int64_t b_phi = s->sync_u32 * 4 + s->T * 2 + s->n_k2 * 16;
-    // K3: dw_tok + gathered z per token, dw_ptr + meta per doc, 4 B per written entry
+    // K3: zdoc per token (contiguous per doc), dw_ptr + meta per doc, 4 B per written entry
     int64_t nnz = 0;
     if (n > 2) gf_shard_theta_nnz(s, &nnz);
-    const int64_t b_theta = s->T * (4 + 2) + (s->D + 1) * 4 + s->D * 8 + nnz * 4;
+    const int64_t b_theta = s->T * 2 + (s->D + 1) * 4 + s->D * 8 + nnz * 4;
     int64_t v[11] = {b_sample, b_phi,    b_theta, s->R, s->n_slices, s->T, nnz, s->stat_launches, s->stat_sample_launches,
                      s->n_ctx,  s->n_doc_blocks};
     for (int i = 0; i < n && i < 11; ++i) st[i] = v[i];

@@ -6,7 +6,11 @@
 //   run_start  u32[R+1]      first token of each run
 //   slices     int4[N]       {word, run_begin, run_end, phi column} heavy-first
 //   k2items    int4[M]       {phi column, tok_begin, tok_end, atomic?}
-//   dw_ptr     u32[D+1], dw_tok u32[T]   doc-word map (corpus.py:201-207)
+//   dw_ptr     u32[D+1]      doc-major token ranges (corpus.py:201-207 dw-map)
+//   zdoc       u16[T]        the same topics in doc-major order (K1 writes
+//                            them, K3 reads each doc contiguously); inside a
+//                            doc, tokens of block-scheduled words come first
+//   run_dwpos  u32[R]        zdoc position of each run's first token
 //   theta_ent  u32[cap]      (count << 16 | topic) rows, fixed capacity
 //                            round4(min(K, L_d)) per doc, ids ascending
 //   theta_meta uint2[D]      {row offset, nnz}
@@ -40,7 +44,8 @@ struct ShardDev {
     int4* slices = nullptr;
     int4* k2items = nullptr;
     uint32_t* dw_ptr = nullptr;
-    uint32_t* dw_tok = nullptr;
+    uint16_t* zdoc = nullptr;
+    uint32_t* run_dwpos = nullptr;
     uint32_t* theta_ent = nullptr;
     uint2* theta_meta = nullptr;
     uint32_t* sync = nullptr;
@@ -50,7 +55,8 @@ struct ShardDev {
     int32_t* slice_ctx = nullptr;            // [N] context of each slice (-1: built in place)
     double* ll_part = nullptr;
     double* ll_sum = nullptr;
-    unsigned long long* errs = nullptr;      // [0] consistency token (min), [1] theta overflow key (min)
+    unsigned long long* errs = nullptr;      // [0] consistency token (min), [1] theta overflow key (min),
+                                             // [2] document with a topic >= K (K3, min)
     unsigned long long* bytes = nullptr;     // [0] sum over runs of nnz (sampler bytes model)
     uint32_t* scratch = nullptr;             // export staging
     size_t scratch_bytes = 0;
@@ -97,6 +103,7 @@ cudaError_t launch_phi_rebuild(gf_shard* s);
 cudaError_t launch_prepare(gf_shard* s);
 cudaError_t launch_contexts(gf_shard* s);
 cudaError_t launch_theta_rebuild(gf_shard* s);
+cudaError_t launch_zdoc_sync(gf_shard* s);
 cudaError_t launch_ll_reduce(gf_shard* s);
 cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt);
 cudaError_t launch_theta_import(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids,

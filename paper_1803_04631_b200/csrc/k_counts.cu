@@ -125,8 +125,7 @@ __host__ __device__ inline int k3_words(int K) { return (K + 31) >> 5; }
 __host__ __device__ inline int k3_warp_u32(int K) { return K + k3_words(K); }
 
 __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
-                                                            const uint32_t* __restrict__ dw_tok,
-                                                            const uint16_t* __restrict__ z, uint32_t* theta_ent,
+                                                            const uint16_t* __restrict__ zdoc, uint32_t* theta_ent,
                                                             uint2* theta_meta, int K, int warps_per_cta,
                                                             unsigned long long* errs) {
     extern __shared__ uint32_t sh[];
@@ -144,8 +143,8 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
         uint32_t nnz;
         if (L <= 32) {
             uint32_t key = 0xffffu;
-            if (lane < (int)L) key = z[dw_tok[b + lane]];
-            if (key >= (uint32_t)K && lane < (int)L) { atomicMin(errs, (unsigned long long)dw_tok[b + lane]); key = 0xffffu; }
+            if (lane < (int)L) key = zdoc[b + lane];
+            if (key >= (uint32_t)K && lane < (int)L) { atomicMin(errs + 2, (unsigned long long)d); key = 0xffffu; }
             key = warp_bitonic_sort(key, lane);
             const uint32_t prev = __shfl_up_sync(kFull, key, 1);
             const bool head = key != 0xffffu && (lane == 0 || key != prev);
@@ -158,13 +157,12 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
             nnz = __popc(heads);
         } else {
             for (uint32_t i = lane; i < L; i += 32) {
-                const uint32_t t = dw_tok[b + i];
-                const uint32_t k = z[t];
+                const uint32_t k = zdoc[b + i];
                 if (k < (uint32_t)K) {
                     atomicAdd(&bins[k], 1u);
                     atomicOr(&bmp[k >> 5], 1u << (k & 31u));
                 } else {
-                    atomicMin(errs, (unsigned long long)t);
+                    atomicMin(errs + 2, (unsigned long long)d);
                 }
             }
             __syncwarp();
@@ -224,9 +222,27 @@ cudaError_t launch_theta_rebuild(gf_shard* s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, theta_rebuild_kernel, wpc * 32, smem);
     const long long need = (s->D + wpc - 1) / wpc;
     const long long grid = std::min<long long>(need, (long long)nsm * std::max(per_sm, 1));
-    theta_rebuild_kernel<<<(unsigned)grid, wpc * 32, smem, s->stream>>>((int)s->D, s->d.dw_ptr, s->d.dw_tok, s->d.z,
+    theta_rebuild_kernel<<<(unsigned)grid, wpc * 32, smem, s->stream>>>((int)s->D, s->d.dw_ptr, s->d.zdoc,
                                                                          s->d.theta_ent, s->d.theta_meta, s->K, wpc,
                                                                          s->d.errs);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ zdoc sync ------
+// zdoc[run_dwpos[r] + i] = z[run_start[r] + i]: the doc-major copy of imported
+// or initial assignments (K1 keeps it current afterwards)
+__global__ void zdoc_sync_kernel(long long R, const uint32_t* __restrict__ run_start,
+                                 const uint32_t* __restrict__ dwpos, const uint16_t* __restrict__ z, uint16_t* zdoc) {
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (long long)gridDim.x * blockDim.x) {
+        const uint32_t t0 = run_start[r], t1 = run_start[r + 1], p = dwpos[r];
+        for (uint32_t t = t0; t < t1; ++t) zdoc[p + (t - t0)] = z[t];
+    }
+}
+
+cudaError_t launch_zdoc_sync(gf_shard* s) {
+    if (s->R == 0) return cudaSuccess;
+    zdoc_sync_kernel<<<148 * 8, 256, 0, s->stream>>>((long long)s->R, s->d.run_start, s->d.run_dwpos, s->d.z,
+                                                     s->d.zdoc);
     return cudaGetLastError();
 }
 

@@ -74,7 +74,9 @@ struct SampleArgs {
     const int4* slices;
     const uint32_t* run_doc;
     const uint32_t* run_start;
+    const uint32_t* run_dwpos;                // zdoc position of each run's first token
     uint16_t* z;
+    uint16_t* zdoc;                           // doc-major copy of z (read by K3)
     const uint2* theta_meta;
     const uint32_t* theta_ent;
     const uint32_t* phi32;
@@ -169,7 +171,8 @@ __device__ __forceinline__ bool keep_own(float ut, uint32_t cnt, float alpha, fl
 // Rows longer than the staging buffer: warp-cooperative, one run, the S part
 // re-streamed per S-branch draw.  Returns S (all lanes).
 __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, float Q, uint32_t v, uint32_t gdoc,
-                                       uint32_t t0, uint32_t t1, uint32_t off, uint32_t nnz, int lane) {
+                                       uint32_t t0, uint32_t t1, uint32_t off, uint32_t nnz, uint32_t dwp,
+                                       int lane) {
     const float* pstar = smem;
     const float* pex = smem + lay_pex(a.K);
     const float* lvl = smem + lay_tree(a.K);
@@ -236,7 +239,7 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, f
             if (keep_own(u.t, cnt, a.alpha, pstar[tpos(zt, a.tm)], pex[zt])) break;
             k = zt;
         }
-        if (lane == 0) a.z[t] = (uint16_t)k;
+        if (lane == 0) { a.z[t] = (uint16_t)k; a.zdoc[dwp + occ] = (uint16_t)k; }
     }
     return S;
 }
@@ -350,11 +353,12 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
         // ---- batch: lane j owns run rb + j ----
         const int r = rb + lane;
         const bool valid = lane < batch && r < sl.z;
-        uint32_t d = 0, t0 = 0, t1 = 0, off = 0, nnz = 0;
+        uint32_t d = 0, t0 = 0, t1 = 0, off = 0, nnz = 0, dwp = 0;
         if (valid) {
             d = __ldg(a.run_doc + r);
             t0 = __ldg(a.run_start + r);
             t1 = __ldg(a.run_start + r + 1);
+            dwp = __ldg(a.run_dwpos + r);
             const uint2 m = __ldg(a.theta_meta + d);
             off = m.x;
             nnz = m.y;
@@ -372,7 +376,8 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
             if (HUGE && ((hmask >> first) & 1u)) {             // rare: row beyond the buffer
                 const float S = huge_run(a, smem, Q, v, __shfl_sync(kFull, gdoc, first),
                                          __shfl_sync(kFull, t0, first), __shfl_sync(kFull, t1, first),
-                                         __shfl_sync(kFull, off, first), __shfl_sync(kFull, nnz, first), lane);
+                                         __shfl_sync(kFull, off, first), __shfl_sync(kFull, nnz, first),
+                                         __shfl_sync(kFull, dwp, first), lane);
                 if (lane == first) myS = S;
                 rem &= rem - 1u;
                 continue;
@@ -492,6 +497,7 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                     const uint32_t ooff = __shfl_sync(kFull, off, own);
                     const uint32_t ovo = __shfl_sync(kFull, vo, own);
                     const uint32_t onnz = __shfl_sync(kFull, nnz, own);
+                    const uint32_t odwp = __shfl_sync(kFull, dwp, own);
                     cown = __shfl_sync(kFull, own, 31);
                     const uint32_t t = base + (uint32_t)lane;
                     if (t < tend) {
@@ -537,6 +543,7 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                             k = zt;                                                   // rejected: redraw
                         }
                         a.z[t] = (uint16_t)k;
+                        a.zdoc[odwp + occ] = (uint16_t)k;
                     }
                 }
             }
@@ -639,7 +646,9 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     a.slices = s->d.slices;
     a.run_doc = s->d.run_doc;
     a.run_start = s->d.run_start;
+    a.run_dwpos = s->d.run_dwpos;
     a.z = s->d.z;
+    a.zdoc = s->d.zdoc;
     a.theta_meta = s->d.theta_meta;
     a.theta_ent = s->d.theta_ent;
     a.phi32 = s->d.sync;
