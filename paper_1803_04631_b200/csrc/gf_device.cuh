@@ -60,10 +60,23 @@ __device__ __forceinline__ uint32_t warp_bitonic_sort(uint32_t key, int lane) {
 // lanes of one gather (entries 8 apart in the row) hit distinct banks; with
 // the natural layout (bank = t % 32) they collide like random addresses.
 // Theta entries store tpos(t) << 2 (a byte offset) in their low 16 bits.
+// t / m is a multiply-high by magic = ceil(2^32 / m): exact for t, m < 2^16.
+struct TPos {
+    uint32_t m, magic;
+};
 __host__ __device__ inline uint32_t tpos_m(int K) { return (uint32_t)(K + 31) / 32u; }
 __host__ __device__ inline uint32_t tpos_slots(int K) { return 32u * tpos_m(K); }
-__device__ __forceinline__ uint32_t tpos(uint32_t t, uint32_t m) { return (t % m) * 32u + t / m; }
-__device__ __forceinline__ uint32_t tpos_inv(uint32_t p, uint32_t m) { return (p & 31u) * m + (p >> 5); }
+__host__ __device__ inline TPos tpos_geom(int K) {
+    TPos g;
+    g.m = tpos_m(K);
+    g.magic = g.m > 1 ? (uint32_t)((0x100000000ULL + g.m - 1) / g.m) : 0u;
+    return g;
+}
+__device__ __forceinline__ uint32_t tpos(uint32_t t, TPos g) {
+    const uint32_t q = g.m > 1 ? __umulhi(t, g.magic) : t;
+    return (t - q * g.m) * 32u + q;
+}
+__device__ __forceinline__ uint32_t tpos_inv(uint32_t p, TPos g) { return (p & 31u) * g.m + (p >> 5); }
 
 __device__ __forceinline__ float prev_float(float x) { return __int_as_float(__float_as_int(x) - 1); }
 

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
     extern __shared__ uint32_t sh[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int NW = k3_words(K);
-    const uint32_t tm = tpos_m(K);
+    const TPos tm = tpos_geom(K);
     uint32_t* bins = sh + (size_t)warp * k3_warp_u32(K);
     uint32_t* bmp = bins + K;
     for (int i = lane; i < k3_warp_u32(K); i += 32) bins[i] = 0u;
@@ -267,7 +267,7 @@ cudaError_t launch_ll_reduce(gf_shard* s) {
 
 // --------------------------------------------------------- theta export ------
 __global__ void theta_export_kernel(int D, const uint2* __restrict__ meta, const uint32_t* __restrict__ ent,
-                                    const int64_t* __restrict__ rowptr, uint16_t* ids, uint16_t* cnt, uint32_t tm) {
+                                    const int64_t* __restrict__ rowptr, uint16_t* ids, uint16_t* cnt, TPos tm) {
     const int lane = threadIdx.x & 31;
     const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -283,7 +283,7 @@ __global__ void theta_export_kernel(int D, const uint2* __restrict__ meta, const
 }
 
 __global__ void theta_import_kernel(int D, uint2* meta, uint32_t* ent, const int64_t* __restrict__ rowptr,
-                                    const uint16_t* __restrict__ ids, const uint16_t* __restrict__ cnt, uint32_t tm) {
+                                    const uint16_t* __restrict__ ids, const uint16_t* __restrict__ cnt, TPos tm) {
     const int lane = threadIdx.x & 31;
     const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -299,14 +299,14 @@ __global__ void theta_import_kernel(int D, uint2* meta, uint32_t* ent, const int
 cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt) {
     if (s->D == 0) return cudaSuccess;
     theta_export_kernel<<<1184, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, s->d.theta_ent, d_rowptr, d_ids,
-                                                     d_cnt, tpos_m(s->K));
+                                                     d_cnt, tpos_geom(s->K));
     return cudaGetLastError();
 }
 
 cudaError_t launch_theta_import(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids, const uint16_t* d_cnt) {
     if (s->D == 0) return cudaSuccess;
     theta_import_kernel<<<1184, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, s->d.theta_ent, d_rowptr, d_ids,
-                                                     d_cnt, tpos_m(s->K));
+                                                     d_cnt, tpos_geom(s->K));
     return cudaGetLastError();
 }
 

@@ -86,17 +86,20 @@ struct SampleArgs {
     const float* ctx_tab;                     // precomputed word contexts (multi-slice words)
     const int32_t* slice_ctx;                 // per slice: context index or -1
     int ctx_stride;                           // floats per context = lay_buf(K, tree.total)
-    uint32_t tm;                              // transposed p* layout: m = ceil(K / 32) (gf_device.cuh)
+    TPos tm;                                  // transposed p* layout (gf_device.cuh)
     double* ll_part;
     unsigned long long* errs;
     unsigned long long* bytes;
 };
 
 // shared-memory layout (floats): p*[32m] at 0 in the transposed topic layout |
-// p*_ex[K] (natural) | Q-tree levels (natural) | pad | warp buffers
+// p*_ex[K] (natural) | Q-tree levels (natural) | Q guide[kGuide + 1] (u32) |
+// pad | warp buffers
+constexpr int kGuide = 256;                   // Q-prefix guide buckets (power of two)
 __host__ __device__ inline int lay_pex(int K) { return (int)tpos_slots(K); }
 __host__ __device__ inline int lay_tree(int K) { return lay_pex(K) + K; }
-__host__ __device__ inline int lay_buf(int K, int tree_total) { return (lay_tree(K) + tree_total + 3) & ~3; }
+__host__ __device__ inline int lay_guide(int K, int tree_total) { return lay_tree(K) + tree_total; }
+__host__ __device__ inline int lay_buf(int K, int tree_total) { return (lay_guide(K, tree_total) + kGuide + 1 + 3) & ~3; }
 
 __device__ __forceinline__ uint32_t phi_at(const SampleArgs& a, int col, int k) {
     return col >= 0 ? (uint32_t)a.phi16[(size_t)col * a.Kp + k] : a.phi32[(size_t)(~col) * a.K + k];
@@ -120,7 +123,7 @@ __device__ __forceinline__ float count_f(uint32_t e) {
 __device__ __forceinline__ float w_of(uint32_t e, const float* smem) {
     return count_f(e) * smem[(e & 0xfffcu) >> 2];
 }
-__device__ __forceinline__ uint32_t topic_of(uint32_t e, uint32_t tm) { return tpos_inv((e & 0xffffu) >> 2, tm); }
+__device__ __forceinline__ uint32_t topic_of(uint32_t e, TPos tm) { return tpos_inv((e & 0xffffu) >> 2, tm); }
 
 // ptree descent (ptree.py:203-225) over the shared-memory levels, one ballot
 // per level (warp-cooperative).
@@ -146,7 +149,7 @@ __device__ __forceinline__ uint32_t first_above(const float* P, uint32_t n, floa
 }
 
 // theta_dz of a sorted row by binary search (thinning of a Q-branch z draw)
-__device__ __forceinline__ uint32_t row_count(const uint32_t* row, uint32_t nnz, uint32_t z, uint32_t tm) {
+__device__ __forceinline__ uint32_t row_count(const uint32_t* row, uint32_t nnz, uint32_t z, TPos tm) {
     uint32_t lo = 0, hi = nnz;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
@@ -289,6 +292,15 @@ __device__ __forceinline__ void build_context(const SampleArgs& a, int col, floa
             lvl[a.tree.off[l] + i] = lvl[a.tree.off[l - 1] + min(32 * i + 31, a.tree.len[l - 1] - 1)];
         __syncthreads();
     }
+    // Q guide: guide[j] = first_above(level 0, thr_j), thr_j = fl((j / G) Q).  A
+    // Q draw with target t = fl(u Q), j = floor(u G), has thr_j <= t <= thr_j+1
+    // (rounding is monotone), so its answer lies in [guide[j], guide[j+1]] and a
+    // search of that range returns exactly the full-range result.
+    uint32_t* guide = reinterpret_cast<uint32_t*>(smem + lay_guide(K, a.tree.total));
+    const float Q = lvl[K - 1];
+    for (int j = tid; j <= kGuide; j += kSampleThreads)
+        guide[j] = first_above(lvl, (uint32_t)K, __fmul_rn((float)j * (1.f / kGuide), Q));
+    __syncthreads();
 }
 
 // One CTA per word that the schedule splits into several slices: its context
@@ -336,6 +348,7 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
     }
     const float Q = lvl[K - 1];
     const float* lvl0 = lvl;
+    const uint32_t* guide = reinterpret_cast<const uint32_t*>(smem + lay_guide(K, a.tree.total));
     float* buf = wbuf + warp * CAPV;
     // per-warp ring of RING pass steps (1 KB each: 32 lanes x 32 B) after the staging buffers
     uint4* ring = reinterpret_cast<uint4*>(wbuf + kWarps * CAPV) + warp * (RING > 0 ? RING : 1) * 64;
@@ -513,7 +526,11 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                             const U3 u = draw_u(a, odoc, v, occ, (uint32_t)retry);
                             const bool isS = __fmul_rn(u.b, __fadd_rn(S, Q)) < S;
                             const float target = __fmul_rn(u.s, isS ? S : Q);
-                            uint32_t g = first_above(isS ? seg : lvl0, isS ? oUp : (uint32_t)K, target);
+                            // Q: only the guide bucket [guide[j], guide[j+1]] (exact, see build_context)
+                            const uint32_t gj = (uint32_t)(u.s * (float)kGuide);
+                            const uint32_t qlo = isS ? 0u : guide[gj];
+                            const uint32_t qn = isS ? oUp : guide[gj + 1] - qlo + 1u;
+                            uint32_t g = first_above((isS ? seg : lvl0) + qlo, qn, target) + qlo;
                             uint32_t cnt = 0;
                             if (isS) {
                                 g = min(g, oU - 1u);
@@ -593,7 +610,7 @@ cudaError_t launch_validate(gf_shard* s) {
     SampleArgs a{};
     a.K = s->K;
     a.Kp = s->Kp;
-    a.tm = tpos_m(s->K);
+    a.tm = tpos_geom(s->K);
     a.slices = s->d.slices;
     a.run_doc = s->d.run_doc;
     a.run_start = s->d.run_start;
@@ -658,7 +675,7 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     a.ctx_tab = s->d.ctx_tab;
     a.slice_ctx = s->d.slice_ctx;
     a.ctx_stride = lay_buf(s->K, s->tree.total);
-    a.tm = tpos_m(s->K);
+    a.tm = tpos_geom(s->K);
     a.ll_part = s->d.ll_part;
     a.errs = s->d.errs;
     a.bytes = s->d.bytes;
