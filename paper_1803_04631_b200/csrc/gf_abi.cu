@@ -339,7 +339,7 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
     // K1 reads one theta row per (doc, word) run; scheduling the slices of all
     // frequent words block by block keeps the rows being read L2-resident, so
     // each row comes from HBM about once per block instead of once per run.
-    const int64_t blk_bytes = (int64_t)env_int("GF_DOCBLOCK_MB", 64) << 20;
+    const int64_t blk_bytes = (int64_t)env_int("GF_DOCBLOCK_KB", 64 << 10) << 10;
     const int64_t min_runs = env_int("GF_SLICE_MINRUNS", 1024);
     std::vector<int32_t> doc_blk((size_t)D);
     int32_t nblk = 0;

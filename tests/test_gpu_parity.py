@@ -464,3 +464,47 @@ def test_two_device_shards_with_summed_sync_buffers_match_one_shard():
     np.testing.assert_array_equal(th.counts, cn)
     for s in shards + [single]:
         s.close()
+
+
+@pytest.mark.parametrize("sched", [("256", "16"), ("64", "8"), ("1000000", "1024")])
+def test_slice_schedule_is_scheduling_only(sched, monkeypatch):
+    """Doc-blocked slice schedules (GF_DOCBLOCK_KB / GF_SLICE_MINRUNS), word
+    contexts and the heavy-first zdoc order are scheduling: the same schedule
+    is bit-deterministic, and against the flat schedule one iteration draws the
+    same topics except where fp32 S differs by association (a row's position
+    in a warp step changes the scan tree: ~1e-7 relative), the loglik agrees to
+    1e-6, and the theta K3 rebuilds from zdoc equals a recount of the z."""
+    K = 256
+    corp = synth.generate(1500, 3000, 250.0, seed=31)
+    ch = cp.partition(corp, 1, K, 7)[0]
+    a, b = 50.0 / K, 0.01
+
+    def run(kb, minruns):
+        monkeypatch.setenv("GF_DOCBLOCK_KB", kb)
+        monkeypatch.setenv("GF_SLICE_MINRUNS", minruns)
+        sh = DeviceShard(K, corp.vocab_size, a, b, seed=3).load(ch)
+        sh.initialize()
+        sh.sample(0)
+        ll = sh.loglik_sum()
+        sh.rebuild_phi()
+        sh.prepare()
+        sh.rebuild_theta()
+        sh.check_errors()
+        out = (sh.get_assignments(), sh.get_theta(), ll, sh.stats())
+        sh.close()
+        return out
+
+    z1, th1, ll1, st1 = run(*sched)
+    z1b, th1b, ll1b, _ = run(*sched)
+    z0, th0, ll0, st0 = run("1000000", "1000000000")
+    np.testing.assert_array_equal(z1, z1b)                   # deterministic
+    assert ll1 == ll1b
+    assert st0["doc_blocks"] == 1
+    if sched[0] != "1000000":
+        assert st1["doc_blocks"] > 1 and st1["word_contexts"] > 0 and st1["slices"] > st0["slices"]
+    assert np.mean(z1 == z0) > 0.9999
+    assert ll1 == pytest.approx(ll0, rel=1e-6)
+    rp, ids, cn = oracle.rebuild_theta(z1, ch.dw_ptr, ch.dw_tok, ch.doc_lo, K)
+    np.testing.assert_array_equal(th1[0], rp)
+    np.testing.assert_array_equal(th1[1], ids)
+    np.testing.assert_array_equal(th1[2], cn)

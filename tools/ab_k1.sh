@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B timing of the hot path under env-var tuning knobs (GPU box).
-# usage: tools/ab_k1.sh WORKLOAD STEPS "ENV1" "ENV2" ...   (ENV like "GF_DOCBLOCK_MB=16 GF_K1=1")
+# usage: tools/ab_k1.sh WORKLOAD STEPS "ENV1" "ENV2" ...   (ENV like "GF_DOCBLOCK_KB=16024 GF_K1=1")
 wl=$1; steps=$2; shift 2
 for cfg in "$@"; do
   env $cfg timeout 900 python bench.py --workload $wl --no-cpu-baseline --no-e2e --steps $steps > gpurun_out/ab.log 2>&1
