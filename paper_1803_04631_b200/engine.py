@@ -13,8 +13,10 @@ section 6.2):
     prepare           Eq. 1 denominators from the global n_k
 
 The allreduce is an integer sum, so the result equals SPEC's pairwise
-reduce_phi / broadcast_phi (SPEC.md:341-358) bit for bit; with the
-token-keyed Philox stream the trained model is identical for every G.
+reduce_phi / broadcast_phi bit for bit.  The Philox
+stream is keyed by token identity, so every G draws from the same uniforms;
+the trained models agree statistically (fp32 S sums may round differently
+when a shard's slice layout changes, which can flip a rare boundary draw).
 """
 
 import time
