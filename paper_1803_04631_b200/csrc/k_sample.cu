@@ -54,6 +54,11 @@ __device__ __forceinline__ void ldg256(const uint32_t* p, uint4& lo, uint4& hi) 
                  : "l"(p));
 }
 
+// TMA bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, bytes % 16 == 0)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // cp.async (LDGSTS) 16 B global -> shared, L2 only; src_bytes 0 zero-fills
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
@@ -70,6 +75,7 @@ struct SampleArgs {
     uint32_t iteration;
     uint32_t doc_lo;
     int eval_only;                            // loglik of the current model only
+    int prefetch;                             // bulk-prefetch each batch's theta rows into L2
     TreeGeom tree;
     const int4* slices;
     const uint32_t* run_doc;
@@ -376,6 +382,10 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
             off = m.x;
             nnz = m.y;
             nbytes += nnz;
+            // the whole row (32-byte granules) into L2 now: the pass then streams
+            // the batch's rows with every line already requested, instead of one
+            // 1 KB warp step in flight at a time
+            if (a.prefetch && nnz) prefetch_l2_bulk(a.theta_ent + off, ((nnz + 7u) & ~7u) * 4u);
         }
         const uint32_t gdoc = a.doc_lo + d;
         const uint32_t U = max(1u, (nnz + 3u) >> 2);          // row length in 16-byte vectors
@@ -648,6 +658,11 @@ static cudaError_t launch_variant(gf_shard* s, const SampleArgs& a) {
     return cudaGetLastError();
 }
 
+static int env_flag(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e && *e ? atoi(e) : dflt;
+}
+
 static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     SampleArgs a{};
     a.K = s->K;
@@ -659,6 +674,7 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     a.iteration = iteration;
     a.doc_lo = (uint32_t)s->doc_lo;
     a.eval_only = eval_only;
+    a.prefetch = (int)env_flag("GF_PREFETCH", 1);
     a.tree = s->tree;
     a.slices = s->d.slices;
     a.run_doc = s->d.run_doc;
