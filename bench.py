@@ -253,9 +253,7 @@ def run_ours(args, world, rank, local):
     shape, K = workload(args.workload, args.topics)
     corp = make_shard_corpus(shape, rank, args.seed)
     lo = rank * shape["num_docs"]
-    chunk = cp.make_chunk(rank, lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, corp.vocab_size, K,
-                          args.seed)
-    freq = np.bincount(chunk.word_ids, minlength=corp.vocab_size).astype(np.int64)
+    freq = np.bincount(corp.word_ids, minlength=corp.vocab_size).astype(np.int64)
     T_local = corp.num_tokens
     T_all = T_local
     if dist:
@@ -268,7 +266,13 @@ def run_ours(args, world, rank, local):
     stream = torch.cuda.current_stream(device)
     sh = DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=42, device=device, global_word_freq=freq,
                      stream=stream)
-    sh.load(chunk)
+    # K4: partition (stable word sort, dw-map, splitmix64 z0) + shard layout on
+    # the device, from the doc-major tokens of this rank's documents
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    sh.load_tokens(lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, seed=args.seed, chunk_id=rank)
+    torch.cuda.synchronize(device)
+    prep_s = time.perf_counter() - t0
     sync_t = sh.sync_tensor() if dist else None
 
     def allreduce_async():
@@ -409,6 +413,10 @@ def run_ours(args, world, rank, local):
             "loglik_per_token": ll,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "preprocess": {"value": T_local / prep_s, "unit": "tokens/s", "seconds": prep_s,
+                           "path": "DeviceShard.load_tokens: H2D of doc-major tokens + K4 partition (CUB radix "
+                                   "sorts, splitmix64 z0) + device layout (runs, slices, zdoc positions)",
+                           "reference": "gibbsflow partition(): ~3.6 s per 10M tokens single-threaded (SURVEY 6)"},
             "clocks": clocks.summary(),
             "gpu_launches": args.steps * launches_per_step,
         }

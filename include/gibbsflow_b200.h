@@ -67,6 +67,14 @@ int gf_partition_chunk(const int32_t* doc_ids, const int32_t* word_ids, int64_t 
                        int32_t* out_doc_ids, int32_t* out_word_ids, uint16_t* out_assignments,
                        int32_t* group_words, int64_t* group_offsets, int64_t* group_sizes,
                        int64_t* num_groups_out, int64_t* dw_ptr, int64_t* dw_tok);
+/* The same outputs as gf_partition_chunk, computed on device `device` (K4,
+ * bit-identical; replaces corpus.py:240-287 for one chunk). */
+int gf_partition_chunk_gpu(int device, const int32_t* doc_ids, const int32_t* word_ids, int64_t num_tokens,
+                           int64_t doc_lo, int64_t doc_hi, int32_t vocab_size, int32_t num_topics,
+                           uint64_t seed, int64_t chunk_id,
+                           int32_t* out_doc_ids, int32_t* out_word_ids, uint16_t* out_assignments,
+                           int32_t* group_words, int64_t* group_offsets, int64_t* group_sizes,
+                           int64_t* num_groups_out, int64_t* dw_ptr, int64_t* dw_tok);
 
 /* ------------------------------------------------ device shard context --
  * One document shard (= one Chunk, C = G, M = 1) resident in
@@ -93,6 +101,15 @@ int gf_shard_load(gf_shard* shard, int64_t doc_lo, int64_t doc_hi, int64_t num_t
                   const int32_t* doc_ids, const int32_t* word_ids, const uint16_t* assignments,
                   int64_t num_groups, const int32_t* group_words, const int64_t* group_offsets,
                   const int64_t* group_sizes, const int64_t* dw_ptr, const int64_t* dw_tok);
+
+/* K4, corpus.py:240-287 partition + corpus.py:201-207 _doc_word_map +
+ * rng.py:20-89 initial topics, on the device: load a shard straight from the
+ * DOC-MAJOR tokens of documents [doc_lo, doc_hi) (the Corpus slice
+ * corpus.py:253-255), chunk id `chunk_id`.  Same shard as partition() +
+ * gf_shard_load, without the host-side sort (stable CUB radix sorts by word
+ * and by local doc, splitmix64 z0 in fp64). */
+int gf_shard_load_tokens(gf_shard* shard, int64_t doc_lo, int64_t doc_hi, int64_t num_tokens,
+                         const int32_t* doc_ids, const int32_t* word_ids, uint64_t seed, int64_t chunk_id);
 
 /* model.py:142-161 rebuild_phi_replica: this shard's phi replica + n_k into the
  * sync buffer (overwritten). */

@@ -36,6 +36,8 @@ SIGNATURES = {
     "gf_stream_uniforms": (_int, [_u64, _u64, _i64, _p]),
     "gf_greedy_boundaries": (_int, [_p, _i64, _i64, _p]),
     "gf_partition_chunk": (_int, [_p, _p, _i64, _i64, _i64, _i32, _i32, _u64, _i64] + [_p] * 9),
+    "gf_partition_chunk_gpu": (_int, [_int, _p, _p, _i64, _i64, _i64, _i32, _i32, _u64, _i64] + [_p] * 9),
+    "gf_shard_load_tokens": (_int, [_p, _i64, _i64, _i64, _p, _p, _u64, _i64]),
     "gf_shard_create": (_int, [_pp, _int, _i32, _i32, _f64, _f64, _u64, _u32]),
     "gf_shard_destroy": (_int, [_p]),
     "gf_shard_set_stream": (_int, [_p, _p]),

@@ -139,8 +139,10 @@ def greedy_boundaries(doc_lengths, num_chunks):
     return [(int(out[2 * c]), int(out[2 * c + 1])) for c in range(num_chunks)]
 
 
-def make_chunk(chunk_id, lo, hi, doc_ids, word_ids, vocab_size, num_topics, seed):
-    """One chunk of partition() from its doc-major tokens (corpus.py:252-286)."""
+def make_chunk(chunk_id, lo, hi, doc_ids, word_ids, vocab_size, num_topics, seed, device=None):
+    """One chunk of partition() from its doc-major tokens (corpus.py:252-286):
+    on the host (native counting sorts), or with `device` on that GPU (K4:
+    stable radix sorts + splitmix64 z0 on the device; bit-identical)."""
     docs = _lib.carr(doc_ids, np.int32)
     words = _lib.carr(word_ids, np.int32)
     n = len(docs)
@@ -153,20 +155,24 @@ def make_chunk(chunk_id, lo, hi, doc_ids, word_ids, vocab_size, num_topics, seed
     ng = np.zeros(1, np.int64)
     dw_ptr = np.empty(hi - lo + 1, np.int64)
     dw_tok = np.empty(n, np.int64)
-    _lib.check(_lib.lib().gf_partition_chunk(
-        _lib.ptr(docs), _lib.ptr(words), n, lo, hi, vocab_size, num_topics,
-        int(seed) & 0xFFFFFFFFFFFFFFFF, chunk_id, _lib.ptr(out_doc), _lib.ptr(out_word),
-        _lib.ptr(out_z), _lib.ptr(gw), _lib.ptr(go), _lib.ptr(gs), _lib.ptr(ng),
-        _lib.ptr(dw_ptr), _lib.ptr(dw_tok)))
+    args = (_lib.ptr(docs), _lib.ptr(words), n, lo, hi, vocab_size, num_topics,
+            int(seed) & 0xFFFFFFFFFFFFFFFF, chunk_id, _lib.ptr(out_doc), _lib.ptr(out_word),
+            _lib.ptr(out_z), _lib.ptr(gw), _lib.ptr(go), _lib.ptr(gs), _lib.ptr(ng),
+            _lib.ptr(dw_ptr), _lib.ptr(dw_tok))
+    if device is None:
+        _lib.check(_lib.lib().gf_partition_chunk(*args))
+    else:
+        _lib.check(_lib.lib().gf_partition_chunk_gpu(int(device), *args))
     k = int(ng[0])
     return Chunk(chunk_id=chunk_id, doc_lo=lo, doc_hi=hi, token_count=n, doc_ids=out_doc,
                  word_ids=out_word, assignments=out_z, group_words=gw[:k].copy(),
                  group_offsets=go[:k].copy(), group_sizes=gs[:k].copy(), dw_ptr=dw_ptr, dw_tok=dw_tok)
 
 
-def partition(corpus, num_chunks, num_topics, seed):
+def partition(corpus, num_chunks, num_topics, seed, device=None):
     """corpus.py:240-287: C chunks of whole documents, word-grouped, with
-    initial topics from Stream(seed, chunk_id)."""
+    initial topics from Stream(seed, chunk_id).  `device`: run the sorts and
+    z0 on that GPU (K4, bit-identical to the host path)."""
     if num_chunks < 1:
         raise PartitionError("need at least one chunk")
     if not 1 <= num_topics < 2**16:
@@ -175,7 +181,7 @@ def partition(corpus, num_chunks, num_topics, seed):
     for cid, (lo, hi) in enumerate(greedy_boundaries(corpus.doc_lengths, num_chunks)):
         a, b = int(corpus.doc_ptr[lo]), int(corpus.doc_ptr[hi])
         chunks.append(make_chunk(cid, lo, hi, corpus.doc_ids[a:b], corpus.word_ids[a:b],
-                                 corpus.vocab_size, num_topics, seed))
+                                 corpus.vocab_size, num_topics, seed, device=device))
     return chunks
 
 

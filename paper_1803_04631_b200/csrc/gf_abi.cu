@@ -124,6 +124,22 @@ int set_layout(gf_shard* s) {
 }
 }  // namespace
 
+namespace gf {
+int shard_fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+int shard_cuda_fail(cudaError_t e, const char* what) { return cuda_fail(e, what); }
+int shard_set_layout(gf_shard* s) { return set_layout(s); }
+int64_t shard_env_int(const char* name, int64_t dflt) { return env_int(name, dflt); }
+void shard_free_device(gf_shard* s) { free_dev(s); }
+}  // namespace gf
+
 extern "C" {
 
 const char* gf_last_error(void) { return g_err.c_str(); }
@@ -295,214 +311,54 @@ int gf_shard_load(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const 
                   const int32_t* word_ids, const uint16_t* z, int64_t ng, const int32_t* gw, const int64_t* go,
                   const int64_t* gs, const int64_t* dw_ptr, const int64_t* dw_tok) {
     CU(cudaSetDevice(s->device), "cudaSetDevice");
-    const int K = s->K, V = s->V;
+    const int V = s->V;
     const int64_t D = doc_hi - doc_lo;
     if (D < 0 || T < 0) return fail(GF_ERR_SHAPE, "negative chunk size");
     if (T >= (int64_t)UINT32_MAX || D >= (int64_t)UINT32_MAX)
         return fail(GF_ERR_CAPACITY, "shard has %lld tokens: split the corpus over more shards", (long long)T);
-    // ---- validate the chunk (corpus.py:160-198 invariants) ----
+    // ---- validate the chunk's directory (corpus.py:160-198 invariants); the
+    // per-token checks run on the device (k_layout.cu k_check_chunk) ----
     int64_t covered = 0;
     for (int64_t g = 0; g < ng; ++g) {
         if (gw[g] < 0 || gw[g] >= V) return fail(GF_ERR_SHAPE, "group word %d outside [0, %d)", gw[g], V);
         if (go[g] < 0 || gs[g] < 0 || go[g] + gs[g] > T) return fail(GF_ERR_SHAPE, "group %lld out of range", (long long)g);
+        if (go[g] != covered) return fail(GF_ERR_SHAPE, "word groups are not consecutive in token order");
+        if (g > 0 && gw[g] <= gw[g - 1]) return fail(GF_ERR_SHAPE, "group words are not ascending");
         covered += gs[g];
     }
     if (covered != T) return fail(GF_ERR_SHAPE, "word groups cover %lld of %lld tokens", (long long)covered, (long long)T);
     if (dw_ptr[0] != 0 || dw_ptr[D] != T) return fail(GF_ERR_SHAPE, "doc-word map does not cover the chunk");
-    for (int64_t t = 0; t < T; ++t) {
-        if (z[t] >= K) return fail(GF_ERR_SHAPE, "assignment %d at token %lld >= K=%d", (int)z[t], (long long)t, K);
-        if (doc_ids[t] < doc_lo || doc_ids[t] >= doc_hi)
-            return fail(GF_ERR_SHAPE, "token %lld: document %d outside [%lld, %lld)", (long long)t, doc_ids[t],
-                        (long long)doc_lo, (long long)doc_hi);
-    }
-    for (int64_t g = 0; g < ng; ++g)
-        for (int64_t t = go[g]; t < go[g] + gs[g]; ++t)
-            if (word_ids[t] != gw[g]) return fail(GF_ERR_SHAPE, "token %lld is not in its word group", (long long)t);
-    // ---- phi layout ----
-    if (s->global_freq.empty()) {
-        s->global_freq.assign(V, 0);
-        for (int64_t g = 0; g < ng; ++g) s->global_freq[gw[g]] += gs[g];
-    }
-    if (int rc = set_layout(s)) return rc;
-    // ---- (doc, word) runs in token order ----
-    std::vector<uint32_t> run_doc, run_start;
-    run_doc.reserve((size_t)(T / 2 + 16));
-    run_start.reserve((size_t)(T / 2 + 16));
-    for (int64_t t = 0; t < T; ++t)
-        if (t == 0 || word_ids[t] != word_ids[t - 1] || doc_ids[t] != doc_ids[t - 1]) {
-            run_doc.push_back((uint32_t)(doc_ids[t] - doc_lo));
-            run_start.push_back((uint32_t)t);
-        }
-    const int64_t R = (int64_t)run_doc.size();
-    run_start.push_back((uint32_t)T);
-    // ---- document blocks: contiguous doc ranges whose theta rows fit in L2 ----
-    // K1 reads one theta row per (doc, word) run; scheduling the slices of all
-    // frequent words block by block keeps the rows being read L2-resident, so
-    // each row comes from HBM about once per block instead of once per run.
-    const int64_t blk_bytes = (int64_t)env_int("GF_DOCBLOCK_KB", 64 << 10) << 10;
-    const int64_t min_runs = env_int("GF_SLICE_MINRUNS", 1024);
-    std::vector<int32_t> doc_blk((size_t)D);
-    int32_t nblk = 0;
-    {
-        int64_t acc = 0;
-        for (int64_t d = 0; d < D; ++d) {
-            const int64_t L = dw_ptr[d + 1] - dw_ptr[d];
-            const int64_t b = 4 * ((std::min<int64_t>(K, L) + 7) & ~7LL);
-            if (acc > 0 && acc + b > blk_bytes) { ++nblk; acc = 0; }
-            doc_blk[d] = nblk;
-            acc += b;
-        }
-        ++nblk;
-    }
-    // ---- heavy-first slices (sort_word_groups_desc order, corpus.py:290-302) ----
-    // A slice is <= kSliceTokens tokens of one word; a frequent word is also cut
-    // at document-block boundaries (pieces of >= min_runs runs).  Slices are then
-    // ordered block-major (stable: heavy-first inside a block); slices spanning
-    // several blocks (rare words: random rows anyway) are spread round-robin.
-    std::vector<int64_t> order((size_t)ng);
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-        return gs[a] != gs[b] ? gs[a] > gs[b] : gw[a] < gw[b];
-    });
-    std::vector<int4> slices, items;
-    std::vector<int32_t> slice_key;
-    std::vector<uint8_t> word_blocked((size_t)V, 0);
-    int64_t rr = 0;
-    for (int64_t gi : order) {
-        if (gs[gi] == 0) continue;
-        const int32_t v = gw[gi];
-        const int col = s->word_col[v];
-        const int64_t t0 = go[gi], t1 = go[gi] + gs[gi];
-        int64_t rb = std::lower_bound(run_start.begin(), run_start.end() - 1, (uint32_t)t0) - run_start.begin();
-        const int64_t re = std::lower_bound(run_start.begin(), run_start.end() - 1, (uint32_t)t1) - run_start.begin();
-        const size_t first = slices.size();
-        const bool blocked = nblk > 1 && re - rb >= 2 * min_runs;
-        word_blocked[v] = blocked;
-        while (rb < re) {
-            const int32_t b0 = doc_blk[run_doc[rb]];
-            int64_t r = rb;
-            while (r < re && (int64_t)run_start[r] - (int64_t)run_start[rb] < gf::kSliceTokens &&
-                   !(blocked && r - rb >= min_runs && doc_blk[run_doc[r]] != b0 && re - r >= min_runs))
-                ++r;
-            slices.push_back(make_int4(v, (int)rb, (int)r, col));
-            const bool local = doc_blk[run_doc[r - 1]] - b0 <= 1;
-            slice_key.push_back(local ? b0 : (int32_t)(rr++ % nblk));
-            rb = r;
-        }
-        if (col >= 0) {
-            items.push_back(make_int4(col, (int)t0, (int)t1, 0));
-        } else {
-            const bool split = slices.size() - first > 1;
-            for (size_t i = first; i < slices.size(); ++i)
-                items.push_back(make_int4(col, (int)run_start[slices[i].y], (int)run_start[slices[i].z], split ? 1 : 0));
-        }
-    }
-    // word contexts: one per word cut into several slices (built once per iteration)
-    std::vector<int32_t> slice_ctx(slices.size(), -1), ctx_cols;
-    {
-        size_t i = 0;
-        while (i < slices.size()) {
-            size_t j = i;
-            while (j < slices.size() && slices[j].x == slices[i].x) ++j;
-            if (j - i > 1) {
-                for (size_t q = i; q < j; ++q) slice_ctx[q] = (int32_t)ctx_cols.size();
-                ctx_cols.push_back(slices[i].w);
-            }
-            i = j;
-        }
-    }
-    {
-        std::vector<int64_t> so(slices.size());
-        std::iota(so.begin(), so.end(), 0);
-        std::stable_sort(so.begin(), so.end(), [&](int64_t a, int64_t b) { return slice_key[a] < slice_key[b]; });
-        std::vector<int4> sorted(slices.size());
-        std::vector<int32_t> sctx(slices.size());
-        for (size_t i = 0; i < so.size(); ++i) { sorted[i] = slices[so[i]]; sctx[i] = slice_ctx[so[i]]; }
-        slices.swap(sorted);
-        slice_ctx.swap(sctx);
-    }
-    s->n_doc_blocks = nblk;
-    if ((int64_t)slices.size() >= (int64_t)INT32_MAX) return fail(GF_ERR_CAPACITY, "too many slices");
-    // ---- doc-word map and theta capacities ----
-    std::vector<uint32_t> dwp((size_t)D + 1);
-    for (int64_t d = 0; d <= D; ++d) dwp[d] = (uint32_t)dw_ptr[d];
-    for (int64_t t = 0; t < T; ++t)
-        if (dw_tok[t] < 0 || dw_tok[t] >= T) return fail(GF_ERR_SHAPE, "doc-word map entry out of range");
-    // doc-major position of every run (zdoc): per doc, the tokens of
-    // block-scheduled words first, then the rest, each in word-sorted order.
-    // K1 writes the heavy part of a block's docs while the block is
-    // L2-resident, so those zdoc sectors are written whole.
-    std::vector<uint32_t> dwpos((size_t)R);
-    {
-        std::vector<uint32_t> heavy_cnt((size_t)D, 0), hcur((size_t)D, 0), lcur((size_t)D, 0);
-        for (int64_t r = 0; r < R; ++r)
-            if (word_blocked[word_ids[run_start[r]]]) heavy_cnt[run_doc[r]] += run_start[r + 1] - run_start[r];
-        for (int64_t r = 0; r < R; ++r) {
-            const uint32_t d = run_doc[r], len = run_start[r + 1] - run_start[r];
-            if (word_blocked[word_ids[run_start[r]]]) { dwpos[r] = dwp[d] + hcur[d]; hcur[d] += len; }
-            else { dwpos[r] = dwp[d] + heavy_cnt[d] + lcur[d]; lcur[d] += len; }
-        }
-    }
-    std::vector<uint2> meta((size_t)D);
-    uint64_t cap = 0;
-    double llc = 0.0;
-    for (int64_t d = 0; d < D; ++d) {
-        const int64_t L = dw_ptr[d + 1] - dw_ptr[d];
-        if (L < 0) return fail(GF_ERR_SHAPE, "doc-word map not monotone");
-        meta[d] = make_uint2((uint32_t)cap, 0u);
-        // 8-entry (32-byte) granules: K1 streams rows with 256-bit loads
-        cap += (uint64_t)((std::min<int64_t>(K, L) + 7) & ~7LL);
-        if (L > 0) llc += (double)L * std::log((double)L + (double)K * s->alpha);
-        if (cap >= (uint64_t)UINT32_MAX) return fail(GF_ERR_CAPACITY, "theta rows exceed 2^32 entries");
-    }
-    s->ll_const = llc;
-    // ---- device buffers ----
-    free_dev(s);
-    auto& dv = s->d;
-    int rc;
-    if ((rc = dev_alloc(&dv.z, T, "z")) || (rc = dev_alloc(&dv.run_doc, R, "runs")) ||
-        (rc = dev_alloc(&dv.run_start, R + 1, "runs")) || (rc = dev_alloc(&dv.slices, slices.size(), "slices")) ||
-        (rc = dev_alloc(&dv.k2items, items.size(), "items")) || (rc = dev_alloc(&dv.dw_ptr, D + 1, "dw_ptr")) ||
-        (rc = dev_alloc(&dv.zdoc, T, "zdoc")) || (rc = dev_alloc(&dv.run_dwpos, R, "runs")) || (rc = dev_alloc(&dv.theta_ent, cap + 4, "theta")) ||
-        (rc = dev_alloc(&dv.theta_meta, D, "theta")) || (rc = dev_alloc(&dv.sync, s->sync_u32, "phi")) ||
-        (rc = dev_alloc(&dv.inv_den, 2 * K, "inv_den")) ||
-        (rc = dev_alloc(&dv.ctx_tab, ctx_cols.size() * (size_t)gf::context_floats(s), "contexts")) ||
-        (rc = dev_alloc(&dv.ctx_cols, ctx_cols.size(), "contexts")) ||
-        (rc = dev_alloc(&dv.slice_ctx, slices.size(), "contexts")) || (rc = dev_alloc(&dv.ll_part, slices.size(), "ll")) ||
-        (rc = dev_alloc(&dv.ll_sum, 1, "ll")) || (rc = dev_alloc(&dv.errs, 3, "errs")) ||
-        (rc = dev_alloc(&dv.bytes, 1, "bytes")))
-        return rc;
-    cudaStream_t st = s->stream;
-    CU(cudaMemcpyAsync(dv.z, z, T * 2, cudaMemcpyHostToDevice, st), "upload");
-    CU(cudaMemcpyAsync(dv.run_doc, run_doc.data(), R * 4, cudaMemcpyHostToDevice, st), "upload");
-    CU(cudaMemcpyAsync(dv.run_start, run_start.data(), (R + 1) * 4, cudaMemcpyHostToDevice, st), "upload");
-    CU(cudaMemcpyAsync(dv.slices, slices.data(), slices.size() * sizeof(int4), cudaMemcpyHostToDevice, st), "upload");
-    if (!ctx_cols.empty())
-        CU(cudaMemcpyAsync(dv.ctx_cols, ctx_cols.data(), ctx_cols.size() * 4, cudaMemcpyHostToDevice, st), "upload");
-    CU(cudaMemcpyAsync(dv.slice_ctx, slice_ctx.data(), slice_ctx.size() * 4, cudaMemcpyHostToDevice, st), "upload");
-    CU(cudaMemcpyAsync(dv.k2items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, st), "upload");
-    CU(cudaMemcpyAsync(dv.dw_ptr, dwp.data(), (D + 1) * 4, cudaMemcpyHostToDevice, st), "upload");
-    CU(cudaMemcpyAsync(dv.run_dwpos, dwpos.data(), R * 4, cudaMemcpyHostToDevice, st), "upload");
-    CU(cudaMemcpyAsync(dv.theta_meta, meta.data(), D * sizeof(uint2), cudaMemcpyHostToDevice, st), "upload");
-    CU(cudaMemsetAsync(dv.theta_ent, 0, (cap + 4) * 4, st), "memset");
-    CU(cudaMemsetAsync(dv.sync, 0, s->sync_u32 * 4, st), "memset");
-    CU(cudaMemsetAsync(dv.errs, 0xff, 24, st), "memset");
-    CU(cudaMemsetAsync(dv.bytes, 0, 8, st), "memset");
-    s->R = R;
-    CU(gf::launch_zdoc_sync(s), "load");
-    CU(cudaStreamSynchronize(st), "load");
-    s->doc_lo = doc_lo;
-    s->doc_hi = doc_hi;
-    s->D = D;
-    s->T = T;
-    s->R = R;
-    s->n_slices = (int64_t)slices.size();
-    s->n_k2 = (int64_t)items.size();
-    s->n_ctx = (int64_t)ctx_cols.size();
-    s->ctx_dirty = true;
-    s->theta_cap = (int64_t)cap;
-    s->loaded = true;
-    return GF_OK;
+    for (int64_t d = 0; d < D; ++d)
+        if (dw_ptr[d + 1] < dw_ptr[d]) return fail(GF_ERR_SHAPE, "doc-word map not monotone");
+    s->loaded = false;
+    return gf::load_chunk(s, doc_lo, doc_hi, T, doc_ids, word_ids, z, ng, gw, go, gs, dw_ptr, dw_tok);
+}
+
+int gf_shard_load_tokens(gf_shard* s, int64_t doc_lo, int64_t doc_hi, int64_t T, const int32_t* doc_ids,
+                         const int32_t* word_ids, uint64_t seed, int64_t chunk_id) {
+    CU(cudaSetDevice(s->device), "cudaSetDevice");
+    const int64_t D = doc_hi - doc_lo;
+    if (D < 0 || T < 0) return fail(GF_ERR_SHAPE, "negative chunk size");
+    if (T >= (int64_t)UINT32_MAX || D >= (int64_t)UINT32_MAX)
+        return fail(GF_ERR_CAPACITY, "shard has %lld tokens: split the corpus over more shards", (long long)T);
+    const uint64_t parts[2] = {seed, (uint64_t)chunk_id};
+    s->loaded = false;
+    return gf::load_tokens(s, doc_lo, doc_hi, T, doc_ids, word_ids, gf_stream_key(parts, 2));
+}
+
+int gf_partition_chunk_gpu(int device, const int32_t* doc_ids, const int32_t* word_ids, int64_t n, int64_t doc_lo,
+                           int64_t doc_hi, int32_t V, int32_t K, uint64_t seed, int64_t chunk_id, int32_t* out_doc,
+                           int32_t* out_word, uint16_t* out_z, int32_t* gw, int64_t* go, int64_t* gs, int64_t* ng_out,
+                           int64_t* dw_ptr, int64_t* dw_tok) {
+    if (K < 1 || K >= 65536) return fail(GF_ERR_VALUE, "topic count %d outside [1, 65536)", K);
+    if (n >= (int64_t)UINT32_MAX || doc_hi - doc_lo >= (int64_t)UINT32_MAX)
+        return fail(GF_ERR_CAPACITY, "chunk has %lld tokens: split the corpus into more chunks", (long long)n);
+    int ndev = 0;
+    gf_device_count(&ndev);
+    if (ndev == 0) return fail(GF_ERR_NODEVICE, "no CUDA device visible: use gf_partition_chunk on the host");
+    const uint64_t parts[2] = {seed, (uint64_t)chunk_id};
+    return gf::partition_to_host(device, doc_ids, word_ids, n, doc_lo, doc_hi, V, K, gf_stream_key(parts, 2), out_doc,
+                                 out_word, out_z, gw, go, gs, ng_out, dw_ptr, dw_tok);
 }
 
 static int need_loaded(gf_shard* s) {

@@ -96,6 +96,30 @@ struct gf_shard {
     bool dirty = false;                      // imported state not yet validated
 };
 
+// shard helpers shared by the ABI (gf_abi.cu) and the K4 layout builder (k_layout.cu)
+namespace gf {
+int shard_fail(int code, const char* fmt, ...);
+int shard_cuda_fail(cudaError_t e, const char* what);
+int shard_set_layout(gf_shard* s);
+int64_t shard_env_int(const char* name, int64_t dflt);
+void shard_free_device(gf_shard* s);
+template <class T>
+int shard_alloc(T** p, size_t count, const char* what) {
+    if (*p) { cudaFree(*p); *p = nullptr; }
+    cudaError_t e = cudaMalloc((void**)p, (count > 0 ? count : 1) * sizeof(T));
+    return e == cudaSuccess ? 0 : shard_cuda_fail(e, what);
+}
+// K4 (k_layout.cu)
+int load_chunk(gf_shard* s, int64_t lo, int64_t hi, int64_t T, const int32_t* doc_ids, const int32_t* word_ids,
+               const uint16_t* z, int64_t ng, const int32_t* gw, const int64_t* go, const int64_t* gs,
+               const int64_t* dw_ptr, const int64_t* dw_tok);
+int load_tokens(gf_shard* s, int64_t lo, int64_t hi, int64_t T, const int32_t* doc_ids, const int32_t* word_ids,
+                uint64_t zkey);
+int partition_to_host(int device, const int32_t* doc_ids, const int32_t* word_ids, int64_t n, int64_t lo, int64_t hi,
+                      int32_t V, int32_t K, uint64_t zkey, int32_t* out_doc, int32_t* out_word, uint16_t* out_z,
+                      int32_t* gw, int64_t* go, int64_t* gs, int64_t* ng_out, int64_t* dw_ptr, int64_t* dw_tok);
+}  // namespace gf
+
 // kernel launchers (k_sample.cu / k_counts.cu / k_ptree.cu)
 namespace gf {
 cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only = 0);

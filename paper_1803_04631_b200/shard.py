@@ -61,6 +61,7 @@ class DeviceShard:
                 raise ValueError("global_word_freq must have vocab_size entries")
             _lib.check(_lib.lib().gf_shard_set_vocab(self._h, _lib.ptr(f)))
         self.chunk = None
+        self._shape = (0, 0)
 
     # ---------------------------------------------------------------- life --
     def close(self):
@@ -99,6 +100,21 @@ class DeviceShard:
                                             _lib.ptr(go), _lib.ptr(gs), _lib.ptr(dp), _lib.ptr(dt)))
         self._keep = None
         self.chunk = c
+        self._shape = (int(c.token_count), int(c.doc_hi - c.doc_lo))
+        return self
+
+    def load_tokens(self, doc_lo, doc_hi, doc_ids, word_ids, seed, chunk_id=0):
+        """K4: load documents [doc_lo, doc_hi) straight from their doc-major
+        tokens (the Corpus slice, corpus.py:253-255) -- partition, dw-map,
+        splitmix64 z0 and the shard layout all on the device.  Equivalent to
+        load(make_chunk(chunk_id, doc_lo, doc_hi, doc_ids, word_ids, V, K, seed));
+        `chunk` stays None (export with get_assignments / get_theta / get_phi)."""
+        d = _lib.carr(doc_ids, np.int32)
+        w = _lib.carr(word_ids, np.int32)
+        _lib.check(_lib.lib().gf_shard_load_tokens(self._h, int(doc_lo), int(doc_hi), len(d), _lib.ptr(d),
+                                                   _lib.ptr(w), int(seed) & 0xFFFFFFFFFFFFFFFF, int(chunk_id)))
+        self.chunk = None
+        self._shape = (len(d), int(doc_hi - doc_lo))
         return self
 
     # -------------------------------------------------------------- kernels --
@@ -147,11 +163,11 @@ class DeviceShard:
     # --------------------------------------------------------- import/export --
     @property
     def num_tokens(self):
-        return int(self.chunk.token_count)
+        return self._shape[0]
 
     @property
     def num_docs(self):
-        return int(self.chunk.doc_hi - self.chunk.doc_lo)
+        return self._shape[1]
 
     def get_assignments(self):
         out = np.empty(self.num_tokens, np.uint16)

@@ -508,3 +508,81 @@ def test_slice_schedule_is_scheduling_only(sched, monkeypatch):
     np.testing.assert_array_equal(th1[0], rp)
     np.testing.assert_array_equal(th1[1], ids)
     np.testing.assert_array_equal(th1[2], cn)
+
+
+# ------------------------------------------------------------------ K4 ------
+@pytest.mark.parametrize("name", ["small", "single", "rand25", "zipf", "zipf_k1024"])
+def test_partition_gpu_matches_reference_golden(name):
+    """K4 (device radix sorts + splitmix64 z0 in fp64) reproduces the reference
+    partition() outputs bit for bit (tests/golden/partition.npz, made by the
+    reference's own corpus.partition)."""
+    g = np.load(os.path.join(GOLD, "partition.npz"))
+    m = next(x for x in json.loads(str(g["meta"])) if x["name"] == name)
+    corp = cp.corpus_from_tokens(g[f"{name}__corpus_doc_ids"], g[f"{name}__corpus_word_ids"], m["V"])
+    for ch in cp.partition(corp, m["C"], m["K"], m["seed"], device=0):
+        pre = f"{name}__c{ch.chunk_id}__"
+        assert [ch.doc_lo, ch.doc_hi, ch.token_count] == g[pre + "range"].tolist()
+        for f in ("doc_ids", "word_ids", "assignments", "group_words", "group_offsets", "group_sizes",
+                  "dw_ptr", "dw_tok"):
+            np.testing.assert_array_equal(getattr(ch, f), g[pre + f], err_msg=f)
+            assert getattr(ch, f).dtype == g[pre + f].dtype
+
+
+@pytest.mark.parametrize("K", [7, 1024, 65535])
+def test_partition_gpu_matches_host_on_larger_corpora(K):
+    corp = synth.generate(3000, 20000, 120.0, seed=K)
+    host = cp.partition(corp, 3, K, 99)
+    dev = cp.partition(corp, 3, K, 99, device=0)
+    for a, b in zip(host, dev):
+        for f in ("doc_ids", "word_ids", "assignments", "group_words", "group_offsets", "group_sizes",
+                  "dw_ptr", "dw_tok"):
+            np.testing.assert_array_equal(getattr(a, f), getattr(b, f), err_msg=f)
+
+
+def test_partition_gpu_input_errors():
+    with pytest.raises(ValueError):
+        cp.make_chunk(0, 0, 2, np.array([0, 1]), np.array([0, 9]), 5, 4, 1, device=0)
+    with pytest.raises(ValueError):
+        cp.make_chunk(0, 0, 2, np.array([0, 3]), np.array([0, 1]), 5, 4, 1, device=0)
+
+
+def test_load_tokens_equals_load_of_the_reference_chunk(monkeypatch):
+    """gf_shard_load_tokens (partition + layout on the device) builds the same
+    shard as partition() + gf_shard_load: same assignments, same counts, the
+    same draws (same slice schedule) and the same loglik."""
+    K = 256
+    corp = synth.generate(2500, 4000, 200.0, seed=12)
+    monkeypatch.setenv("GF_DOCBLOCK_KB", "256")
+    monkeypatch.setenv("GF_SLICE_MINRUNS", "16")
+    ch = cp.partition(corp, 1, K, 77)[0]
+    a, b = 50.0 / K, 0.01
+    outs = []
+    for mode in ("chunk", "tokens"):
+        sh = DeviceShard(K, corp.vocab_size, a, b, seed=5)
+        if mode == "chunk":
+            sh.load(ch)
+        else:
+            sh.load_tokens(0, corp.num_docs, corp.doc_ids, corp.word_ids, seed=77, chunk_id=0)
+        z0 = sh.get_assignments()
+        sh.initialize()
+        th0 = sh.get_theta()
+        for it in range(2):
+            sh.sample(it)
+            sh.rebuild_phi()
+            sh.prepare()
+            sh.rebuild_theta()
+        sh.check_errors()
+        outs.append((z0, th0, sh.get_assignments(), sh.get_phi(), sh.get_theta(), sh.loglik_sum(), sh.stats()))
+        sh.close()
+    (z0a, th0a, za, pa, tha, lla, sta), (z0b, th0b, zb, pb, thb, llb, stb) = outs
+    np.testing.assert_array_equal(z0a, ch.assignments)
+    np.testing.assert_array_equal(z0b, ch.assignments)
+    for x, y in zip(th0a, th0b):
+        np.testing.assert_array_equal(x, y)
+    assert sta["slices"] == stb["slices"] and sta["doc_blocks"] == stb["doc_blocks"] > 1
+    np.testing.assert_array_equal(za, zb)
+    np.testing.assert_array_equal(pa[0], pb[0])
+    np.testing.assert_array_equal(pa[1], pb[1])
+    for x, y in zip(tha, thb):
+        np.testing.assert_array_equal(x, y)
+    assert lla == llb
