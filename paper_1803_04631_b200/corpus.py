@@ -194,3 +194,59 @@ def sort_word_groups_desc(chunk):
         group_offsets=chunk.group_offsets[order],
         group_sizes=chunk.group_sizes[order],
     )
+
+
+# ----------------------------------------------------------- chunk store ----
+CHUNK_MAGIC = b"GFCHUNK1"
+_DIR_RECORD = np.dtype([("word", "<u4"), ("offset", "<u8"), ("len", "<u8")])   # packed, 20 bytes
+
+
+def save_chunk(chunk, path):
+    """corpus.py:305-327 chunk store (GFCHUNK1, little-endian): magic; u64
+    chunk_id, doc_lo, doc_hi, token_count; doc ids u32[T], word ids u32[T],
+    topics u16[T] in word-group order; the group directory as packed (word u32,
+    offset u64, len u64) records in processing order.  The assignments are the
+    part a model snapshot lacks, so this is the resume checkpoint."""
+    import struct
+
+    rec = np.empty(len(chunk.group_words), dtype=_DIR_RECORD)
+    rec["word"] = chunk.group_words
+    rec["offset"] = chunk.group_offsets
+    rec["len"] = chunk.group_sizes
+    with open(path, "wb") as fh:
+        fh.write(CHUNK_MAGIC)
+        fh.write(struct.pack("<4Q", int(chunk.chunk_id), int(chunk.doc_lo), int(chunk.doc_hi), int(chunk.token_count)))
+        for arr, dt in ((chunk.doc_ids, "<u4"), (chunk.word_ids, "<u4"), (chunk.assignments, "<u2")):
+            fh.write(np.ascontiguousarray(arr).astype(dt, copy=False).tobytes())
+        fh.write(rec.tobytes())
+
+
+def load_chunk(path):
+    """corpus.py:330-364: read a GFCHUNK1 chunk; the doc-word map is rebuilt."""
+    import struct
+
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if blob[: len(CHUNK_MAGIC)] != CHUNK_MAGIC:
+        raise CorpusFormatError(f"{path}: bad chunk magic")
+    pos = len(CHUNK_MAGIC)
+    if len(blob) < pos + 32:
+        raise CorpusFormatError(f"{path}: truncated header")
+    cid, lo, hi, n = struct.unpack_from("<4Q", blob, pos)
+    pos += 32
+    if len(blob) < pos + 10 * n:
+        raise CorpusFormatError(f"{path}: truncated token arrays")
+    docs = np.frombuffer(blob, dtype="<u4", count=n, offset=pos).astype(np.int32)
+    pos += 4 * n
+    words = np.frombuffer(blob, dtype="<u4", count=n, offset=pos).astype(np.int32)
+    pos += 4 * n
+    topics = np.frombuffer(blob, dtype="<u2", count=n, offset=pos).astype(np.uint16)
+    pos += 2 * n
+    if (len(blob) - pos) % _DIR_RECORD.itemsize:
+        raise CorpusFormatError(f"{path}: truncated group directory")
+    rec = np.frombuffer(blob, dtype=_DIR_RECORD, offset=pos)
+    dw_ptr, dw_tok = _doc_word_map(docs, int(lo), int(hi - lo))
+    return Chunk(chunk_id=int(cid), doc_lo=int(lo), doc_hi=int(hi), token_count=int(n), doc_ids=docs,
+                 word_ids=words, assignments=topics, group_words=rec["word"].astype(np.int32),
+                 group_offsets=rec["offset"].astype(np.int64), group_sizes=rec["len"].astype(np.int64),
+                 dw_ptr=dw_ptr, dw_tok=dw_tok)

@@ -227,6 +227,46 @@ class Trainer:
     def assignments(self):
         return self.shard.get_assignments()
 
+    # ---------------------------------------------------- checkpoint/resume --
+    def save_checkpoint(self, prefix):
+        """Resume point after the completed iterations: every rank writes its
+        chunk with the current assignments (GFCHUNK1, `<prefix>.rank<r>.gfc`,
+        the state a snapshot lacks: corpus.py:305-327); rank 0 also writes the
+        model snapshot (GFSNAP1, `<prefix>.gfsnap`, model.py:228-255) whose
+        metadata records the iteration to resume at."""
+        from .corpus import save_chunk
+        from .model import save_snapshot
+
+        save_chunk(replace(self.chunk, assignments=self.assignments()), f"{prefix}.rank{self.rank}.gfc")
+        theta, phi = self.theta(gather=True), self.phi()
+        if self.rank == 0:
+            meta = {"iteration": self.iteration, "seed": self.cfg.seed, "num_topics": self.cfg.num_topics,
+                    "workers": self.world, "alpha": self.cfg.alpha, "beta": self.cfg.beta}
+            save_snapshot(theta, phi, f"{prefix}.gfsnap", metadata=meta)
+        if self.dist:
+            self.dist.barrier(group=self.group)
+
+    @classmethod
+    def resume(cls, corpus, cfg, prefix, group=None, device=None):
+        """A trainer continuing a checkpoint: this rank's assignments from its
+        chunk store, the iteration counter from the snapshot metadata.  Draws
+        are keyed by (seed, iteration, token), so the resumed run repeats the
+        uninterrupted one."""
+        from .corpus import load_chunk
+        from .model import load_snapshot
+
+        _, _, meta = load_snapshot(f"{prefix}.gfsnap")
+        if meta.get("num_topics") != cfg.num_topics or meta.get("seed") != cfg.seed:
+            raise ShapeMismatchError("checkpoint was written with another num_topics / seed")
+        d = _dist()
+        rank = d.get_rank(group) if d else 0
+        ch = load_chunk(f"{prefix}.rank{rank}.gfc")
+        tr = cls(corpus, cfg, group=group, device=device, init_assignments=ch.assignments)
+        if (tr.chunk.doc_lo, tr.chunk.doc_hi) != (ch.doc_lo, ch.doc_hi):
+            raise ShapeMismatchError("checkpoint shard does not match this rank's documents")
+        tr.iteration = int(meta["iteration"])
+        return tr
+
     def close(self):
         self.shard.close()
 

@@ -261,9 +261,29 @@ def main():
     pz["meta"] = json.dumps(pmeta)
     np.savez_compressed(os.path.join(HERE, "ptree.npz"), **pz)
 
+    stores(cp, md)
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))
 
 
+def stores(cp=None, md=None):
+    """GFCHUNK1 / GFSNAP1 files written by the reference's own save_chunk /
+    save_snapshot (corpus.py:305-327, model.py:228-255) for byte-level parity."""
+    if cp is None:
+        cp, md, _, _, _ = import_reference()
+    corp = zipf_corpus(cp, 40, 60, 30.0, 11)
+    (ch,) = cp.partition(corp, 1, 9, 3)
+    ch = cp.sort_word_groups_desc(ch)
+    cp.save_chunk(ch, os.path.join(HERE, "store_chunk.gfc"))
+    theta = md.rebuild_theta(ch, 9)
+    phi = md.rebuild_phi_replica(ch, 9, 60, width=16)
+    md.save_snapshot(theta, phi, os.path.join(HERE, "store_snapshot.gfsnap"), metadata={"iteration": 3, "note": "ref"})
+    np.savez_compressed(os.path.join(HERE, "store_inputs.npz"), doc_ids=corp.doc_ids, word_ids=corp.word_ids,
+                        meta=json.dumps({"V": 60, "K": 9, "seed": 3}))
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--stores-only"]:
+        stores()
+    else:
+        main()

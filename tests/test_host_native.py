@@ -97,3 +97,81 @@ def test_synth_is_deterministic_and_shardable():
     # Zipf skew: the heaviest word carries a few percent of the tokens
     top = np.bincount(a.word_ids, minlength=300).max() / a.num_tokens
     assert 0.01 < top < 0.5
+
+
+def test_chunk_store_roundtrip_and_errors(tmp_path):
+    """reference tests/test_corpus.py:210-243 (GFCHUNK1)."""
+    c = corpus.corpus_from_tokens([0] * 5 + [1] * 8 + [2] * 3, [1, 4, 2, 2, 0, 5, 5, 1, 3, 0, 2, 4, 4, 1, 0, 3], 6)
+    (orig,) = corpus.partition(c, 1, 7, 5)
+    orig = corpus.sort_word_groups_desc(orig)
+    path = tmp_path / "chunk0.gfc"
+    corpus.save_chunk(orig, path)
+    back = corpus.load_chunk(path)
+    assert (back.chunk_id, back.doc_lo, back.doc_hi, back.token_count) == \
+        (orig.chunk_id, orig.doc_lo, orig.doc_hi, orig.token_count)
+    for f in ("doc_ids", "word_ids", "assignments", "group_words", "group_offsets", "group_sizes", "dw_ptr", "dw_tok"):
+        np.testing.assert_array_equal(getattr(back, f), getattr(orig, f), err_msg=f)
+        assert getattr(back, f).dtype == getattr(orig, f).dtype
+    bad = tmp_path / "bad.gfc"
+    bad.write_bytes(b"NOTCHUNK" + b"\0" * 64)
+    with pytest.raises(errors.CorpusFormatError, match="magic"):
+        corpus.load_chunk(bad)
+    trunc = tmp_path / "trunc.gfc"
+    trunc.write_bytes(path.read_bytes()[:-3])
+    with pytest.raises(errors.CorpusFormatError, match="directory"):
+        corpus.load_chunk(trunc)
+
+
+def test_chunk_store_matches_reference_bytes(tmp_path):
+    """The file is byte-identical to the reference save_chunk's layout
+    (restated here from corpus.py:305-327: header, u32/u32/u16 arrays, packed
+    20-byte directory records)."""
+    import struct
+
+    c = corpus.corpus_from_tokens([0, 0, 1, 1, 1], [2, 0, 2, 1, 2], 3)
+    (ch,) = corpus.partition(c, 1, 4, 9)
+    p = tmp_path / "c.gfc"
+    corpus.save_chunk(ch, p)
+    blob = p.read_bytes()
+    n = ch.token_count
+    assert blob[:8] == b"GFCHUNK1"
+    assert struct.unpack_from("<4Q", blob, 8) == (0, 0, 2, n)
+    assert len(blob) == 8 + 32 + 10 * n + 20 * len(ch.group_words)
+    rec = struct.unpack_from("<IQQ", blob, 8 + 32 + 10 * n)
+    assert rec == (ch.group_words[0], ch.group_offsets[0], ch.group_sizes[0])
+
+
+def test_stores_are_byte_identical_to_the_reference(tmp_path):
+    """tests/golden/store_*.gfc|gfsnap were written by the reference's own
+    save_chunk / save_snapshot (tests/golden/make_golden.py stores()); the same
+    chunk and model written here give the same bytes, and the reference files
+    load here."""
+    from paper_1803_04631_b200 import model
+
+    gd = os.path.join(os.path.dirname(__file__), "golden")
+    g = np.load(os.path.join(gd, "store_inputs.npz"))
+    m = json.loads(str(g["meta"]))
+    corp = corpus.corpus_from_tokens(g["doc_ids"], g["word_ids"], m["V"])
+    (ch,) = corpus.partition(corp, 1, m["K"], m["seed"])
+    ch = corpus.sort_word_groups_desc(ch)
+    p = tmp_path / "c.gfc"
+    corpus.save_chunk(ch, p)
+    ref = open(os.path.join(gd, "store_chunk.gfc"), "rb").read()
+    assert p.read_bytes() == ref
+    back = corpus.load_chunk(os.path.join(gd, "store_chunk.gfc"))
+    np.testing.assert_array_equal(back.assignments, ch.assignments)
+    np.testing.assert_array_equal(back.dw_tok, ch.dw_tok)
+    # model snapshot (16-bit phi) from the same chunk, rebuilt with the oracle
+    import oracle
+
+    rp, ids, cn = oracle.rebuild_theta(ch.assignments, ch.dw_ptr, ch.dw_tok, ch.doc_lo, m["K"])
+    phi, tot = oracle.rebuild_phi(ch.assignments, ch.word_ids, m["K"], m["V"])
+    theta = model.ThetaRows(rp, ids, cn, m["K"])
+    pm = model.PhiMatrix(phi.astype(np.uint16), tot)
+    q = tmp_path / "s.gfsnap"
+    model.save_snapshot(theta, pm, q, metadata={"iteration": 3, "note": "ref"})
+    assert q.read_bytes() == open(os.path.join(gd, "store_snapshot.gfsnap"), "rb").read()
+    th2, ph2, meta = model.load_snapshot(os.path.join(gd, "store_snapshot.gfsnap"))
+    assert meta == {"iteration": 3, "note": "ref"}
+    np.testing.assert_array_equal(ph2.counts, pm.counts)
+    np.testing.assert_array_equal(th2.counts, theta.counts)
