@@ -102,8 +102,11 @@ struct SampleArgs {
 // p*_ex[K] (natural) | Q-tree levels (natural) | Q guide[kGuide + 1] (u32) |
 // pad | warp buffers
 constexpr int kGuide = 256;                   // Q-prefix guide buckets (power of two)
+// p*_ex lives in shared memory for K <= 2048; above that it is evaluated on
+// demand (only a thinning test needs it) so a third CTA fits on the SM
+__host__ __device__ inline bool pex_in_smem(int K) { return K <= 2048; }
 __host__ __device__ inline int lay_pex(int K) { return (int)tpos_slots(K); }
-__host__ __device__ inline int lay_tree(int K) { return lay_pex(K) + K; }
+__host__ __device__ inline int lay_tree(int K) { return lay_pex(K) + (pex_in_smem(K) ? K : 0); }
 __host__ __device__ inline int lay_guide(int K, int tree_total) { return lay_tree(K) + tree_total; }
 __host__ __device__ inline int lay_buf(int K, int tree_total) { return (lay_guide(K, tree_total) + kGuide + 1 + 3) & ~3; }
 
@@ -170,6 +173,14 @@ __device__ __forceinline__ uint32_t row_count(const uint32_t* row, uint32_t nnz,
     return 0;
 }
 
+// p*_ex(z) = (phi_vz - 1 + b) / (n_z - 1 + V b): from the shared table, or for
+// large K from the word's phi column and the prepared reciprocal
+__device__ __forceinline__ float pex_of(const SampleArgs& a, const float* pex, int col, uint32_t z) {
+    if (pex_in_smem(a.K)) return pex[z];
+    const uint32_t ph = phi_at(a, col, (int)z);
+    return ph ? __fmul_rn(__fadd_rn((float)(ph - 1u), a.beta), __ldg(a.inv_den + a.K + z)) : 0.f;
+}
+
 // keep a draw of the token's own topic with probability p_ex(z) / p(z)
 __device__ __forceinline__ bool keep_own(float ut, uint32_t cnt, float alpha, float ps, float pex) {
     const float num = __fmul_rn(__fadd_rn((float)cnt - 1.f, alpha), pex);
@@ -181,7 +192,7 @@ __device__ __forceinline__ bool keep_own(float ut, uint32_t cnt, float alpha, fl
 // re-streamed per S-branch draw.  Returns S (all lanes).
 __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, float Q, uint32_t v, uint32_t gdoc,
                                        uint32_t t0, uint32_t t1, uint32_t off, uint32_t nnz, uint32_t dwp,
-                                       int lane) {
+                                       int col, int lane) {
     const float* pstar = smem;
     const float* pex = smem + lay_pex(a.K);
     const float* lvl = smem + lay_tree(a.K);
@@ -241,11 +252,12 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, f
                 if (k == zt) cnt = row_count(row, nnz, zt, a.tm);
             }
             if (k != zt) break;
-            if (zt >= (uint32_t)a.K || cnt == 0u || pex[zt] == 0.f) {
+            const float pz = zt < (uint32_t)a.K ? pex_of(a, pex, col, zt) : 0.f;
+            if (zt >= (uint32_t)a.K || cnt == 0u || pz == 0.f) {
                 if (lane == 0) atomicMin(a.errs, (unsigned long long)t);
                 break;
             }
-            if (keep_own(u.t, cnt, a.alpha, pstar[tpos(zt, a.tm)], pex[zt])) break;
+            if (keep_own(u.t, cnt, a.alpha, pstar[tpos(zt, a.tm)], pz)) break;
             k = zt;
         }
         if (lane == 0) { a.z[t] = (uint16_t)k; a.zdoc[dwp + occ] = (uint16_t)k; }
@@ -272,7 +284,7 @@ __device__ __forceinline__ void build_context(const SampleArgs& a, int col, floa
             const float ps = __fmul_rn(__fadd_rn((float)ph, a.beta), __ldg(a.inv_den + k));
             pstar[tpos((uint32_t)k, a.tm)] = ps;
             // (phi - 1 + b) / (n_k - 1 + V b), the reciprocal precomputed by prepare
-            pex[k] = ph ? __fmul_rn(__fadd_rn((float)(ph - 1u), a.beta), __ldg(a.inv_den + K + k)) : 0.f;
+            if (pex_in_smem(K)) pex[k] = ph ? __fmul_rn(__fadd_rn((float)(ph - 1u), a.beta), __ldg(a.inv_den + K + k)) : 0.f;
             acc = __fadd_rn(acc, __fmul_rn(a.alpha, ps));
             lvl[k] = acc;
         }
@@ -400,7 +412,7 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                 const float S = huge_run(a, smem, Q, v, __shfl_sync(kFull, gdoc, first),
                                          __shfl_sync(kFull, t0, first), __shfl_sync(kFull, t1, first),
                                          __shfl_sync(kFull, off, first), __shfl_sync(kFull, nnz, first),
-                                         __shfl_sync(kFull, dwp, first), lane);
+                                         __shfl_sync(kFull, dwp, first), col, lane);
                 if (lane == first) myS = S;
                 rem &= rem - 1u;
                 continue;
@@ -562,11 +574,12 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                                 if (k == zt) cnt = row_count(row, onnz, zt, a.tm);
                             }
                             if (k != zt) break;
-                            if (zt >= (uint32_t)K || cnt == 0u || pex[zt] == 0.f) {   // inconsistent state
+                            const float pz = zt < (uint32_t)K ? pex_of(a, pex, col, zt) : 0.f;
+                            if (zt >= (uint32_t)K || cnt == 0u || pz == 0.f) {   // inconsistent state
                                 atomicMin(a.errs, (unsigned long long)t);
                                 break;
                             }
-                            if (keep_own(u.t, cnt, a.alpha, pstar[tpos(zt, a.tm)], pex[zt])) break;
+                            if (keep_own(u.t, cnt, a.alpha, pstar[tpos(zt, a.tm)], pz)) break;
                             k = zt;                                                   // rejected: redraw
                         }
                         a.z[t] = (uint16_t)k;
@@ -728,15 +741,10 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
         const char* env = getenv("GF_K1");
         var = env ? atoi(env) : 0;
     }
-    if (s->K > (int)(4 * kCapV)) return launch_variant<kCapV, 3, 0, true>(s, a);
-    if (s->K > 2048 || var == 0) return launch_variant<kCapV, 4, 0, false>(s, a);
-    switch (var) {
-        case 2: return launch_variant<512, 3, 4, false>(s, a);
-        case 3: return launch_variant<1024, 3, 3, false>(s, a);
-        case 4: return launch_variant<256, 4, 4, false>(s, a);
-        case 5: return launch_variant<512, 4, 2, false>(s, a);
-        default: return launch_variant<512, 4, 3, false>(s, a);
-    }
+    if (s->K > (int)(4 * kCapV)) return launch_variant<kCapV, 3, 0, true>(s, a);   // rows can outgrow staging
+    if (s->K > 2048) return launch_variant<kCapV, 3, 0, false>(s, a);                // p*_ex on demand: 3 CTAs/SM
+    if (var == 1) return launch_variant<512, 4, 3, false>(s, a);                     // cp.async ring (A/B)
+    return launch_variant<kCapV, 4, 0, false>(s, a);
 }
 
 }  // namespace gf
