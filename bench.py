@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--cpu-sample-docs", type=int, default=0, help="docs in the bounded CPU sample (0: auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     return ap.parse_args()
 
 
@@ -243,13 +244,28 @@ def run_ours(args, world, rank, local):
     from paper_1803_04631_b200.shard import DeviceShard
 
     dist = None
+    # one rank per GPU; --dist-backend gloo (with more ranks than GPUs) is the
+    # single-GPU smoke test of the multi-rank path -- NCCL refuses two ranks on
+    # one device
+    device = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(device)
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    device = local
-    torch.cuda.set_device(device)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
+        else:
+            dist.init_process_group(args.dist_backend)
+
+    def ar(t, op=None, async_op=False):
+        """all_reduce; gloo gets a host copy of device tensors (smoke path)"""
+        op = dist.ReduceOp.SUM if op is None else op
+        if args.dist_backend == "gloo" and t.is_cuda:
+            c = t.cpu()
+            dist.all_reduce(c, op=op)
+            t.copy_(c)
+            return None
+        return dist.all_reduce(t, op=op, async_op=async_op)
     shape, K = workload(args.workload, args.topics)
     corp = make_shard_corpus(shape, rank, args.seed)
     lo = rank * shape["num_docs"]
@@ -258,10 +274,10 @@ def run_ours(args, world, rank, local):
     T_all = T_local
     if dist:
         t = torch.as_tensor(freq).cuda()
-        dist.all_reduce(t)
+        ar(t)
         freq = t.cpu().numpy()
         tt = torch.tensor([T_local], dtype=torch.int64, device="cuda")
-        dist.all_reduce(tt)
+        ar(tt)
         T_all = int(tt.item())
     stream = torch.cuda.current_stream(device)
     sh = DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=42, device=device, global_word_freq=freq,
@@ -276,7 +292,7 @@ def run_ours(args, world, rank, local):
     sync_t = sh.sync_tensor() if dist else None
 
     def allreduce_async():
-        return dist.all_reduce(sync_t, async_op=True) if dist else None
+        return ar(sync_t, async_op=True) if dist else None
 
     # initial counts
     sh.rebuild_phi()
@@ -338,14 +354,14 @@ def run_ours(args, world, rank, local):
     ms_total = start.elapsed_time(stop)
     if dist:
         t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ar(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
     value = T_all / (ms_step / 1e3)
     ll = sh.loglik_sum()
     if dist:
         t = torch.tensor([ll], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t)
+        ar(t)
         ll = float(t.item())
     ll /= T_all
     sh.check_errors()
@@ -378,7 +394,7 @@ def run_ours(args, world, rank, local):
         el = time.perf_counter() - t0
         if dist:
             t = torch.tensor([el], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ar(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         e2e = {"value": T_all * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": 2 * T_local,
                "d2h_bytes_per_step": 2 * T_local + 8, "api": "DeviceShard.set_assignments/iterate/"
@@ -399,7 +415,8 @@ def run_ours(args, world, rank, local):
                 "workload": f"{args.workload}-shaped synthetic LDA corpus, K={K}, one shard per GPU",
                 "docs_per_gpu": shape["num_docs"], "vocab": corp.vocab_size, "tokens_per_gpu": T_local,
                 "tokens_total": T_all, "topics": K, "iterations": [args.warmup, args.warmup + args.steps],
-                "parallelism": f"doc-shard dp{world} + NCCL allreduce of phi" if world > 1 else "dp1",
+                "parallelism": (f"doc-shard dp{world} + {args.dist_backend.upper()} allreduce of phi" if world > 1
+                                else "dp1"),
                 "l2": "inputs larger than L2 (z 2T B, theta 4*NNZ B, phi >= 200 MB vs 126 MB L2)",
                 "runs": st["runs"], "slices": st["slices"], "word_contexts": st["word_contexts"],
                 "doc_blocks": st["doc_blocks"],
