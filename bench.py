@@ -1,7 +1,7 @@
 """Benchmark: sampled tokens/s of the B200 CuLDA_CGS hot path (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload nytimes|pubmed|tiny] [--topics 1024]
+                    [--workload nytimes|pubmed|z4shard|tiny] [--topics 1024]
 
 A step is one full deferred training iteration over the shard (K1 sample +
 fused loglik, K2 phi rebuild, [NCCL allreduce of the phi sync buffer], K3
@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="nytimes", choices=["nytimes", "pubmed", "tiny"])
+    ap.add_argument("--workload", default="nytimes", choices=["nytimes", "pubmed", "tiny", "z4shard"])
     ap.add_argument("--topics", type=int, default=None)
     ap.add_argument("--seed", type=int, default=20261017)
     ap.add_argument("--cpu-sample-docs", type=int, default=0, help="docs in the bounded CPU sample (0: auto)")

@@ -4,6 +4,9 @@ Shapes used by the benchmark (BASELINE.json configs):
   tiny     D=1,000     V=1,000    mean length 100   (~100K tokens), K=32
   nytimes  D=299,752   V=101,636  mean length 332   (~99.5M tokens), K=1024
   pubmed   D=8,200,000 V=141,043  mean length 90    (~738M tokens), K=1024
+  z4shard  D=5,000,000 V=1,000,000 mean length 100  (~500M tokens): one GPU's
+           document shard of BASELINE configs[4] (~4B tokens, V=1M, K=1024,
+           doc-sharded across 8 B200s)
 """
 
 import numpy as np
@@ -15,6 +18,7 @@ SHAPES = {
     "tiny": dict(num_docs=1_000, vocab_size=1_000, mean_len=100.0),
     "nytimes": dict(num_docs=299_752, vocab_size=101_636, mean_len=332.08),
     "pubmed": dict(num_docs=8_200_000, vocab_size=141_043, mean_len=89.98),
+    "z4shard": dict(num_docs=5_000_000, vocab_size=1_000_000, mean_len=100.0),
 }
 
 
