@@ -383,12 +383,21 @@ def run_ours(args, world, rank, local):
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            sh.set_assignments(z_host)        # H2D of the step's input assignments
-            step(it)
+            # one step from host state: H2D of the input assignments, the counts
+            # of that state (K2 [+ allreduce] + prepare + K3 -- a rebuild from z
+            # needs no consistency validation), K1, D2H of the new assignments
+            # and of the loglik
+            sh.set_assignments(z_host)
+            sh.rebuild_phi()
+            w = allreduce_async()
+            if w:
+                w.wait()
+            sh.prepare()
+            sh.rebuild_theta()
+            sh.sample(it)
             it += 1
-            z_out[:] = 0
-            sh.get_assignments_into(z_out)    # D2H of the new assignments
-            lls = sh.loglik_sum()             # D2H of the step's loglik
+            sh.get_assignments_into(z_out)
+            lls = sh.loglik_sum()
             z_host, z_out = z_out, z_host
         barrier()
         el = time.perf_counter() - t0
@@ -397,8 +406,9 @@ def run_ours(args, world, rank, local):
             ar(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         e2e = {"value": T_all * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": 2 * T_local,
-               "d2h_bytes_per_step": 2 * T_local + 8, "api": "DeviceShard.set_assignments/iterate/"
-                                                            "get_assignments (C ABI, pinned host buffers)"}
+               "d2h_bytes_per_step": 2 * T_local + 8, "api": "DeviceShard.set_assignments, rebuild_phi/prepare/"
+                                                            "rebuild_theta, sample, get_assignments_into, loglik_sum "
+                                                            "(C ABI, pinned host buffers)"}
         del lls
 
     cpu = None

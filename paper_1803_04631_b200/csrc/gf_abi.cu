@@ -370,12 +370,14 @@ static int need_loaded(gf_shard* s) {
 int gf_shard_rebuild_phi(gf_shard* s) {
     if (int rc = need_loaded(s)) return rc;
     CU(gf::launch_phi_rebuild(s), "rebuild_phi");
+    s->stale_phi = false;
     return GF_OK;
 }
 
 int gf_shard_rebuild_theta(gf_shard* s) {
     if (int rc = need_loaded(s)) return rc;
     CU(gf::launch_theta_rebuild(s), "rebuild_theta");
+    s->stale_theta = false;
     return GF_OK;
 }
 
@@ -386,9 +388,9 @@ int gf_shard_prepare(gf_shard* s) {
 }
 
 static int validate_if_dirty(gf_shard* s) {
-    if (s->dirty) {
+    if (s->stale_theta || s->stale_phi) {
         CU(gf::launch_validate(s), "validate");
-        s->dirty = false;
+        s->stale_theta = s->stale_phi = false;
     }
     return GF_OK;
 }
@@ -493,7 +495,7 @@ int gf_shard_set_assignments(gf_shard* s, const uint16_t* in) {
     CU(cudaMemcpyAsync(s->d.z, in, s->T * 2, cudaMemcpyHostToDevice, s->stream), "set_assignments");
     CU(gf::launch_zdoc_sync(s), "set_assignments");
     CU(cudaStreamSynchronize(s->stream), "set_assignments");
-    s->dirty = true;
+    s->stale_theta = s->stale_phi = true;
     return GF_OK;
 }
 
@@ -568,7 +570,7 @@ int gf_shard_set_theta(gf_shard* s, const int64_t* row_ptr, const uint16_t* ids,
     cudaFree(drp);
     cudaFree(dids);
     if (e != cudaSuccess) return cuda_fail(e, "set_theta");
-    s->dirty = true;
+    s->stale_theta = true;
     return GF_OK;
 }
 
@@ -620,7 +622,7 @@ int gf_shard_set_phi(gf_shard* s, const uint32_t* counts_kv, const int64_t* tota
     cudaFree(din);
     cudaFree(dcol);
     if (e != cudaSuccess) return cuda_fail(e, "set_phi");
-    s->dirty = true;
+    s->stale_phi = true;
     return GF_OK;
 }
 

@@ -93,7 +93,10 @@ struct gf_shard {
     cudaEvent_t ev[6] = {};
     float last_ms[4] = {0, 0, 0, 0};
     bool timing = true;
-    bool dirty = false;                      // imported state not yet validated
+    // imported state not yet validated: an import (set_assignments / set_theta /
+    // set_phi) marks the count structures it may have made inconsistent; a
+    // rebuild from z makes that structure consistent by construction
+    bool stale_theta = false, stale_phi = false;
 };
 
 // shard helpers shared by the ABI (gf_abi.cu) and the K4 layout builder (k_layout.cu)
