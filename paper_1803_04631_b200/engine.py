@@ -247,7 +247,7 @@ class Trainer:
             self.dist.barrier(group=self.group)
 
     @classmethod
-    def resume(cls, corpus, cfg, prefix, group=None, device=None):
+    def resume(cls, corpus, cfg, prefix, group=None, device=None, shard_factory=None):
         """A trainer continuing a checkpoint: this rank's assignments from its
         chunk store, the iteration counter from the snapshot metadata.  Draws
         are keyed by (seed, iteration, token), so the resumed run repeats the
@@ -261,7 +261,8 @@ class Trainer:
         d = _dist()
         rank = d.get_rank(group) if d else 0
         ch = load_chunk(f"{prefix}.rank{rank}.gfc")
-        tr = cls(corpus, cfg, group=group, device=device, init_assignments=ch.assignments)
+        tr = cls(corpus, cfg, group=group, device=device, shard_factory=shard_factory,
+                 init_assignments=ch.assignments)
         if (tr.chunk.doc_lo, tr.chunk.doc_hi) != (ch.doc_lo, ch.doc_hi):
             raise ShapeMismatchError("checkpoint shard does not match this rank's documents")
         tr.iteration = int(meta["iteration"])
