@@ -41,6 +41,7 @@ extern "C" {
 #define GF_ERR_PARTITION 7   /* PartitionError        errors.py:12  */
 #define GF_ERR_EMPTY 8       /* EmptyDistributionError errors.py:24 */
 #define GF_ERR_NODEVICE 9    /* no CUDA device: the product path refuses to run */
+#define GF_ERR_FORMAT 10     /* CorpusFormatError     errors.py:8   (UCI input) */
 
 const char* gf_last_error(void);
 int gf_abi_version(void);
@@ -61,6 +62,15 @@ int gf_greedy_boundaries(const int64_t* doc_lengths, int64_t num_docs, int64_t n
 /* corpus.py:252-286, one chunk of partition(): inputs are the chunk's tokens in
  * corpus (doc-major) order; outputs are the Chunk arrays.  group_* must hold
  * V entries; *num_groups_out receives the used length. */
+/* corpus.py:79-145 load_uci_bow / _read_bow_header: validate a UCI docword
+ * file (header D, W, NNZ, then NNZ "docID wordID count" triples; same checks
+ * and error texts) and count its tokens; header = {D, W, NNZ}. */
+int gf_uci_scan(const char* docword_path, int64_t* header, int64_t* num_tokens);
+/* ... and expand it into doc-major tokens (corpus.py:42-76 corpus_from_tokens:
+ * stable document order, empty documents dropped, ids compacted). */
+int gf_uci_tokens(const char* docword_path, int64_t num_tokens, int32_t* doc_ids, int32_t* word_ids,
+                  int64_t* num_docs_out);
+
 int gf_partition_chunk(const int32_t* doc_ids, const int32_t* word_ids, int64_t num_tokens,
                        int64_t doc_lo, int64_t doc_hi, int32_t vocab_size, int32_t num_topics,
                        uint64_t seed, int64_t chunk_id,

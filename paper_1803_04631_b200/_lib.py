@@ -66,6 +66,8 @@ SIGNATURES = {
     "gf_shard_reset_stats": (_int, [_p]),
     "gf_shard_last_times": (_int, [_p, _p, _int]),
     "gf_ptree_sample": (_int, [_int, _p, _i64, _i32, _p, _i64, _p]),
+    "gf_uci_scan": (_int, [ctypes.c_char_p, _p, _p]),
+    "gf_uci_tokens": (_int, [ctypes.c_char_p, _i64, _p, _p, _p]),
     "gf_synth_lengths": (_int, [_u64, _i64, _i64, _f64, _f64, _p]),
     "gf_synth_tokens": (_int, [_u64, _i64, _i64, _p, _i32, _i32, _f64, _f64, _p, _p]),
 }
@@ -80,6 +82,7 @@ _ERRORS = {
     7: errors.PartitionError,
     8: errors.EmptyDistributionError,
     9: errors.NoDeviceError,
+    10: errors.CorpusFormatError,
 }
 
 _lib = None

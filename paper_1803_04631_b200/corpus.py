@@ -8,6 +8,7 @@ doc-word map, splitmix64 initial topics) runs in the native library
 reference (tests/test_host_native.py against tests/golden/partition.npz).
 """
 
+import os
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -59,6 +60,56 @@ def corpus_from_tokens(doc_ids, word_ids, vocab_size, vocab=None):
         word_ids=word_ids.astype(np.int32),
         vocab=vocab if vocab is not None else _LazyVocab(int(vocab_size)),
     )
+
+
+def _read_bow_header(lines):
+    """corpus.py:79-91: the three UCI header lines (D, W, NNZ)."""
+    if len(lines) < 3:
+        raise CorpusFormatError("docword header truncated: expected 3 lines")
+    out = []
+    for lineno, raw in enumerate(lines[:3], start=1):
+        try:
+            out.append(int(raw.strip()))
+        except ValueError:
+            raise CorpusFormatError(f"docword line {lineno}: malformed header value {raw.strip()!r}") from None
+    return tuple(out)
+
+
+def _read_vocab(vocab_path, num_words):
+    """corpus.py:148-157."""
+    with open(vocab_path, "r", encoding="utf-8") as fh:
+        vocab = [line.rstrip("\n") for line in fh]
+    while vocab and vocab[-1] == "":
+        vocab.pop()
+    if len(vocab) != num_words:
+        raise CorpusFormatError(f"vocab file has {len(vocab)} entries, docword header says {num_words}")
+    return vocab
+
+
+def load_uci_bow(docword_path, vocab_path):
+    """corpus.py:94-145: a UCI bag-of-words corpus (docword + vocab files).
+    Native parse (gf_uci_scan / gf_uci_tokens: same checks, same error texts)
+    and expansion of each "docID wordID count" triple into `count` tokens in
+    document order; empty documents are dropped."""
+    import ctypes
+
+    path = os.fsencode(docword_path)
+    hdr = np.zeros(3, np.int64)
+    n = ctypes.c_int64()
+    _lib.check(_lib.lib().gf_uci_scan(path, _lib.ptr(hdr), ctypes.byref(n)))
+    num_words = int(hdr[1])
+    vocab = _read_vocab(vocab_path, num_words)
+    if n.value == 0:
+        raise CorpusFormatError("corpus has no tokens")
+    docs = np.empty(n.value, np.int32)
+    words = np.empty(n.value, np.int32)
+    nd = ctypes.c_int64()
+    _lib.check(_lib.lib().gf_uci_tokens(path, n.value, _lib.ptr(docs), _lib.ptr(words), ctypes.byref(nd)))
+    lengths = np.bincount(docs, minlength=nd.value).astype(np.int64)
+    ptr = np.zeros(nd.value + 1, np.int64)
+    np.cumsum(lengths, out=ptr[1:])
+    return Corpus(num_docs=int(nd.value), vocab_size=num_words, num_tokens=int(n.value), doc_lengths=lengths,
+                  doc_ptr=ptr, doc_ids=docs, word_ids=words, vocab=vocab)
 
 
 class _LazyVocab(list):

@@ -280,6 +280,28 @@ def stores(cp=None, md=None):
     md.save_snapshot(theta, phi, os.path.join(HERE, "store_snapshot.gfsnap"), metadata={"iteration": 3, "note": "ref"})
     np.savez_compressed(os.path.join(HERE, "store_inputs.npz"), doc_ids=corp.doc_ids, word_ids=corp.word_ids,
                         meta=json.dumps({"V": 60, "K": 9, "seed": 3}))
+    # UCI bag of words (corpus.py:94-157): unsorted triples, empty documents,
+    # blank lines, padding spaces -- loaded by the reference itself
+    r = np.random.default_rng(5)
+    D, W = 40, 25
+    trip = {(int(d), int(w)): int(c) for d, w, c in zip(r.integers(1, D + 1, 300), r.integers(1, W + 1, 300),
+                                                          r.integers(1, 6, 300)) if d % 7}
+    items = list(trip.items())
+    r.shuffle(items)
+    lines = [str(D), " %d " % W, str(len(items))]
+    for i, ((d, w), c) in enumerate(items):
+        lines.append(f"{d}  {w} {c}" if i % 5 else f" {d} {w}\t{c} ")
+        if i % 17 == 0:
+            lines.append("   ")
+    with open(os.path.join(HERE, "uci_docword.txt"), "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+    with open(os.path.join(HERE, "uci_vocab.txt"), "w") as fh:
+        fh.write("\n".join(f"w{i}" for i in range(W)) + "\n\n")
+    c = cp.load_uci_bow(os.path.join(HERE, "uci_docword.txt"), os.path.join(HERE, "uci_vocab.txt"))
+    np.savez_compressed(os.path.join(HERE, "uci_expected.npz"), doc_ids=c.doc_ids, word_ids=c.word_ids,
+                        doc_lengths=c.doc_lengths, doc_ptr=c.doc_ptr, vocab=np.array(c.vocab),
+                        meta=json.dumps({"num_docs": c.num_docs, "vocab_size": c.vocab_size,
+                                         "num_tokens": c.num_tokens}))
 
 
 if __name__ == "__main__":

@@ -175,3 +175,69 @@ def test_stores_are_byte_identical_to_the_reference(tmp_path):
     assert meta == {"iteration": 3, "note": "ref"}
     np.testing.assert_array_equal(ph2.counts, pm.counts)
     np.testing.assert_array_equal(th2.counts, theta.counts)
+
+
+# ------------------------------------------------- UCI bag of words (8f-4) ---
+def _write_bow(tmp_path, header, triples, vocab):
+    """reference tests/test_corpus.py:8-14"""
+    docword = tmp_path / "docword.txt"
+    docword.write_text("\n".join([str(x) for x in header] + [f"{d} {w} {c}" for d, w, c in triples]) + "\n")
+    vocab_file = tmp_path / "vocab.txt"
+    vocab_file.write_text("\n".join(vocab) + "\n")
+    return str(docword), str(vocab_file)
+
+
+def test_uci_cases_of_the_reference_tests(tmp_path):
+    """reference tests/test_corpus.py:23-81 TestLoadUciBow, case by case."""
+    c = corpus.load_uci_bow(*_write_bow(tmp_path, (2, 3, 3), [(1, 1, 2), (1, 3, 1), (2, 2, 1)], ["a", "b", "c"]))
+    assert (c.num_docs, c.vocab_size, c.num_tokens) == (2, 3, 4)
+    assert c.doc_lengths.tolist() == [3, 1] and c.vocab == ["a", "b", "c"]
+    assert sorted(c.word_ids[c.doc_slice(0)].tolist()) == [0, 0, 2] and c.word_ids[c.doc_slice(1)].tolist() == [1]
+    c = corpus.load_uci_bow(*_write_bow(tmp_path, (1, 1, 1), [(1, 1, 1)], ["only"]))
+    assert (c.num_docs, c.vocab_size, c.num_tokens) == (1, 1, 1)
+    assert corpus._read_bow_header(["299752", "101636", "69679427"])[:2] == (299752, 101636)
+    c = corpus.load_uci_bow(*_write_bow(tmp_path, (4, 2, 2), [(1, 1, 2), (4, 2, 1)], ["a", "b"]))
+    assert c.num_docs == 2 and c.doc_lengths.tolist() == [2, 1]
+    cases = [((2, 3, "oops"), [], ["a", "b", "c"], "line 3"),
+             ((2, 3, 1), [(3, 1, 1)], ["a", "b", "c"], "docID 3"),
+             ((2, 3, 1), [(1, 9, 1)], ["a", "b", "c"], "wordID 9"),
+             ((2, 3, 1), [(1, 1, 0)], ["a", "b", "c"], "count 0"),
+             ((2, 3, 1), [(1, 1, 1)], ["a", "b"], "vocab"),
+             ((2, 3, 5), [(1, 1, 1)], ["a", "b", "c"], "expected 5")]
+    for hdr, trip, voc, match in cases:
+        with pytest.raises(errors.CorpusFormatError, match=match):
+            corpus.load_uci_bow(*_write_bow(tmp_path, hdr, trip, voc))
+
+
+def test_uci_messages_equal_the_reference_text(tmp_path):
+    """exact texts of corpus.py:84-91, 112-131, 154-156"""
+    def msg(hdr, trip, voc):
+        with pytest.raises(errors.CorpusFormatError) as e:
+            corpus.load_uci_bow(*_write_bow(tmp_path, hdr, trip, voc))
+        return str(e.value)
+    assert msg((2, 3, "oops"), [], ["a"]) == "docword line 3: malformed header value 'oops'"
+    assert msg((2, 3, 1), [(3, 1, 1)], ["a", "b", "c"]) == "docword line 4: docID 3 outside [1, 2]"
+    assert msg((2, 3, 2), [(1, 1, 1), (1, 9, 1)], ["a", "b", "c"]) == "docword line 5: wordID 9 outside [1, 3]"
+    assert msg((2, 3, 1), [(1, 1, 0)], ["a", "b", "c"]) == "docword line 4: count 0 must be > 0"
+    assert msg((2, 3, 1), [(1, 1, 1)], ["a", "b"]) == "vocab file has 2 entries, docword header says 3"
+    assert msg((2, 3, 5), [(1, 1, 1)], ["a", "b", "c"]) == "docword body: expected 5 triples, found 1"
+    p = tmp_path / "x.txt"
+    p.write_text("2\n3\n1\n1 1\n")
+    with pytest.raises(errors.CorpusFormatError, match="^docword line 4: expected 3 fields$"):
+        corpus.load_uci_bow(str(p), _write_bow(tmp_path, (1,), [], ["a", "b", "c"])[1])
+    p.write_text("2\n3\n")
+    with pytest.raises(errors.CorpusFormatError, match="header truncated"):
+        corpus.load_uci_bow(str(p), str(p))
+
+
+def test_uci_matches_the_reference_loader():
+    """tests/golden/uci_*: an unsorted file with empty documents, blank lines and
+    padded fields, loaded by the reference's load_uci_bow (make_golden.py)."""
+    gd = os.path.join(os.path.dirname(__file__), "golden")
+    g = np.load(os.path.join(gd, "uci_expected.npz"))
+    m = json.loads(str(g["meta"]))
+    c = corpus.load_uci_bow(os.path.join(gd, "uci_docword.txt"), os.path.join(gd, "uci_vocab.txt"))
+    assert (c.num_docs, c.vocab_size, c.num_tokens) == (m["num_docs"], m["vocab_size"], m["num_tokens"])
+    for f in ("doc_ids", "word_ids", "doc_lengths", "doc_ptr"):
+        np.testing.assert_array_equal(getattr(c, f), g[f], err_msg=f)
+    assert c.vocab == g["vocab"].tolist()
