@@ -137,13 +137,27 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
     for (int i = lane; i < k3_warp_u32(K); i += 32) bins[i] = 0u;
     __syncwarp();
     const unsigned lt = (1u << lane) - 1u;
-    for (int d = blockIdx.x * warps_per_cta + warp; d < D; d += gridDim.x * warps_per_cta) {
-        const uint32_t b = dw_ptr[d], L = dw_ptr[d + 1] - b;
-        const uint32_t off = theta_meta[d].x;
+    // software pipeline over this warp's documents d, d+s, d+2s: the next
+    // document's first 32 topics and the one after's (dw_ptr, meta) are in
+    // flight while the current one is counted
+    const int s = gridDim.x * warps_per_cta;
+    auto meta_of = [&](int dd, uint32_t& mb, uint32_t& mL, uint32_t& mo) {
+        mb = mL = mo = 0u;
+        if (dd < D) { mb = dw_ptr[dd]; mL = dw_ptr[dd + 1] - mb; mo = theta_meta[dd].x; }
+    };
+    int d = blockIdx.x * warps_per_cta + warp;
+    uint32_t b, L, off, b1, L1, o1;
+    meta_of(d, b, L, off);
+    meta_of(d + s, b1, L1, o1);
+    uint32_t zf = (d < D && (uint32_t)lane < L) ? zdoc[b + lane] : 0xffffu;   // first 32 topics of d
+    for (; d < D; d += s) {
+        uint32_t b2, L2, o2;
+        meta_of(d + 2 * s, b2, L2, o2);
+        const uint32_t zn = (d + s < D && (uint32_t)lane < L1) ? zdoc[b1 + lane] : 0xffffu;
         uint32_t nnz;
         if (L <= 32) {
             uint32_t key = 0xffffu;
-            if (lane < (int)L) key = zdoc[b + lane];
+            if (lane < (int)L) key = zf;
             if (key >= (uint32_t)K && lane < (int)L) { atomicMin(errs + 2, (unsigned long long)d); key = 0xffffu; }
             key = warp_bitonic_sort(key, lane);
             const uint32_t prev = __shfl_up_sync(kFull, key, 1);
@@ -156,15 +170,23 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
             }
             nnz = __popc(heads);
         } else {
-            for (uint32_t i = lane; i < L; i += 32) {
-                const uint32_t k = zdoc[b + i];
+            auto count = [&](uint32_t k) {
                 if (k < (uint32_t)K) {
                     atomicAdd(&bins[k], 1u);
                     atomicOr(&bmp[k >> 5], 1u << (k & 31u));
                 } else {
                     atomicMin(errs + 2, (unsigned long long)d);
                 }
-            }
+            };
+            // the next 96 topics load together (independent), then count
+            const uint32_t i1 = lane + 32u, i2 = lane + 64u, i3 = lane + 96u;
+            const uint32_t k1 = i1 < L ? zdoc[b + i1] : 0u, k2 = i2 < L ? zdoc[b + i2] : 0u,
+                           k3 = i3 < L ? zdoc[b + i3] : 0u;
+            count(zf);                                          // L > 32: every lane has one
+            if (i1 < L) count(k1);
+            if (i2 < L) count(k2);
+            if (i3 < L) count(k3);
+            for (uint32_t i = lane + 128u; i < L; i += 32) count(zdoc[b + i]);
             __syncwarp();
             uint32_t base = 0, mx = 0;
             for (int c = 0; c < NW; c += 32) {
@@ -198,6 +220,9 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
         // as 32-byte granules and relies on (count 0) pads contributing nothing
         if ((uint32_t)lane < ((8u - (nnz & 7u)) & 7u)) theta_ent[off + nnz + lane] = 0u;
         if (lane == 0) theta_meta[d].y = nnz;
+        b = b1; L = L1; off = o1;
+        b1 = b2; L1 = L2; o1 = o2;
+        zf = zn;
     }
 }
 
