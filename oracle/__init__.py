@@ -68,6 +68,9 @@ def lib():
         L.gfo_loglik_naive.restype = _f64
         L.gfo_loglik_naive.argtypes = [_i32, _i32, _f64, _f64, _i64, _p, _p, _p, _p, _p, _p, _p, _p,
                                        ctypes.c_int]
+        L.gfo_loglik_sq.restype = _f64
+        L.gfo_loglik_sq.argtypes = [_i32, _i32, _f64, _f64, _i64, _p, _p, _i64, _p, _p, _p, _p, _p, _p,
+                                    ctypes.c_int]
         _lib = L
     return _lib
 
@@ -285,6 +288,17 @@ def loglik_naive(K, V, alpha, beta, tok_doc, tok_word, th_ptr, th_ids, th_cnt, d
             _c(th_ids, np.uint16), _c(th_cnt, np.uint16), _c(doc_len, np.int64),
             _c(phi_counts, np.uint32), _c(phi_totals, np.int64)]
     return lib().gfo_loglik_naive(K, V, alpha, beta, len(args[0]), *[_ptr(a) for a in args], nthreads)
+
+
+def loglik_sq(K, V, alpha, beta, tok_doc, tok_word, doc_lo, th_ptr, th_ids, th_cnt, doc_len_local,
+              phi_counts, phi_totals, nthreads=0):
+    """SPEC.md:402-410 in the S + Q form, O(T K_d): word-grouped tokens (a
+    partitioned chunk), theta rows and doc lengths over the chunk's local docs."""
+    args = [_c(tok_doc, np.int32), _c(tok_word, np.int32)]
+    rest = [_c(th_ptr, np.int64), _c(th_ids, np.uint16), _c(th_cnt, np.uint16), _c(doc_len_local, np.int64),
+            _c(phi_counts, np.uint32), _c(phi_totals, np.int64)]
+    return lib().gfo_loglik_sq(K, V, alpha, beta, len(args[0]), _ptr(args[0]), _ptr(args[1]), int(doc_lo),
+                               *[_ptr(a) for a in rest], nthreads)
 
 
 # -------------------------------------------------------------- engine ------

@@ -496,3 +496,55 @@ double gfo_loglik_naive(int32_t K, int32_t V, double alpha, double beta, int64_t
     }
     return acc / (double)T;
 }
+
+/* loglik_per_token in the S + Q form (equal to SPEC.md:405 by
+ * sum_k (theta_dk + a) p*_vk = S_full + a sum_k p*_vk), O(T K_d + W K): tokens
+ * word-grouped (a partitioned chunk), theta rows over local docs
+ * [doc_lo, doc_lo + D), doc_len indexed locally.  Per-segment partials summed in
+ * segment order: deterministic for any thread count.  For large corpora where
+ * gfo_loglik_naive's O(T K) is too slow (tools/trajectory.py). */
+double gfo_loglik_sq(int32_t K, int32_t V, double alpha, double beta, int64_t T, const int32_t* tok_doc,
+                     const int32_t* tok_word, int64_t doc_lo, const int64_t* th_ptr, const uint16_t* th_ids,
+                     const uint16_t* th_cnt, const int64_t* doc_len, const uint32_t* phi, const int64_t* totals,
+                     int nthreads) {
+    if (T == 0) return 0.0;
+    int64_t* seg = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T + 1));
+    int64_t nseg = 0;
+    for (int64_t t = 0; t < T; ++t)
+        if (t == 0 || tok_word[t] != tok_word[t - 1]) seg[nseg++] = t;
+    seg[nseg] = T;
+    double* part = (double*)calloc((size_t)nseg, sizeof(double));
+    const double vb = (double)V * beta;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel
+#endif
+    {
+        double* pstar = (double*)malloc(sizeof(double) * (size_t)K);
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+        for (int64_t s = 0; s < nseg; ++s) {
+            const int32_t v = tok_word[seg[s]];
+            double q = 0.0;
+            for (int32_t k = 0; k < K; ++k) {
+                pstar[k] = ((double)phi[(int64_t)k * V + v] + beta) / ((double)totals[k] + vb);
+                q += alpha * pstar[k];
+            }
+            double acc = 0.0;
+            for (int64_t t = seg[s]; t < seg[s + 1]; ++t) {
+                const int64_t d = tok_doc[t] - doc_lo;
+                double sf = 0.0;
+                for (int64_t j = th_ptr[d]; j < th_ptr[d + 1]; ++j) sf += (double)th_cnt[j] * pstar[th_ids[j]];
+                acc += log((sf + q) / ((double)doc_len[d] + (double)K * alpha));
+            }
+            part[s] = acc;
+        }
+        free(pstar);
+    }
+    double total = 0.0;
+    for (int64_t s = 0; s < nseg; ++s) total += part[s];
+    free(part);
+    free(seg);
+    return total / (double)T;
+}

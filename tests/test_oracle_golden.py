@@ -356,3 +356,21 @@ def test_spec_reduce_examples():
         s, rounds = oracle.reduce_phi_pairwise(reps)
         np.testing.assert_array_equal(s, np.sum(reps, axis=0))
         assert len(rounds) == int(np.ceil(np.log2(G)))
+
+
+def test_loglik_sq_form_equals_naive_formula():
+    """The O(T K_d) S + Q form used for large trajectories equals SPEC.md:405."""
+    from paper_1803_04631_b200 import corpus as cp
+    from paper_1803_04631_b200 import synth
+
+    K = 24
+    corp = synth.generate(150, 300, 40.0, seed=4)
+    ch = cp.partition(corp, 1, K, 3)[0]
+    rp, ids, cn = oracle.rebuild_theta(ch.assignments, ch.dw_ptr, ch.dw_tok, 0, K)
+    phi, tot = oracle.rebuild_phi(ch.assignments, ch.word_ids, K, corp.vocab_size)
+    a, b = 50.0 / K, 0.01
+    naive = oracle.loglik_naive(K, corp.vocab_size, a, b, ch.doc_ids, ch.word_ids, rp, ids, cn,
+                                corp.doc_lengths, phi, tot)
+    sq = oracle.loglik_sq(K, corp.vocab_size, a, b, ch.doc_ids, ch.word_ids, 0, rp, ids, cn, corp.doc_lengths,
+                          phi, tot)
+    assert sq == pytest.approx(naive, rel=1e-12)
