@@ -50,9 +50,9 @@ def main():
     T = corp.num_tokens
 
     # ---- GPU ----
-    sh = DeviceShard(K, corp.vocab_size, a, b, seed=42).load(ch)
-    sh.initialize()
     st = torch.cuda.current_stream()
+    sh = DeviceShard(K, corp.vocab_size, a, b, seed=42, stream=st).load(ch)   # events bracket its kernels
+    sh.initialize()
     gpu_ll, gpu_t = [], []
     acc = 0.0
     for it in range(args.gpu_iters):
