@@ -612,3 +612,38 @@ def test_checkpoint_resume_repeats_the_uninterrupted_run(tmp_path):
     np.testing.assert_array_equal(tr.theta().counts, th_full.counts)
     assert first + rest == full
     tr.close()
+
+
+@pytest.mark.parametrize("K", [8192, 16384])
+def test_large_k_streaming_path(K):
+    """K > 4096: rows can outgrow the warp's staging buffer and take the
+    warp-cooperative streaming path (huge_run); draws agree with the oracle's
+    thin form and the counts stay exact."""
+    corp = synth.generate(60, 400, 9000.0, seed=K % 97)          # long documents: nnz up to ~K
+    ch = cp.partition(corp, 1, K, 5)[0]
+    a, b = 50.0 / K, 0.01
+    rp, ids, cn = oracle.rebuild_theta(ch.assignments, ch.dw_ptr, ch.dw_tok, 0, K)
+    assert np.diff(rp).max() > 4096                             # some rows need the streaming path
+    phi, tot = oracle.rebuild_phi(ch.assignments, ch.word_ids, K, corp.vocab_size)
+    with DeviceShard(K, corp.vocab_size, a, b, seed=9) as sh:
+        sh.load(ch)
+        sh.initialize()
+        sh.sample(0)
+        sh.check_errors()
+        z = sh.get_assignments()
+        ll = sh.loglik_sum() / corp.num_tokens
+        sh.rebuild_phi()
+        sh.prepare()
+        sh.rebuild_theta()
+        sh.check_errors()
+        grp, gids, gcn = sh.get_theta()
+    want = oracle.sample_tokens(K, corp.vocab_size, a, b, 9, 0, ch.doc_ids, ch.word_ids, ch.assignments, 0,
+                                rp, ids, cn, phi, tot, mode="thin")
+    assert np.mean(z == want) > 0.995
+    ll_ref = oracle.loglik_sq(K, corp.vocab_size, a, b, ch.doc_ids, ch.word_ids, 0, rp, ids, cn,
+                              corp.doc_lengths, phi, tot)
+    assert ll == pytest.approx(ll_ref, rel=1e-6)
+    r2, i2, c2 = oracle.rebuild_theta(z, ch.dw_ptr, ch.dw_tok, 0, K)
+    np.testing.assert_array_equal(grp, r2)
+    np.testing.assert_array_equal(gids, i2)
+    np.testing.assert_array_equal(gcn, c2)

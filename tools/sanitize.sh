@@ -1,0 +1,12 @@
+#!/bin/bash
+# compute-sanitizer passes over small end-to-end cases (GPU box): memcheck,
+# racecheck (shared-memory hazards), synccheck, initcheck.
+set -u
+PY='import __graft_entry__ as g; g.smoke()'
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 99 python -c "$PY" > gpurun_out/san_$tool.log 2>&1
+  echo "$tool rc=$? $(grep -m1 'ERROR SUMMARY' gpurun_out/san_$tool.log)"
+done
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py -m gpu -x -q \
+  -k "load_tokens or partition_gpu_matches_host or checkpoint or large_k" > gpurun_out/san_memcheck_tests.log 2>&1
+echo "memcheck(tests) rc=$? $(grep -m1 'ERROR SUMMARY' gpurun_out/san_memcheck_tests.log) $(tail -1 gpurun_out/san_memcheck_tests.log)"
