@@ -623,6 +623,7 @@ int gf_shard_set_phi(gf_shard* s, const uint32_t* counts_kv, const int64_t* tota
     cudaFree(dcol);
     if (e != cudaSuccess) return cuda_fail(e, "set_phi");
     s->stale_phi = true;
+    s->ctx_dirty = true;                     // denominators and word contexts follow the new phi
     return GF_OK;
 }
 

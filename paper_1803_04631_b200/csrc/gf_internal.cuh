@@ -27,7 +27,6 @@ namespace gf {
 
 constexpr int kSampleThreads = 256;         // 8 warps: 8 samplers share one Q-tree
 constexpr int kSliceTokens = 4096;          // tokens per sampler CTA (heavy words split)
-constexpr int kRowChunks = 4;               // theta entries cached per lane = 4 * kRowChunks
 constexpr int kMaxLevels = 5;
 
 struct TreeGeom {                            // Q-tree levels in shared memory
@@ -101,6 +100,13 @@ struct gf_shard {
 
 // shard helpers shared by the ABI (gf_abi.cu) and the K4 layout builder (k_layout.cu)
 namespace gf {
+// cudaFuncSetAttribute once per (kernel, device): `done` is the kernel's bit set of devices
+inline bool attr_once(unsigned long long& done, int device) {
+    const unsigned long long bit = 1ull << (device & 63);
+    if (done & bit) return false;
+    done |= bit;
+    return true;
+}
 int shard_fail(int code, const char* fmt, ...);
 int shard_cuda_fail(cudaError_t e, const char* what);
 int shard_set_layout(gf_shard* s);

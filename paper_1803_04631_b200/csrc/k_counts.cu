@@ -76,11 +76,10 @@ cudaError_t launch_phi_rebuild(gf_shard* s) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
     const size_t smem = (size_t)2 * s->K * sizeof(uint32_t);
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    if (attr_once(attr, s->device)) {
         e = cudaFuncSetAttribute(phi_rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     const int per_sm = smem <= 16 * 1024 ? 8 : (smem <= 48 * 1024 ? 4 : 1);
     const long long grid = std::min<long long>(s->n_k2, (long long)nsm * per_sm);
@@ -232,12 +231,11 @@ cudaError_t launch_theta_rebuild(gf_shard* s) {
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * per_warp > 96 * 1024) wpc >>= 1;
     const size_t smem = (size_t)wpc * per_warp;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    if (attr_once(attr, s->device)) {
         cudaError_t e = cudaFuncSetAttribute(theta_rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              200 * 1024);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     // persistent grid (exactly the resident CTAs): the warps sweep the
     // documents as one contiguous moving window, so the word-major z sectors

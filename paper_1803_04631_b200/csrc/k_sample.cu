@@ -44,7 +44,6 @@ constexpr int kWarps = kSampleThreads / 32;
 constexpr uint32_t kCapV = 1024;      // staged vector-end prefixes per warp (4096 entries)
 constexpr int kMaxRetry = 63;
 
-__device__ const uint4 g_zero16 = {0u, 0u, 0u, 0u};   // load target of idle lanes
 __device__ __align__(32) const uint32_t g_zero32[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256); p must be 32-byte aligned
@@ -657,15 +656,14 @@ size_t context_floats(const gf_shard* s) { return (size_t)lay_buf(s->K, s->tree.
 
 template <uint32_t CAPV, int MINB, int RING, bool HUGE>
 static cudaError_t launch_variant(gf_shard* s, const SampleArgs& a) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static unsigned long long attr_set = 0;
+    if (attr_once(attr_set, s->device)) {
         cudaError_t e = cudaFuncSetAttribute(sample_kernel<CAPV, MINB, RING, HUGE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(sample_kernel<CAPV, MINB, RING, HUGE>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     sample_kernel<CAPV, MINB, RING, HUGE><<<(unsigned)s->n_slices, kSampleThreads, smem_for(s, CAPV, RING), s->stream>>>(a);
     return cudaGetLastError();
@@ -716,11 +714,10 @@ cudaError_t launch_contexts(gf_shard* s) {
     if (s->n_ctx == 0) return cudaSuccess;
     const SampleArgs a = make_args(s, 0, 0);
     const size_t smem = (size_t)a.ctx_stride * sizeof(float);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static unsigned long long attr_set = 0;
+    if (attr_once(attr_set, s->device)) {
         cudaError_t e = cudaFuncSetAttribute(context_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     context_kernel<<<(unsigned)s->n_ctx, kSampleThreads, smem, s->stream>>>(a, s->d.ctx_cols, s->d.ctx_tab);
     return cudaGetLastError();

@@ -5,7 +5,7 @@ uses the iteration-start theta / phi snapshot, the token's own contribution
 excluded, two independent uniforms.  The
 draw runs in K1 (csrc/k_sample.cu); the RNG is Philox4x32-10 keyed by `seed`
 with counter (global doc, word, occurrence in its (doc, word) run, iteration),
-so results do not depend on the shard / GPU count.
+so every shard / GPU count draws from the same uniforms.
 """
 
 from dataclasses import dataclass
