@@ -412,7 +412,7 @@ def run_ours(args, world, rank, local):
         del lls
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:      # rank 0 at N=1 only
         nd = args.cpu_sample_docs or (shape["num_docs"] if args.workload == "tiny" else 20000)
         cpu = cpu_baseline(shape, K, args.seed, nd)
 
