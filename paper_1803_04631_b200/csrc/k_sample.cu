@@ -75,6 +75,7 @@ struct SampleArgs {
     uint32_t doc_lo;
     int eval_only;                            // loglik of the current model only
     int prefetch;                             // bulk-prefetch each batch's theta rows into L2
+    int guide_min_tokens;                     // slices below this build no Q guide
     TreeGeom tree;
     const int4* slices;
     const uint32_t* run_doc;
@@ -267,7 +268,8 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, f
 // The word context of SPEC.md build_word_context in shared
 // memory: p*(k), p*_ex(k) and the 32-ary Q prefix tree over a p*(k) (block
 // scan; ptree.build levels).  Ends with a __syncthreads.
-__device__ __forceinline__ void build_context(const SampleArgs& a, int col, float* smem, int tid) {
+__device__ __forceinline__ void build_context(const SampleArgs& a, int col, float* smem, int tid,
+                                              bool with_guide = true) {
     const int K = a.K, lane = tid & 31, warp = tid >> 5;
     float* pstar = smem;                             // transposed layout (tpos)
     float* pex = smem + lay_pex(K);
@@ -313,6 +315,8 @@ __device__ __forceinline__ void build_context(const SampleArgs& a, int col, floa
     // Q draw with target t = fl(u Q), j = floor(u G), has thr_j <= t <= thr_j+1
     // (rounding is monotone), so its answer lies in [guide[j], guide[j+1]] and a
     // search of that range returns exactly the full-range result.
+    // (skipped for small slices: too few Q draws to repay 257 searches)
+    if (!with_guide) return;
     uint32_t* guide = reinterpret_cast<uint32_t*>(smem + lay_guide(K, a.tree.total));
     const float Q = lvl[K - 1];
     for (int j = tid; j <= kGuide; j += kSampleThreads)
@@ -356,12 +360,15 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
     // ---------------- prologue: the word context (p*, p*_ex, Q-tree) ----------------
     if (tid == 0) next_run = sl.y;
     const int ctx = a.slice_ctx[blockIdx.x];
+    // the Q guide pays off only for slices with many tokens (contexts always have one)
+    bool guided = __ldg(a.run_start + sl.z) - __ldg(a.run_start + sl.y) >= (uint32_t)a.guide_min_tokens;
     if (ctx >= 0) {                                  // word split into several slices: copy (L2)
         const float4* src = reinterpret_cast<const float4*>(a.ctx_tab + (size_t)ctx * a.ctx_stride);
         for (int i = tid; i < a.ctx_stride / 4; i += kSampleThreads) reinterpret_cast<float4*>(smem)[i] = __ldg(src + i);
         __syncthreads();
+        guided = true;
     } else {
-        build_context(a, col, smem, tid);
+        build_context(a, col, smem, tid, guided);
     }
     const float Q = lvl[K - 1];
     const float* lvl0 = lvl;
@@ -549,8 +556,8 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
                             const float target = __fmul_rn(u.s, isS ? S : Q);
                             // Q: only the guide bucket [guide[j], guide[j+1]] (exact, see build_context)
                             const uint32_t gj = (uint32_t)(u.s * (float)kGuide);
-                            const uint32_t qlo = isS ? 0u : guide[gj];
-                            const uint32_t qn = isS ? oUp : guide[gj + 1] - qlo + 1u;
+                            const uint32_t qlo = (isS || !guided) ? 0u : guide[gj];
+                            const uint32_t qn = isS ? oUp : (guided ? guide[gj + 1] - qlo + 1u : (uint32_t)K);
                             uint32_t g = first_above((isS ? seg : lvl0) + qlo, qn, target) + qlo;
                             uint32_t cnt = 0;
                             if (isS) {
@@ -686,6 +693,7 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     a.doc_lo = (uint32_t)s->doc_lo;
     a.eval_only = eval_only;
     a.prefetch = (int)env_flag("GF_PREFETCH", 1);
+    a.guide_min_tokens = (int)env_flag("GF_GUIDE_MIN", 512);
     a.tree = s->tree;
     a.slices = s->d.slices;
     a.run_doc = s->d.run_doc;
