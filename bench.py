@@ -377,17 +377,32 @@ def run_ours(args, world, rank, local):
     # ---- end to end through the public API with host buffers (pinned) ----
     e2e = None
     if not args.no_e2e:
-        z_host = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
-        z_out = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
-        z_host[:] = sh.get_assignments()
+        # one step from host state: H2D of the input assignments (pinned), the
+        # counts of that state (K2 [+ allreduce] + prepare + K3: a rebuild from z
+        # needs no consistency validation), K1, D2H of the new assignments and of
+        # the loglik.  The copies go in chunks on two copy streams: chunk c of
+        # the step's output is read back and, as soon as it lands, sent as chunk
+        # c of the next step's input, so the two PCIe directions run concurrently.
+        z_in = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
+        z_io = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
+        z_in[:] = sh.get_assignments()
+        nchunk = 16
+        bounds = np.linspace(0, T_local, nchunk + 1).astype(np.int64)
+        d2h_s, h2d_s = torch.cuda.Stream(device), torch.cuda.Stream(device)
+
+        def upload(host, after=None):
+            for c in range(nchunk):
+                if after is not None:
+                    h2d_s.wait_event(after[c])
+                sh.copy_assignments_async(host, bounds[c], bounds[c + 1] - bounds[c], True, h2d_s)
+            return h2d_s.record_event()
+
         barrier()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            # one step from host state: H2D of the input assignments, the counts
-            # of that state (K2 [+ allreduce] + prepare + K3 -- a rebuild from z
-            # needs no consistency validation), K1, D2H of the new assignments
-            # and of the loglik
-            sh.set_assignments(z_host)
+        ev_in = upload(z_in)
+        for i in range(args.steps):
+            stream.wait_event(ev_in)
+            sh.assignments_imported()
             sh.rebuild_phi()
             w = allreduce_async()
             if w:
@@ -396,9 +411,16 @@ def run_ours(args, world, rank, local):
             sh.rebuild_theta()
             sh.sample(it)
             it += 1
-            sh.get_assignments_into(z_out)
-            lls = sh.loglik_sum()
-            z_host, z_out = z_out, z_host
+            ev_k1 = stream.record_event()
+            d2h_s.wait_event(ev_k1)
+            landed = []
+            for c in range(nchunk):
+                sh.copy_assignments_async(z_io, bounds[c], bounds[c + 1] - bounds[c], False, d2h_s)
+                landed.append(d2h_s.record_event())
+            if i + 1 < args.steps:
+                ev_in = upload(z_io, after=landed)
+            lls = sh.loglik_sum()             # D2H of the step's loglik
+        torch.cuda.synchronize(device)
         barrier()
         el = time.perf_counter() - t0
         if dist:
@@ -406,9 +428,10 @@ def run_ours(args, world, rank, local):
             ar(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         e2e = {"value": T_all * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": 2 * T_local,
-               "d2h_bytes_per_step": 2 * T_local + 8, "api": "DeviceShard.set_assignments, rebuild_phi/prepare/"
-                                                            "rebuild_theta, sample, get_assignments_into, loglik_sum "
-                                                            "(C ABI, pinned host buffers)"}
+               "d2h_bytes_per_step": 2 * T_local + 8,
+               "api": "DeviceShard.copy_assignments_async (16 chunks per direction, two copy streams, pinned "
+                      "host buffers) + assignments_imported, rebuild_phi/prepare/rebuild_theta, sample, "
+                      "loglik_sum (C ABI)"}
         del lls
 
     cpu = None

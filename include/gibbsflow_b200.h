@@ -164,6 +164,14 @@ int gf_sync_layout(const int64_t* global_word_freq, int32_t vocab_size, int32_t 
 /* import / export (host buffers, caller-allocated) */
 int gf_shard_get_assignments(gf_shard* shard, uint16_t* out);      /* word-group order */
 int gf_shard_set_assignments(gf_shard* shard, const uint16_t* in);
+/* Asynchronous piecewise transfer of assignments [offset, offset + count) between
+ * a (pinned) host buffer and the shard, on `stream` (a cudaStream_t; NULL: the
+ * shard's stream), direction 1 = host -> device, 0 = device -> host.  After a
+ * complete host -> device import, gf_shard_assignments_imported (stream-ordered
+ * after the copies) refreshes the doc-major copy and marks the counts stale. */
+int gf_shard_copy_assignments_async(gf_shard* shard, void* host, int64_t offset, int64_t count, int to_device,
+                                    void* stream);
+int gf_shard_assignments_imported(gf_shard* shard);
 int gf_shard_theta_nnz(gf_shard* shard, int64_t* nnz_out);
 /* ThetaRows (model.py:20-47) of the shard's docs: row_ptr[D_s+1] (local), ids, counts */
 int gf_shard_get_theta(gf_shard* shard, int64_t* row_ptr, uint16_t* topic_ids, uint16_t* counts);

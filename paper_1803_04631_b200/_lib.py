@@ -56,6 +56,8 @@ SIGNATURES = {
     "gf_sync_layout": (_int, [_p, _i32, _i32, _u32, _p, _p]),
     "gf_shard_get_assignments": (_int, [_p, _p]),
     "gf_shard_set_assignments": (_int, [_p, _p]),
+    "gf_shard_copy_assignments_async": (_int, [_p, _p, _i64, _i64, _int, _p]),
+    "gf_shard_assignments_imported": (_int, [_p]),
     "gf_shard_theta_nnz": (_int, [_p, _p]),
     "gf_shard_get_theta": (_int, [_p, _p, _p, _p]),
     "gf_shard_set_theta": (_int, [_p, _p, _p, _p]),

@@ -499,6 +499,25 @@ int gf_shard_set_assignments(gf_shard* s, const uint16_t* in) {
     return GF_OK;
 }
 
+int gf_shard_copy_assignments_async(gf_shard* s, void* host, int64_t offset, int64_t count, int to_device,
+                                    void* stream) {
+    if (int rc = need_loaded(s)) return rc;
+    if (offset < 0 || count < 0 || offset + count > s->T) return fail(GF_ERR_SHAPE, "assignment range out of bounds");
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    uint16_t* dev = s->d.z + offset;
+    uint16_t* h = static_cast<uint16_t*>(host) + offset;
+    if (to_device) CU(cudaMemcpyAsync(dev, h, count * 2, cudaMemcpyHostToDevice, st), "copy_assignments");
+    else CU(cudaMemcpyAsync(h, dev, count * 2, cudaMemcpyDeviceToHost, st), "copy_assignments");
+    return GF_OK;
+}
+
+int gf_shard_assignments_imported(gf_shard* s) {
+    if (int rc = need_loaded(s)) return rc;
+    CU(gf::launch_zdoc_sync(s), "assignments_imported");
+    s->stale_theta = s->stale_phi = true;
+    return GF_OK;
+}
+
 static int fetch_meta(gf_shard* s, std::vector<uint2>& meta) {
     meta.resize((size_t)s->D);
     if (s->D) CU(cudaMemcpyAsync(meta.data(), s->d.theta_meta, s->D * sizeof(uint2), cudaMemcpyDeviceToHost, s->stream),

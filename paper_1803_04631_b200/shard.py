@@ -186,6 +186,22 @@ class DeviceShard:
             raise ValueError("assignments length mismatch")
         _lib.check(_lib.lib().gf_shard_set_assignments(self._h, _lib.ptr(z)))
 
+    def copy_assignments_async(self, host, offset, count, to_device, stream=None):
+        """Asynchronous copy of assignments [offset, offset + count) between the
+        pinned uint16 `host` array (full length) and the device, on `stream`
+        (torch.cuda.Stream / raw handle; None: the shard's stream)."""
+        if host.dtype != np.uint16 or not host.flags.c_contiguous or len(host) != self.num_tokens:
+            raise ValueError("host must be a contiguous uint16 array of num_tokens entries")
+        handle = getattr(stream, "cuda_stream", stream)
+        _lib.check(_lib.lib().gf_shard_copy_assignments_async(
+            self._h, _lib.ptr(host), int(offset), int(count), 1 if to_device else 0,
+            ctypes.c_void_p(int(handle)) if handle else None))
+
+    def assignments_imported(self):
+        """After a complete host -> device import by copy_assignments_async
+        (stream-ordered after it): refresh the doc-major copy, counts go stale."""
+        _lib.check(_lib.lib().gf_shard_assignments_imported(self._h))
+
     def get_theta(self):
         """(row_ptr int64[D_s+1], topic_ids uint16, counts uint16) of local rows."""
         nnz = ctypes.c_int64()

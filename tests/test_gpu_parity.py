@@ -647,3 +647,48 @@ def test_large_k_streaming_path(K):
     np.testing.assert_array_equal(grp, r2)
     np.testing.assert_array_equal(gids, i2)
     np.testing.assert_array_equal(gcn, c2)
+
+
+def test_async_chunked_assignment_copies():
+    """copy_assignments_async (chunks, copy streams) + assignments_imported: the
+    e2e path of bench.py -- what comes back is what the device holds, and an
+    imported state rebuilds the reference counts."""
+    import torch
+
+    K = 32
+    corp = synth.generate(300, 600, 50.0, seed=14)
+    ch = cp.partition(corp, 1, K, 2)[0]
+    T = corp.num_tokens
+    host = torch.empty(T, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=1, stream=torch.cuda.current_stream()) as sh:
+        sh.load(ch)
+        sh.initialize()
+        sh.sample(0)
+        cuts = np.linspace(0, T, 7).astype(int)
+        torch.cuda.current_stream().synchronize()
+        for c in range(6):
+            sh.copy_assignments_async(host, cuts[c], cuts[c + 1] - cuts[c], False, s1 if c % 2 else s2)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(host, sh.get_assignments())
+        new = ((host.astype(np.int64) * 7 + 3) % K).astype(np.uint16)
+        host[:] = new
+        for c in range(6):
+            sh.copy_assignments_async(host, cuts[c], cuts[c + 1] - cuts[c], True, s1)
+        torch.cuda.current_stream().wait_stream(s1)
+        sh.assignments_imported()
+        sh.rebuild_phi()
+        sh.prepare()
+        sh.rebuild_theta()
+        sh.check_errors()
+        np.testing.assert_array_equal(sh.get_assignments(), new)
+        rp, ids, cn = oracle.rebuild_theta(new, ch.dw_ptr, ch.dw_tok, 0, K)
+        grp, gids, gcn = sh.get_theta()
+        np.testing.assert_array_equal(grp, rp)
+        np.testing.assert_array_equal(gids, ids)
+        np.testing.assert_array_equal(gcn, cn)
+        phi, tot = oracle.rebuild_phi(new, ch.word_ids, K, corp.vocab_size)
+        gphi, gtot = sh.get_phi()
+        np.testing.assert_array_equal(gphi, phi)
+        with pytest.raises(errors.ShapeMismatchError):
+            sh.copy_assignments_async(host, T - 1, 5, True)
