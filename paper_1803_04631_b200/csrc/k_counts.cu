@@ -32,10 +32,23 @@ __global__ void __launch_bounds__(256) phi_rebuild_kernel(const int4* __restrict
         const int4 w = items[it];
         const int col = w.x, t0 = w.y, t1 = w.z;
         const bool atomic = w.w != 0;
-        for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-            const int k = z[t];
+        // 16-byte loads (8 topics per thread) over the 8-aligned body, scalar head/tail
+        auto count = [&](int t, int k) {
             if (k < K) atomicAdd(&bins[k], 1u);
             else atomicMin(errs, (unsigned long long)t);
+        };
+        const int a0 = min(t1, (t0 + 7) & ~7), a1 = max(a0, t1 & ~7);
+        for (int t = t0 + threadIdx.x; t < a0; t += blockDim.x) count(t, z[t]);
+        for (int t = a1 + threadIdx.x; t < t1; t += blockDim.x) count(t, z[t]);
+        const uint4* zv = reinterpret_cast<const uint4*>(z);
+        for (int q = (a0 >> 3) + threadIdx.x; q < (a1 >> 3); q += blockDim.x) {
+            const uint4 v = __ldg(zv + q);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                count(8 * q + 2 * i, (int)(w[i] & 0xffffu));
+                count(8 * q + 2 * i + 1, (int)(w[i] >> 16));
+            }
         }
         __syncthreads();
         if ((long long)(t1 - t0) * 8 >= K) {
