@@ -249,7 +249,9 @@ def run_ours(args, world, rank, local):
     # one device
     device = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(device)
-    if world > 1:
+    # GF_FORCE_DIST=1: run the distributed code path even with one rank (a
+    # one-rank NCCL group exercises the sync-buffer allreduce on one GPU)
+    if world > 1 or os.environ.get("GF_FORCE_DIST") == "1":
         import torch.distributed as dist
 
         if args.dist_backend == "nccl":
@@ -448,7 +450,7 @@ def run_ours(args, world, rank, local):
                 "workload": f"{args.workload}-shaped synthetic LDA corpus, K={K}, one shard per GPU",
                 "docs_per_gpu": shape["num_docs"], "vocab": corp.vocab_size, "tokens_per_gpu": T_local,
                 "tokens_total": T_all, "topics": K, "iterations": [args.warmup, args.warmup + args.steps],
-                "parallelism": (f"doc-shard dp{world} + {args.dist_backend.upper()} allreduce of phi" if world > 1
+                "parallelism": (f"doc-shard dp{world} + {args.dist_backend.upper()} allreduce of phi" if dist
                                 else "dp1"),
                 "l2": "inputs larger than L2 (z 2T B, theta 4*NNZ B, phi >= 200 MB vs 126 MB L2)",
                 "runs": st["runs"], "slices": st["slices"], "word_contexts": st["word_contexts"],
