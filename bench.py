@@ -388,7 +388,7 @@ def run_ours(args, world, rank, local):
         z_in = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
         z_io = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
         z_in[:] = sh.get_assignments()
-        nchunk = 16
+        nchunk = int(os.environ.get("GF_E2E_CHUNKS", "16"))
         bounds = np.linspace(0, T_local, nchunk + 1).astype(np.int64)
         d2h_s, h2d_s = torch.cuda.Stream(device), torch.cuda.Stream(device)
 
