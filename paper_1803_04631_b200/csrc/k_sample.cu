@@ -40,7 +40,6 @@
 
 namespace gf {
 
-constexpr int kWarps = kSampleThreads / 32;
 constexpr uint32_t kCapV = 1024;      // staged vector-end prefixes per warp (4096 entries)
 constexpr int kMaxRetry = 63;
 
@@ -268,14 +267,16 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, f
 // The word context of SPEC.md build_word_context in shared
 // memory: p*(k), p*_ex(k) and the 32-ary Q prefix tree over a p*(k) (block
 // scan; ptree.build levels).  Ends with a __syncthreads.
+template <int NT>
 __device__ __forceinline__ void build_context(const SampleArgs& a, int col, float* smem, int tid,
                                               bool with_guide = true) {
+    constexpr int NW = NT / 32;
     const int K = a.K, lane = tid & 31, warp = tid >> 5;
     float* pstar = smem;                             // transposed layout (tpos)
     float* pex = smem + lay_pex(K);
     float* lvl = smem + lay_tree(K);
-    __shared__ float wtot[kWarps];
-    const int ipt = (K + kSampleThreads - 1) / kSampleThreads;
+    __shared__ float wtot[NW];
+    const int ipt = (K + NT - 1) / NT;
     const int k0 = tid * ipt;
     float acc = 0.f;
     for (int i = 0; i < ipt; ++i) {
@@ -295,7 +296,7 @@ __device__ __forceinline__ void build_context(const SampleArgs& a, int col, floa
     __syncthreads();
     if (tid == 0) {
         float run = 0.f;
-        for (int w = 0; w < kWarps; ++w) { const float t = wtot[w]; wtot[w] = run; run = __fadd_rn(run, t); }
+        for (int w = 0; w < NW; ++w) { const float t = wtot[w]; wtot[w] = run; run = __fadd_rn(run, t); }
     }
     __syncthreads();
     float excl = __shfl_up_sync(kFull, incl, 1);
@@ -307,7 +308,7 @@ __device__ __forceinline__ void build_context(const SampleArgs& a, int col, floa
     }
     __syncthreads();
     for (int l = 1; l < a.tree.nlev; ++l) {
-        for (int i = tid; i < a.tree.len[l]; i += kSampleThreads)
+        for (int i = tid; i < a.tree.len[l]; i += NT)
             lvl[a.tree.off[l] + i] = lvl[a.tree.off[l - 1] + min(32 * i + 31, a.tree.len[l - 1] - 1)];
         __syncthreads();
     }
@@ -319,7 +320,7 @@ __device__ __forceinline__ void build_context(const SampleArgs& a, int col, floa
     if (!with_guide) return;
     uint32_t* guide = reinterpret_cast<uint32_t*>(smem + lay_guide(K, a.tree.total));
     const float Q = lvl[K - 1];
-    for (int j = tid; j <= kGuide; j += kSampleThreads)
+    for (int j = tid; j <= kGuide; j += NT)
         guide[j] = first_above(lvl, (uint32_t)K, __fmul_rn((float)j * (1.f / kGuide), Q));
     __syncthreads();
 }
@@ -327,20 +328,22 @@ __device__ __forceinline__ void build_context(const SampleArgs& a, int col, floa
 // One CTA per word that the schedule splits into several slices: its context
 // is built once per iteration (same code, so bit-identical) and the slices
 // copy it instead of rebuilding it.
-__global__ void __launch_bounds__(kSampleThreads) context_kernel(SampleArgs a, const int32_t* __restrict__ cols,
+template <int NT>
+__global__ void __launch_bounds__(NT) context_kernel(SampleArgs a, const int32_t* __restrict__ cols,
                                                                   float* out) {
     extern __shared__ float smem[];
-    build_context(a, cols[blockIdx.x], smem, threadIdx.x);
+    build_context<NT>(a, cols[blockIdx.x], smem, threadIdx.x);
     float4* dst = reinterpret_cast<float4*>(out + (size_t)blockIdx.x * a.ctx_stride);
-    for (int i = threadIdx.x; i < a.ctx_stride / 4; i += kSampleThreads) dst[i] = reinterpret_cast<const float4*>(smem)[i];
+    for (int i = threadIdx.x; i < a.ctx_stride / 4; i += NT) dst[i] = reinterpret_cast<const float4*>(smem)[i];
 }
 
 // CAPV: staged vector ends per warp; MINB: CTAs per SM; RING: depth of the
 // per-warp cp.async ring of pass steps (0: direct 256-bit loads); HUGE:
 // compile the streaming path (needed only when K > 4*CAPV)
 constexpr uint32_t VEC = 2;                  // 16-byte vectors per lane per pass step (32 B)
-template <uint32_t CAPV, int MINB, int RING, bool HUGE>
-__global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs a) {
+template <int NT, uint32_t CAPV, int MINB, int RING, bool HUGE>
+__global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
+    constexpr int kWarps = NT / 32;
     extern __shared__ float smem[];
     const int K = a.K;
     float* pstar = smem;                            // p*(tpos(k))  (byte offset = theta topic field)
@@ -364,11 +367,11 @@ __global__ void __launch_bounds__(kSampleThreads, MINB) sample_kernel(SampleArgs
     bool guided = __ldg(a.run_start + sl.z) - __ldg(a.run_start + sl.y) >= (uint32_t)a.guide_min_tokens;
     if (ctx >= 0) {                                  // word split into several slices: copy (L2)
         const float4* src = reinterpret_cast<const float4*>(a.ctx_tab + (size_t)ctx * a.ctx_stride);
-        for (int i = tid; i < a.ctx_stride / 4; i += kSampleThreads) reinterpret_cast<float4*>(smem)[i] = __ldg(src + i);
+        for (int i = tid; i < a.ctx_stride / 4; i += NT) reinterpret_cast<float4*>(smem)[i] = __ldg(src + i);
         __syncthreads();
         guided = true;
     } else {
-        build_context(a, col, smem, tid, guided);
+        build_context<NT>(a, col, smem, tid, guided);
     }
     const float Q = lvl[K - 1];
     const float* lvl0 = lvl;
@@ -654,25 +657,25 @@ cudaError_t launch_validate(gf_shard* s) {
     return cudaGetLastError();
 }
 
-static size_t smem_for(const gf_shard* s, uint32_t capv, int ring) {
-    return (size_t)(lay_buf(s->K, s->tree.total) + kWarps * capv) * sizeof(float) + (size_t)kWarps * ring * 1024;
+static size_t smem_for(const gf_shard* s, int nt, uint32_t capv, int ring) {
+    return (size_t)(lay_buf(s->K, s->tree.total) + (nt / 32) * capv) * sizeof(float) + (size_t)(nt / 32) * ring * 1024;
 }
 
-size_t sample_smem_bytes(const gf_shard* s) { return smem_for(s, kCapV, 0); }
+size_t sample_smem_bytes(const gf_shard* s) { return smem_for(s, kSampleThreads, kCapV, 0); }
 size_t context_floats(const gf_shard* s) { return (size_t)lay_buf(s->K, s->tree.total); }
 
-template <uint32_t CAPV, int MINB, int RING, bool HUGE>
+template <int NT, uint32_t CAPV, int MINB, int RING, bool HUGE>
 static cudaError_t launch_variant(gf_shard* s, const SampleArgs& a) {
     static unsigned long long attr_set = 0;
     if (attr_once(attr_set, s->device)) {
-        cudaError_t e = cudaFuncSetAttribute(sample_kernel<CAPV, MINB, RING, HUGE>,
+        cudaError_t e = cudaFuncSetAttribute(sample_kernel<NT, CAPV, MINB, RING, HUGE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(sample_kernel<CAPV, MINB, RING, HUGE>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        e = cudaFuncSetAttribute(sample_kernel<NT, CAPV, MINB, RING, HUGE>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
     }
-    sample_kernel<CAPV, MINB, RING, HUGE><<<(unsigned)s->n_slices, kSampleThreads, smem_for(s, CAPV, RING), s->stream>>>(a);
+    sample_kernel<NT, CAPV, MINB, RING, HUGE><<<(unsigned)s->n_slices, NT, smem_for(s, NT, CAPV, RING), s->stream>>>(a);
     return cudaGetLastError();
 }
 
@@ -717,17 +720,27 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     return a;
 }
 
+// block size of the sampler (and context) kernels for this K
+static int sample_block(int K) { return K > 2048 ? 256 : 128; }
+
 cudaError_t launch_contexts(gf_shard* s) {
     s->ctx_dirty = false;
     if (s->n_ctx == 0) return cudaSuccess;
     const SampleArgs a = make_args(s, 0, 0);
     const size_t smem = (size_t)a.ctx_stride * sizeof(float);
+    // the same block size as the sampler variant of this K (sample_block), so
+    // copied contexts equal in-place builds bit for bit
     static unsigned long long attr_set = 0;
     if (attr_once(attr_set, s->device)) {
-        cudaError_t e = cudaFuncSetAttribute(context_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(context_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(context_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
     }
-    context_kernel<<<(unsigned)s->n_ctx, kSampleThreads, smem, s->stream>>>(a, s->d.ctx_cols, s->d.ctx_tab);
+    if (sample_block(s->K) == 128)
+        context_kernel<128><<<(unsigned)s->n_ctx, 128, smem, s->stream>>>(a, s->d.ctx_cols, s->d.ctx_tab);
+    else
+        context_kernel<256><<<(unsigned)s->n_ctx, 256, smem, s->stream>>>(a, s->d.ctx_cols, s->d.ctx_tab);
     return cudaGetLastError();
 }
 
@@ -746,10 +759,13 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
         const char* env = getenv("GF_K1");
         var = env ? atoi(env) : 0;
     }
-    if (s->K > (int)(4 * kCapV)) return launch_variant<kCapV, 3, 0, true>(s, a);   // rows can outgrow staging
-    if (s->K > 2048) return launch_variant<kCapV, 3, 0, false>(s, a);                // p*_ex on demand: 3 CTAs/SM
-    if (var == 1) return launch_variant<512, 4, 3, false>(s, a);                     // cp.async ring (A/B)
-    return launch_variant<kCapV, 4, 0, false>(s, a);
+    if (s->K > (int)(4 * kCapV)) return launch_variant<256, kCapV, 3, 0, true>(s, a);   // rows can outgrow staging
+    if (s->K > 2048) return launch_variant<256, kCapV, 3, 0, false>(s, a);   // p*_ex on demand: 3 x 8 warps/SM
+    if (var == 1) return launch_variant<256, 512, 4, 3, false>(s, a);         // cp.async ring (A/B)
+    if (var == 2) return launch_variant<256, kCapV, 4, 0, false>(s, a);       // 8-warp CTAs (A/B)
+    // 4-warp CTAs, 8 per SM: a slice's tail (warps idle at the final barrier
+    // while the last batch finishes) strands half as many warps
+    return launch_variant<128, 768, 8, 0, false>(s, a);
 }
 
 }  // namespace gf
