@@ -75,41 +75,50 @@ def make_shard_corpus(shape, rank, seed):
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
     """SM clock and throttle reasons sampled during the timed region: NVML every
-    ~2 ms (nvidia-smi as a fallback)."""
+    ~2 ms (initialised up front, plus one sample at entry and exit so even a
+    short region has readings; nvidia-smi as a fallback)."""
 
     def __init__(self, device):
         self.device = device
         self.rows = []                       # (sm_mhz, sm_max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
-
-    def _run(self):
+        self._nv = None
         try:
             import pynvml
 
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            h = pynvml.nvmlDeviceGetHandleByIndex(device)
             mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                 pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
-            while not self._stop.is_set():
-                self.rows.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx, reasons(h)))
-                self._stop.wait(0.002)
-            return
+            self._nv = lambda: (pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx, reasons(h))
         except Exception:
-            pass
-        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
-        while not self._stop.is_set():
+            self._nv = None
+
+    def _sample(self):
+        if self._nv is not None:
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                a, b, c = [x.strip() for x in out.stdout.strip().split(",")]
-                self.rows.append((float(a), float(b), int(c, 16)))
+                self.rows.append(self._nv())
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            return
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
+        try:
+            out = subprocess.run(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+            a, b, c = [x.strip() for x in out.stdout.strip().split(",")]
+            self.rows.append((float(a), float(b), int(c, 16)))
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._sample()
+            self._stop.wait(0.002 if self._nv is not None else 0.1)
 
     def __enter__(self):
+        self._sample()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -117,6 +126,7 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        self._sample()
 
     # NVML clocks-event reason bits
     BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
