@@ -11,6 +11,8 @@
 //                            them, K3 reads each doc contiguously); inside a
 //                            doc, tokens of block-scheduled words come first
 //   run_dwpos  u32[R]        zdoc position of each run's first token
+//   run_rec    uint4[R]      {doc, run_start, run_dwpos, theta offset}: K1's one
+//                            16-byte load per run
 //   theta_ent  u32[cap]      (count << 16 | topic) rows, fixed capacity
 //                            round4(min(K, L_d)) per doc, ids ascending
 //   theta_meta uint2[D]      {row offset, nnz}
@@ -45,6 +47,7 @@ struct ShardDev {
     uint32_t* dw_ptr = nullptr;
     uint16_t* zdoc = nullptr;
     uint32_t* run_dwpos = nullptr;
+    uint4* run_rec = nullptr;                // per run {doc, first token, zdoc position, theta row offset} (K1)
     uint32_t* theta_ent = nullptr;
     uint2* theta_meta = nullptr;
     uint32_t* sync = nullptr;

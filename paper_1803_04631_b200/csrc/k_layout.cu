@@ -210,6 +210,11 @@ __global__ void k_dwpos(int64_t R, const uint32_t* run_start, const uint32_t* ru
     }
 }
 
+__global__ void k_run_rec(int64_t R, const uint32_t* run_doc, const uint32_t* run_start, const uint32_t* dwpos,
+                          const uint2* meta, uint4* rec) {
+    GRID_STRIDE(r, R) rec[r] = make_uint4(run_doc[r], run_start[r], dwpos[r], meta[run_doc[r]].x);
+}
+
 // gf_shard_load checks of an uploaded chunk (corpus.py:160-198 invariants):
 // errs[0] token with z >= K, [1] token outside [lo, hi), [2] token outside its
 // word group, [3] dw-map entry out of range
@@ -425,7 +430,7 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
     auto& dv = s->d;
     int rc;
     if ((rc = shard_alloc(&dv.z, T, "z")) || (rc = shard_alloc(&dv.run_doc, R, "runs")) ||
-        (rc = shard_alloc(&dv.run_start, R + 1, "runs")) || (rc = shard_alloc(&dv.run_dwpos, R, "runs")) ||
+        (rc = shard_alloc(&dv.run_start, R + 1, "runs")) || (rc = shard_alloc(&dv.run_dwpos, R, "runs")) || (rc = shard_alloc(&dv.run_rec, R, "runs")) ||
         (rc = shard_alloc(&dv.dw_ptr, D + 1, "dw_ptr")) || (rc = shard_alloc(&dv.zdoc, T, "zdoc")) ||
         (rc = shard_alloc(&dv.theta_ent, cap + 8, "theta")) || (rc = shard_alloc(&dv.theta_meta, D, "theta")) ||
         (rc = shard_alloc(&dv.sync, s->sync_u32, "phi")) || (rc = shard_alloc(&dv.inv_den, 2 * K, "inv_den")) ||
@@ -575,6 +580,7 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
            "zdoc");
         k_dwpos<<<blocks_for(R), 256, 0, st>>>(R, dv.run_start, dv.run_doc, run_group, d_ginfo, inv, S, c.dw_ptr,
                                                dv.run_dwpos);
+        k_run_rec<<<blocks_for(R), 256, 0, st>>>(R, dv.run_doc, dv.run_start, dv.run_dwpos, dv.theta_meta, dv.run_rec);
     }
     CK(cudaMemsetAsync(dv.theta_ent, 0, (cap + 8) * 4, st), "memset");
     CK(cudaMemsetAsync(dv.sync, 0, s->sync_u32 * 4, st), "memset");

@@ -80,6 +80,7 @@ struct SampleArgs {
     const uint32_t* run_doc;
     const uint32_t* run_start;
     const uint32_t* run_dwpos;                // zdoc position of each run's first token
+    const uint4* run_rec;                     // {doc, first token, zdoc position, theta offset}
     uint16_t* z;
     uint16_t* zdoc;                           // doc-major copy of z (read by K3)
     const uint2* theta_meta;
@@ -394,20 +395,22 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
         const int r = rb + lane;
         const bool valid = lane < batch && r < sl.z;
         uint32_t d = 0, t0 = 0, t1 = 0, off = 0, nnz = 0, dwp = 0;
+        const int nval = min(batch, sl.z - rb);                   // valid lanes [0, nval)
         if (valid) {
-            d = __ldg(a.run_doc + r);
-            t0 = __ldg(a.run_start + r);
-            t1 = __ldg(a.run_start + r + 1);
-            dwp = __ldg(a.run_dwpos + r);
-            const uint2 m = __ldg(a.theta_meta + d);
-            off = m.x;
-            nnz = m.y;
+            const uint4 rec = __ldg(a.run_rec + r);                 // one 16-byte load per run
+            d = rec.x;
+            t0 = rec.y;
+            dwp = rec.z;
+            off = rec.w;
+            nnz = __ldg(&a.theta_meta[d].y);                        // this iteration's row length
             nbytes += nnz;
             // the whole row (32-byte granules) into L2 now: the pass then streams
             // the batch's rows with every line already requested, instead of one
             // 1 KB warp step in flight at a time
             if (a.prefetch && nnz) prefetch_l2_bulk(a.theta_ent + off, ((nnz + 7u) & ~7u) * 4u);
         }
+        t1 = __shfl_down_sync(kFull, t0, 1);                        // the next run's first token
+        if (lane == nval - 1) t1 = __ldg(a.run_start + r + 1);
         const uint32_t gdoc = a.doc_lo + d;
         const uint32_t U = max(1u, (nnz + 3u) >> 2);          // row length in 16-byte vectors
         const uint32_t Up = (U + VEC - 1u) / VEC * VEC;       // ... padded to whole lanes
@@ -702,6 +705,7 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     a.run_doc = s->d.run_doc;
     a.run_start = s->d.run_start;
     a.run_dwpos = s->d.run_dwpos;
+    a.run_rec = s->d.run_rec;
     a.z = s->d.z;
     a.zdoc = s->d.zdoc;
     a.theta_meta = s->d.theta_meta;
