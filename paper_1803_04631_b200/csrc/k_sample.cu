@@ -57,15 +57,6 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// cp.async (LDGSTS) 16 B global -> shared, L2 only; src_bytes 0 zero-fills
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
 struct SampleArgs {
     int K, Kp;
     float alpha, beta, vbeta;
@@ -338,11 +329,11 @@ __global__ void __launch_bounds__(NT) context_kernel(SampleArgs a, const int32_t
     for (int i = threadIdx.x; i < a.ctx_stride / 4; i += NT) dst[i] = reinterpret_cast<const float4*>(smem)[i];
 }
 
-// CAPV: staged vector ends per warp; MINB: CTAs per SM; RING: depth of the
-// per-warp cp.async ring of pass steps (0: direct 256-bit loads); HUGE:
-// compile the streaming path (needed only when K > 4*CAPV)
+// NT: threads per CTA; CAPV: staged vector ends per warp; MINB: CTAs per SM;
+// PF: keep the pass's next 1 KB step in flight; HUGE: compile the streaming
+// path (needed only when K > 4*CAPV)
 constexpr uint32_t VEC = 2;                  // 16-byte vectors per lane per pass step (32 B)
-template <int NT, uint32_t CAPV, int MINB, int RING, bool HUGE>
+template <int NT, uint32_t CAPV, int MINB, bool PF, bool HUGE>
 __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     constexpr int kWarps = NT / 32;
     extern __shared__ float smem[];
@@ -378,8 +369,6 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     const float* lvl0 = lvl;
     const uint32_t* guide = reinterpret_cast<const uint32_t*>(smem + lay_guide(K, a.tree.total));
     float* buf = wbuf + warp * CAPV;
-    // per-warp ring of RING pass steps (1 KB each: 32 lanes x 32 B) after the staging buffers
-    uint4* ring = reinterpret_cast<uint4*>(wbuf + kWarps * CAPV) + warp * (RING > 0 ? RING : 1) * 64;
     // runs per grab: 32 (one per lane) unless the slice is too small to give
     // every warp at least two grabs -- then smaller grabs keep all 8 warps busy
     const int batch = min(32, max(1, (sl.z - sl.y + 2 * kWarps - 1) / (2 * kWarps)));
@@ -448,61 +437,41 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
 
             // ---- 1. entry-parallel pass: segmented prefix of p1 over the concatenated rows ----
             // each lane owns VEC consecutive vectors (4*VEC entries) of ONE row per step
-            // (rows are laid out VEC-aligned), so 128*VEC entries advance per warp step.
-            // With RING > 0 the warp's 1 KB steps are fetched RING-1 steps ahead by
-            // cp.async into a shared-memory ring (no registers held by loads in flight).
-            uint32_t qf = 0, sf = 0;
-            int cpf = first - 1;                                            // fetch cursor: run of vector qf-1
-            auto fetch = [&]() {
-                if (qf < Utot) {
-                    const uint32_t hb = (sel && vo - qf < 32u * VEC) ? (1u << ((vo - qf) / VEC)) : 0u;
-                    const unsigned M = __reduce_or_sync(kFull, hb);
-                    const int ri = min(cpf + __popc(M & lane_le), 31);
-                    const uint32_t rvo = __shfl_sync(kFull, vo, ri);
-                    const uint32_t roff = __shfl_sync(kFull, off, ri);
-                    const uint32_t qL = qf + VEC * (uint32_t)lane;
-                    const bool act = qL < Utot;
-                    const uint32_t* src = act ? a.theta_ent + roff + 4u * (qL - rvo) : &g_zero32[0];
-                    uint4* dst = ring + sf * 64u + 2u * (uint32_t)lane;
-                    cp_async16(dst, src, act ? 16u : 0u);
-                    cp_async16(dst + 1, src + 4, act ? 16u : 0u);
-                    cpf = __shfl_sync(kFull, ri, 31);
-                    qf += 32u * VEC;
-                    sf = sf + 1u == (uint32_t)RING ? 0u : sf + 1u;
-                }
-                cp_async_commit();
+            // (rows are laid out VEC-aligned), so 128*VEC entries advance per warp step:
+            // one 256-bit load per lane, the warp reads 1 KB contiguous per step (rows
+            // are 32-byte aligned and zero-padded to 8 entries by K3).  With PF the
+            // next step's load is issued before the current step is summed and
+            // scanned (one step in flight ahead, in registers).
+            int cprev = first - 1;                                          // run holding vector q-1
+            auto issue = [&](uint32_t qs, unsigned& Ms, uint4& x0, uint4& x1) {
+                const uint32_t hb = (sel && vo - qs < 32u * VEC) ? (1u << ((vo - qs) / VEC)) : 0u;
+                Ms = __reduce_or_sync(kFull, hb);                           // run heads in step qs
+                const int ri = min(cprev + __popc(Ms & lane_le), 31);
+                const uint32_t rvo = __shfl_sync(kFull, vo, ri);
+                const uint32_t roff = __shfl_sync(kFull, off, ri);
+                const uint32_t qL = qs + VEC * (uint32_t)lane;
+                const uint32_t* src = qL < Utot ? a.theta_ent + roff + 4u * (qL - rvo) : &g_zero32[0];
+                ldg256(src, x0, x1);
+                cprev = min(cprev + __popc(Ms), 31);                        // lane 31's row
             };
-            if (RING > 0) {
-#pragma unroll
-                for (int i = 0; i < RING - 1; ++i) fetch();
-            }
-            int cprev = first - 1;                                          // run holding vector q0-1
-            uint32_t sc = 0;
+            unsigned Mn = 0u;
+            uint4 n0 = make_uint4(0u, 0u, 0u, 0u), n1 = n0;
+            if (PF) issue(0u, Mn, n0, n1);
             float carry = 0.f;
             for (uint32_t q0 = 0; q0 < Utot; q0 += 32u * VEC) {
-                const uint32_t hb = (sel && vo - q0 < 32u * VEC) ? (1u << ((vo - q0) / VEC)) : 0u;
-                const unsigned M = __reduce_or_sync(kFull, hb);           // run heads in this step
+                unsigned M;
+                uint4 e[VEC];
+                if (PF) {
+                    M = Mn;
+                    e[0] = n0;
+                    e[1] = n1;
+                    if (q0 + 32u * VEC < Utot) issue(q0 + 32u * VEC, Mn, n0, n1);
+                } else {
+                    issue(q0, M, e[0], e[1]);
+                }
                 const unsigned mle = M & lane_le;
                 const uint32_t qL = q0 + VEC * (uint32_t)lane;
                 const bool act = qL < Utot;
-                uint4 e[VEC];
-                if (RING > 0) {
-                    fetch();
-                    cp_async_wait<(RING > 0 ? RING - 1 : 0)>();
-                    const uint4* src = ring + sc * 64u + 2u * (uint32_t)lane;
-                    e[0] = src[0];
-                    e[1] = src[1];
-                    sc = sc + 1u == (uint32_t)RING ? 0u : sc + 1u;
-                } else {
-                    const int ri = min(cprev + __popc(mle), 31);
-                    const uint32_t rvo = __shfl_sync(kFull, vo, ri);
-                    const uint32_t roff = __shfl_sync(kFull, off, ri);
-                    // one 256-bit load per lane: the warp reads 1 KB contiguous per step
-                    // (rows are 32-byte aligned and zero-padded to 8 entries by K3)
-                    const uint32_t* src = act ? a.theta_ent + roff + 4u * (qL - rvo) : &g_zero32[0];
-                    ldg256(src, e[0], e[1]);
-                    cprev = __shfl_sync(kFull, ri, 31);
-                }
                 float p[VEC];                                               // prefix at each vector end
 #pragma unroll
                 for (int i = 0; i < VEC; ++i)                               // independent pair sums (ILP)
@@ -660,25 +629,25 @@ cudaError_t launch_validate(gf_shard* s) {
     return cudaGetLastError();
 }
 
-static size_t smem_for(const gf_shard* s, int nt, uint32_t capv, int ring) {
-    return (size_t)(lay_buf(s->K, s->tree.total) + (nt / 32) * capv) * sizeof(float) + (size_t)(nt / 32) * ring * 1024;
+static size_t smem_for(const gf_shard* s, int nt, uint32_t capv) {
+    return (size_t)(lay_buf(s->K, s->tree.total) + (nt / 32) * capv) * sizeof(float);
 }
 
-size_t sample_smem_bytes(const gf_shard* s) { return smem_for(s, kSampleThreads, kCapV, 0); }
+size_t sample_smem_bytes(const gf_shard* s) { return smem_for(s, kSampleThreads, kCapV); }
 size_t context_floats(const gf_shard* s) { return (size_t)lay_buf(s->K, s->tree.total); }
 
-template <int NT, uint32_t CAPV, int MINB, int RING, bool HUGE>
+template <int NT, uint32_t CAPV, int MINB, bool PF, bool HUGE>
 static cudaError_t launch_variant(gf_shard* s, const SampleArgs& a) {
     static unsigned long long attr_set = 0;
     if (attr_once(attr_set, s->device)) {
-        cudaError_t e = cudaFuncSetAttribute(sample_kernel<NT, CAPV, MINB, RING, HUGE>,
+        cudaError_t e = cudaFuncSetAttribute(sample_kernel<NT, CAPV, MINB, PF, HUGE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(sample_kernel<NT, CAPV, MINB, RING, HUGE>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        e = cudaFuncSetAttribute(sample_kernel<NT, CAPV, MINB, PF, HUGE>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
     }
-    sample_kernel<NT, CAPV, MINB, RING, HUGE><<<(unsigned)s->n_slices, NT, smem_for(s, NT, CAPV, RING), s->stream>>>(a);
+    sample_kernel<NT, CAPV, MINB, PF, HUGE><<<(unsigned)s->n_slices, NT, smem_for(s, NT, CAPV), s->stream>>>(a);
     return cudaGetLastError();
 }
 
@@ -763,13 +732,14 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
         const char* env = getenv("GF_K1");
         var = env ? atoi(env) : 0;
     }
-    if (s->K > (int)(4 * kCapV)) return launch_variant<256, kCapV, 3, 0, true>(s, a);   // rows can outgrow staging
-    if (s->K > 2048) return launch_variant<256, kCapV, 3, 0, false>(s, a);   // p*_ex on demand: 3 x 8 warps/SM
-    if (var == 1) return launch_variant<256, 512, 4, 3, false>(s, a);         // cp.async ring (A/B)
-    if (var == 2) return launch_variant<256, kCapV, 4, 0, false>(s, a);       // 8-warp CTAs (A/B)
+    if (s->K > (int)(4 * kCapV)) return launch_variant<256, kCapV, 3, true, true>(s, a);    // rows can outgrow staging
+    if (s->K > 2048) return launch_variant<256, kCapV, 3, true, false>(s, a);    // p*_ex on demand: 3 x 8 warps/SM
+    if (var == 2) return launch_variant<256, kCapV, 4, true, false>(s, a);        // 8-warp CTAs (A/B)
+    if (var == 3) return launch_variant<128, 768, 8, false, false>(s, a);         // no pass prefetch (A/B)
     // 4-warp CTAs, 8 per SM: a slice's tail (warps idle at the final barrier
-    // while the last batch finishes) strands half as many warps
-    return launch_variant<128, 768, 8, 0, false>(s, a);
+    // while the last batch finishes) strands half as many warps; the pass keeps
+    // its next 1 KB step in flight
+    return launch_variant<128, 768, 8, true, false>(s, a);
 }
 
 }  // namespace gf
