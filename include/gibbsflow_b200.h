@@ -192,7 +192,9 @@ int gf_shard_phi_argmax(gf_shard* shard, int64_t* max_count, int32_t* topic, int
 int gf_shard_stats(gf_shard* shard, int64_t* stats, int num_stats);
 int gf_shard_reset_stats(gf_shard* shard);
 /* CUDA-event time (ms) of the kernels of the last gf_shard_iterate:
- * ms[0] sample, [1] phi rebuild (+memset), [2] prepare, [3] theta rebuild. */
+ * ms[0] sample (+ loglik reduce), [1] phi rebuild (+memset; theta rebuild runs
+ * beside it on an internal stream), [2] prepare (+ word contexts), [3] theta
+ * rebuild time not hidden behind [1] + [2]. */
 int gf_shard_last_times(gf_shard* shard, float* ms, int num);
 
 /* ------------------------------------------------------ ptree primitive --

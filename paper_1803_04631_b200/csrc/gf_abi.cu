@@ -288,6 +288,9 @@ int gf_shard_destroy(gf_shard* s) {
     free_dev(s);
     for (auto& ev : s->ev)
         if (ev) cudaEventDestroy(ev);
+    if (s->aux) { cudaStreamSynchronize(s->aux); cudaStreamDestroy(s->aux); }
+    if (s->fork) cudaEventDestroy(s->fork);
+    if (s->join) cudaEventDestroy(s->join);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
     return GF_OK;
@@ -415,17 +418,28 @@ int gf_shard_iterate(gf_shard* s, uint32_t iteration) {
     if (int rc = need_loaded(s)) return rc;
     if (int rc = validate_if_dirty(s)) return rc;
     cudaStream_t st = s->stream;
+    if (!s->aux) {
+        CU(cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking), "iterate");
+        CU(cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming), "iterate");
+        CU(cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming), "iterate");
+    }
     if (s->timing) cudaEventRecord(s->ev[0], st);
     CU(gf::launch_sample(s, iteration), "sample");
+    CU(gf::launch_ll_reduce(s), "loglik");
     if (s->timing) cudaEventRecord(s->ev[1], st);
+    // K3 (theta from zdoc) on the aux stream beside K2 (phi from z) + prepare:
+    // independent inputs and outputs; the caller's next call waits for both
+    CU(cudaEventRecord(s->fork, st), "iterate");
+    CU(cudaStreamWaitEvent(s->aux, s->fork, 0), "iterate");
+    CU(gf::launch_theta_rebuild(s, s->aux), "rebuild_theta");
+    CU(cudaEventRecord(s->join, s->aux), "iterate");
     CU(gf::launch_phi_rebuild(s), "rebuild_phi");
     if (s->timing) cudaEventRecord(s->ev[2], st);
     CU(gf::launch_prepare(s), "prepare");
     if (s->timing) cudaEventRecord(s->ev[3], st);
-    CU(gf::launch_theta_rebuild(s), "rebuild_theta");
+    CU(cudaStreamWaitEvent(st, s->join, 0), "iterate");
     if (s->timing) cudaEventRecord(s->ev[4], st);
-    CU(gf::launch_ll_reduce(s), "loglik");
-    s->stat_launches = 5;  // sample, phi_rebuild, prepare, theta_rebuild, ll_reduce
+    s->stat_launches = 5 + (s->n_ctx > 0);  // sample, ll_reduce, theta, phi, prepare (+ contexts)
     s->stat_sample_launches++;
     return GF_OK;
 }

@@ -93,6 +93,8 @@ struct gf_shard {
     int64_t stat_launches = 0;
     int64_t stat_sample_launches = 0;
     cudaEvent_t ev[6] = {};
+    cudaStream_t aux = nullptr;              // gf_shard_iterate: K3 beside K2 + prepare
+    cudaEvent_t fork = nullptr, join = nullptr;
     float last_ms[4] = {0, 0, 0, 0};
     bool timing = true;
     // imported state not yet validated: an import (set_assignments / set_theta /
@@ -138,7 +140,7 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only = 0);
 cudaError_t launch_phi_rebuild(gf_shard* s);
 cudaError_t launch_prepare(gf_shard* s);
 cudaError_t launch_contexts(gf_shard* s);
-cudaError_t launch_theta_rebuild(gf_shard* s);
+cudaError_t launch_theta_rebuild(gf_shard* s, cudaStream_t st = nullptr);
 cudaError_t launch_zdoc_sync(gf_shard* s);
 cudaError_t launch_ll_reduce(gf_shard* s);
 cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt);

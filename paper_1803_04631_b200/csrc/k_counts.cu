@@ -238,8 +238,9 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
     }
 }
 
-cudaError_t launch_theta_rebuild(gf_shard* s) {
+cudaError_t launch_theta_rebuild(gf_shard* s, cudaStream_t st) {
     if (s->D == 0) return cudaSuccess;
+    if (!st) st = s->stream;
     const size_t per_warp = (size_t)k3_warp_u32(s->K) * 4;
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * per_warp > 96 * 1024) wpc >>= 1;
@@ -258,7 +259,7 @@ cudaError_t launch_theta_rebuild(gf_shard* s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, theta_rebuild_kernel, wpc * 32, smem);
     const long long need = (s->D + wpc - 1) / wpc;
     const long long grid = std::min<long long>(need, (long long)nsm * std::max(per_sm, 1));
-    theta_rebuild_kernel<<<(unsigned)grid, wpc * 32, smem, s->stream>>>((int)s->D, s->d.dw_ptr, s->d.zdoc,
+    theta_rebuild_kernel<<<(unsigned)grid, wpc * 32, smem, st>>>((int)s->D, s->d.dw_ptr, s->d.zdoc,
                                                                          s->d.theta_ent, s->d.theta_meta, s->K, wpc,
                                                                          s->d.errs);
     return cudaGetLastError();

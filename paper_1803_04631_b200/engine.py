@@ -180,13 +180,16 @@ class Trainer:
         it = self.iteration
         t0 = time.perf_counter()
         sh = self.shard
-        sh.sample(it)
-        sh.rebuild_phi()
-        work = self._allreduce_sync(async_op=True)
-        sh.rebuild_theta()                       # overlaps the phi allreduce
-        if work is not None:
-            work.wait()
-        sh.prepare()
+        if self.world == 1:
+            sh.iterate(it)                       # K1, then K3 beside K2 + prepare (gf_shard_iterate)
+        else:
+            sh.sample(it)
+            sh.rebuild_phi()
+            work = self._allreduce_sync(async_op=True)
+            sh.rebuild_theta()                   # overlaps the phi allreduce
+            if work is not None:
+                work.wait()
+            sh.prepare()
         ll = None
         if self.cfg.eval_every and it % self.cfg.eval_every == 0:
             ll = float(self._allreduce_np(np.array([sh.loglik_sum()], np.float64))[0]) / self.num_tokens

@@ -263,4 +263,4 @@ class DeviceShard:
     def last_times(self):
         ms = np.zeros(4, np.float32)
         _lib.check(_lib.lib().gf_shard_last_times(self._h, _lib.ptr(ms), 4))
-        return dict(zip(["sample", "phi", "prepare", "theta"], ms.tolist()))
+        return dict(zip(["sample", "phi", "prepare", "theta_exposed"], ms.tolist()))

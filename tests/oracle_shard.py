@@ -89,6 +89,13 @@ class OracleShard:
                                       self.chunk.doc_ids, self.chunk.word_ids, self.z, self.chunk.doc_lo,
                                       rp, ids, cn, self.phi, self.totals, mode="thin")
 
+    def iterate(self, iteration):
+        """gf_shard_iterate's order: sample, then the counts of the new state."""
+        self.sample(iteration)
+        self.rebuild_phi()
+        self.prepare()
+        self.rebuild_theta()
+
     def loglik_sum(self):
         return self.ll
 
