@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--phi-sync", default="nccl", choices=["nccl", "peer"],
+                    help="N>1: phi sum by all_reduce, or by the IPC peer-memory exchange kernel")
     return ap.parse_args()
 
 
@@ -150,12 +152,13 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram read+write bytes per K1 launch from the committed ncu --set full capture."""
+def ncu_traffic(workload, K):
+    """dram read+write bytes per K1 launch from the committed ncu --set full
+    capture of the same workload and K (None when there is none)."""
     p = os.path.join(ROOT, "profiles", "sample_kernel_traffic.json")
     try:
         with open(p) as fh:
-            return json.load(fh)
+            return json.load(fh).get(f"{workload}-{K}")
     except Exception:
         return None
 
@@ -302,8 +305,16 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize(device)
     prep_s = time.perf_counter() - t0
     sync_t = sh.sync_tensor() if dist else None
+    peer = bool(dist) and args.phi_sync == "peer"
+    if peer:          # map every rank's sync buffer; the phi sum becomes one kernel (k_peer.cu)
+        handles = [None] * world
+        dist.all_gather_object(handles, sh.peer_handle())
+        sh.peer_open(rank, world, handles)
 
     def allreduce_async():
+        if peer:
+            sh.peer_allreduce()               # stream-ordered on the compute stream
+            return None
         return ar(sync_t, async_op=True) if dist else None
 
     # initial counts
@@ -390,11 +401,11 @@ def run_ours(args, world, rank, local):
     st = sh.stats()
     # own kernels per step: sample + ll_reduce, phi_rebuild, theta_rebuild,
     # prepare (+ context_kernel when some word is split into several slices)
-    launches_per_step = 5 + (1 if st["word_contexts"] > 0 else 0)
+    launches_per_step = 5 + (1 if st["word_contexts"] > 0 else 0) + (1 if peer else 0)
     k1_ms = acc[0] / args.steps
     peak, peak_src = measured_peak()
     achieved = st["sample_bytes"] / (k1_ms / 1e3) / 1e9
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(args.workload, K)
 
     # ---- end to end through the public API with host buffers (pinned) ----
     e2e = None
@@ -470,7 +481,8 @@ def run_ours(args, world, rank, local):
                 "workload": f"{args.workload}-shaped synthetic LDA corpus, K={K}, one shard per GPU",
                 "docs_per_gpu": shape["num_docs"], "vocab": corp.vocab_size, "tokens_per_gpu": T_local,
                 "tokens_total": T_all, "topics": K, "iterations": [args.warmup, args.warmup + args.steps],
-                "parallelism": (f"doc-shard dp{world} + {args.dist_backend.upper()} allreduce of phi" if dist
+                "parallelism": ((f"doc-shard dp{world} + peer-memory phi exchange kernel" if peer else
+                                 f"doc-shard dp{world} + {args.dist_backend.upper()} allreduce of phi") if dist
                                 else "dp1"),
                 "l2": "inputs larger than L2 (z 2T B, theta 4*NNZ B, phi >= 200 MB vs 126 MB L2)",
                 "runs": st["runs"], "slices": st["slices"], "word_contexts": st["word_contexts"],

@@ -141,7 +141,9 @@ int gf_shard_sample(gf_shard* shard, uint32_t iteration);
 /* SPEC.md:402-410 loglik_per_token numerator for the CURRENT theta / phi
  * (no draws): read it back with gf_shard_loglik_sum. */
 int gf_shard_evaluate(gf_shard* shard);
-/* Convenience: sample -> rebuild_phi -> prepare -> rebuild_theta (one GPU). */
+/* One deferred iteration: sample -> rebuild_phi [-> peer phi
+ * exchange when a peer group is open] -> prepare, with rebuild_theta on an
+ * internal stream beside everything after the sample. */
 int gf_shard_iterate(gf_shard* shard, uint32_t iteration);
 /* Sum over this shard's tokens of log p(w | d) for the model the last
  * gf_shard_sample started from (synchronises the stream). */
@@ -154,6 +156,22 @@ int gf_shard_synchronize(gf_shard* shard);
  * phi16 columns | n_k].  Summing the buffers of all ranks elementwise as
  * uint32 (e.g. NCCL allreduce sum) yields the global phi and n_k exactly. */
 int gf_shard_sync_buffer(gf_shard* shard, void** device_ptr, int64_t* num_u32);
+/* Peer-memory phi exchange (replaces the all_reduce of the sync buffer, i.e.
+ * SPEC reduce_phi/broadcast_phi, on one NVLink/NVSwitch node).
+ * 1. gf_shard_peer_handle -> GF_PEER_HANDLE_BYTES of IPC handles (after load);
+ * 2. exchange them between ranks (any host channel, e.g. torch.distributed);
+ * 3. gf_shard_peer_open(rank, world, handles of ranks 0..world-1 concatenated);
+ * 4. per iteration gf_shard_peer_allreduce after rebuild_phi (stream-ordered;
+ *    every rank must call it the same number of times) -- gf_shard_iterate
+ *    does it itself once the group is open.  A reload invalidates the group.
+ * A peer that stops participating makes the exchange time out (~20 s) and the
+ * next gf_shard_check_errors report GF_ERR_TRAINING. */
+#define GF_PEER_HANDLE_BYTES 128
+#define GF_MAX_PEERS 8
+int gf_shard_peer_handle(gf_shard* shard, void* handle_out);
+int gf_shard_peer_open(gf_shard* shard, int rank, int world, const void* handles);
+int gf_shard_peer_allreduce(gf_shard* shard);
+int gf_shard_peer_close(gf_shard* shard);
 /* Host-only: the sync-buffer layout a shard derives from the global word
  * frequencies.  word_col_out[v] >= 0: 16-bit column index; < 0: ~(32-bit
  * column index).  layout_out = {phi16 offset, n_k offset, total} in uint32
@@ -187,12 +205,12 @@ int gf_shard_phi_argmax(gf_shard* shard, int64_t* max_count, int32_t* topic, int
 /* live counters for the roofline: stats[0] = K1 algorithmic bytes per sample
  * launch (averaged over the launches since the last reset), [1] = K2 bytes,
  * [2] = K3 bytes, [3] = runs, [4] = slices, [5] = tokens, [6] = theta nnz,
- * [7] = kernels launched by gf_shard_iterate, [8] = sample launches since reset,
+ * [7] = kernels launched by gf_shard_iterate (incl. the peer exchange), [8] = sample launches since reset,
  * [9] = precomputed word contexts, [10] = document blocks of the slice schedule. */
 int gf_shard_stats(gf_shard* shard, int64_t* stats, int num_stats);
 int gf_shard_reset_stats(gf_shard* shard);
 /* CUDA-event time (ms) of the kernels of the last gf_shard_iterate:
- * ms[0] sample (+ loglik reduce), [1] phi rebuild (+memset; theta rebuild runs
+ * ms[0] sample (+ loglik reduce), [1] phi rebuild (+memset, + peer exchange; theta rebuild runs
  * beside it on an internal stream), [2] prepare (+ word contexts), [3] theta
  * rebuild time not hidden behind [1] + [2]. */
 int gf_shard_last_times(gf_shard* shard, float* ms, int num);

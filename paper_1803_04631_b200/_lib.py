@@ -53,6 +53,10 @@ SIGNATURES = {
     "gf_shard_check_errors": (_int, [_p]),
     "gf_shard_synchronize": (_int, [_p]),
     "gf_shard_sync_buffer": (_int, [_p, _pp, _p]),
+    "gf_shard_peer_handle": (_int, [_p, _p]),
+    "gf_shard_peer_open": (_int, [_p, _int, _int, _p]),
+    "gf_shard_peer_allreduce": (_int, [_p]),
+    "gf_shard_peer_close": (_int, [_p]),
     "gf_sync_layout": (_int, [_p, _i32, _i32, _u32, _p, _p]),
     "gf_shard_get_assignments": (_int, [_p, _p]),
     "gf_shard_set_assignments": (_int, [_p, _p]),

@@ -285,6 +285,7 @@ int gf_shard_destroy(gf_shard* s) {
     if (!s) return GF_OK;
     cudaSetDevice(s->device);
     if (s->stream) cudaStreamSynchronize(s->stream);
+    gf::peer_close(s);
     free_dev(s);
     for (auto& ev : s->ev)
         if (ev) cudaEventDestroy(ev);
@@ -417,6 +418,8 @@ int gf_shard_evaluate(gf_shard* s) {
 int gf_shard_iterate(gf_shard* s, uint32_t iteration) {
     if (int rc = need_loaded(s)) return rc;
     if (int rc = validate_if_dirty(s)) return rc;
+    if (s->peer.world > 1 && s->peer.sync != s->d.sync)
+        return fail(GF_ERR_VALUE, "peer group opened before the last load: exchange handles and reopen");
     cudaStream_t st = s->stream;
     if (!s->aux) {
         CU(cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking), "iterate");
@@ -434,12 +437,14 @@ int gf_shard_iterate(gf_shard* s, uint32_t iteration) {
     CU(gf::launch_theta_rebuild(s, s->aux), "rebuild_theta");
     CU(cudaEventRecord(s->join, s->aux), "iterate");
     CU(gf::launch_phi_rebuild(s), "rebuild_phi");
+    if (s->peer.world > 1) CU(gf::launch_peer_allreduce(s, st), "peer_allreduce");
     if (s->timing) cudaEventRecord(s->ev[2], st);
     CU(gf::launch_prepare(s), "prepare");
     if (s->timing) cudaEventRecord(s->ev[3], st);
     CU(cudaStreamWaitEvent(st, s->join, 0), "iterate");
     if (s->timing) cudaEventRecord(s->ev[4], st);
-    s->stat_launches = 5 + (s->n_ctx > 0);  // sample, ll_reduce, theta, phi, prepare (+ contexts)
+    // sample, ll_reduce, theta, phi, prepare (+ contexts) (+ peer exchange)
+    s->stat_launches = 5 + (s->n_ctx > 0) + (s->peer.world > 1);
     s->stat_sample_launches++;
     return GF_OK;
 }
@@ -471,10 +476,13 @@ int gf_shard_synchronize(gf_shard* s) {
 
 int gf_shard_check_errors(gf_shard* s) {
     if (int rc = need_loaded(s)) return rc;
-    unsigned long long e[3];
-    CU(cudaMemcpyAsync(e, s->d.errs, 24, cudaMemcpyDeviceToHost, s->stream), "errors");
+    unsigned long long e[4];
+    CU(cudaMemcpyAsync(e, s->d.errs, 32, cudaMemcpyDeviceToHost, s->stream), "errors");
     CU(cudaStreamSynchronize(s->stream), "errors");
-    CU(cudaMemsetAsync(s->d.errs, 0xff, 24, s->stream), "errors");
+    CU(cudaMemsetAsync(s->d.errs, 0xff, 32, s->stream), "errors");
+    if (e[3] != ~0ULL)
+        return fail(GF_ERR_TRAINING, "rank %d: phi peer exchange timed out waiting for a peer (block %llu)",
+                    s->peer.rank, e[3]);
     if (e[1] != ~0ULL) {
         const long long d = (long long)(e[1] >> 32) + s->doc_lo;
         return fail(GF_ERR_OVERFLOW, "document %lld: topic count %llu exceeds 16-bit range", d,
@@ -493,6 +501,34 @@ int gf_shard_sync_buffer(gf_shard* s, void** p, int64_t* n) {
     if (int rc = need_loaded(s)) return rc;
     *p = s->d.sync;
     *n = s->sync_u32;
+    return GF_OK;
+}
+
+int gf_shard_peer_handle(gf_shard* s, void* out) {
+    if (int rc = need_loaded(s)) return rc;
+    cudaSetDevice(s->device);
+    return gf::peer_handle(s, out);
+}
+
+int gf_shard_peer_open(gf_shard* s, int rank, int world, const void* handles) {
+    if (int rc = need_loaded(s)) return rc;
+    cudaSetDevice(s->device);
+    return gf::peer_open(s, rank, world, handles);
+}
+
+int gf_shard_peer_allreduce(gf_shard* s) {
+    if (int rc = need_loaded(s)) return rc;
+    if (s->peer.world < 1 || s->peer.sync != s->d.sync)
+        return fail(GF_ERR_VALUE, "no peer group open on this shard's current sync buffer");
+    cudaSetDevice(s->device);
+    if (s->peer.world > 1) CU(gf::launch_peer_allreduce(s, s->stream), "peer_allreduce");
+    return GF_OK;
+}
+
+int gf_shard_peer_close(gf_shard* s) {
+    cudaSetDevice(s->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    gf::peer_close(s);
     return GF_OK;
 }
 

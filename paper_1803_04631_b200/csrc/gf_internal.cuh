@@ -58,10 +58,24 @@ struct ShardDev {
     double* ll_part = nullptr;
     double* ll_sum = nullptr;
     unsigned long long* errs = nullptr;      // [0] consistency token (min), [1] theta overflow key (min),
-                                             // [2] document with a topic >= K (K3, min)
+                                             // [2] document with a topic >= K (K3, min),
+                                             // [3] peer exchange block that timed out (min)
     unsigned long long* bytes = nullptr;     // [0] sum over runs of nnz (sampler bytes model)
     uint32_t* scratch = nullptr;             // export staging
     size_t scratch_bytes = 0;
+};
+
+constexpr int kMaxPeers = 8;                 // ranks of one NVLink/NVSwitch node
+
+// peer-memory phi exchange (k_peer.cu): every rank's sync buffer and signal
+// slots mapped into this process (own entries are the local pointers)
+struct PeerGroup {
+    int rank = 0, world = 0;                 // world 0: not open
+    uint32_t* buf[kMaxPeers] = {};
+    uint32_t* sig[kMaxPeers] = {};
+    uint32_t* own_sig = nullptr;             // this rank's signal slots (cudaMalloc, exported)
+    uint32_t* sync = nullptr;                // the sync buffer the group was opened on
+    uint32_t epoch = 0;
 };
 
 }  // namespace gf
@@ -96,6 +110,7 @@ struct gf_shard {
     cudaStream_t aux = nullptr;              // gf_shard_iterate: K3 beside K2 + prepare
     cudaEvent_t fork = nullptr, join = nullptr;
     float last_ms[4] = {0, 0, 0, 0};
+    gf::PeerGroup peer;                      // open: gf_shard_iterate reduces phi over peer memory
     bool timing = true;
     // imported state not yet validated: an import (set_assignments / set_theta /
     // set_phi) marks the count structures it may have made inconsistent; a
@@ -123,6 +138,11 @@ int shard_alloc(T** p, size_t count, const char* what) {
     cudaError_t e = cudaMalloc((void**)p, (count > 0 ? count : 1) * sizeof(T));
     return e == cudaSuccess ? 0 : shard_cuda_fail(e, what);
 }
+// peer-memory phi exchange (k_peer.cu)
+int peer_handle(gf_shard* s, void* out);
+int peer_open(gf_shard* s, int rank, int world, const void* handles);
+void peer_close(gf_shard* s);
+cudaError_t launch_peer_allreduce(gf_shard* s, cudaStream_t st);
 // K4 (k_layout.cu)
 int load_chunk(gf_shard* s, int64_t lo, int64_t hi, int64_t T, const int32_t* doc_ids, const int32_t* word_ids,
                const uint16_t* z, int64_t ng, const int32_t* gw, const int64_t* go, const int64_t* gs,

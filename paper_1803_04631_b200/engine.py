@@ -48,6 +48,7 @@ class TrainConfig:
     eval_every: int = 1
     heavy_threshold: int = 65535         # device phi: 16-bit columns below it
     check_conservation: bool = False
+    phi_sync: str = "nccl"               # G > 1: "nccl" all_reduce, or "peer" (IPC peer-memory kernel)
 
     def __post_init__(self):
         if not 1 <= self.num_topics < 2**16:
@@ -63,6 +64,8 @@ class TrainConfig:
         if self.chunks_per_worker != 1:
             raise ValueError("only WorkSchedule1 (M = 1): every configured corpus fits in HBM")
         phi_dtype(self.phi_width)
+        if self.phi_sync not in ("nccl", "peer"):
+            raise ValueError(f"phi_sync must be 'nccl' or 'peer', not {self.phi_sync!r}")
 
 
 @dataclass
@@ -137,7 +140,14 @@ class Trainer:
                                    heavy_threshold=cfg.heavy_threshold, global_word_freq=self.global_freq,
                                    stream=stream)
         self.shard.load(self.chunk)
-        self._sync_t = self.shard.sync_tensor() if self.world > 1 else None
+        self._peer = self.world > 1 and cfg.phi_sync == "peer"
+        if self._peer:
+            # map every rank's sync buffer (same node): the phi sum becomes one
+            # kernel on the shard's stream (gf_shard_peer_allreduce)
+            parts = [None] * self.world
+            self.dist.all_gather_object(parts, self.shard.peer_handle(), group=self.group)
+            self.shard.peer_open(self.rank, self.world, parts)
+        self._sync_t = self.shard.sync_tensor() if self.world > 1 and not self._peer else None
         self.num_tokens = corpus.num_tokens
         self.iteration = 0
         # counts from the initial assignments
@@ -172,6 +182,9 @@ class Trainer:
     def _allreduce_sync(self, async_op=False):
         if self.world == 1:
             return None
+        if self._peer:
+            self.shard.peer_allreduce()
+            return None
         return self.dist.all_reduce(self._sync_t, group=self.group, async_op=async_op)
 
     # -------------------------------------------------------------- steps --
@@ -180,8 +193,8 @@ class Trainer:
         it = self.iteration
         t0 = time.perf_counter()
         sh = self.shard
-        if self.world == 1:
-            sh.iterate(it)                       # K1, then K3 beside K2 + prepare (gf_shard_iterate)
+        if self.world == 1 or self._peer:
+            sh.iterate(it)                       # K1, then K3 beside K2 (+ peer phi exchange) + prepare
         else:
             sh.sample(it)
             sh.rebuild_phi()

@@ -160,6 +160,29 @@ class DeviceShard:
         _lib.check(_lib.lib().gf_shard_sync_buffer(self._h, ctypes.byref(p), ctypes.byref(n)))
         return torch.as_tensor(_CudaArray(p.value, n.value, "<i4", self), device=f"cuda:{self.device}")
 
+    # ------------------------------------------- peer-memory phi exchange --
+    PEER_HANDLE_BYTES = 128
+
+    def peer_handle(self):
+        """IPC handles (bytes) of this shard's sync buffer and signal slots."""
+        buf = ctypes.create_string_buffer(self.PEER_HANDLE_BYTES)
+        _lib.check(_lib.lib().gf_shard_peer_handle(self._h, buf))
+        return buf.raw
+
+    def peer_open(self, rank, world, handles):
+        """Map the other ranks' buffers; `handles` = the ranks' peer_handle() in rank order."""
+        blob = b"".join(handles)
+        if len(handles) != world or len(blob) != world * self.PEER_HANDLE_BYTES:
+            raise ValueError("need one peer handle per rank")
+        _lib.check(_lib.lib().gf_shard_peer_open(self._h, int(rank), int(world), blob))
+
+    def peer_allreduce(self):
+        """Sum the sync buffers of the peer group in place (stream-ordered)."""
+        _lib.check(_lib.lib().gf_shard_peer_allreduce(self._h))
+
+    def peer_close(self):
+        _lib.check(_lib.lib().gf_shard_peer_close(self._h))
+
     # --------------------------------------------------------- import/export --
     @property
     def num_tokens(self):
