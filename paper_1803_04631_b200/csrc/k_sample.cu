@@ -115,10 +115,10 @@ __device__ __forceinline__ U3 draw_u(const SampleArgs& a, uint32_t gdoc, uint32_
 }
 
 // p1 term of one theta entry (count << 16 | topic << 2) against p* at shared offset 0
-// The count converts without the quarter-rate I2F: one PRMT builds the float
+// The count converts without the quarter-rate I2F: one LEA.HI builds the float
 // 2^23 + count (count in the low mantissa bits), one FADD removes 2^23 (exact).
 __device__ __forceinline__ float count_f(uint32_t e) {
-    return __int_as_float(__byte_perm(e, 0x4B000000u, 0x7432)) - 8388608.f;
+    return __int_as_float(0x4B000000u + (e >> 16)) - 8388608.f;
 }
 __device__ __forceinline__ float w_of(uint32_t e, const float* smem) {
     return count_f(e) * smem[(e & 0xfffcu) >> 2];
@@ -474,8 +474,8 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
                 const bool act = qL < Utot;
                 float p[VEC];                                               // prefix at each vector end
 #pragma unroll
-                for (int i = 0; i < VEC; ++i)                               // independent pair sums (ILP)
-                    p[i] = (w_of(e[i].x, smem) + w_of(e[i].y, smem)) + (w_of(e[i].z, smem) + w_of(e[i].w, smem));
+                for (int i = 0; i < VEC; ++i)                               // FMUL + 3 FFMA per vector
+                    p[i] = ((w_of(e[i].x, smem) + w_of(e[i].y, smem)) + w_of(e[i].z, smem)) + w_of(e[i].w, smem);
                 p[1] += p[0];
                 const int head = mle ? 31 - __clz(mle) : -1;                // my segment's first lane
                 const int lim = max(head, 0);
