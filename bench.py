@@ -216,6 +216,44 @@ def cpu_baseline(shape, K, seed, ndocs, iters=2):
                       f"OpenMP C, {threads} threads)"}
 
 
+def reference_components(shape, K, seed, ndocs):
+    """Time the UNMODIFIED reference package (baseline/_ref/gibbsflow, installed
+    offline from /root/reference/pkg) on the same document sample: its own
+    partition (corpus.py:240-287), rebuild_theta (model.py:109-124) and
+    rebuild_phi_replica (model.py:142-161), single-threaded numpy/numba as
+    shipped -- the CPU counterparts of K4, K3 and K2.  None when
+    the package is not installed."""
+    import tempfile
+
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "gibbsflow")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="gf_numba_"))
+    sys.path.insert(0, ref)
+    try:
+        from gibbsflow import corpus as rc
+        from gibbsflow import model as rm
+    finally:
+        sys.path.remove(ref)
+    from paper_1803_04631_b200 import synth
+
+    corp = synth.generate(ndocs, shape["vocab_size"], shape["mean_len"], seed=seed)
+    rcorp = rc.corpus_from_tokens(corp.doc_ids, corp.word_ids, corp.vocab_size)
+    T = int(rcorp.num_tokens)
+    rc.partition(rcorp, 1, K, seed)                      # numba JIT outside the timing
+    out = {"sample": f"{ndocs} docs ({T} tokens), K={K}, reference package as installed (single thread)"}
+    t0 = time.perf_counter()
+    chunk = rc.partition(rcorp, 1, K, seed)[0]
+    out["partition_tokens_per_s"] = T / (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    rm.rebuild_theta(chunk, K)
+    out["rebuild_theta_tokens_per_s"] = T / (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    rm.rebuild_phi_replica(chunk, K, corp.vocab_size)
+    out["rebuild_phi_tokens_per_s"] = T / (time.perf_counter() - t0)
+    return out
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -245,6 +283,7 @@ def run_reference(args, world, rank):
                          "sample": f"{ndocs} docs ({T} tokens); the reference package has no sampler, so the "
                                    f"oracle port (oracle/gf_oracle.c) runs the SPEC algorithm"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_components": reference_components(shape, K, args.seed, min(ndocs, 5000)),
     }
     print(json.dumps(line), flush=True)
 
