@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=12)
     ap.add_argument("--seed", type=int, default=20261017)
     ap.add_argument("--tag", default="r1d")
+    ap.add_argument("--out-dir", default="profiles")
     args = ap.parse_args()
 
     import torch
@@ -93,7 +94,7 @@ def main():
 
     n = min(len(cpu_ll), len(gpu_ll))
     rel = [abs(gpu_ll[i] - cpu_ll[i]) / abs(cpu_ll[i]) for i in range(n)]
-    out = os.path.join(ROOT, "profiles", f"{args.tag}_loglik_{args.workload}")
+    out = os.path.join(ROOT, args.out_dir, f"{args.tag}_loglik_{args.workload}")
     with open(out + ".csv", "w") as fh:
         fh.write("iteration,gpu_elapsed_s,gpu_loglik_per_token,cpu_elapsed_s,cpu_loglik_per_token\n")
         for i in range(len(gpu_ll)):
