@@ -458,16 +458,48 @@ def run_ours(args, world, rank, local):
         z_in = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
         z_io = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
         z_in[:] = sh.get_assignments()
-        nchunk = int(os.environ.get("GF_E2E_CHUNKS", "16"))
-        bounds = np.linspace(0, T_local, nchunk + 1).astype(np.int64)
-        d2h_s, h2d_s = torch.cuda.Stream(device), torch.cuda.Stream(device)
+        # streamed sampling: the schedule is split into P word-group phases, so
+        # phase p's assignments travel back (and out again as the next step's
+        # input) while phases p+1.. sample; only the last phase's round trip is
+        # exposed.  Reload the same tokens with a phase-major schedule; the state
+        # carries over through z (the counts are rebuilt from it every step).
+        nphase = int(os.environ.get("GF_E2E_PHASES", "16"))
+        if nphase > 1:
+            sh.set_phases(nphase)
+            sh.load_tokens(lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, seed=args.seed, chunk_id=rank)
+            if peer:
+                handles = [None] * world
+                dist.all_gather_object(handles, sh.peer_handle())
+                sh.peer_open(rank, world, handles)
+            sync_t = sh.sync_tensor() if dist else None
+        nphase = sh.num_phases
+        ranges = [sh.phase_range(p) for p in range(nphase)]
+        nchunk = max(nphase, int(os.environ.get("GF_E2E_CHUNKS", "16")))
+        per = max(1, nchunk // nphase)
+        pieces = [[(int(x), int(y)) for x, y in zip(np.linspace(a0, b0, per + 1).astype(np.int64)[:-1],
+                                                     np.linspace(a0, b0, per + 1).astype(np.int64)[1:]) if y > x]
+                  for a0, b0 in ranges]
+        d2h_s, h2d_s, alt = torch.cuda.Stream(device), torch.cuda.Stream(device), torch.cuda.Stream(device)
 
-        def upload(host, after=None):
-            for c in range(nchunk):
-                if after is not None:
-                    h2d_s.wait_event(after[c])
-                sh.copy_assignments_async(host, bounds[c], bounds[c + 1] - bounds[c], True, h2d_s)
+        def upload(host):
+            for ps in pieces:
+                for x, y in ps:
+                    sh.copy_assignments_async(host, x, y - x, True, h2d_s)
             return h2d_s.record_event()
+
+        def counts_from_z():
+            # K3 (theta from zdoc) on the side stream beside K2 [+ allreduce] + prepare
+            k = stream.record_event()
+            side.wait_event(k)
+            sh.set_stream(side)
+            sh.rebuild_theta()
+            sh.set_stream(stream)
+            sh.rebuild_phi()
+            w = allreduce_async()
+            if w:
+                w.wait()
+            sh.prepare()
+            stream.wait_stream(side)
 
         barrier()
         t0 = time.perf_counter()
@@ -475,22 +507,31 @@ def run_ours(args, world, rank, local):
         for i in range(args.steps):
             stream.wait_event(ev_in)
             sh.assignments_imported()
-            sh.rebuild_phi()
-            w = allreduce_async()
-            if w:
-                w.wait()
-            sh.prepare()
-            sh.rebuild_theta()
-            sh.sample(it)
+            counts_from_z()
+            last = i + 1 == args.steps
+            ready = stream.record_event()
+            alt.wait_event(ready)
+            done = [None, None]
+            for p in range(nphase):
+                # phases alternate between two streams (they are independent), so a
+                # phase's tail CTAs overlap the next phase's start; the last phase
+                # (it also reduces the loglik) waits for the other stream
+                ps = stream if p % 2 == 0 else alt
+                if p == nphase - 1 and done[1 - p % 2] is not None:
+                    ps.wait_event(done[1 - p % 2])
+                sh.set_stream(ps)
+                sh.sample_phase(it, p)
+                done[p % 2] = ps.record_event()
+                d2h_s.wait_event(done[p % 2])
+                for x, y in pieces[p]:
+                    sh.copy_assignments_async(z_io, x, y - x, False, d2h_s)
+                    if not last:             # out again as the next step's input once it landed
+                        h2d_s.wait_event(d2h_s.record_event())
+                        sh.copy_assignments_async(z_io, x, y - x, True, h2d_s)
+            sh.set_stream(stream)
+            stream.wait_stream(alt)
             it += 1
-            ev_k1 = stream.record_event()
-            d2h_s.wait_event(ev_k1)
-            landed = []
-            for c in range(nchunk):
-                sh.copy_assignments_async(z_io, bounds[c], bounds[c + 1] - bounds[c], False, d2h_s)
-                landed.append(d2h_s.record_event())
-            if i + 1 < args.steps:
-                ev_in = upload(z_io, after=landed)
+            ev_in = h2d_s.record_event()
             lls = sh.loglik_sum()             # D2H of the step's loglik
         torch.cuda.synchronize(device)
         barrier()
@@ -501,9 +542,10 @@ def run_ours(args, world, rank, local):
             el = float(t.item())
         e2e = {"value": T_all * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": 2 * T_local,
                "d2h_bytes_per_step": 2 * T_local + 8,
-               "api": "DeviceShard.copy_assignments_async (16 chunks per direction, two copy streams, pinned "
-                      "host buffers) + assignments_imported, rebuild_phi/prepare/rebuild_theta, sample, "
-                      "loglik_sum (C ABI)"}
+               "api": f"DeviceShard.copy_assignments_async (pinned host buffers, two copy streams) + "
+                      f"assignments_imported, rebuild_phi/prepare/rebuild_theta, sample_phase x {nphase} "
+                      f"(each phase's assignments copied back and out while later phases sample), "
+                      f"loglik_sum (C ABI)"}
         del lls
 
     cpu = None

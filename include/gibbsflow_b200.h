@@ -141,6 +141,16 @@ int gf_shard_sample(gf_shard* shard, uint32_t iteration);
 /* SPEC.md:402-410 loglik_per_token numerator for the CURRENT theta / phi
  * (no draws): read it back with gf_shard_loglik_sum. */
 int gf_shard_evaluate(gf_shard* shard);
+/* Sampling phases (streamed sampling): split the slice schedule into P phases
+ * of contiguous word groups, ~T/P tokens each, so the host can copy phase p's
+ * assignments z[tok_begin, tok_end) (word-group order) while later phases
+ * sample.  gf_shard_set_phases applies at the next load (default 1).
+ * gf_shard_sample_phase(p) for p = 0..P-1 in order is one gf_shard_sample
+ * (same draws, same loglik; the loglik reduction runs after phase P-1). */
+int gf_shard_set_phases(gf_shard* shard, int num_phases);
+int gf_shard_num_phases(gf_shard* shard, int* num_phases_out);
+int gf_shard_phase_range(gf_shard* shard, int phase, int64_t* tok_begin, int64_t* tok_end);
+int gf_shard_sample_phase(gf_shard* shard, uint32_t iteration, int phase);
 /* One deferred iteration: sample -> rebuild_phi [-> peer phi
  * exchange when a peer group is open] -> prepare, with rebuild_theta on an
  * internal stream beside everything after the sample. */

@@ -49,6 +49,10 @@ SIGNATURES = {
     "gf_shard_sample": (_int, [_p, _u32]),
     "gf_shard_iterate": (_int, [_p, _u32]),
     "gf_shard_evaluate": (_int, [_p]),
+    "gf_shard_set_phases": (_int, [_p, _int]),
+    "gf_shard_num_phases": (_int, [_p, _p]),
+    "gf_shard_phase_range": (_int, [_p, _int, _p, _p]),
+    "gf_shard_sample_phase": (_int, [_p, _u32, _int]),
     "gf_shard_loglik_sum": (_int, [_p, _p]),
     "gf_shard_check_errors": (_int, [_p]),
     "gf_shard_synchronize": (_int, [_p]),

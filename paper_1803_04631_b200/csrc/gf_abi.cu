@@ -408,6 +408,41 @@ int gf_shard_sample(gf_shard* s, uint32_t iteration) {
     return GF_OK;
 }
 
+int gf_shard_set_phases(gf_shard* s, int num_phases) {
+    if (num_phases < 1 || num_phases > 255) return fail(GF_ERR_VALUE, "phases must be in [1, 255]");
+    s->n_phases = num_phases;     // applies at the next load (the slice schedule is built there)
+    return GF_OK;
+}
+
+int gf_shard_num_phases(gf_shard* s, int* out) {
+    if (int rc = need_loaded(s)) return rc;
+    *out = (int)s->phase_slice0.size() - 1;
+    return GF_OK;
+}
+
+int gf_shard_phase_range(gf_shard* s, int phase, int64_t* tok_begin, int64_t* tok_end) {
+    if (int rc = need_loaded(s)) return rc;
+    if (phase < 0 || phase + 1 >= (int)s->phase_tok0.size()) return fail(GF_ERR_VALUE, "phase %d out of range", phase);
+    *tok_begin = s->phase_tok0[phase];
+    *tok_end = s->phase_tok0[phase + 1];
+    return GF_OK;
+}
+
+int gf_shard_sample_phase(gf_shard* s, uint32_t iteration, int phase) {
+    if (int rc = need_loaded(s)) return rc;
+    const int P = (int)s->phase_slice0.size() - 1;
+    if (phase < 0 || phase >= P) return fail(GF_ERR_VALUE, "phase %d out of range [0, %d)", phase, P);
+    if (phase == 0)
+        if (int rc = validate_if_dirty(s)) return rc;
+    const int64_t a = s->phase_slice0[phase], b = s->phase_slice0[phase + 1];
+    CU(gf::launch_sample_range(s, iteration, 0, a, b - a), "sample");
+    if (phase == P - 1) {
+        CU(gf::launch_ll_reduce(s), "loglik");
+        s->stat_sample_launches++;
+    }
+    return GF_OK;
+}
+
 int gf_shard_evaluate(gf_shard* s) {
     if (int rc = need_loaded(s)) return rc;
     CU(gf::launch_sample(s, 0, 1), "evaluate");

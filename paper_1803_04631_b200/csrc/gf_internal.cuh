@@ -97,6 +97,11 @@ struct gf_shard {
     int64_t doc_lo = 0, doc_hi = 0, D = 0, T = 0, R = 0, n_slices = 0, n_k2 = 0;
     int64_t theta_cap = 0;
     int64_t n_doc_blocks = 1;
+    // sampling phases (gf_shard_set_phases): the slice schedule is phase-major;
+    // phase p owns the word groups whose tokens are z[phase_tok0[p], phase_tok0[p+1])
+    // and the slices [phase_slice0[p], phase_slice0[p+1])
+    int n_phases = 1;
+    std::vector<int64_t> phase_slice0{0, 0}, phase_tok0{0, 0};
     int64_t n_ctx = 0;
     bool ctx_dirty = true;                   // phi / n_k changed since the last prepare
     double ll_const = 0.0;                    // sum_d L_d log(L_d + K alpha)
@@ -157,6 +162,7 @@ int partition_to_host(int device, const int32_t* doc_ids, const int32_t* word_id
 // kernel launchers (k_sample.cu / k_counts.cu / k_ptree.cu)
 namespace gf {
 cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only = 0);
+cudaError_t launch_sample_range(gf_shard* s, uint32_t iteration, int eval_only, int64_t slice0, int64_t n);
 cudaError_t launch_phi_rebuild(gf_shard* s);
 cudaError_t launch_prepare(gf_shard* s);
 cudaError_t launch_contexts(gf_shard* s);

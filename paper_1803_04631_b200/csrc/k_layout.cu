@@ -140,14 +140,17 @@ __global__ void k_slice_begin(int64_t R, const uint32_t* flag, const uint32_t* s
 
 // schedule key: document block (or round-robin for groups not block-scheduled)
 // << 40 | heavy-first rank << 20 | slice ordinal inside its group
+// (sampling phase << 56 on top when the schedule is split into phases)
 __global__ void k_slice_keys(int64_t N, int64_t R, const uint32_t* srb, const uint32_t* run_group,
                              const uint32_t* run_doc, const int32_t* doc_blk, const uint32_t* g_info,
-                             const uint32_t* g_slice0, int nblk, unsigned long long* key, uint32_t* val) {
+                             const uint32_t* g_slice0, const uint8_t* g_phase, int nblk, unsigned long long* key,
+                             uint32_t* val) {
     GRID_STRIDE(s, N) {
         const uint32_t r = srb[s], g = run_group[r];
         const bool blocked = (g_info[g] >> 31) != 0u;
         const uint64_t b = blocked ? (uint64_t)doc_blk[run_doc[r]] : (uint64_t)(s % nblk);
-        key[s] = (b << 40) | ((uint64_t)(g_info[g] & 0xFFFFFu) << 20) | (uint64_t)((uint32_t)s - g_slice0[g]);
+        const uint64_t ph = g_phase ? (uint64_t)g_phase[g] : 0ull;
+        key[s] = (ph << 56) | (b << 40) | ((uint64_t)(g_info[g] & 0xFFFFFu) << 20) | (uint64_t)((uint32_t)s - g_slice0[g]);
         val[s] = (uint32_t)s;
     }
 }
@@ -524,6 +527,29 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
         if (gnsl[g] > (1u << 20)) return shard_fail(GF_ERR_CAPACITY, "a word has more than 2^20 slices");
         if (gnsl[g] > 1) { gctx[g] = (int32_t)ctx_cols.size(); ctx_cols.push_back(gcol[g]); }
     }
+    // sampling phases: word groups cut into P contiguous z ranges of ~T/P tokens
+    // (groups are in ascending word order, so phase p's tokens are one z range)
+    const int P = std::max(1, std::min(s->n_phases, 255));
+    if (nblk >= (1 << 16)) return shard_fail(GF_ERR_CAPACITY, "more than 2^16 document blocks");
+    std::vector<uint8_t> gphase((size_t)ng, 0);
+    s->phase_slice0.assign((size_t)P + 1, 0);
+    s->phase_tok0.assign((size_t)P + 1, T);
+    s->phase_tok0[0] = 0;
+    for (int64_t g = 0; g < ng; ++g) {
+        const int ph = T > 0 ? (int)std::min<int64_t>(P - 1, (int64_t)go[g] * P / T) : 0;
+        gphase[g] = (uint8_t)ph;
+        s->phase_slice0[ph + 1] += gnsl[g];
+    }
+    for (int p = P - 1; p >= 1; --p)   // first token of phase p = first group of phase >= p
+        for (int64_t g = 0; g < ng; ++g)
+            if (gphase[g] >= p) { s->phase_tok0[p] = go[g]; break; }
+    for (int p = 0; p < P; ++p) s->phase_slice0[p + 1] += s->phase_slice0[p];
+    uint8_t* d_gphase = nullptr;
+    if (P > 1) {
+        d_gphase = static_cast<uint8_t*>(sc.get((size_t)std::max<int64_t>(ng, 1)));
+        CK(sc.err, "layout scratch");
+        if (ng) CK(cudaMemcpyAsync(d_gphase, gphase.data(), ng, cudaMemcpyHostToDevice, st), "layout");
+    }
     int32_t* d_gctx = reinterpret_cast<int32_t*>(sc.u32(ng));
     uint32_t* d_gnsl = sc.u32(ng);
     unsigned long long* skey = static_cast<unsigned long long*>(sc.get((size_t)std::max<int64_t>(N, 1) * 8));
@@ -544,7 +570,7 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
     if (N > 0) {
         // block-major, heavy-first inside a block, slice order inside a word
         k_slice_keys<<<blocks_for(N), 256, 0, st>>>(N, R, srb, run_group, dv.run_doc, d_docblk, d_ginfo, d_gslice0,
-                                                   nblk, skey, sval);
+                                                   d_gphase, nblk, skey, sval);
         CK(cub_call(sc, [&](void* t, size_t& b) {
                return cub::DeviceRadixSort::SortPairs(t, b, skey, skey2, sval, sorder, N, 0, 64, st);
            }),

@@ -637,7 +637,7 @@ size_t sample_smem_bytes(const gf_shard* s) { return smem_for(s, kSampleThreads,
 size_t context_floats(const gf_shard* s) { return (size_t)lay_buf(s->K, s->tree.total); }
 
 template <int NT, uint32_t CAPV, int MINB, bool PF, bool HUGE>
-static cudaError_t launch_variant(gf_shard* s, const SampleArgs& a) {
+static cudaError_t launch_variant(gf_shard* s, const SampleArgs& a, int64_t n) {
     static unsigned long long attr_set = 0;
     if (attr_once(attr_set, s->device)) {
         cudaError_t e = cudaFuncSetAttribute(sample_kernel<NT, CAPV, MINB, PF, HUGE>,
@@ -647,7 +647,7 @@ static cudaError_t launch_variant(gf_shard* s, const SampleArgs& a) {
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
     }
-    sample_kernel<NT, CAPV, MINB, PF, HUGE><<<(unsigned)s->n_slices, NT, smem_for(s, NT, CAPV), s->stream>>>(a);
+    sample_kernel<NT, CAPV, MINB, PF, HUGE><<<(unsigned)n, NT, smem_for(s, NT, CAPV), s->stream>>>(a);
     return cudaGetLastError();
 }
 
@@ -718,12 +718,21 @@ cudaError_t launch_contexts(gf_shard* s) {
 }
 
 cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
-    if (s->n_slices == 0) return cudaSuccess;
+    return launch_sample_range(s, iteration, eval_only, 0, s->n_slices);
+}
+
+// slices [slice0, slice0 + n) of the schedule (a phase, gf_shard_sample_phase):
+// the kernel sees the range through offset slice / context / loglik pointers
+cudaError_t launch_sample_range(gf_shard* s, uint32_t iteration, int eval_only, int64_t slice0, int64_t n) {
+    if (n <= 0) return cudaSuccess;
     if (s->ctx_dirty) {                           // phi changed since the last prepare
         cudaError_t e = launch_prepare(s);
         if (e != cudaSuccess) return e;
     }
-    const SampleArgs a = make_args(s, iteration, eval_only);
+    SampleArgs a = make_args(s, iteration, eval_only);
+    a.slices += slice0;
+    a.slice_ctx += slice0;
+    a.ll_part += slice0;
     // tuning knob GF_K1 (variant id, A/B runs); rows can only outgrow the
     // staging buffer when K > 4*CAPV -- otherwise the streaming path (a
     // register-hungry call) is compiled out
@@ -732,14 +741,14 @@ cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only) {
         const char* env = getenv("GF_K1");
         var = env ? atoi(env) : 0;
     }
-    if (s->K > (int)(4 * kCapV)) return launch_variant<256, kCapV, 3, true, true>(s, a);    // rows can outgrow staging
-    if (s->K > 2048) return launch_variant<256, kCapV, 3, true, false>(s, a);    // p*_ex on demand: 3 x 8 warps/SM
-    if (var == 2) return launch_variant<256, kCapV, 4, true, false>(s, a);        // 8-warp CTAs (A/B)
-    if (var == 3) return launch_variant<128, 768, 8, false, false>(s, a);         // no pass prefetch (A/B)
+    if (s->K > (int)(4 * kCapV)) return launch_variant<256, kCapV, 3, true, true>(s, a, n);    // rows can outgrow staging
+    if (s->K > 2048) return launch_variant<256, kCapV, 3, true, false>(s, a, n);    // p*_ex on demand: 3 x 8 warps/SM
+    if (var == 2) return launch_variant<256, kCapV, 4, true, false>(s, a, n);        // 8-warp CTAs (A/B)
+    if (var == 3) return launch_variant<128, 768, 8, false, false>(s, a, n);         // no pass prefetch (A/B)
     // 4-warp CTAs, 8 per SM: a slice's tail (warps idle at the final barrier
     // while the last batch finishes) strands half as many warps; the pass keeps
     // its next 1 KB step in flight
-    return launch_variant<128, 768, 8, true, false>(s, a);
+    return launch_variant<128, 768, 8, true, false>(s, a, n);
 }
 
 }  // namespace gf

@@ -42,7 +42,7 @@ def sync_layout(global_word_freq, num_topics, heavy_threshold=65535):
 
 class DeviceShard:
     def __init__(self, num_topics, vocab_size, alpha, beta, seed=0, device=0,
-                 heavy_threshold=65535, global_word_freq=None, stream=None):
+                 heavy_threshold=65535, global_word_freq=None, stream=None, phases=1):
         self.K = int(num_topics)
         self.V = int(vocab_size)
         self.alpha = float(alpha)
@@ -55,6 +55,8 @@ class DeviceShard:
         self.heavy_threshold = int(heavy_threshold)
         if stream is not None:
             self.set_stream(stream)
+        if phases != 1:
+            self.set_phases(phases)
         if global_word_freq is not None:
             f = _lib.carr(global_word_freq, np.int64)
             if len(f) != self.V:
@@ -129,6 +131,26 @@ class DeviceShard:
 
     def sample(self, iteration):
         _lib.check(_lib.lib().gf_shard_sample(self._h, int(iteration)))
+
+    # ------------------------------------------ streamed sampling (phases) --
+    def set_phases(self, num_phases):
+        """Split the slice schedule into word-group phases (applies at the next load)."""
+        _lib.check(_lib.lib().gf_shard_set_phases(self._h, int(num_phases)))
+
+    @property
+    def num_phases(self):
+        n = ctypes.c_int()
+        _lib.check(_lib.lib().gf_shard_num_phases(self._h, ctypes.byref(n)))
+        return n.value
+
+    def phase_range(self, phase):
+        """(tok_begin, tok_end): the assignments (word-group order) phase `phase` samples."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib().gf_shard_phase_range(self._h, int(phase), ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def sample_phase(self, iteration, phase):
+        _lib.check(_lib.lib().gf_shard_sample_phase(self._h, int(iteration), int(phase)))
 
     def iterate(self, iteration):
         _lib.check(_lib.lib().gf_shard_iterate(self._h, int(iteration)))
