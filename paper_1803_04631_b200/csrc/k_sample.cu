@@ -43,7 +43,6 @@ namespace gf {
 constexpr uint32_t kCapV = 1024;      // staged vector-end prefixes per warp (4096 entries)
 constexpr int kMaxRetry = 63;
 
-__device__ __align__(32) const uint32_t g_zero32[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256); p must be 32-byte aligned
 __device__ __forceinline__ void ldg256(const uint32_t* p, uint4& lo, uint4& hi) {
@@ -85,6 +84,7 @@ struct SampleArgs {
     int ctx_stride;                           // floats per context = lay_buf(K, tree.total)
     TPos tm;                                  // transposed p* layout (gf_device.cuh)
     double* ll_part;
+    uint32_t zero_ent;                        // theta_ent index of a zero 32-byte granule (= capacity)
     unsigned long long* errs;
     unsigned long long* bytes;
 };
@@ -117,6 +117,17 @@ __device__ __forceinline__ U3 draw_u(const SampleArgs& a, uint32_t gdoc, uint32_
 // p1 term of one theta entry (count << 16 | topic << 2) against p* at shared offset 0
 // The count converts without the quarter-rate I2F: one LEA.HI builds the float
 // 2^23 + count (count in the low mantissa bits), one FADD removes 2^23 (exact).
+__device__ __forceinline__ uint32_t shl_clamped(uint32_t x, uint32_t n) {
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));   // PTX: n >= 32 gives 0
+    return r;
+}
+// %lanemask_le as one S2R instead of a mask kept live (or rebuilt) across the pass
+__device__ __forceinline__ unsigned lanemask_le() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+    return m;
+}
 __device__ __forceinline__ float count_f(uint32_t e) {
     return __int_as_float(0x4B000000u + (e >> 16)) - 8388608.f;
 }
@@ -443,14 +454,19 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
             // next step's load is issued before the current step is summed and
             // scanned (one step in flight ahead, in registers).
             int cprev = first - 1;                                          // run holding vector q-1
+            const uint32_t hv = sel ? vo : 0xFFFFFFFFu;                     // my row's head vector
             auto issue = [&](uint32_t qs, unsigned& Ms, uint4& x0, uint4& x1) {
-                const uint32_t hb = (sel && vo - qs < 32u * VEC) ? (1u << ((vo - qs) / VEC)) : 0u;
+                // bit (vo - qs) / VEC when my row starts in step qs: a shift by >= 32
+                // (row outside the step, or no row) yields 0 (shl clamps)
+                const uint32_t hb = shl_clamped(1u, (hv - qs) / VEC);
                 Ms = __reduce_or_sync(kFull, hb);                           // run heads in step qs
-                const int ri = min(cprev + __popc(Ms & lane_le), 31);
+                const int ri = min(cprev + __popc(Ms & lanemask_le()), 31);
                 const uint32_t rvo = __shfl_sync(kFull, vo, ri);
                 const uint32_t roff = __shfl_sync(kFull, off, ri);
                 const uint32_t qL = qs + VEC * (uint32_t)lane;
-                const uint32_t* src = qL < Utot ? a.theta_ent + roff + 4u * (qL - rvo) : &g_zero32[0];
+                const uint32_t idx = roff + 4u * (qL - rvo);                // entry index (< 2^32)
+                // lanes past the sub-batch read the zero granule after the last row
+                const uint32_t* src = a.theta_ent + (qL < Utot ? idx : a.zero_ent);
                 ldg256(src, x0, x1);
                 cprev = min(cprev + __popc(Ms), 31);                        // lane 31's row
             };
@@ -469,7 +485,7 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
                 } else {
                     issue(q0, M, e[0], e[1]);
                 }
-                const unsigned mle = M & lane_le;
+                const unsigned mle = M & lanemask_le();
                 const uint32_t qL = q0 + VEC * (uint32_t)lane;
                 const bool act = qL < Utot;
                 float p[VEC];                                               // prefix at each vector end
@@ -668,6 +684,7 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     a.doc_lo = (uint32_t)s->doc_lo;
     a.eval_only = eval_only;
     a.prefetch = (int)env_flag("GF_PREFETCH", 1);
+    a.zero_ent = (uint32_t)s->theta_cap;
     a.guide_min_tokens = (int)env_flag("GF_GUIDE_MIN", 512);
     a.tree = s->tree;
     a.slices = s->d.slices;
