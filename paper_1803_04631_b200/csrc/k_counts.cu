@@ -134,9 +134,9 @@ cudaError_t launch_prepare(gf_shard* s) {
 // topic << 2) (the topic pre-scaled to a byte offset into K1's shared p*
 // table), ascending topic, in the fixed-capacity row; nnz into meta.y.
 __host__ __device__ inline int k3_words(int K) { return (K + 31) >> 5; }
-__host__ __device__ inline int k3_warp_u32(int K) { return K + k3_words(K); }
+__host__ __device__ inline int k3_warp_u32(int K) { return K + 2 * k3_words(K); }   // bins | bitmap | word ranks
 
-__global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
+__global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
                                                             const uint16_t* __restrict__ zdoc, uint32_t* theta_ent,
                                                             uint2* theta_meta, int K, int warps_per_cta,
                                                             unsigned long long* errs) {
@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
     const TPos tm = tpos_geom(K);
     uint32_t* bins = sh + (size_t)warp * k3_warp_u32(K);
     uint32_t* bmp = bins + K;
-    for (int i = lane; i < k3_warp_u32(K); i += 32) bins[i] = 0u;
+    uint32_t* wpre = bmp + NW;                     // distinct topics below each bitmap word
+    for (int i = lane; i < K + NW; i += 32) bins[i] = 0u;
     __syncwarp();
     const unsigned lt = (1u << lane) - 1u;
     // software pipeline over this warp's documents d, d+s, d+2s: the next
@@ -181,6 +182,54 @@ __global__ void __launch_bounds__(256) theta_rebuild_kernel(int D, const uint32_
                 theta_ent[off + __popc(heads & lt)] = (tpos(key, tm) << 2) | ((next - lane) << 16);
             }
             nnz = __popc(heads);
+        } else if (L <= 128) {
+            // token-parallel emit (32 < L <= 128, the tokens stay in registers):
+            // the first occurrence of each topic (atomicAdd returned 0) writes
+            // its entry at its rank = distinct topics below it (word prefix +
+            // popc inside the word) -- no per-bitmap-word loop, no divergence
+            const uint32_t i1 = lane + 32u, i2 = lane + 64u, i3 = lane + 96u;
+            const uint32_t kk[4] = {zf, i1 < L ? zdoc[b + i1] : 0xffffu, i2 < L ? zdoc[b + i2] : 0xffffu,
+                                    i3 < L ? zdoc[b + i3] : 0xffffu};
+            bool fst[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t k = kk[j];
+                fst[j] = false;
+                if (k < (uint32_t)K) {
+                    fst[j] = atomicAdd(&bins[k], 1u) == 0u;
+                    if (fst[j]) atomicOr(&bmp[k >> 5], 1u << (k & 31u));
+                } else if ((uint32_t)lane + 32u * j < L) {
+                    atomicMin(errs + 2, (unsigned long long)d);
+                }
+            }
+            __syncwarp();
+            uint32_t base = 0;
+            for (int c = 0; c < NW; c += 32) {
+                const int w = c + lane;
+                const uint32_t pc = w < NW ? __popc(bmp[w]) : 0u;
+                uint32_t incl = pc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                if (w < NW) wpre[w] = base + incl - pc;
+                base += __shfl_sync(kFull, incl, 31);
+            }
+            nnz = base;
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (fst[j]) {
+                    const uint32_t k = kk[j], w = k >> 5;
+                    const uint32_t r = wpre[w] + __popc(bmp[w] & ((1u << (k & 31u)) - 1u));
+                    theta_ent[off + r] = (tpos(k, tm) << 2) | (bins[k] << 16);    // <= 128: no overflow
+                }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (fst[j]) { bins[kk[j]] = 0u; bmp[kk[j] >> 5] = 0u; }
+            __syncwarp();
         } else {
             auto count = [&](uint32_t k) {
                 if (k < (uint32_t)K) {
