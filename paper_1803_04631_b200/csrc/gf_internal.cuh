@@ -95,6 +95,7 @@ struct gf_shard {
     int64_t n_heavy = 0, n_light = 0;
     int64_t off_phi16_u32 = 0, off_nk_u32 = 0, sync_u32 = 0;
     int64_t doc_lo = 0, doc_hi = 0, D = 0, T = 0, R = 0, n_slices = 0, n_k2 = 0;
+    int64_t n_k2_big = 0;                    // K2 items [0, n_k2_big) per CTA, the rest (<= 32 tokens) per warp
     int64_t theta_cap = 0;
     int64_t n_doc_blocks = 1;
     // sampling phases (gf_shard_set_phases): the slice schedule is phase-major;

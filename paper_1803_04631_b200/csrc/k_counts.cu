@@ -18,7 +18,11 @@ namespace gf {
 // are word-grouped, so the item is one contiguous z range) and writes only
 // the nonzero cells into the pre-zeroed sync buffer; n_k is accumulated per
 // CTA in shared memory and flushed with K atomics at the end.
-__global__ void __launch_bounds__(256) phi_rebuild_kernel(const int4* __restrict__ items, int n_items,
+// Items of <= 32 tokens (the rare words of a large vocabulary) go to single
+// warps instead: one topic per lane, __match_any_sync groups equal topics and
+// the group leader writes the cell -- no shared histogram, no block barriers.
+// The layout puts the CTA items first ([0, n_big)) and the warp items after.
+__global__ void __launch_bounds__(256) phi_rebuild_kernel(const int4* __restrict__ items, int n_items, int n_big,
                                                           const uint16_t* __restrict__ z, uint32_t* sync,
                                                           int K, int Kp, long long off16, long long offnk,
                                                           unsigned long long* errs) {
@@ -28,7 +32,7 @@ __global__ void __launch_bounds__(256) phi_rebuild_kernel(const int4* __restrict
     for (int k = threadIdx.x; k < 2 * K; k += blockDim.x) sh[k] = 0;
     __syncthreads();
     uint16_t* phi16 = reinterpret_cast<uint16_t*>(sync + off16);
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = blockIdx.x; it < n_big; it += gridDim.x) {
         const int4 w = items[it];
         const int col = w.x, t0 = w.y, t1 = w.z;
         const bool atomic = w.w != 0;
@@ -77,6 +81,28 @@ __global__ void __launch_bounds__(256) phi_rebuild_kernel(const int4* __restrict
         }
         __syncthreads();
     }
+    // ---- warp items ----
+    const int lane = threadIdx.x & 31;
+    const int nw = (int)(blockDim.x >> 5);
+    for (int it = n_big + blockIdx.x * nw + (int)(threadIdx.x >> 5); it < n_items; it += gridDim.x * nw) {
+        const int4 w = items[it];
+        const int col = w.x, t = w.y + lane;
+        bool valid = t < w.z;
+        const uint32_t k = valid ? (uint32_t)z[t] : 0xFFFFFFFFu;
+        if (valid && k >= (uint32_t)K) {
+            atomicMin(errs, (unsigned long long)t);
+            valid = false;
+        }
+        const unsigned grp = __match_any_sync(kFull, valid ? k : 0xFFFFFFFFu);
+        if (valid && lane == __ffs(grp) - 1) {
+            const uint32_t c = (uint32_t)__popc(grp);
+            atomicAdd(&nks[k], c);
+            if (col >= 0) phi16[(size_t)col * Kp + k] = (uint16_t)c;
+            else if (w.w != 0) atomicAdd(&sync[(size_t)(~col) * K + k], c);
+            else sync[(size_t)(~col) * K + k] = c;
+        }
+    }
+    __syncthreads();
     uint32_t* nk = sync + offnk;
     for (int k = threadIdx.x; k < K; k += blockDim.x)
         if (nks[k]) atomicAdd(&nk[k], nks[k]);
@@ -95,9 +121,11 @@ cudaError_t launch_phi_rebuild(gf_shard* s) {
         if (e != cudaSuccess) return e;
     }
     const int per_sm = smem <= 16 * 1024 ? 8 : (smem <= 48 * 1024 ? 4 : 1);
-    const long long grid = std::min<long long>(s->n_k2, (long long)nsm * per_sm);
-    phi_rebuild_kernel<<<(unsigned)grid, 256, smem, s->stream>>>(s->d.k2items, (int)s->n_k2, s->d.z, s->d.sync, s->K,
-                                                                  s->Kp, s->off_phi16_u32, s->off_nk_u32, s->d.errs);
+    const long long grid = std::min<long long>(std::max<long long>(s->n_k2_big, (s->n_k2 - s->n_k2_big + 7) / 8),
+                                               (long long)nsm * per_sm);
+    phi_rebuild_kernel<<<(unsigned)grid, 256, smem, s->stream>>>(s->d.k2items, (int)s->n_k2, (int)s->n_k2_big, s->d.z,
+                                                                  s->d.sync, s->K, s->Kp, s->off_phi16_u32,
+                                                                  s->off_nk_u32, s->d.errs);
     return cudaGetLastError();
 }
 

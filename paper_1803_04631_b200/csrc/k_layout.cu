@@ -194,6 +194,10 @@ __global__ void k_items_emit(int64_t N, int64_t R, int64_t ng, int64_t T, const 
     }
 }
 
+struct BigItem {
+    __host__ __device__ bool operator()(const int4& w) const { return w.z - w.y > 32; }
+};
+
 // zdoc positions (heavy-first inside each document)
 __global__ void k_inverse(int64_t T, const uint32_t* dw_tok, uint32_t* inv) { GRID_STRIDE(q, T) inv[dw_tok[q]] = (uint32_t)q; }
 
@@ -590,9 +594,20 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
         M = read_u32(st, iflag + N + ng - 1) + read_u32(st, ipos + N + ng - 1);
     }
     if ((rc = shard_alloc(&dv.k2items, M, "items"))) return rc;
-    if (M > 0)
+    int64_t Mbig = 0;
+    if (M > 0) {
+        int4* staged = static_cast<int4*>(sc.get((size_t)M * sizeof(int4)));
+        int* d_nsel = reinterpret_cast<int*>(sc.u32(1));
+        CK(sc.err, "layout scratch");
         k_items_emit<<<blocks_for(N + ng), 256, 0, st>>>(N, R, ng, T, srb, run_group, dv.run_start, d_gcol, d_gnsl,
-                                                         c.go, iflag, ipos, dv.k2items);
+                                                         c.go, iflag, ipos, staged);
+        // CTA items (> 32 tokens) first, warp items after (K2's two loops)
+        CK(cub_call(sc, [&](void* t, size_t& b) {
+               return cub::DevicePartition::If(t, b, staged, dv.k2items, d_nsel, (int)M, BigItem(), st);
+           }),
+           "items");
+        Mbig = read_u32(st, reinterpret_cast<uint32_t*>(d_nsel));
+    }
     // ---- zdoc positions: heavy-first inside each document ----
     if (T > 0) {
         uint32_t* inv = flag;                 // reuse: [T]
@@ -618,6 +633,7 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
     s->R = R;
     s->n_slices = N;
     s->n_k2 = M;
+    s->n_k2_big = Mbig;
     s->n_ctx = (int64_t)ctx_cols.size();
     s->n_doc_blocks = nblk;
     s->ctx_dirty = true;
