@@ -501,6 +501,8 @@ def run_ours(args, world, rank, local):
             sh.prepare()
             stream.wait_stream(side)
 
+        sh.copy_assignments_async(z_in, 0, 1, True, h2d_s)   # allocates the import staging buffer
+        torch.cuda.synchronize(device)
         barrier()
         t0 = time.perf_counter()
         ev_in = upload(z_in)

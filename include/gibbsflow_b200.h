@@ -194,9 +194,11 @@ int gf_shard_get_assignments(gf_shard* shard, uint16_t* out);      /* word-group
 int gf_shard_set_assignments(gf_shard* shard, const uint16_t* in);
 /* Asynchronous piecewise transfer of assignments [offset, offset + count) between
  * a (pinned) host buffer and the shard, on `stream` (a cudaStream_t; NULL: the
- * shard's stream), direction 1 = host -> device, 0 = device -> host.  After a
- * complete host -> device import, gf_shard_assignments_imported (stream-ordered
- * after the copies) refreshes the doc-major copy and marks the counts stale. */
+ * shard's stream), direction 1 = host -> device, 0 = device -> host.  Host ->
+ * device pieces land in a staging buffer (allocated on the first such call);
+ * gf_shard_assignments_imported (stream-ordered after the copies) applies them:
+ * per run, only runs whose topics differ rewrite z and the doc-major copy.
+ * It marks the counts stale (rebuild_phi / rebuild_theta next). */
 int gf_shard_copy_assignments_async(gf_shard* shard, void* host, int64_t offset, int64_t count, int to_device,
                                     void* stream);
 int gf_shard_assignments_imported(gf_shard* shard);

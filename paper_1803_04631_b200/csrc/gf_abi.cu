@@ -83,7 +83,7 @@ int dev_alloc(T** p, size_t count, const char* what) {
 
 void free_dev(gf_shard* s) {
     auto& d = s->d;
-    void* ptrs[] = {d.z, d.run_doc, d.run_start, d.slices, d.k2items, d.dw_ptr, d.zdoc, d.run_dwpos, d.run_rec, d.theta_ent,
+    void* ptrs[] = {d.z, d.zstage, d.run_doc, d.run_start, d.slices, d.k2items, d.dw_ptr, d.zdoc, d.run_dwpos, d.run_rec, d.theta_ent,
                     d.theta_meta, d.sync, d.inv_den, d.ctx_tab, d.ctx_cols, d.slice_ctx, d.ll_part, d.ll_sum,
                     d.errs, d.bytes, d.scratch};
     for (void* p : ptrs)
@@ -589,7 +589,11 @@ int gf_shard_copy_assignments_async(gf_shard* s, void* host, int64_t offset, int
     if (int rc = need_loaded(s)) return rc;
     if (offset < 0 || count < 0 || offset + count > s->T) return fail(GF_ERR_SHAPE, "assignment range out of bounds");
     cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
-    uint16_t* dev = s->d.z + offset;
+    if (to_device && !s->d.zstage) {   // host -> device imports are staged, applied by _imported
+        cudaSetDevice(s->device);
+        CU(cudaMalloc((void**)&s->d.zstage, std::max<int64_t>(s->T, 1) * 2), "copy_assignments (staging)");
+    }
+    uint16_t* dev = (to_device ? s->d.zstage : s->d.z) + offset;
     uint16_t* h = static_cast<uint16_t*>(host) + offset;
     if (to_device) CU(cudaMemcpyAsync(dev, h, count * 2, cudaMemcpyHostToDevice, st), "copy_assignments");
     else CU(cudaMemcpyAsync(h, dev, count * 2, cudaMemcpyDeviceToHost, st), "copy_assignments");
@@ -598,7 +602,8 @@ int gf_shard_copy_assignments_async(gf_shard* s, void* host, int64_t offset, int
 
 int gf_shard_assignments_imported(gf_shard* s) {
     if (int rc = need_loaded(s)) return rc;
-    CU(gf::launch_zdoc_sync(s), "assignments_imported");
+    if (!s->d.zstage) return fail(GF_ERR_VALUE, "no staged assignments: gf_shard_copy_assignments_async(to_device=1) first");
+    CU(gf::launch_import_staged(s), "assignments_imported");
     s->stale_theta = s->stale_phi = true;
     return GF_OK;
 }

@@ -46,6 +46,7 @@ struct ShardDev {
     int4* k2items = nullptr;
     uint32_t* dw_ptr = nullptr;
     uint16_t* zdoc = nullptr;
+    uint16_t* zstage = nullptr;              // async imports land here (allocated on first use)
     uint32_t* run_dwpos = nullptr;
     uint4* run_rec = nullptr;                // per run {doc, first token, zdoc position, theta row offset} (K1)
     uint32_t* theta_ent = nullptr;
@@ -169,6 +170,7 @@ cudaError_t launch_prepare(gf_shard* s);
 cudaError_t launch_contexts(gf_shard* s);
 cudaError_t launch_theta_rebuild(gf_shard* s, cudaStream_t st = nullptr);
 cudaError_t launch_zdoc_sync(gf_shard* s);
+cudaError_t launch_import_staged(gf_shard* s);
 cudaError_t launch_ll_reduce(gf_shard* s);
 cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt);
 cudaError_t launch_theta_import(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids,

@@ -353,6 +353,37 @@ __global__ void zdoc_sync_kernel(long long R, const uint32_t* __restrict__ run_s
     }
 }
 
+// Staged import (gf_shard_copy_assignments_async to the device + _imported):
+// per run, compare the staged topics with the resident ones and write z and
+// its doc-major copy only for runs that changed.  A full scatter of zdoc is a
+// random 2-byte permutation of T tokens (26 ms on PubMed-shape, DRAM
+// read-modify-write of every sector); a round trip that hands the sampler's
+// own output back costs only the coalesced compare.
+__global__ void import_staged_kernel(long long R, const uint32_t* __restrict__ run_start,
+                                     const uint32_t* __restrict__ dwpos, const uint16_t* __restrict__ zin,
+                                     uint16_t* z, uint16_t* zdoc) {
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (long long)gridDim.x * blockDim.x) {
+        const uint32_t t0 = run_start[r], t1 = run_start[r + 1];
+        bool diff = false;
+        for (uint32_t t = t0; t < t1; ++t) diff |= zin[t] != z[t];
+        if (diff) {
+            const uint32_t p = dwpos[r];
+            for (uint32_t t = t0; t < t1; ++t) {
+                const uint16_t k = zin[t];
+                z[t] = k;
+                zdoc[p + (t - t0)] = k;
+            }
+        }
+    }
+}
+
+cudaError_t launch_import_staged(gf_shard* s) {
+    if (s->R == 0) return cudaSuccess;
+    import_staged_kernel<<<148 * 8, 256, 0, s->stream>>>((long long)s->R, s->d.run_start, s->d.run_dwpos, s->d.zstage,
+                                                         s->d.z, s->d.zdoc);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_zdoc_sync(gf_shard* s) {
     if (s->R == 0) return cudaSuccess;
     zdoc_sync_kernel<<<148 * 8, 256, 0, s->stream>>>((long long)s->R, s->d.run_start, s->d.run_dwpos, s->d.z,

@@ -649,6 +649,46 @@ def test_large_k_streaming_path(K):
     np.testing.assert_array_equal(gcn, c2)
 
 
+def test_staged_import_applies_exactly_the_changed_runs():
+    """Async imports are staged and applied per run where the topics differ:
+    an unchanged round trip, then a sparse edit (every 7th token, plus the
+    first and last token), each followed by the counts, must leave z, the
+    doc-major copy (checked through K3) and phi equal to the oracle's."""
+    import torch
+
+    K = 64
+    corp = synth.generate(400, 800, 60.0, seed=19)
+    ch = cp.partition(corp, 1, K, 4)[0]
+    T = corp.num_tokens
+    host = torch.empty(T, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
+    with DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=2, stream=torch.cuda.current_stream()) as sh:
+        sh.load(ch)
+        sh.initialize()
+        sh.sample(0)
+        for edit in (False, True):
+            sh.copy_assignments_async(host, 0, T, False)
+            torch.cuda.synchronize()
+            if edit:
+                idx = np.r_[0, np.arange(3, T, 7), T - 1]
+                host[idx] = ((host[idx].astype(np.int64) + 5) % K).astype(np.uint16)
+            want = host.copy()
+            sh.copy_assignments_async(host, 0, T, True)
+            sh.assignments_imported()
+            sh.rebuild_phi()
+            sh.prepare()
+            sh.rebuild_theta()
+            sh.check_errors()
+            np.testing.assert_array_equal(sh.get_assignments(), want)
+            rp, ids, cn = oracle.rebuild_theta(want, ch.dw_ptr, ch.dw_tok, 0, K)
+            grp, gids, gcn = sh.get_theta()
+            np.testing.assert_array_equal(gids, ids)
+            np.testing.assert_array_equal(gcn, cn)
+            phi, tot = oracle.rebuild_phi(want, ch.word_ids, K, corp.vocab_size)
+            np.testing.assert_array_equal(sh.get_phi()[0], phi)
+            sh.sample(1)                     # the sampler sees the imported state
+            sh.check_errors()
+
+
 def test_async_chunked_assignment_copies():
     """copy_assignments_async (chunks, copy streams) + assignments_imported: the
     e2e path of bench.py -- what comes back is what the device holds, and an
