@@ -2,11 +2,12 @@ import time, sys, torch, numpy as np
 sys.path.insert(0, ".")
 from paper_1803_04631_b200 import synth, corpus as cp
 from paper_1803_04631_b200.shard import DeviceShard
-corp = synth.shaped("nytimes", seed=20261017)
+import os
+corp = synth.shaped(os.environ.get("WL", "nytimes"), seed=20261017)
 K = 1024
 st = torch.cuda.current_stream()
 z = None
-for P in (1, 4, 8):
+for P in (1, 16):
     sh = DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=42, stream=st, phases=P)
     sh.load_tokens(0, corp.num_docs, corp.doc_ids, corp.word_ids, seed=20261017, chunk_id=0)
     if z is None:
