@@ -105,6 +105,59 @@ def _rank_main(rank, world, port, out):
     dist.destroy_process_group()
 
 
+def _rank_exchange_only(rank, world, port, out):
+    """Raw exchange at world 3: slabs of unequal length (n not divisible by 3 or 4)."""
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1803_04631_b200.corpus import greedy_boundaries, make_chunk
+    from paper_1803_04631_b200.shard import DeviceShard
+
+    corp = synth_corpus = _corpus()
+    K, V = 61, synth_corpus.vocab_size                   # odd K: packed u16 columns have a pad cell
+    lo, hi = greedy_boundaries(corp.doc_lengths, world)[rank]
+    a, b = int(corp.doc_ptr[lo]), int(corp.doc_ptr[hi])
+    chunk = make_chunk(rank, lo, hi, corp.doc_ids[a:b], corp.word_ids[a:b], V, K, 7)
+    freq = torch.as_tensor(np.bincount(chunk.word_ids, minlength=V).astype(np.int64))
+    dist.all_reduce(freq)
+    sh = DeviceShard(K, V, 50.0 / K, 0.01, seed=5, device=0, heavy_threshold=60, global_word_freq=freq.numpy())
+    sh.load(chunk)
+    sh.rebuild_phi()
+    sh.synchronize()
+    mine = sh.sync_tensor().cpu()
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    expect = torch.stack(parts).view(torch.int32).sum(0, dtype=torch.int64).to(torch.int32)
+    handles = [None] * world
+    dist.all_gather_object(handles, sh.peer_handle())
+    sh.peer_open(rank, world, handles)
+    sh.peer_allreduce()
+    sh.synchronize()
+    sh.check_errors()
+    ok = bool(torch.equal(sh.sync_tensor().cpu(), expect))
+    flags = [None] * world
+    dist.all_gather_object(flags, (ok, int(mine.numel())))
+    if rank == 0:
+        np.save(out, np.array([f[0] for f in flags] + [flags[0][1]], dtype=np.int64))
+    sh.peer_close()
+    sh.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_exchange_three_ranks():
+    import torch.multiprocessing as mp
+
+    out = os.path.join(tempfile.mkdtemp(), "peer3.npy")
+    mp.spawn(_rank_exchange_only, args=(3, _free_port(), out), nprocs=3, join=True)
+    r = np.load(out)
+    assert r[-1] % 3 != 0 or r[-1] % 4 != 0        # the slabs really are uneven / unaligned
+    assert r[:-1].tolist() == [1, 1, 1]
+
+
 @pytest.fixture(scope="module")
 def peer_result():
     import torch.multiprocessing as mp

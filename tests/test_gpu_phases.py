@@ -112,3 +112,22 @@ def test_phase_arguments_are_checked(chunk):
     with pytest.raises(ValueError, match="phases must be"):
         sh.set_phases(0)
     sh.close()
+
+
+def test_more_phases_than_word_groups():
+    """Phases beyond the number of word groups are empty (no launch) and the
+    phase sequence still equals one sample."""
+    corp = synth.generate(60, 40, 30.0, seed=3)
+    ch = cp.partition(corp, 1, K, 1)[0]
+    a, b = _shard(corp, ch, 1), _shard(corp, ch, 100)
+    assert b.num_phases == 100
+    ranges = [b.phase_range(p) for p in range(100)]
+    assert sum(1 for x, y in ranges if y > x) <= ch.num_groups
+    assert ranges[0][0] == 0 and ranges[-1][1] == ch.token_count
+    a.sample(0)
+    for p in range(100):
+        b.sample_phase(0, p)
+    assert a.loglik_sum() == pytest.approx(b.loglik_sum(), rel=1e-6)
+    assert np.mean(a.get_assignments() == b.get_assignments()) > 0.999
+    a.close()
+    b.close()
