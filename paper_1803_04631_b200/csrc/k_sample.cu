@@ -279,7 +279,10 @@ __device__ __forceinline__ void build_context(const SampleArgs& a, int col, floa
     float* pex = smem + lay_pex(K);
     float* lvl = smem + lay_tree(K);
     __shared__ float wtot[NW];
-    const int ipt = (K + NT - 1) / NT;
+    // ipt consecutive topics per thread, ipt odd: the 32 lanes of a warp then
+    // touch 32 distinct banks at every step i (an even ipt = 8 was an 8-way
+    // conflict on lvl / pex); the last threads may have fewer topics
+    const int ipt = ((K + NT - 1) / NT) | 1;
     const int k0 = tid * ipt;
     float acc = 0.f;
     for (int i = 0; i < ipt; ++i) {
