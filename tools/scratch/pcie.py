@@ -1,3 +1,5 @@
+"""PCIe microbenchmark (GPU box): pinned H2D, D2H, both directions at once and
+the chunked D2H->H2D round trip bench.py's e2e leg uses, for a 199 MB buffer."""
 import torch, time
 n = 199 * 1024 * 1024 // 2
 h1 = torch.empty(n, dtype=torch.int16).pin_memory(); h2 = torch.empty(n, dtype=torch.int16).pin_memory()

@@ -1,3 +1,5 @@
+"""K1 time under phase-major schedules (GPU box): one launch vs P sample_phase
+launches for P in (1, 16) on WL=nytimes|pubmed, from the state after 3 iterations."""
 import time, sys, torch, numpy as np
 sys.path.insert(0, ".")
 from paper_1803_04631_b200 import synth, corpus as cp
