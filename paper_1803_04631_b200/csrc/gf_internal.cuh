@@ -67,6 +67,7 @@ struct ShardDev {
 };
 
 constexpr int kMaxPeers = 8;                 // ranks of one NVLink/NVSwitch node
+constexpr int kLlSlots = 160;                // ll_sum: [0] sum, [1..148] chunk sums, [159] ticket
 
 // peer-memory phi exchange (k_peer.cu): every rank's sync buffer and signal
 // slots mapped into this process (own entries are the local pointers)

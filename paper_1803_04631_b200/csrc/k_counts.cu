@@ -392,21 +392,43 @@ cudaError_t launch_zdoc_sync(gf_shard* s) {
 }
 
 // ----------------------------------------------------------- ll reduce ------
-__global__ void ll_reduce_kernel(const double* __restrict__ part, long long n, double* out) {
+// Deterministic two-level sum: CTA c reduces the fixed chunk [c n/G, (c+1) n/G)
+// in a fixed order, the last CTA to finish (atomic ticket) adds the G chunk
+// sums in index order.  out[0] = sum; out[1..G] chunk sums; out[kLlSlots-1]
+// holds the ticket (reset by the last CTA).
+constexpr int kLlBlocks = 148;
+__global__ void __launch_bounds__(256) ll_reduce_kernel(const double* __restrict__ part, long long n, double* out) {
     __shared__ double sh[256];
+    __shared__ bool last;
+    const long long lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
     double s = 0.0;
-    for (long long i = threadIdx.x; i < n; i += 256) s += part[i];
+    for (long long i = lo + threadIdx.x; i < hi; i += 256) s += part[i];
     sh[threadIdx.x] = s;
     __syncthreads();
     for (int o = 128; o > 0; o >>= 1) {
         if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
         __syncthreads();
     }
-    if (threadIdx.x == 0) out[0] = sh[0];
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(out + kLlSlots - 1);
+    if (threadIdx.x == 0) {
+        out[1 + blockIdx.x] = sh[0];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double t = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(out + 1 + b);
+        out[0] = t;
+        *ticket = 0u;
+    }
 }
 
 cudaError_t launch_ll_reduce(gf_shard* s) {
-    ll_reduce_kernel<<<1, 256, 0, s->stream>>>(s->d.ll_part, s->n_slices, s->d.ll_sum);
+    const long long n = s->n_slices;
+    const int g = (int)std::max<long long>(1, std::min<long long>(kLlBlocks, (n + 2047) / 2048));
+    ll_reduce_kernel<<<g, 256, 0, s->stream>>>(s->d.ll_part, n, s->d.ll_sum);
     return cudaGetLastError();
 }
 

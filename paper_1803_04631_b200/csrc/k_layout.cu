@@ -440,7 +440,7 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
         (rc = shard_alloc(&dv.dw_ptr, D + 1, "dw_ptr")) || (rc = shard_alloc(&dv.zdoc, T, "zdoc")) ||
         (rc = shard_alloc(&dv.theta_ent, cap + 8, "theta")) || (rc = shard_alloc(&dv.theta_meta, D, "theta")) ||
         (rc = shard_alloc(&dv.sync, s->sync_u32, "phi")) || (rc = shard_alloc(&dv.inv_den, 2 * K, "inv_den")) ||
-        (rc = shard_alloc(&dv.ll_sum, 1, "ll")) || (rc = shard_alloc(&dv.errs, 4, "errs")) ||
+        (rc = shard_alloc(&dv.ll_sum, kLlSlots, "ll")) || (rc = shard_alloc(&dv.errs, 4, "errs")) ||
         (rc = shard_alloc(&dv.bytes, 1, "bytes")))
         return rc;
     if (T > 0) {
@@ -625,6 +625,7 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
     CK(cudaMemsetAsync(dv.theta_ent, 0, (cap + 8) * 4, st), "memset");
     CK(cudaMemsetAsync(dv.sync, 0, s->sync_u32 * 4, st), "memset");
     CK(cudaMemsetAsync(dv.errs, 0xff, 32, st), "memset");
+    CK(cudaMemsetAsync(dv.ll_sum, 0, kLlSlots * sizeof(double), st), "memset");
     CK(cudaMemsetAsync(dv.bytes, 0, 8, st), "memset");
     s->doc_lo = lo;
     s->doc_hi = hi;
