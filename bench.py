@@ -463,9 +463,16 @@ def run_ours(args, world, rank, local):
         # input) while phases p+1.. sample; only the last phase's round trip is
         # exposed.  Reload the same tokens with a phase-major schedule; the state
         # carries over through z (the counts are rebuilt from it every step).
-        nphase = int(os.environ.get("GF_E2E_PHASES", "16"))
+        spec = os.environ.get("GF_E2E_PHASES", "geo:9")
+        if spec.startswith("geo:"):       # halving phase sizes: 1/2, 1/4, ..., last two equal
+            n = int(spec[4:])
+            cuts = [1.0 - 0.5 ** (p + 1) for p in range(n - 1)] + [1.0]
+            nphase, phase_arg = n, cuts
+        else:
+            nphase = int(spec)
+            phase_arg = nphase
         if nphase > 1:
-            sh.set_phases(nphase)
+            sh.set_phases(phase_arg)
             sh.load_tokens(lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, seed=args.seed, chunk_id=rank)
             if peer:
                 handles = [None] * world
@@ -475,10 +482,12 @@ def run_ours(args, world, rank, local):
         nphase = sh.num_phases
         ranges = [sh.phase_range(p) for p in range(nphase)]
         nchunk = max(nphase, int(os.environ.get("GF_E2E_CHUNKS", "16")))
-        per = max(1, nchunk // nphase)
-        pieces = [[(int(x), int(y)) for x, y in zip(np.linspace(a0, b0, per + 1).astype(np.int64)[:-1],
-                                                     np.linspace(a0, b0, per + 1).astype(np.int64)[1:]) if y > x]
-                  for a0, b0 in ranges]
+        target = max(1, T_local // nchunk)          # pieces of ~T/nchunk tokens inside each phase
+        pieces = []
+        for a0, b0 in ranges:
+            per = max(1, int(round((b0 - a0) / target)))
+            cut = np.linspace(a0, b0, per + 1).astype(np.int64)
+            pieces.append([(int(x), int(y)) for x, y in zip(cut[:-1], cut[1:]) if y > x])
         d2h_s, h2d_s, alt = torch.cuda.Stream(device), torch.cuda.Stream(device), torch.cuda.Stream(device)
 
         def upload(host):

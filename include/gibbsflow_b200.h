@@ -148,6 +148,10 @@ int gf_shard_evaluate(gf_shard* shard);
  * gf_shard_sample_phase(p) for p = 0..P-1 in order is one gf_shard_sample
  * (same draws, same loglik; the loglik reduction runs after phase P-1). */
 int gf_shard_set_phases(gf_shard* shard, int num_phases);
+/* Uneven phases: phase p holds the word groups starting below cuts[p] * T
+ * (cumulative token fractions, strictly increasing, cuts[P-1] = 1.0), e.g.
+ * halving sizes so only a small last phase's copies stay exposed. */
+int gf_shard_set_phase_cuts(gf_shard* shard, const double* cuts, int num_phases);
 int gf_shard_num_phases(gf_shard* shard, int* num_phases_out);
 int gf_shard_phase_range(gf_shard* shard, int phase, int64_t* tok_begin, int64_t* tok_end);
 int gf_shard_sample_phase(gf_shard* shard, uint32_t iteration, int phase);

@@ -411,6 +411,17 @@ int gf_shard_sample(gf_shard* s, uint32_t iteration) {
 int gf_shard_set_phases(gf_shard* s, int num_phases) {
     if (num_phases < 1 || num_phases > 255) return fail(GF_ERR_VALUE, "phases must be in [1, 255]");
     s->n_phases = num_phases;     // applies at the next load (the slice schedule is built there)
+    s->phase_cuts.clear();
+    return GF_OK;
+}
+
+int gf_shard_set_phase_cuts(gf_shard* s, const double* cuts, int num_phases) {
+    if (num_phases < 1 || num_phases > 255) return fail(GF_ERR_VALUE, "phases must be in [1, 255]");
+    for (int p = 0; p < num_phases; ++p)
+        if (!(cuts[p] > (p ? cuts[p - 1] : 0.0)) || cuts[p] > 1.0 || (p == num_phases - 1 && cuts[p] != 1.0))
+            return fail(GF_ERR_VALUE, "phase cuts must increase strictly and end at 1.0");
+    s->n_phases = num_phases;
+    s->phase_cuts.assign(cuts, cuts + num_phases);
     return GF_OK;
 }
 

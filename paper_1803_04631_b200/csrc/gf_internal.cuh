@@ -104,6 +104,7 @@ struct gf_shard {
     // phase p owns the word groups whose tokens are z[phase_tok0[p], phase_tok0[p+1])
     // and the slices [phase_slice0[p], phase_slice0[p+1])
     int n_phases = 1;
+    std::vector<double> phase_cuts;          // optional cumulative token fractions (gf_shard_set_phase_cuts)
     std::vector<int64_t> phase_slice0{0, 0}, phase_tok0{0, 0};
     int64_t n_ctx = 0;
     bool ctx_dirty = true;                   // phi / n_k changed since the last prepare

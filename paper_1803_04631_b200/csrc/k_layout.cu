@@ -540,7 +540,12 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
     s->phase_tok0.assign((size_t)P + 1, T);
     s->phase_tok0[0] = 0;
     for (int64_t g = 0; g < ng; ++g) {
-        const int ph = T > 0 ? (int)std::min<int64_t>(P - 1, (int64_t)go[g] * P / T) : 0;
+        int ph = 0;
+        if (T > 0 && (int)s->phase_cuts.size() == P) {   // phase p ends at token cut[p] * T
+            while (ph < P - 1 && (double)go[g] >= s->phase_cuts[ph] * (double)T) ++ph;
+        } else if (T > 0) {
+            ph = (int)std::min<int64_t>(P - 1, (int64_t)go[g] * P / T);
+        }
         gphase[g] = (uint8_t)ph;
         s->phase_slice0[ph + 1] += gnsl[g];
     }

@@ -55,7 +55,7 @@ class DeviceShard:
         self.heavy_threshold = int(heavy_threshold)
         if stream is not None:
             self.set_stream(stream)
-        if phases != 1:
+        if np.ndim(phases) != 0 or phases != 1:
             self.set_phases(phases)
         if global_word_freq is not None:
             f = _lib.carr(global_word_freq, np.int64)
@@ -134,8 +134,14 @@ class DeviceShard:
 
     # ------------------------------------------ streamed sampling (phases) --
     def set_phases(self, num_phases):
-        """Split the slice schedule into word-group phases (applies at the next load)."""
-        _lib.check(_lib.lib().gf_shard_set_phases(self._h, int(num_phases)))
+        """Split the slice schedule into word-group phases (applies at the next load):
+        an int P gives ~T/P tokens each; a sequence gives cumulative token
+        fractions (strictly increasing, ending at 1.0)."""
+        if np.ndim(num_phases) == 0:
+            _lib.check(_lib.lib().gf_shard_set_phases(self._h, int(num_phases)))
+        else:
+            cuts = np.ascontiguousarray(num_phases, dtype=np.float64)
+            _lib.check(_lib.lib().gf_shard_set_phase_cuts(self._h, _lib.ptr(cuts), len(cuts)))
 
     @property
     def num_phases(self):

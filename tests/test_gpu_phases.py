@@ -131,3 +131,30 @@ def test_more_phases_than_word_groups():
     assert np.mean(a.get_assignments() == b.get_assignments()) > 0.999
     a.close()
     b.close()
+
+
+def test_uneven_phase_cuts():
+    """set_phases(sequence): phase p holds the groups starting below cuts[p] * T."""
+    corp = synth.generate(1200, 2500, 180.0, seed=41)
+    ch = cp.partition(corp, 1, K, 9)[0]
+    cuts = [0.5, 0.75, 0.875, 1.0]
+    sh = _shard(corp, ch, cuts)
+    assert sh.num_phases == 4
+    T = ch.token_count
+    starts = np.asarray(ch.group_offsets)
+    for p, c in enumerate(cuts):
+        lo, hi = sh.phase_range(p)
+        inside = starts[(starts >= lo) & (starts < hi)]
+        assert np.all(inside < c * T)                         # every group of phase p starts below its cut
+        if p + 1 < len(cuts) and hi < T:
+            assert hi >= c * T                               # and the next group starts at or above it
+    one = _shard(corp, ch, 1)
+    one.sample(0)
+    for p in range(4):
+        sh.sample_phase(0, p)
+    assert np.mean(one.get_assignments() == sh.get_assignments()) > 0.9999
+    for bad in ([0.5, 0.4, 1.0], [0.5, 0.9], [0.0, 1.0]):
+        with pytest.raises(ValueError, match="phase cuts"):
+            sh.set_phases(bad)
+    one.close()
+    sh.close()
