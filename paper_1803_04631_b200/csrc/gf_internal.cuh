@@ -61,7 +61,7 @@ struct ShardDev {
     unsigned long long* errs = nullptr;      // [0] consistency token (min), [1] theta overflow key (min),
                                              // [2] document with a topic >= K (K3, min),
                                              // [3] peer exchange block that timed out (min)
-    unsigned long long* bytes = nullptr;     // [0] sum over runs of nnz (sampler bytes model)
+    unsigned long long* bytes = nullptr;     // [0] sum over runs of nnz (sampler bytes model), [1] import flag
     uint32_t* scratch = nullptr;             // export staging
     size_t scratch_bytes = 0;
 };

@@ -359,9 +359,28 @@ __global__ void zdoc_sync_kernel(long long R, const uint32_t* __restrict__ run_s
 // random 2-byte permutation of T tokens (26 ms on PubMed-shape, DRAM
 // read-modify-write of every sector); a round trip that hands the sampler's
 // own output back costs only the coalesced compare.
-__global__ void import_staged_kernel(long long R, const uint32_t* __restrict__ run_start,
-                                     const uint32_t* __restrict__ dwpos, const uint16_t* __restrict__ zin,
-                                     uint16_t* z, uint16_t* zdoc) {
+// first a 16-byte compare of the whole staged array against z: when nothing
+// differs (a round trip of the sampler's own output) the per-run pass exits
+// at once instead of reading every run's bounds
+__global__ void staged_diff_kernel(long long T, const uint16_t* __restrict__ zin, const uint16_t* __restrict__ z,
+                                   unsigned int* any) {
+    const long long nv = T >> 3, stride = (long long)gridDim.x * blockDim.x;
+    bool d = false;
+    const uint4* a = reinterpret_cast<const uint4*>(zin);
+    const uint4* b = reinterpret_cast<const uint4*>(z);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const uint4 x = __ldcs(a + i), y = __ldg(b + i);
+        d |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+    }
+    for (long long t = nv * 8 + (long long)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += stride)
+        d |= zin[t] != z[t];
+    if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(any, 1u);
+}
+
+__global__ void import_staged_gate(long long R, const uint32_t* __restrict__ run_start,
+                                   const uint32_t* __restrict__ dwpos, const uint16_t* __restrict__ zin, uint16_t* z,
+                                   uint16_t* zdoc, const unsigned int* any) {
+    if (*any == 0u) return;                   // nothing changed
     for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (long long)gridDim.x * blockDim.x) {
         const uint32_t t0 = run_start[r], t1 = run_start[r + 1];
         bool diff = false;
@@ -379,8 +398,13 @@ __global__ void import_staged_kernel(long long R, const uint32_t* __restrict__ r
 
 cudaError_t launch_import_staged(gf_shard* s) {
     if (s->R == 0) return cudaSuccess;
-    import_staged_kernel<<<148 * 8, 256, 0, s->stream>>>((long long)s->R, s->d.run_start, s->d.run_dwpos, s->d.zstage,
-                                                         s->d.z, s->d.zdoc);
+    // bytes[1]: the "any staged topic differs" flag
+    unsigned int* any = reinterpret_cast<unsigned int*>(s->d.bytes + 1);
+    cudaError_t e = cudaMemsetAsync(any, 0, 4, s->stream);
+    if (e != cudaSuccess) return e;
+    staged_diff_kernel<<<148 * 8, 256, 0, s->stream>>>((long long)s->T, s->d.zstage, s->d.z, any);
+    import_staged_gate<<<148 * 8, 256, 0, s->stream>>>((long long)s->R, s->d.run_start, s->d.run_dwpos, s->d.zstage,
+                                                       s->d.z, s->d.zdoc, any);
     return cudaGetLastError();
 }
 

@@ -441,7 +441,7 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
         (rc = shard_alloc(&dv.theta_ent, cap + 8, "theta")) || (rc = shard_alloc(&dv.theta_meta, D, "theta")) ||
         (rc = shard_alloc(&dv.sync, s->sync_u32, "phi")) || (rc = shard_alloc(&dv.inv_den, 2 * K, "inv_den")) ||
         (rc = shard_alloc(&dv.ll_sum, kLlSlots, "ll")) || (rc = shard_alloc(&dv.errs, 4, "errs")) ||
-        (rc = shard_alloc(&dv.bytes, 1, "bytes")))
+        (rc = shard_alloc(&dv.bytes, 2, "bytes")))
         return rc;
     if (T > 0) {
         k_run_scatter<<<blocks_for(T), 256, 0, st>>>(c.doc, flag, rid, T, dv.run_start, dv.run_doc);
