@@ -8,7 +8,7 @@ o=gpurun_out
 python -c "import __graft_entry__ as g; g.smoke()" > $o/${tag}_smoke.log 2>&1; echo "smoke rc=$? $(tail -1 $o/${tag}_smoke.log)"
 timeout 1200 python -m pytest tests -m gpu -q > $o/${tag}_gputests.log 2>&1; echo "gpu tests: $(tail -1 $o/${tag}_gputests.log)"
 # bench lines: the default command, the other workloads, the K sweep, the reference arm
-timeout 900 python bench.py > $o/${tag}_bench_nyt.json 2> $o/${tag}_bench_nyt.err
+t0=$(date +%s); timeout 900 python bench.py > $o/${tag}_bench_nyt.json 2> $o/${tag}_bench_nyt.err; echo "default bench wall: $(( $(date +%s) - t0 )) s"
 timeout 900 python bench.py --workload pubmed > $o/${tag}_bench_pm.json 2> $o/${tag}_bench_pm.err
 timeout 900 python bench.py --workload z4shard --no-cpu-baseline > $o/${tag}_bench_z4.json 2> $o/${tag}_bench_z4.err
 for k in 128 256 4096; do
