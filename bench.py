@@ -337,7 +337,14 @@ def run_ours(args, world, rank, local):
     sh = DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=42, device=device, global_word_freq=freq,
                      stream=stream)
     # K4: partition (stable word sort, dw-map, splitmix64 z0) + shard layout on
-    # the device, from the doc-major tokens of this rank's documents
+    # the device, from the doc-major tokens of this rank's documents.  A small
+    # warm-up load first, so one-time CUDA costs (lazy module loading, first
+    # allocations) stay out of the preprocessing throughput
+    nw = min(corp.num_docs, 2000)
+    tw = int(np.searchsorted(corp.doc_ids, nw))
+    with DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=42, device=device, global_word_freq=freq,
+                     stream=stream) as warm:
+        warm.load_tokens(lo, lo + nw, corp.doc_ids[:tw] + lo, corp.word_ids[:tw], seed=args.seed, chunk_id=rank)
     torch.cuda.synchronize(device)
     t0 = time.perf_counter()
     sh.load_tokens(lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, seed=args.seed, chunk_id=rank)
