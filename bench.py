@@ -589,6 +589,7 @@ def run_ours(args, world, rank, local):
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic["bytes_per_launch"] if traffic else None,
+                         "frac_of_nominal_8tbs": achieved / 8000.0,
                          "kernel": "gf::sample_kernel (K1)", "algorithmic_bytes_per_launch": st["sample_bytes"],
                          "kernel_ms": k1_ms, "peak_source": peak_src},
             "kernel_ms": {"sample": acc[0] / args.steps, "phi_rebuild": acc[1] / args.steps,
