@@ -364,7 +364,6 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     const int4 sl = a.slices[blockIdx.x];
     const uint32_t v = (uint32_t)sl.x;
     const int col = sl.w;
-    const unsigned lane_le = (2u << lane) - 1u;     // lanes 0..lane
 
     // ---------------- prologue: the word context (p*, p*_ex, Q-tree) ----------------
     if (tid == 0) next_run = sl.y;
@@ -526,7 +525,7 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
                 for (uint32_t base = __shfl_sync(kFull, t0, first); base < tend; base += 32u) {
                     const uint32_t th = (sel && t0 - base < 32u) ? (1u << (t0 - base)) : 0u;
                     const unsigned M = __reduce_or_sync(kFull, th);
-                    const int own = min(cown + __popc(M & lane_le), 31);
+                    const int own = min(cown + __popc(M & lanemask_le()), 31);
                     const uint32_t ot0 = __shfl_sync(kFull, t0, own);
                     const uint32_t odoc = __shfl_sync(kFull, gdoc, own);
                     const uint32_t ooff = __shfl_sync(kFull, off, own);
