@@ -1,19 +1,31 @@
 """Benchmark: sampled tokens/s of the B200 CuLDA_CGS hot path (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload nytimes|pubmed|z4shard|tiny] [--topics 1024]
+                    [--workload pubmed|nytimes|z4shard|tiny] [--topics 1024]
+                    [--scaling strong|weak] [--shard r/N]
 
-A step is one full deferred training iteration over the shard (K1 sample +
-fused loglik, K2 phi rebuild, [NCCL allreduce of the phi sync buffer], K3
-theta rebuild, prepare) with every input resident in HBM.  N=1 runs the
-NYTimes-shaped configuration (BASELINE.json configs[1]: 299,752 docs,
-V=101,636, ~99.5M tokens, K=1024).  Under torchrun each rank owns one
-NYTimes-shaped document shard of an N-times larger corpus over the same
-vocabulary ("weak" scaling) and the replicas are summed with NCCL.
+A step is one full deferred training iteration (K1 sample + fused loglik, K2
+phi rebuild, [phi allreduce], K3 theta rebuild, prepare) with every input
+resident in HBM.  The default workload is the north star's headline: the
+PubMed-shaped corpus (BASELINE.json configs[2]: 8.2M docs, V=141,043,
+~738M tokens) at K=1024.  Under torchrun the SAME corpus is split over the N
+ranks ("strong" scaling): rank r owns documents greedy_boundaries(doc
+lengths, N)[r] (corpus.py:210-237, C = G) and generates only those, and the
+phi replicas are summed with NCCL every iteration.  `--scaling weak` gives
+every rank its own full-size corpus instead (z4shard is always weak: it is
+one GPU's share of BASELINE configs[4]).
 
---impl reference times the CPU implementation of the same path on the host
-cores (the reference package has no sampler, so this is the oracle port in
-oracle/: OpenMP C, all threads) on a bounded document sample.
+`--shard r/N` runs ONE rank's shard of an N-way split on one GPU (full
+vocabulary, no collective): the per-rank step time of the N-GPU run, minus the
+allreduce, measured on a single GPU.
+
+`--impl reference` times the CPU implementation of the same path on the host
+cores.  The reference package has no sampler, so each step is one deferred
+iteration of the oracle port (oracle/: the SPEC sampler + rebuild_theta +
+rebuild_phi, OpenMP C, all threads) over a bounded document sample of the
+same corpus, which it generates with oracle/gf_synth_ref.c (identical to the
+product generator, no product library) and partitions with the reference
+package's own `partition` (baseline/_ref) when it is installed.
 """
 
 import argparse
@@ -32,6 +44,18 @@ sys.path.insert(0, ROOT)
 METRIC = "sampled tokens/sec"
 UNIT = "tokens/s"
 
+# BASELINE.json config shapes: docs, vocabulary, mean length
+SHAPES = {
+    "tiny": dict(num_docs=1_000, vocab_size=1_000, mean_len=100.0),
+    "nytimes": dict(num_docs=299_752, vocab_size=101_636, mean_len=332.08),
+    "pubmed": dict(num_docs=8_200_000, vocab_size=141_043, mean_len=89.98),
+    "z4shard": dict(num_docs=5_000_000, vocab_size=1_000_000, mean_len=100.0),
+}
+CORPUS_SEED = 20261017
+TRAIN_SEED = 42
+# documents in the bounded CPU sample (about 9M tokens PubMed-shape, 6.6M NYTimes-shape)
+CPU_SAMPLE_DOCS = {"tiny": 1_000, "nytimes": 20_000, "pubmed": 100_000, "z4shard": 100_000}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -39,16 +63,22 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="nytimes", choices=["nytimes", "pubmed", "tiny", "z4shard"])
+    ap.add_argument("--workload", default="pubmed", choices=sorted(SHAPES))
     ap.add_argument("--topics", type=int, default=None)
-    ap.add_argument("--seed", type=int, default=20261017)
+    ap.add_argument("--seed", type=int, default=CORPUS_SEED)
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
+                    help="N>1: split one corpus over the ranks (strong, default) or one corpus per rank (weak)")
+    ap.add_argument("--shard", default=None, help="r/N: run rank r's shard of an N-way split on one GPU")
     ap.add_argument("--cpu-sample-docs", type=int, default=0, help="docs in the bounded CPU sample (0: auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--phi-sync", default="nccl", choices=["nccl", "peer"],
                     help="N>1: phi sum by all_reduce, or by the IPC peer-memory exchange kernel")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.scaling is None:
+        a.scaling = "weak" if a.workload == "z4shard" else "strong"
+    return a
 
 
 def dist_env():
@@ -58,20 +88,39 @@ def dist_env():
     return world, rank, local
 
 
-def workload(name, topics):
-    from paper_1803_04631_b200 import synth
-
-    shape = dict(synth.SHAPES[name])
-    K = topics or (32 if name == "tiny" else 1024)
-    return shape, K
+def topics_of(args):
+    return args.topics or (32 if args.workload == "tiny" else 1024)
 
 
-def make_shard_corpus(shape, rank, seed):
-    """This rank's document shard: docs [rank*D, (rank+1)*D) of the global corpus."""
-    from paper_1803_04631_b200 import synth
+def split_of(args, world, rank):
+    """(parts, part): which greedy_boundaries split this process runs."""
+    if args.shard:
+        r, n = (int(x) for x in args.shard.split("/"))
+        if not 0 <= r < n:
+            raise SystemExit(f"--shard {args.shard}: need 0 <= r < N")
+        return n, r
+    if args.scaling == "strong":
+        return world, rank
+    return 1, 0
 
-    D = shape["num_docs"]
-    return synth.generate(D, shape["vocab_size"], shape["mean_len"], seed=seed, doc_begin=rank * D)
+
+def make_config(args, world, tokens_total):
+    """The `config` object: identical for both arms of the same command."""
+    shape = SHAPES[args.workload]
+    parts, part = split_of(args, world, 0)
+    docs_total = shape["num_docs"] * (world if args.scaling == "weak" and not args.shard else 1)
+    c = {
+        "workload": f"{args.workload}-shaped synthetic LDA corpus, K={topics_of(args)}",
+        "docs_total": docs_total, "vocab": shape["vocab_size"], "tokens_total": int(tokens_total),
+        "topics": topics_of(args), "alpha": 50.0 / topics_of(args), "beta": 0.01,
+        "iterations": [args.warmup, args.warmup + args.steps],
+        "scaling": "shard-proxy" if args.shard else args.scaling,
+        "parallelism": (f"rank {args.shard} of a doc-sharded dp{parts} (one GPU, no collective)" if args.shard else
+                        (f"doc-shard dp{world} (greedy_boundaries) + phi allreduce" if world > 1 else "dp1")),
+        "l2": "inputs larger than L2 (z 2T B, theta 4*NNZ B, phi >= 200 MB vs 126 MB L2)",
+        "corpus_seed": args.seed, "train_seed": TRAIN_SEED,
+    }
+    return c
 
 
 # ------------------------------------------------------------------ clocks --
@@ -153,8 +202,10 @@ def measured_peak():
 
 
 def ncu_traffic(workload, K):
-    """dram read+write bytes per K1 launch from the committed ncu --set full
-    capture of the same workload and K (None when there is none)."""
+    """DRAM read+write bytes per K1 launch from the committed `ncu --set full`
+    capture of the same workload and K (None when there is none).  ncu cannot
+    run inside the timed region, so this is a labelled lookup: the entry names
+    its capture file and the iteration it profiled."""
     p = os.path.join(ROOT, "profiles", "sample_kernel_traffic.json")
     try:
         with open(p) as fh:
@@ -164,66 +215,92 @@ def ncu_traffic(workload, K):
 
 
 # -------------------------------------------------------------- CPU side --
-def cpu_iteration(sub, K, seed, iteration, threads):
-    """One deferred iteration of the oracle port on a document sample: sample
-    (SPEC sampler, OpenMP) + theta rebuild + phi rebuild.  Returns seconds."""
+def cpu_sample_state(args, K, ndocs):
+    """The first `ndocs` documents of the benchmark corpus, generated by the
+    oracle's generator (no product library) and partitioned by the reference
+    package's own partition() when it is installed (baseline/_ref), else by
+    the oracle's restatement of it; the initial counts by the oracle."""
     import oracle
 
-    ch, rp, ids, cn, phi, tot = sub
+    shape = SHAPES[args.workload]
+    corp = oracle.synth_generate(ndocs, shape["vocab_size"], shape["mean_len"], seed=args.seed)
+    part_by = "oracle.partition (restatement of corpus.py:240-287)"
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    chunk = None
+    if os.path.isdir(os.path.join(ref, "gibbsflow")):
+        try:
+            import tempfile
+
+            os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="gf_numba_"))
+            sys.path.insert(0, ref)
+            try:
+                from gibbsflow import corpus as rc
+            finally:
+                sys.path.remove(ref)
+            rcorp = rc.corpus_from_tokens(corp["doc_ids"], corp["word_ids"], corp["V"])
+            c = rc.partition(rcorp, 1, K, TRAIN_SEED)[0]
+            chunk = dict(doc_ids=c.doc_ids, word_ids=c.word_ids, assignments=c.assignments, dw_ptr=c.dw_ptr,
+                         dw_tok=c.dw_tok)
+            part_by = "gibbsflow.corpus.partition (the reference package, baseline/_ref)"
+        except Exception as e:                                # noqa: BLE001 -- fall back to the restatement
+            part_by = f"oracle.partition (reference package failed: {type(e).__name__})"
+            chunk = None
+    if chunk is None:
+        chunk = oracle.partition(corp, 1, K, TRAIN_SEED)[0]
+    z = np.ascontiguousarray(chunk["assignments"], dtype=np.uint16).copy()
+    st = {"V": corp["V"], "T": corp["T"], "doc_ids": np.ascontiguousarray(chunk["doc_ids"], np.int32),
+          "word_ids": np.ascontiguousarray(chunk["word_ids"], np.int32), "z": z,
+          "dw_ptr": np.ascontiguousarray(chunk["dw_ptr"], np.int64),
+          "dw_tok": np.ascontiguousarray(chunk["dw_tok"], np.int64), "partitioned_by": part_by}
+    st["theta"] = oracle.rebuild_theta(z, st["dw_ptr"], st["dw_tok"], 0, K)
+    phi, tot = oracle.rebuild_phi(z, st["word_ids"], K, st["V"])
+    st["phi"] = (phi.astype(np.uint32), tot)
+    return st
+
+
+def cpu_iteration(st, K, iteration, threads):
+    """One deferred iteration of the oracle port on the sample: sample (SPEC
+    sampler, OpenMP) + theta rebuild + phi rebuild.  Returns seconds."""
+    import oracle
+
     a, b = 50.0 / K, 0.01
+    rp, ids, cn = st["theta"]
+    phi, tot = st["phi"]
     t0 = time.perf_counter()
-    z = oracle.sample_tokens(K, ch.vocab, a, b, seed, iteration, ch.doc_ids, ch.word_ids, ch.z, 0, rp, ids, cn,
-                             phi, tot, nthreads=threads)
-    rp2, ids2, cn2 = oracle.rebuild_theta(z, ch.dw_ptr, ch.dw_tok, 0, K)
-    phi2, tot2 = oracle.rebuild_phi(z, ch.word_ids, K, ch.vocab)
+    z = oracle.sample_tokens(K, st["V"], a, b, TRAIN_SEED, iteration, st["doc_ids"], st["word_ids"], st["z"], 0,
+                             rp, ids, cn, phi, tot, nthreads=threads)
+    theta = oracle.rebuild_theta(z, st["dw_ptr"], st["dw_tok"], 0, K)
+    phi2, tot2 = oracle.rebuild_phi(z, st["word_ids"], K, st["V"])
     dt = time.perf_counter() - t0
-    ch.z = z
-    return dt, (ch, rp2, ids2, cn2, phi2.astype(np.uint32), tot2)
+    st["z"], st["theta"], st["phi"] = z, theta, (phi2.astype(np.uint32), tot2)
+    return dt
 
 
-class _SubChunk:
-    pass
+def cpu_sample_text(args, st, ndocs, threads):
+    shape = SHAPES[args.workload]
+    return (f"the first {ndocs} of the {shape['num_docs']} documents ({st['T']} tokens) of the same corpus, "
+            f"K={topics_of(args)}; step = one deferred iteration (SPEC sampler + rebuild_theta + rebuild_phi) of "
+            f"the oracle port (oracle/gf_oracle.c, OpenMP C, {threads} threads; the reference package has no "
+            f"sampler); chunk from {st['partitioned_by']}")
 
 
-def cpu_sample_state(shape, K, seed, ndocs):
-    import oracle
-    from paper_1803_04631_b200 import corpus as cp
-    from paper_1803_04631_b200 import synth
-
-    corp = synth.generate(ndocs, shape["vocab_size"], shape["mean_len"], seed=seed)
-    chunk = cp.partition(corp, 1, K, seed)[0]
-    ch = _SubChunk()
-    ch.vocab = corp.vocab_size
-    ch.doc_ids, ch.word_ids, ch.z = chunk.doc_ids, chunk.word_ids, chunk.assignments.copy()
-    ch.dw_ptr, ch.dw_tok = chunk.dw_ptr, chunk.dw_tok
-    ch.T = corp.num_tokens
-    rp, ids, cn = oracle.rebuild_theta(ch.z, ch.dw_ptr, ch.dw_tok, 0, K)
-    phi, tot = oracle.rebuild_phi(ch.z, ch.word_ids, K, ch.vocab)
-    return ch, rp, ids, cn, phi.astype(np.uint32), tot
-
-
-def cpu_baseline(shape, K, seed, ndocs, iters=2):
+def cpu_baseline(args, K, ndocs, iters=2):
     threads = os.cpu_count() or 1
-    sub = cpu_sample_state(shape, K, seed, ndocs)
-    T = sub[0].T
-    times = []
-    for it in range(iters):
-        dt, sub = cpu_iteration(sub, K, seed, it, threads)
-        times.append(dt)
-    return {"value": T / float(np.mean(times)), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{ndocs} docs ({T} tokens) of the same {shape['num_docs']}-doc shape, K={K}; "
-                      f"mean of {iters} full deferred iterations (oracle sampler + theta + phi rebuild, "
-                      f"OpenMP C, {threads} threads)"}
+    st = cpu_sample_state(args, K, ndocs)
+    times = [cpu_iteration(st, K, it, threads) for it in range(iters)]
+    return {"value": st["T"] / float(np.mean(times)), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": cpu_sample_text(args, st, ndocs, threads) + f"; mean of {iters} iterations"}
 
 
-def reference_components(shape, K, seed, ndocs):
+def reference_components(args, K, ndocs):
     """Time the UNMODIFIED reference package (baseline/_ref/gibbsflow, installed
-    offline from /root/reference/pkg) on the same document sample: its own
+    offline from /root/reference/pkg) on a document sample: its own
     partition (corpus.py:240-287), rebuild_theta (model.py:109-124) and
     rebuild_phi_replica (model.py:142-161), single-threaded numpy/numba as
-    shipped -- the CPU counterparts of K4, K3 and K2.  None when
-    the package is not installed."""
+    shipped -- the CPU counterparts of K4, K3 and K2."""
     import tempfile
+
+    import oracle
 
     ref = os.path.join(ROOT, "baseline", "_ref")
     if not os.path.isdir(os.path.join(ref, "gibbsflow")):
@@ -235,64 +312,118 @@ def reference_components(shape, K, seed, ndocs):
         from gibbsflow import model as rm
     finally:
         sys.path.remove(ref)
-    from paper_1803_04631_b200 import synth
-
-    corp = synth.generate(ndocs, shape["vocab_size"], shape["mean_len"], seed=seed)
-    rcorp = rc.corpus_from_tokens(corp.doc_ids, corp.word_ids, corp.vocab_size)
+    shape = SHAPES[args.workload]
+    corp = oracle.synth_generate(ndocs, shape["vocab_size"], shape["mean_len"], seed=args.seed)
+    rcorp = rc.corpus_from_tokens(corp["doc_ids"], corp["word_ids"], corp["V"])
     T = int(rcorp.num_tokens)
-    rc.partition(rcorp, 1, K, seed)                      # numba JIT outside the timing
+    rc.partition(rcorp, 1, K, TRAIN_SEED)                      # numba JIT outside the timing
     out = {"sample": f"{ndocs} docs ({T} tokens), K={K}, reference package as installed (single thread)"}
     t0 = time.perf_counter()
-    chunk = rc.partition(rcorp, 1, K, seed)[0]
+    chunk = rc.partition(rcorp, 1, K, TRAIN_SEED)[0]
     out["partition_tokens_per_s"] = T / (time.perf_counter() - t0)
     t0 = time.perf_counter()
     rm.rebuild_theta(chunk, K)
     out["rebuild_theta_tokens_per_s"] = T / (time.perf_counter() - t0)
     t0 = time.perf_counter()
-    rm.rebuild_phi_replica(chunk, K, corp.vocab_size)
+    rm.rebuild_phi_replica(chunk, K, corp["V"])
     out["rebuild_phi_tokens_per_s"] = T / (time.perf_counter() - t0)
     return out
+
+
+def corpus_tokens_total(args, world):
+    """Tokens one step processes over the whole job, from the document lengths
+    alone (the oracle's generator: the reference arm loads no product code)."""
+    import oracle
+
+    shape = SHAPES[args.workload]
+    D = shape["num_docs"]
+    if args.shard:
+        parts, part = split_of(args, world, 0)
+        L = oracle.synth_lengths(args.seed, D, shape["mean_len"])
+        lo, hi = oracle.greedy_boundaries(L, parts)[part]
+        return int(L[lo:hi].sum())
+    if args.scaling == "weak" and world > 1:
+        return sum(int(oracle.synth_lengths(args.seed, D, shape["mean_len"], doc_begin=r * D).sum())
+                   for r in range(world))
+    return int(oracle.synth_lengths(args.seed, D, shape["mean_len"]).sum())
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    shape, K = workload(args.workload, args.topics)
-    ndocs = args.cpu_sample_docs or (shape["num_docs"] if args.workload == "tiny" else 20000)
+    K = topics_of(args)
+    ndocs = args.cpu_sample_docs or min(CPU_SAMPLE_DOCS[args.workload], SHAPES[args.workload]["num_docs"])
     threads = os.cpu_count() or 1
-    sub = cpu_sample_state(shape, K, args.seed, ndocs)
-    T = sub[0].T
+    st = cpu_sample_state(args, K, ndocs)
     it = 0
     for _ in range(args.warmup):
-        _, sub = cpu_iteration(sub, K, args.seed, it, threads)
+        cpu_iteration(st, K, it, threads)
         it += 1
     times = []
     for _ in range(args.steps):
-        dt, sub = cpu_iteration(sub, K, args.seed, it, threads)
-        times.append(dt)
+        times.append(cpu_iteration(st, K, it, threads))
         it += 1
-    v = T / float(np.mean(times))
+    v = st["T"] / float(np.mean(times))
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
+        "scaling": "shard-proxy" if args.shard else args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}-shaped synthetic LDA corpus (bounded CPU sample)",
-                   "docs": ndocs, "tokens": T, "topics": K, "vocab": shape["vocab_size"]},
+        "config": make_config(args, world, corpus_tokens_total(args, world)),
         "impl": "reference",
+        "sample": {"docs": ndocs, "tokens": st["T"]},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{ndocs} docs ({T} tokens); the reference package has no sampler, so the "
-                                   f"oracle port (oracle/gf_oracle.c) runs the SPEC algorithm"},
+                         "sample": cpu_sample_text(args, st, ndocs, threads)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "reference_components": reference_components(shape, K, args.seed, min(ndocs, 5000)),
+        "reference_components": reference_components(args, K, min(ndocs, 5000)),
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ ours ----
+def rank_corpus(args, world, rank):
+    """(corpus of this rank's documents with doc ids relative to lo, lo, T of the
+    whole run): strong scaling and --shard split the global corpus with
+    greedy_boundaries; weak scaling gives each rank its own full-size corpus."""
+    from paper_1803_04631_b200 import corpus as cp
+    from paper_1803_04631_b200 import synth
+
+    shape = SHAPES[args.workload]
+    D = shape["num_docs"]
+    parts, part = split_of(args, world, rank)
+    if parts == 1:
+        lo = rank * D if (args.scaling == "weak" and world > 1) else 0
+        corp = synth.generate(D, shape["vocab_size"], shape["mean_len"], seed=args.seed, doc_begin=lo)
+        return corp, lo
+    L = synth.doc_lengths(args.seed, D, shape["mean_len"])
+    lo, hi = cp.greedy_boundaries(L, parts)[part]
+    corp = synth.generate(hi - lo, shape["vocab_size"], shape["mean_len"], seed=args.seed, doc_begin=lo)
+    return corp, lo
+
+
+def global_word_freq(args, world):
+    """Word frequencies of the whole corpus for --shard (the N-GPU run allreduces
+    the ranks' counts; one GPU recounts the corpus in pieces)."""
+    from paper_1803_04631_b200 import synth
+
+    shape = SHAPES[args.workload]
+    freq = np.zeros(shape["vocab_size"], np.int64)
+    step = 1_000_000
+    for b in range(0, shape["num_docs"], step):
+        c = synth.generate(min(step, shape["num_docs"] - b), shape["vocab_size"], shape["mean_len"], seed=args.seed,
+                           doc_begin=b)
+        freq += np.bincount(c.word_ids, minlength=shape["vocab_size"])
+    return freq
+
+
+def kernel_block(name, ms, nbytes, peak):
+    gbs = nbytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    return {"kernel": name, "ms": ms, "algorithmic_bytes": int(nbytes), "achieved_gbs": gbs, "frac": gbs / peak}
+
+
 def run_ours(args, world, rank, local):
     import torch
 
-    from paper_1803_04631_b200 import corpus as cp
     from paper_1803_04631_b200.shard import DeviceShard
 
     dist = None
@@ -320,12 +451,14 @@ def run_ours(args, world, rank, local):
             t.copy_(c)
             return None
         return dist.all_reduce(t, op=op, async_op=async_op)
-    shape, K = workload(args.workload, args.topics)
-    corp = make_shard_corpus(shape, rank, args.seed)
-    lo = rank * shape["num_docs"]
+
+    K = topics_of(args)
+    corp, lo = rank_corpus(args, world, rank)
     freq = np.bincount(corp.word_ids, minlength=corp.vocab_size).astype(np.int64)
     T_local = corp.num_tokens
     T_all = T_local
+    if args.shard:
+        freq = global_word_freq(args, world)
     if dist:
         t = torch.as_tensor(freq).cuda()
         ar(t)
@@ -334,20 +467,21 @@ def run_ours(args, world, rank, local):
         ar(tt)
         T_all = int(tt.item())
     stream = torch.cuda.current_stream(device)
-    sh = DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=42, device=device, global_word_freq=freq,
+    sh = DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=TRAIN_SEED, device=device, global_word_freq=freq,
                      stream=stream)
+    chunk_id = int(args.shard.split("/")[0]) if args.shard else rank
     # K4: partition (stable word sort, dw-map, splitmix64 z0) + shard layout on
     # the device, from the doc-major tokens of this rank's documents.  A small
     # warm-up load first, so one-time CUDA costs (lazy module loading, first
     # allocations) stay out of the preprocessing throughput
     nw = min(corp.num_docs, 2000)
     tw = int(np.searchsorted(corp.doc_ids, nw))
-    with DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=42, device=device, global_word_freq=freq,
+    with DeviceShard(K, corp.vocab_size, 50.0 / K, 0.01, seed=TRAIN_SEED, device=device, global_word_freq=freq,
                      stream=stream) as warm:
-        warm.load_tokens(lo, lo + nw, corp.doc_ids[:tw] + lo, corp.word_ids[:tw], seed=args.seed, chunk_id=rank)
+        warm.load_tokens(lo, lo + nw, corp.doc_ids[:tw] + lo, corp.word_ids[:tw], seed=TRAIN_SEED, chunk_id=chunk_id)
     torch.cuda.synchronize(device)
     t0 = time.perf_counter()
-    sh.load_tokens(lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, seed=args.seed, chunk_id=rank)
+    sh.load_tokens(lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, seed=TRAIN_SEED, chunk_id=chunk_id)
     torch.cuda.synchronize(device)
     prep_s = time.perf_counter() - t0
     sync_t = sh.sync_tensor() if dist else None
@@ -372,7 +506,9 @@ def run_ours(args, world, rank, local):
     sh.rebuild_theta()
     sh.check_errors()
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    # per step: [0] step start, [1] K1 end, [2] K2 end, [3] allreduce + prepare end,
+    # [4] step end (main stream); K3's own start / end on the side stream
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
 
     side = torch.cuda.Stream(device)
 
@@ -388,7 +524,11 @@ def run_ours(args, world, rank, local):
             ev[1].record(stream)
         side.wait_event(k1)
         sh.set_stream(side)
+        if ev:
+            ev[5].record(side)
         sh.rebuild_theta()                    # K3, concurrent with K2 / allreduce / prepare
+        if ev:
+            ev[6].record(side)
         sh.set_stream(stream)
         sh.rebuild_phi()
         if ev:
@@ -422,33 +562,35 @@ def run_ours(args, world, rank, local):
     with clocks:
         start.record(stream)
         for i in range(args.steps):
-            step(it, evs[i])                  # per-kernel events on the launching stream
+            step(it, evs[i])                  # per-kernel events on the launching streams
             it += 1
         stop.record(stream)
         barrier()
-    acc = np.zeros(4)
+    acc = np.zeros(5)
     for ev in evs:
         acc += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]),
-                ev[3].elapsed_time(ev[4])]
+                ev[3].elapsed_time(ev[4]), ev[5].elapsed_time(ev[6])]
+    acc /= args.steps
     ms_total = start.elapsed_time(stop)
     if dist:
         t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
         ar(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = T_all / (ms_step / 1e3)
+    T_step = T_local if args.shard else T_all
+    value = T_step / (ms_step / 1e3)
     ll = sh.loglik_sum()
     if dist:
         t = torch.tensor([ll], dtype=torch.float64, device="cuda")
         ar(t)
         ll = float(t.item())
-    ll /= T_all
+    ll /= T_step
     sh.check_errors()
     st = sh.stats()
     # own kernels per step: sample + ll_reduce, phi_rebuild, theta_rebuild,
     # prepare (+ context_kernel when some word is split into several slices)
     launches_per_step = 5 + (1 if st["word_contexts"] > 0 else 0) + (1 if peer else 0)
-    k1_ms = acc[0] / args.steps
+    k1_ms = acc[0]
     peak, peak_src = measured_peak()
     achieved = st["sample_bytes"] / (k1_ms / 1e3) / 1e9
     traffic = ncu_traffic(args.workload, K)
@@ -480,7 +622,8 @@ def run_ours(args, world, rank, local):
             phase_arg = nphase
         if nphase > 1:
             sh.set_phases(phase_arg)
-            sh.load_tokens(lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, seed=args.seed, chunk_id=rank)
+            sh.load_tokens(lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, seed=TRAIN_SEED,
+                           chunk_id=chunk_id)
             if peer:
                 handles = [None] * world
                 dist.all_gather_object(handles, sh.peer_handle())
@@ -558,7 +701,7 @@ def run_ours(args, world, rank, local):
             t = torch.tensor([el], dtype=torch.float64, device="cuda")
             ar(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": T_all * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": 2 * T_local,
+        e2e = {"value": T_step * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": 2 * T_local,
                "d2h_bytes_per_step": 2 * T_local + 8,
                "api": f"DeviceShard.copy_assignments_async (pinned host buffers, two copy streams) + "
                       f"assignments_imported, rebuild_phi/prepare/rebuild_theta, sample_phase x {nphase} "
@@ -568,33 +711,36 @@ def run_ours(args, world, rank, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:      # rank 0 at N=1 only
-        nd = args.cpu_sample_docs or (shape["num_docs"] if args.workload == "tiny" else 20000)
-        cpu = cpu_baseline(shape, K, args.seed, nd)
+        nd = args.cpu_sample_docs or min(CPU_SAMPLE_DOCS[args.workload], SHAPES[args.workload]["num_docs"])
+        cpu = cpu_baseline(args, K, nd)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "shard-proxy" if args.shard else args.scaling,
             "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {
-                "workload": f"{args.workload}-shaped synthetic LDA corpus, K={K}, one shard per GPU",
-                "docs_per_gpu": shape["num_docs"], "vocab": corp.vocab_size, "tokens_per_gpu": T_local,
-                "tokens_total": T_all, "topics": K, "iterations": [args.warmup, args.warmup + args.steps],
-                "parallelism": ((f"doc-shard dp{world} + peer-memory phi exchange kernel" if peer else
-                                 f"doc-shard dp{world} + {args.dist_backend.upper()} allreduce of phi") if dist
-                                else "dp1"),
-                "l2": "inputs larger than L2 (z 2T B, theta 4*NNZ B, phi >= 200 MB vs 126 MB L2)",
-                "runs": st["runs"], "slices": st["slices"], "word_contexts": st["word_contexts"],
-                "doc_blocks": st["doc_blocks"],
-            },
+            "config": make_config(args, world, T_step),
+            "layout": {"docs_this_rank": corp.num_docs, "tokens_this_rank": T_local, "runs": st["runs"],
+                       "slices": st["slices"], "word_contexts": st["word_contexts"],
+                       "doc_blocks": st["doc_blocks"], "theta_nnz_after_last_step": st["theta_nnz"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic["bytes_per_launch"] if traffic else None,
+                         "traffic_source": (f"{traffic['source']} (committed ncu --set full capture; not this run)"
+                                            if traffic else None),
                          "frac_of_nominal_8tbs": achieved / 8000.0,
                          "kernel": "gf::sample_kernel (K1)", "algorithmic_bytes_per_launch": st["sample_bytes"],
                          "kernel_ms": k1_ms, "peak_source": peak_src},
-            "kernel_ms": {"sample": acc[0] / args.steps, "phi_rebuild": acc[1] / args.steps,
-                          "allreduce_and_prepare": acc[2] / args.steps,
-                          "theta_rebuild_exposed": acc[3] / args.steps},
+            "kernels": {
+                "phi_rebuild": kernel_block("gf::phi_rebuild_kernel (K2, + sync-buffer memset)", acc[1],
+                                            st["phi_bytes"], peak),
+                "theta_rebuild": kernel_block("gf::theta_rebuild_kernel (K3, side stream)", acc[4],
+                                              st["theta_bytes"], peak),
+                "note": "K2 and K3 run concurrently (main / side stream), so each time includes the other's "
+                        "contention",
+            },
+            "kernel_ms": {"sample": acc[0], "phi_rebuild": acc[1], "allreduce_and_prepare": acc[2],
+                          "theta_rebuild_exposed": acc[3], "theta_rebuild": acc[4]},
             "loglik_per_token": ll,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -71,6 +71,10 @@ def lib():
         L.gfo_loglik_sq.restype = _f64
         L.gfo_loglik_sq.argtypes = [_i32, _i32, _f64, _f64, _i64, _p, _p, _i64, _p, _p, _p, _p, _p, _p,
                                     ctypes.c_int]
+        L.gfo_synth_lengths.restype = ctypes.c_int
+        L.gfo_synth_lengths.argtypes = [_u64, _i64, _i64, _f64, _f64, _p]
+        L.gfo_synth_tokens.restype = ctypes.c_int
+        L.gfo_synth_tokens.argtypes = [_u64, _i64, _i64, _p, _i32, _i32, _f64, _f64, _p, _p]
         _lib = L
     return _lib
 
@@ -109,6 +113,37 @@ def token_uniforms(seed, iteration, doc, word, occ):
     u1, u2 = _f64(), _f64()
     lib().gfo_token_uniforms(seed, iteration, doc, word, occ, ctypes.byref(u1), ctypes.byref(u2))
     return u1.value, u2.value
+
+
+# ------------------------------------------------- synthetic corpora ----
+def synth_lengths(seed, num_docs, mean_len, sigma=0.6, doc_begin=0):
+    """Document lengths of the benchmark corpus (gf_synth_ref.c; equal to the
+    product generator's gf_synth_lengths)."""
+    out = np.empty(int(num_docs), np.int64)
+    if lib().gfo_synth_lengths(seed & 0xFFFFFFFFFFFFFFFF, int(doc_begin), int(num_docs), float(mean_len),
+                               float(sigma), _ptr(out)) != 0:
+        raise ValueError("bad synthetic corpus shape")
+    return out
+
+
+def synth_generate(num_docs, vocab_size, mean_len, seed=20261017, k_true=100, zipf_s=1.07, doc_alpha=0.1,
+                   sigma=0.6, doc_begin=0):
+    """Documents [doc_begin, doc_begin + num_docs) of the benchmark corpus as a
+    corpus_from_tokens dict (doc ids relative to doc_begin) -- the arrays
+    paper_1803_04631_b200.synth.generate returns, without the product library."""
+    lengths = synth_lengths(seed, num_docs, mean_len, sigma, doc_begin)
+    ptr = np.zeros(len(lengths) + 1, np.int64)
+    np.cumsum(lengths, out=ptr[1:])
+    T = int(ptr[-1])
+    docs = np.empty(T, np.int32)
+    words = np.empty(T, np.int32)
+    if lib().gfo_synth_tokens(seed & 0xFFFFFFFFFFFFFFFF, int(doc_begin), int(num_docs), _ptr(ptr), int(vocab_size),
+                              int(k_true), float(zipf_s), float(doc_alpha), _ptr(docs), _ptr(words)) != 0:
+        raise ValueError("bad synthetic corpus shape")
+    if doc_begin:
+        docs -= np.int32(doc_begin)
+    return dict(doc_ids=docs, word_ids=words, doc_lengths=lengths, doc_ptr=ptr, D=int(num_docs),
+                V=int(vocab_size), T=T)
 
 
 # ------------------------------------------------------------- corpus.py ----

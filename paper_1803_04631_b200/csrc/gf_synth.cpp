@@ -57,9 +57,10 @@ uint64_t key_of(uint64_t seed, uint64_t a, uint64_t b) {
 }
 
 template <class F>
-void par(int64_t n, F f) {
+void par(int64_t n, F f, int64_t min_parallel = 4096) {
     unsigned nt = std::max(1u, std::min(std::thread::hardware_concurrency(), 32u));
-    if (n < 4096) nt = 1;
+    if (n < min_parallel) nt = 1;
+    nt = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt, n));
     std::vector<std::thread> th;
     for (unsigned i = 0; i < nt; ++i) th.emplace_back([=] { f(n * i / nt, n * (i + 1) / nt); });
     for (auto& t : th) t.join();
@@ -94,16 +95,17 @@ int gf_synth_tokens(uint64_t seed, int64_t doc_begin, int64_t num_docs, const in
     // Zipfian head (the corpus-wide law stays heavy-tailed, like NYTimes /
     // PubMed) while the topics disagree on which words lead
     std::vector<int32_t> perm((size_t)k_true * V);
-    {
+    // (one topic per task: the orders are independent)
+    par(k_true, [&](int64_t a, int64_t b) {
         std::vector<double> key((size_t)V);
-        for (int32_t k = 0; k < k_true; ++k) {
+        for (int64_t k = a; k < b; ++k) {
             int32_t* p = perm.data() + (size_t)k * V;
             Rng r(key_of(seed, 2, (uint64_t)k));
             for (int32_t w = 0; w < V; ++w) key[w] = std::log((double)w + 1.0) + r.normal();
             std::iota(p, p + V, 0);
             std::sort(p, p + V, [&](int32_t x, int32_t y) { return key[x] < key[y] || (key[x] == key[y] && x < y); });
         }
-    }
+    }, 2);
     par(num_docs, [&](int64_t a, int64_t b) {
         std::vector<double> mix((size_t)k_true);
         for (int64_t i = a; i < b; ++i) {

@@ -55,3 +55,35 @@ def test_our_arm_line():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
     assert d["gpu_launches"] >= 5 * d["steps"]
     assert d["config"]["workload"].startswith("tiny")
+
+
+def test_reference_arm_loads_no_product_code():
+    """The --impl reference arm must not touch the product library: its corpus
+    comes from the oracle's generator and its chunk from the reference's own
+    partition (or the oracle's restatement)."""
+    code = (
+        "import sys, runpy, json\n"
+        f"sys.argv = ['bench.py', '--impl', 'reference', '--workload', 'tiny', '--steps', '1', '--warmup', '1']\n"
+        f"runpy.run_path({os.path.join(ROOT, 'bench.py')!r}, run_name='__main__')\n"
+        "maps = open('/proc/self/maps').read()\n"
+        "print(json.dumps({'so': 'libgfb200' in maps,\n"
+        "                  'pkg': any(m.startswith('paper_1803_04631_b200') for m in sys.modules)}))\n"
+    )
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    verdict = json.loads(p.stdout.strip().splitlines()[-1])
+    assert verdict == {"so": False, "pkg": False}
+
+
+def test_both_arms_describe_the_same_config():
+    """Same command, same `config` object (the driver compares the arms)."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    ns = type("A", (), dict(workload="tiny", topics=None, seed=bench.CORPUS_SEED, scaling="strong", shard=None,
+                            warmup=3, steps=5))()
+    c1 = bench.make_config(ns, 1, bench.corpus_tokens_total(ns, 1))
+    from paper_1803_04631_b200 import synth
+
+    T = synth.generate(1000, 1000, 100.0, seed=bench.CORPUS_SEED).num_tokens
+    assert c1 == bench.make_config(ns, 1, T)

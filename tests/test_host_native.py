@@ -241,3 +241,18 @@ def test_uci_matches_the_reference_loader():
     for f in ("doc_ids", "word_ids", "doc_lengths", "doc_ptr"):
         np.testing.assert_array_equal(getattr(c, f), g[f], err_msg=f)
     assert c.vocab == g["vocab"].tolist()
+
+
+@pytest.mark.parametrize("nd,V,mean,seed,begin", [(300, 1000, 60.0, 1, 0), (2000, 141043, 89.98, 20261017, 4321),
+                                                  (50, 101636, 332.08, 20261017, 299000)])
+def test_oracle_generator_equals_the_product_generator(nd, V, mean, seed, begin):
+    """bench.py's reference arm builds its corpus with oracle/gf_synth_ref.c;
+    it must be the product generator's corpus, array for array."""
+    import oracle
+
+    a = oracle.synth_generate(nd, V, mean, seed=seed, doc_begin=begin)
+    b = synth.generate(nd, V, mean, seed=seed, doc_begin=begin)
+    assert a["T"] == b.num_tokens
+    np.testing.assert_array_equal(a["doc_lengths"], b.doc_lengths)
+    np.testing.assert_array_equal(a["doc_ids"], b.doc_ids)
+    np.testing.assert_array_equal(a["word_ids"], b.word_ids)
