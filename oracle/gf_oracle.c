@@ -331,11 +331,43 @@ int gfo_sample_tokens(int32_t K, int32_t V, double alpha, double beta, uint64_t 
     return status;
 }
 
+/* Exact draw from the exclusion-adjusted conditional by two sequential passes
+ * over k = 0..K-1 (theta row merged in topic order): the thinning loop's
+ * fallback once it has rejected its 64th proposal, so the kept topic follows
+ * the exclusion-adjusted Eq. 1 whatever the acceptance rate (a capped loop
+ * that simply kept z would over-weight z by the chance of 64 rejections).
+ * Weights: (theta_dk + a) p*(k) for k != z, (theta_dz - 1 + a) p*_ex(z). */
+static int32_t exact_excluded_draw(int32_t K, double alpha, const double* pstar, double pex_z,
+                                   const uint16_t* ids, const uint16_t* cnts, int64_t n, int32_t zt,
+                                   double u) {
+    double tot = 0.0;
+    int64_t j = 0;
+    for (int32_t k = 0; k < K; ++k) {
+        double c = 0.0;
+        if (j < n && ids[j] == k) c = (double)cnts[j++];
+        tot += k == zt ? (c - 1.0 + alpha) * pex_z : (c + alpha) * pstar[k];
+    }
+    const double target = u * tot;
+    double acc = 0.0;
+    int32_t last = 0;
+    j = 0;
+    for (int32_t k = 0; k < K; ++k) {
+        double c = 0.0;
+        if (j < n && ids[j] == k) c = (double)cnts[j++];
+        const double w = k == zt ? (c - 1.0 + alpha) * pex_z : (c + alpha) * pstar[k];
+        if (w > 0.0) last = k;
+        acc += w;
+        if (acc > target) return k;
+    }
+    return last;
+}
+
 /* The product kernel's form of the same draw (csrc/k_sample.cu): exclusion by
  * THINNING.  Draw k from the exclusion-free S+Q mixture of SPEC.md:267-275 with
  * uniforms (b, s) of Philox block (doc, word, occ | retry << 26, iteration); if
  * k == z keep it with probability (theta_dz - 1 + a) p*_ex(z) / ((theta_dz + a) p*(z))
- * (uniform t), else redraw with retry + 1.  The kept k follows the same
+ * (uniform t), else redraw with retry + 1; the 64th rejection ends in one
+ * exact draw (exact_excluded_draw, uniform = word 3 of that block).  The kept k follows the same
  * exclusion-adjusted Eq. 1 distribution as gfo_sample_tokens (tests compare
  * both against gfo_conditional); this variant exists so the device can be
  * checked draw for draw. */
@@ -430,6 +462,11 @@ int gfo_sample_tokens_thin(int32_t K, int32_t V, double alpha, double beta, uint
                         break;
                     }
                     if (ut * ((double)cnt + alpha) * pstar[zt] < ((double)cnt - 1.0 + alpha) * pex[zt]) break;
+                    if (retry == 63) {   /* 64 rejections: one exact draw (4th word of this block) */
+                        const double uf = (double)(r[3] >> 8) * (1.0 / 16777216.0);
+                        k = exact_excluded_draw(K, alpha, pstar, pex[zt], th_ids + r0, th_cnt + r0, r1 - r0, zt, uf);
+                        break;
+                    }
                     k = zt;
                 }
                 z[t] = (uint16_t)k;

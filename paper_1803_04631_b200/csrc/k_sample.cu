@@ -30,9 +30,10 @@
 // is applied by thinning: draw k from the exclusion-free S+Q mixture; if
 // k == z keep it with probability
 //   p_ex(z) / p(z) = (theta_dz - 1 + a) p*_ex(z) / ((theta_dz + a) p*(z)),
-// else redraw (fresh Philox block: occurrence | retry << 26).  Accepted draws
-// follow exactly the exclusion-adjusted Eq. 1 that sample_sparse defines,
-// without a per-token search for z in the row.
+// else redraw (fresh Philox block: occurrence | retry << 26); the 64th
+// rejection ends in one exact sequential draw (exact_excluded_draw).  Accepted
+// draws follow exactly the exclusion-adjusted Eq. 1 that sample_sparse
+// defines, without a per-token search for z in the row.
 #include "gf_internal.cuh"
 #include "gf_device.cuh"
 
@@ -190,6 +191,47 @@ __device__ __forceinline__ bool keep_own(float ut, uint32_t cnt, float alpha, fl
     return __fmul_rn(ut, den) < num;
 }
 
+// Exact draw from the exclusion-adjusted conditional: two sequential passes over
+// k = 0..K-1 with the sorted theta row merged in (one lane).  The thinning
+// loop's fallback after its 64th rejected proposal, so the kept topic follows
+// the exclusion-adjusted Eq. 1 at any acceptance rate (keeping z after a cap
+// would over-weight it by the chance of 64 rejections).  Weights
+// (theta_dk + a) p*(k) for k != z and (theta_dz - 1 + a) p*_ex(z); the oracle's
+// thin mode does the same in fp64 (oracle/gf_oracle.c exact_excluded_draw).
+// (scalar arguments: a reference to the kernel's parameter struct across a
+// call would copy the struct to local memory in every thread)
+// The uniform is word 3 of the last rejected proposal's Philox block, recomputed
+// here so the draw loop keeps no extra register live.
+__device__ __noinline__ uint32_t exact_excluded_draw(int K, float alpha, TPos tm, const float* pstar,
+                                                     const uint32_t* row, uint32_t nnz, uint32_t z, float pex_z,
+                                                     uint4 ctr, uint2 key) {
+    const float u = u24(philox4x32_10(ctr, key).w);
+    float tot = 0.f;
+    for (int pass = 0; pass < 2; ++pass) {
+        const float target = __fmul_rn(u, tot);
+        float acc = 0.f;
+        uint32_t j = 0, last = 0, e = nnz ? __ldg(row) : 0u;
+        for (uint32_t k = 0; k < (uint32_t)K; ++k) {
+            float c = 0.f;
+            if (j < nnz && topic_of(e, tm) == k) {
+                c = (float)(e >> 16);
+                ++j;
+                e = j < nnz ? __ldg(row + j) : 0u;
+            }
+            const float w = k == z ? __fmul_rn(__fadd_rn(c - 1.f, alpha), pex_z)
+                                   : __fmul_rn(__fadd_rn(c, alpha), pstar[tpos(k, tm)]);
+            acc = __fadd_rn(acc, w);
+            if (pass == 1) {
+                if (w > 0.f) last = k;
+                if (acc > target) return k;
+            }
+        }
+        if (pass == 1) return last;
+        tot = acc;
+    }
+    return z;
+}
+
 // Rows longer than the staging buffer: warp-cooperative, one run, the S part
 // re-streamed per S-branch draw.  Returns S (all lanes).
 __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, float Q, uint32_t v, uint32_t gdoc,
@@ -260,6 +302,11 @@ __device__ __noinline__ float huge_run(const SampleArgs& a, const float* smem, f
                 break;
             }
             if (keep_own(u.t, cnt, a.alpha, pstar[tpos(zt, a.tm)], pz)) break;
+            if (retry == kMaxRetry) {                       // 64 rejections: one exact draw
+                k = exact_excluded_draw(a.K, a.alpha, a.tm, pstar, row, nnz, zt, pz,
+                                        make_uint4(gdoc, v, occ | ((uint32_t)kMaxRetry << 26), a.iteration), a.key);
+                break;
+            }
             k = zt;
         }
         if (lane == 0) { a.z[t] = (uint16_t)k; a.zdoc[dwp + occ] = (uint16_t)k; }
@@ -579,6 +626,11 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
                                 break;
                             }
                             if (keep_own(u.t, cnt, a.alpha, pstar[tpos(zt, a.tm)], pz)) break;
+                            if (retry == kMaxRetry) {                 // 64 rejections: one exact draw
+                                k = exact_excluded_draw(a.K, a.alpha, a.tm, pstar, row, onnz, zt, pz,
+                                    make_uint4(odoc, v, occ | ((uint32_t)kMaxRetry << 26), a.iteration), a.key);
+                                break;
+                            }
                             k = zt;                                                   // rejected: redraw
                         }
                         a.z[t] = (uint16_t)k;

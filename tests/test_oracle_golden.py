@@ -374,3 +374,44 @@ def test_loglik_sq_form_equals_naive_formula():
     sq = oracle.loglik_sq(K, corp.vocab_size, a, b, ch.doc_ids, ch.word_ids, 0, rp, ids, cn, corp.doc_lengths,
                           phi, tot)
     assert sq == pytest.approx(naive, rel=1e-12)
+
+
+def low_acceptance_state(K=100, V=5, seed=0):
+    """A token that is the only occurrence of its word in its topic z (phi_vz = 1)
+    in a document dominated by z: thinning rejects a z proposal ~97% of the time
+    (the 64-try cap is reached with probability ~0.16), and under the exact
+    conditional the token leaves z with probability ~0.66."""
+    r = np.random.default_rng(seed)
+    th = np.zeros(K, np.int64)
+    z = 7
+    th[z] = 100
+    others = r.choice([k for k in range(K) if k != z], 30, replace=False)
+    np.add.at(th, r.choice(others, 100), 1)
+    phi = r.integers(0, 3, (K, V)).astype(np.uint32)
+    v = 2
+    phi[:, v] = 0
+    phi[z, v] = 1
+    tot = phi.sum(axis=1).astype(np.int64) + r.integers(1000, 5000, K)
+    return th, z, phi, tot, v
+
+
+def test_thinning_is_exact_at_low_acceptance():
+    """the thinning loop must not keep z after its retry cap -- the
+    64th rejection ends in an exact draw, so even a state where most proposals
+    of z are rejected samples the exclusion-adjusted Eq. 1."""
+    K, V, alpha, beta = 100, 5, 0.5, 0.01
+    th, z, phi, tot, v = low_acceptance_state(K, V)
+    ids = np.flatnonzero(th).astype(np.uint16)
+    p, _ = oracle.conditional(K, V, alpha, beta, th, phi[:, v], tot, z)
+    ps = (phi[:, v] + beta) / (tot + V * beta)
+    full = (th + alpha) * ps
+    rej = (full[z] - (th[z] - 1 + alpha) * (phi[z, v] - 1 + beta) / (tot[z] - 1 + V * beta)) / full.sum()
+    assert rej ** 64 > 0.1                                   # the cap is really exercised
+    n = 1_000_000
+    zp = oracle.sample_tokens(K, V, alpha, beta, 42, 3, np.zeros(n, np.int32), np.full(n, v, np.int32),
+                              np.full(n, z, np.uint16), 0, np.array([0, len(ids)]), ids,
+                              th[ids].astype(np.uint16), phi, tot, mode="thin")
+    hist = np.bincount(zp, minlength=K)
+    keep = p * n >= 5
+    assert stats.chisquare(hist[keep], p[keep] / p[keep].sum() * hist[keep].sum())[1] > 0.001
+    assert abs(hist[z] / n - p[z]) < 0.003
