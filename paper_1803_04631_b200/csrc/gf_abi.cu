@@ -96,6 +96,9 @@ void free_dev(gf_shard* s) {
 extern "C" int gf_sync_layout(const int64_t* freq, int32_t V, int32_t K, uint32_t thr, int32_t* word_col,
                               int64_t* layout) {  // hybrid phi columns from global frequencies
     if (V < 1 || K < 1) return fail(GF_ERR_VALUE, "bad layout dimensions");
+    // a 16-bit column must never hold a cell above 65535 (nor carry into its
+    // neighbour in the packed u32 sum), so light words are <= 65535 tokens
+    if (thr > 65535u) return fail(GF_ERR_VALUE, "heavy_threshold %u exceeds 65535 (16-bit phi columns)", thr);
     const int64_t Kp = K + (K & 1);
     int64_t h = 0, l = 0;
     for (int v = 0; v < V; ++v) {
@@ -241,6 +244,8 @@ int gf_shard_create(gf_shard** out, int device, int32_t K, int32_t V, double alp
     if (K > 16384) return fail(GF_ERR_CAPACITY, "K=%d: the device sampler supports K <= 16384", K);
     if (V < 1) return fail(GF_ERR_VALUE, "vocab_size must be >= 1");
     if (!(alpha > 0) || !(beta > 0)) return fail(GF_ERR_VALUE, "alpha and beta must be > 0");
+    if (heavy_threshold > 65535u)
+        return fail(GF_ERR_VALUE, "heavy_threshold %u exceeds 65535 (16-bit phi columns)", heavy_threshold);
     int ndev = 0;
     gf_device_count(&ndev);
     if (ndev == 0) return fail(GF_ERR_NODEVICE, "no CUDA device visible: the B200 sampler has no CPU fallback");

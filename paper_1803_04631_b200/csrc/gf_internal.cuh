@@ -17,7 +17,8 @@
 //                            round4(min(K, L_d)) per doc, ids ascending
 //   theta_meta uint2[D]      {row offset, nnz}
 //   sync       u32[...]      [phi32 | phi16 packed | n_k]: word-major phi
-//                            columns (one contiguous K-vector per word)
+//                            columns (one contiguous K-vector per word), plus
+//                            one word after n_k: K2's work-item counter
 //   inv_den    f32[K]        1 / (n_k + V beta)
 #pragma once
 #include <cstdint>
@@ -97,7 +98,6 @@ struct gf_shard {
     int64_t n_heavy = 0, n_light = 0;
     int64_t off_phi16_u32 = 0, off_nk_u32 = 0, sync_u32 = 0;
     int64_t doc_lo = 0, doc_hi = 0, D = 0, T = 0, R = 0, n_slices = 0, n_k2 = 0;
-    int64_t n_k2_big = 0;                    // K2 items [0, n_k2_big) per CTA, the rest (<= 32 tokens) per warp
     int64_t theta_cap = 0;
     int64_t n_doc_blocks = 1;
     // sampling phases (gf_shard_set_phases): the slice schedule is phase-major;

@@ -11,95 +11,117 @@
 namespace gf {
 
 // ---------------------------------------------------------------- K2 ------
-// Work items are (phi column, token range): one item per light word (the
-// whole group, <= heavy_threshold tokens so its 16-bit cells cannot
-// overflow), one item per slice of a heavy word (32-bit cells, global
-// atomics).  Each CTA histograms an item's topics in shared memory (tokens
-// are word-grouped, so the item is one contiguous z range) and writes only
-// the nonzero cells into the pre-zeroed sync buffer; n_k is accumulated per
-// CTA in shared memory and flushed with K atomics at the end.
-// Items of <= 32 tokens (the rare words of a large vocabulary) go to single
-// warps instead: one topic per lane, __match_any_sync groups equal topics and
-// the group leader writes the cell -- no shared histogram, no block barriers.
-// The layout puts the CTA items first ([0, n_big)) and the warp items after.
-__global__ void __launch_bounds__(256) phi_rebuild_kernel(const int4* __restrict__ items, int n_items, int n_big,
-                                                          const uint16_t* __restrict__ z, uint32_t* sync,
-                                                          int K, int Kp, long long off16, long long offnk,
-                                                          unsigned long long* errs) {
+// One WARP per work item, items claimed dynamically (one global atomic per
+// item).  An item is (phi column, token range): a light word's whole group
+// (<= heavy_threshold <= 65535 tokens, 16-bit column), a slice of a heavy word
+// (<= 4096 tokens, 32-bit column, global atomics when the word has several
+// slices), or an empty item for a light word absent from the shard.  Tokens
+// are word-grouped, so an item is one contiguous z range: the warp streams it
+// with 16-byte loads and counts into its private PACKED histogram in shared
+// memory (two 16-bit bins per u32 word; an item has <= 65535 tokens, so a bin
+// cannot carry into its neighbour), then
+//   light: writes the whole packed column densely (16-byte stores, zeros
+//          included) -- the light region needs no memset;
+//   heavy: adds its nonzero cells to the pre-zeroed 32-bit column;
+// and clears the histogram it read.  n_k accumulates per CTA in shared memory
+// (nonzero cells only) and is flushed with K atomics at the end.  No block
+// barrier inside the item loop: each warp keeps its own loads in flight.
+constexpr int kK2Warps = 8;
+
+__device__ __forceinline__ void k2_count(uint32_t* bins, uint32_t k, int K, uint32_t t, unsigned long long* errs) {
+    if (k < (uint32_t)K) atomicAdd(&bins[k >> 1], 1u << ((k & 1u) << 4));
+    else atomicMin(errs, (unsigned long long)t);
+}
+
+__global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* __restrict__ items, int n_items,
+                                                                    const uint16_t* __restrict__ z, uint32_t* sync,
+                                                                    int K, int Kp, long long off16, long long offnk,
+                                                                    int nwarps_per_cta, unsigned int* next_item,
+                                                                    unsigned long long* errs) {
     extern __shared__ uint32_t sh[];
-    uint32_t* bins = sh;
-    uint32_t* nks = sh + K;
-    for (int k = threadIdx.x; k < 2 * K; k += blockDim.x) sh[k] = 0;
+    const int KW = Kp >> 1;                                   // packed words per histogram
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* nks = sh;                                       // [K] this CTA's n_k
+    uint32_t* bins = sh + ((K + 3) & ~3) + (size_t)warp * ((KW + 3) & ~3);
+    for (int i = threadIdx.x; i < K; i += blockDim.x) nks[i] = 0u;
+    for (int i = lane; i < KW; i += 32) bins[i] = 0u;
     __syncthreads();
-    uint16_t* phi16 = reinterpret_cast<uint16_t*>(sync + off16);
-    for (int it = blockIdx.x; it < n_big; it += gridDim.x) {
-        const int4 w = items[it];
-        const int col = w.x, t0 = w.y, t1 = w.z;
-        const bool atomic = w.w != 0;
-        // 16-byte loads (8 topics per thread) over the 8-aligned body, scalar head/tail
-        auto count = [&](int t, int k) {
-            if (k < K) atomicAdd(&bins[k], 1u);
-            else atomicMin(errs, (unsigned long long)t);
-        };
-        const int a0 = min(t1, (t0 + 7) & ~7), a1 = max(a0, t1 & ~7);
-        for (int t = t0 + threadIdx.x; t < a0; t += blockDim.x) count(t, z[t]);
-        for (int t = a1 + threadIdx.x; t < t1; t += blockDim.x) count(t, z[t]);
-        const uint4* zv = reinterpret_cast<const uint4*>(z);
-        for (int q = (a0 >> 3) + threadIdx.x; q < (a1 >> 3); q += blockDim.x) {
-            const uint4 v = __ldg(zv + q);
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    // 16-byte column stores need a 16-byte aligned packed column
+    const bool vec_cols = (KW & 3) == 0 && (off16 & 3) == 0;
+    uint32_t* phi16w = sync + off16;                           // packed light columns (u32 words)
+    const uint4* zv = reinterpret_cast<const uint4*>(z);
+    if (warp < nwarps_per_cta) {
+        while (true) {
+            int it = 0;
+            if (lane == 0) it = (int)atomicAdd(next_item, 1u);
+            it = __shfl_sync(kFull, it, 0);
+            if (it >= n_items) break;
+            const int4 w = __ldg(items + it);
+            const int col = w.x;
+            const uint32_t t0 = (uint32_t)w.y, t1 = (uint32_t)w.z;
+            // ---- count: scalar head / tail, 16-byte body (8 topics per lane, two loads in flight) ----
+            const uint32_t a0 = min(t1, (t0 + 7u) & ~7u), a1 = max(a0, t1 & ~7u);
+            if (t0 + lane < a0) k2_count(bins, z[t0 + lane], K, t0 + lane, errs);
+            if (a1 + lane < t1) k2_count(bins, z[a1 + lane], K, a1 + lane, errs);
+            uint32_t q = (a0 >> 3) + lane;
+            const uint32_t qe = a1 >> 3;
+            for (; q + 32u < qe; q += 64u) {
+                const uint4 v0 = __ldg(zv + q), v1 = __ldg(zv + q + 32u);
+                const uint32_t e[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                count(8 * q + 2 * i, (int)(w[i] & 0xffffu));
-                count(8 * q + 2 * i + 1, (int)(w[i] >> 16));
-            }
-        }
-        __syncthreads();
-        if ((long long)(t1 - t0) * 8 >= K) {
-            for (int k = threadIdx.x; k < K; k += blockDim.x) {
-                const uint32_t c = bins[k];
-                if (c) {
-                    bins[k] = 0;
-                    nks[k] += c;
-                    if (col >= 0) phi16[(size_t)col * Kp + k] = (uint16_t)c;
-                    else if (atomic) atomicAdd(&sync[(size_t)(~col) * K + k], c);
-                    else sync[(size_t)(~col) * K + k] = c;
+                for (int i = 0; i < 8; ++i) {
+                    const uint32_t tb = 8u * (i < 4 ? q : q + 32u) + 2u * (i & 3);
+                    k2_count(bins, e[i] & 0xffffu, K, tb, errs);
+                    k2_count(bins, e[i] >> 16, K, tb + 1u, errs);
                 }
             }
-        } else {
-            for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-                const int k = z[t];
-                if (k >= K) continue;
-                const uint32_t c = atomicExch(&bins[k], 0u);
-                if (c) {
-                    atomicAdd(&nks[k], c);
-                    if (col >= 0) phi16[(size_t)col * Kp + k] = (uint16_t)c;
-                    else if (atomic) atomicAdd(&sync[(size_t)(~col) * K + k], c);
-                    else sync[(size_t)(~col) * K + k] = c;
+            if (q < qe) {
+                const uint4 v0 = __ldg(zv + q);
+                const uint32_t e[4] = {v0.x, v0.y, v0.z, v0.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    k2_count(bins, e[i] & 0xffffu, K, 8u * q + 2u * i, errs);
+                    k2_count(bins, e[i] >> 16, K, 8u * q + 2u * i + 1u, errs);
                 }
             }
-        }
-        __syncthreads();
-    }
-    // ---- warp items ----
-    const int lane = threadIdx.x & 31;
-    const int nw = (int)(blockDim.x >> 5);
-    for (int it = n_big + blockIdx.x * nw + (int)(threadIdx.x >> 5); it < n_items; it += gridDim.x * nw) {
-        const int4 w = items[it];
-        const int col = w.x, t = w.y + lane;
-        bool valid = t < w.z;
-        const uint32_t k = valid ? (uint32_t)z[t] : 0xFFFFFFFFu;
-        if (valid && k >= (uint32_t)K) {
-            atomicMin(errs, (unsigned long long)t);
-            valid = false;
-        }
-        const unsigned grp = __match_any_sync(kFull, valid ? k : 0xFFFFFFFFu);
-        if (valid && lane == __ffs(grp) - 1) {
-            const uint32_t c = (uint32_t)__popc(grp);
-            atomicAdd(&nks[k], c);
-            if (col >= 0) phi16[(size_t)col * Kp + k] = (uint16_t)c;
-            else if (w.w != 0) atomicAdd(&sync[(size_t)(~col) * K + k], c);
-            else sync[(size_t)(~col) * K + k] = c;
+            __syncwarp();
+            // ---- flush: every packed word once (lane-strided), cleared behind ----
+            if (col >= 0) {
+                uint32_t* dst = phi16w + (size_t)col * KW;
+                if (vec_cols) {
+                    for (int j = lane; j < (KW >> 2); j += 32) {
+                        const uint4 b = reinterpret_cast<const uint4*>(bins)[j];
+                        reinterpret_cast<uint4*>(bins)[j] = make_uint4(0u, 0u, 0u, 0u);
+                        reinterpret_cast<uint4*>(dst)[j] = b;
+                        const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const uint32_t k = 8u * j + 2u * i;
+                            if (bw[i] & 0xffffu) atomicAdd(&nks[k], bw[i] & 0xffffu);
+                            if (bw[i] >> 16) atomicAdd(&nks[k + 1], bw[i] >> 16);
+                        }
+                    }
+                } else {
+                    for (int j = lane; j < KW; j += 32) {
+                        const uint32_t b = bins[j];
+                        bins[j] = 0u;
+                        dst[j] = b;
+                        if (b & 0xffffu) atomicAdd(&nks[2 * j], b & 0xffffu);
+                        if (b >> 16) atomicAdd(&nks[2 * j + 1], b >> 16);
+                    }
+                }
+            } else {
+                uint32_t* dst = sync + (size_t)(~col) * K;
+                for (int j = lane; j < KW; j += 32) {
+                    const uint32_t b = bins[j];
+                    if (!b) continue;
+                    bins[j] = 0u;
+                    const uint32_t k = 2u * j, c0 = b & 0xffffu, c1 = b >> 16;
+                    if (c0) { atomicAdd(&nks[k], c0); atomicAdd(dst + k, c0); }
+                    if (c1) { atomicAdd(&nks[k + 1], c1); atomicAdd(dst + k + 1, c1); }
+                }
+            }
+            __syncwarp();
         }
     }
     __syncthreads();
@@ -108,24 +130,36 @@ __global__ void __launch_bounds__(256) phi_rebuild_kernel(const int4* __restrict
         if (nks[k]) atomicAdd(&nk[k], nks[k]);
 }
 
+// bytes of the K2 shared memory: the CTA's n_k plus one packed histogram per warp
+static size_t k2_smem(int K, int Kp, int warps) {
+    return ((size_t)((K + 3) & ~3) + (size_t)warps * (((Kp >> 1) + 3) & ~3)) * sizeof(uint32_t);
+}
+
 cudaError_t launch_phi_rebuild(gf_shard* s) {
     s->ctx_dirty = true;
-    cudaError_t e = cudaMemsetAsync(s->d.sync, 0, (size_t)s->sync_u32 * 4, s->stream);
+    // only the 32-bit columns (atomic adds) and n_k need zeroing: every 16-bit
+    // column is rewritten whole by its item; the last word is the item counter
+    cudaError_t e = cudaMemsetAsync(s->d.sync, 0, (size_t)s->off_phi16_u32 * 4, s->stream);
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(s->d.sync + s->off_nk_u32, 0, ((size_t)s->sync_u32 - s->off_nk_u32 + 1) * 4, s->stream);
     if (e != cudaSuccess || s->n_k2 == 0) return e;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
-    const size_t smem = (size_t)2 * s->K * sizeof(uint32_t);
+    // 8 warps per CTA up to K = 8192 (16 KB histograms), 4 above
+    const int warps = s->Kp > 8192 ? 4 : kK2Warps;
+    const size_t smem = k2_smem(s->K, s->Kp, warps);
     static unsigned long long attr = 0;
     if (attr_once(attr, s->device)) {
-        e = cudaFuncSetAttribute(phi_rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        e = cudaFuncSetAttribute(phi_rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
     }
-    const int per_sm = smem <= 16 * 1024 ? 8 : (smem <= 48 * 1024 ? 4 : 1);
-    const long long grid = std::min<long long>(std::max<long long>(s->n_k2_big, (s->n_k2 - s->n_k2_big + 7) / 8),
-                                               (long long)nsm * per_sm);
-    phi_rebuild_kernel<<<(unsigned)grid, 256, smem, s->stream>>>(s->d.k2items, (int)s->n_k2, (int)s->n_k2_big, s->d.z,
-                                                                  s->d.sync, s->K, s->Kp, s->off_phi16_u32,
-                                                                  s->off_nk_u32, s->d.errs);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_rebuild_kernel, kK2Warps * 32, smem);
+    const long long need = (s->n_k2 + warps - 1) / warps;
+    const long long grid = std::max<long long>(1, std::min<long long>(need, (long long)nsm * std::max(per_sm, 1)));
+    phi_rebuild_kernel<<<(unsigned)grid, kK2Warps * 32, smem, s->stream>>>(
+        s->d.k2items, (int)s->n_k2, s->d.z, s->d.sync, s->K, s->Kp, s->off_phi16_u32, s->off_nk_u32, warps,
+        s->d.sync + s->sync_u32, s->d.errs);
     return cudaGetLastError();
 }
 
@@ -214,49 +248,85 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
             // token-parallel emit (32 < L <= 128, the tokens stay in registers):
             // the first occurrence of each topic (atomicAdd returned 0) writes
             // its entry at its rank = distinct topics below it (word prefix +
-            // popc inside the word) -- no per-bitmap-word loop, no divergence
-            const uint32_t i1 = lane + 32u, i2 = lane + 64u, i3 = lane + 96u;
-            const uint32_t kk[4] = {zf, i1 < L ? zdoc[b + i1] : 0xffffu, i2 < L ? zdoc[b + i2] : 0xffffu,
-                                    i3 < L ? zdoc[b + i3] : 0xffffu};
+            // popc inside the word) -- no per-bitmap-word loop, no divergence.
+            // Only the ncol = ceil(L / 32) register columns the document fills
+            // are touched (warp-uniform).
+            const uint32_t ncol = (L + 31u) >> 5;
+            uint32_t kk[4] = {zf, 0xffffu, 0xffffu, 0xffffu};
+#pragma unroll
+            for (uint32_t j = 1; j < 4; ++j)
+                if (j < ncol && lane + 32u * j < L) kk[j] = zdoc[b + lane + 32u * j];
             bool fst[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t k = kk[j];
+            for (uint32_t j = 0; j < 4; ++j) {
                 fst[j] = false;
-                if (k < (uint32_t)K) {
-                    fst[j] = atomicAdd(&bins[k], 1u) == 0u;
-                    if (fst[j]) atomicOr(&bmp[k >> 5], 1u << (k & 31u));
-                } else if ((uint32_t)lane + 32u * j < L) {
-                    atomicMin(errs + 2, (unsigned long long)d);
+                if (j < ncol) {
+                    const uint32_t k = kk[j];
+                    if (k < (uint32_t)K) {
+                        fst[j] = atomicAdd(&bins[k], 1u) == 0u;
+                        if (fst[j]) atomicOr(&bmp[k >> 5], 1u << (k & 31u));
+                    } else if ((uint32_t)lane + 32u * j < L) {
+                        atomicMin(errs + 2, (unsigned long long)d);
+                    }
                 }
             }
             __syncwarp();
-            uint32_t base = 0;
-            for (int c = 0; c < NW; c += 32) {
-                const int w = c + lane;
-                const uint32_t pc = w < NW ? __popc(bmp[w]) : 0u;
+            if (NW <= 32) {
+                // K <= 1024: lane w holds bitmap word w and the distinct topics
+                // below it in registers; the emit fetches both by shuffle
+                const uint32_t word = lane < NW ? bmp[lane] : 0u;
+                if (lane < NW) bmp[lane] = 0u;
+                const uint32_t pc = __popc(word);
                 uint32_t incl = pc;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const uint32_t y = __shfl_up_sync(kFull, incl, o);
                     if (lane >= o) incl += y;
                 }
-                if (w < NW) wpre[w] = base + incl - pc;
-                base += __shfl_sync(kFull, incl, 31);
-            }
-            nnz = base;
-            __syncwarp();
+                nnz = __shfl_sync(kFull, incl, 31);
+                const uint32_t pre = incl - pc;
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (fst[j]) {
-                    const uint32_t k = kk[j], w = k >> 5;
-                    const uint32_t r = wpre[w] + __popc(bmp[w] & ((1u << (k & 31u)) - 1u));
-                    theta_ent[off + r] = (tpos(k, tm) << 2) | (bins[k] << 16);    // <= 128: no overflow
+                for (uint32_t j = 0; j < 4; ++j) {
+                    if (j < ncol) {
+                        const uint32_t k = kk[j], w = (k >> 5) & 31u;
+                        const uint32_t ww = __shfl_sync(kFull, word, w), pw = __shfl_sync(kFull, pre, w);
+                        if (fst[j])
+                            theta_ent[off + pw + __popc(ww & ((1u << (k & 31u)) - 1u))] =
+                                (tpos(k, tm) << 2) | (bins[k] << 16);     // <= 128: no overflow
+                    }
                 }
-            __syncwarp();
+                __syncwarp();
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (fst[j]) { bins[kk[j]] = 0u; bmp[kk[j] >> 5] = 0u; }
+                for (uint32_t j = 0; j < 4; ++j)
+                    if (j < ncol && fst[j]) bins[kk[j]] = 0u;
+            } else {
+                uint32_t base = 0;
+                for (int c = 0; c < NW; c += 32) {
+                    const int w = c + lane;
+                    const uint32_t pc = w < NW ? __popc(bmp[w]) : 0u;
+                    uint32_t incl = pc;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    if (w < NW) wpre[w] = base + incl - pc;
+                    base += __shfl_sync(kFull, incl, 31);
+                }
+                nnz = base;
+                __syncwarp();
+#pragma unroll
+                for (uint32_t j = 0; j < 4; ++j)
+                    if (j < ncol && fst[j]) {
+                        const uint32_t k = kk[j], w = k >> 5;
+                        const uint32_t r = wpre[w] + __popc(bmp[w] & ((1u << (k & 31u)) - 1u));
+                        theta_ent[off + r] = (tpos(k, tm) << 2) | (bins[k] << 16);    // <= 128: no overflow
+                    }
+                __syncwarp();
+#pragma unroll
+                for (uint32_t j = 0; j < 4; ++j)
+                    if (j < ncol && fst[j]) { bins[kk[j]] = 0u; bmp[kk[j] >> 5] = 0u; }
+            }
             __syncwarp();
         } else {
             auto count = [&](uint32_t k) {

@@ -168,7 +168,8 @@ __global__ void k_slice_emit(int64_t N, int64_t R, const uint32_t* order, const 
 }
 
 // K2 work items (unsorted slice order): one per slice of a u32-column word
-// (atomic when the word has several slices), one per u16-column group
+// (atomic when the word has several slices), one per u16-column group, plus
+// (appended on the host) an empty item per absent u16-column word
 __global__ void k_items_flags(int64_t N, int64_t R, int64_t ng, const uint32_t* srb, const uint32_t* run_group,
                               const int32_t* g_col, uint32_t* flag) {
     GRID_STRIDE(i, N + ng) {
@@ -194,9 +195,6 @@ __global__ void k_items_emit(int64_t N, int64_t R, int64_t ng, int64_t T, const 
     }
 }
 
-struct BigItem {
-    __host__ __device__ bool operator()(const int4& w) const { return w.z - w.y > 32; }
-};
 
 // zdoc positions (heavy-first inside each document)
 __global__ void k_inverse(int64_t T, const uint32_t* dw_tok, uint32_t* inv) { GRID_STRIDE(q, T) inv[dw_tok[q]] = (uint32_t)q; }
@@ -439,7 +437,7 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
         (rc = shard_alloc(&dv.run_start, R + 1, "runs")) || (rc = shard_alloc(&dv.run_dwpos, R, "runs")) || (rc = shard_alloc(&dv.run_rec, R, "runs")) ||
         (rc = shard_alloc(&dv.dw_ptr, D + 1, "dw_ptr")) || (rc = shard_alloc(&dv.zdoc, T, "zdoc")) ||
         (rc = shard_alloc(&dv.theta_ent, cap + 8, "theta")) || (rc = shard_alloc(&dv.theta_meta, D, "theta")) ||
-        (rc = shard_alloc(&dv.sync, s->sync_u32, "phi")) || (rc = shard_alloc(&dv.inv_den, 2 * K, "inv_den")) ||
+        (rc = shard_alloc(&dv.sync, s->sync_u32 + 1, "phi")) || (rc = shard_alloc(&dv.inv_den, 2 * K, "inv_den")) ||
         (rc = shard_alloc(&dv.ll_sum, kLlSlots, "ll")) || (rc = shard_alloc(&dv.errs, 4, "errs")) ||
         (rc = shard_alloc(&dv.bytes, 2, "bytes")))
         return rc;
@@ -598,21 +596,25 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
            "items");
         M = read_u32(st, iflag + N + ng - 1) + read_u32(st, ipos + N + ng - 1);
     }
-    if ((rc = shard_alloc(&dv.k2items, M, "items"))) return rc;
-    int64_t Mbig = 0;
-    if (M > 0) {
-        int4* staged = static_cast<int4*>(sc.get((size_t)M * sizeof(int4)));
-        int* d_nsel = reinterpret_cast<int*>(sc.u32(1));
-        CK(sc.err, "layout scratch");
-        k_items_emit<<<blocks_for(N + ng), 256, 0, st>>>(N, R, ng, T, srb, run_group, dv.run_start, d_gcol, d_gnsl,
-                                                         c.go, iflag, ipos, staged);
-        // CTA items (> 32 tokens) first, warp items after (K2's two loops)
-        CK(cub_call(sc, [&](void* t, size_t& b) {
-               return cub::DevicePartition::If(t, b, staged, dv.k2items, d_nsel, (int)M, BigItem(), st);
-           }),
-           "items");
-        Mbig = read_u32(st, reinterpret_cast<uint32_t*>(d_nsel));
+    // light words absent from this shard still own a 16-bit column: K2 writes
+    // every light column densely (no memset of the light region), so each
+    // absent one gets an empty item that writes its zeros
+    std::vector<int4> zero_items;
+    {
+        std::vector<uint8_t> present((size_t)V, 0);
+        for (int64_t g = 0; g < ng; ++g) present[gw[g]] = 1;
+        for (int32_t v = 0; v < V; ++v)
+            if (!present[v] && s->word_col[v] >= 0) zero_items.push_back(make_int4(s->word_col[v], 0, 0, 0));
     }
+    if ((rc = shard_alloc(&dv.k2items, M + (int64_t)zero_items.size(), "items"))) return rc;
+    if (M > 0)
+        k_items_emit<<<blocks_for(N + ng), 256, 0, st>>>(N, R, ng, T, srb, run_group, dv.run_start, d_gcol, d_gnsl,
+                                                         c.go, iflag, ipos, dv.k2items);
+    if (!zero_items.empty())
+        CK(cudaMemcpyAsync(dv.k2items + M, zero_items.data(), zero_items.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                           st),
+           "items");
+    M += (int64_t)zero_items.size();
     // ---- zdoc positions: heavy-first inside each document ----
     if (T > 0) {
         uint32_t* inv = flag;                 // reuse: [T]
@@ -639,7 +641,6 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
     s->R = R;
     s->n_slices = N;
     s->n_k2 = M;
-    s->n_k2_big = Mbig;
     s->n_ctx = (int64_t)ctx_cols.size();
     s->n_doc_blocks = nblk;
     s->ctx_dirty = true;

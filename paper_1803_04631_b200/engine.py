@@ -64,6 +64,8 @@ class TrainConfig:
         if self.chunks_per_worker != 1:
             raise ValueError("only WorkSchedule1 (M = 1): every configured corpus fits in HBM")
         phi_dtype(self.phi_width)
+        if not 0 <= self.heavy_threshold <= 65535:
+            raise ValueError(f"heavy_threshold {self.heavy_threshold} outside [0, 65535] (16-bit phi columns)")
         if self.phi_sync not in ("nccl", "peer"):
             raise ValueError(f"phi_sync must be 'nccl' or 'peer', not {self.phi_sync!r}")
 
@@ -121,11 +123,15 @@ class Trainer:
             if z0.shape != (self.chunk.token_count,):
                 raise ShapeMismatchError(f"init_assignments has {z0.size} entries, shard has {self.chunk.token_count}")
             self.chunk = replace(self.chunk, assignments=z0)
-        freq = np.bincount(self.chunk.word_ids, minlength=V).astype(np.int64)
-        self.global_freq = self._allreduce_np(freq)
         if device is None:
             device = self._local_device()
         self.device = device
+        if self.world > 1 and self._backend() == "nccl":
+            import torch
+
+            torch.cuda.set_device(device)          # before the first NCCL collective (one GPU per rank)
+        freq = np.bincount(self.chunk.word_ids, minlength=V).astype(np.int64)
+        self.global_freq = self._allreduce_np(freq)
         if shard_factory is None:
             from .shard import DeviceShard
 
@@ -134,7 +140,6 @@ class Trainer:
         if self.world > 1 and self._backend() == "nccl":
             import torch
 
-            torch.cuda.set_device(device)
             stream = torch.cuda.current_stream(device)
         self.shard = shard_factory(K, V, cfg.alpha, cfg.beta, seed=cfg.seed, device=device,
                                    heavy_threshold=cfg.heavy_threshold, global_word_freq=self.global_freq,
@@ -172,7 +177,7 @@ class Trainer:
         import torch
 
         if self._backend() == "nccl":
-            t = torch.as_tensor(arr).cuda()
+            t = torch.as_tensor(arr).to(f"cuda:{self.device}")
             self.dist.all_reduce(t, group=self.group)
             return t.cpu().numpy()
         t = torch.as_tensor(arr).clone()

@@ -50,7 +50,12 @@ def sample_chunk(chunk, phi, theta, ctx, cfg=None, iteration=0, seed=None, devic
 
     if seed is None:
         seed = getattr(cfg, "seed", 0) if cfg is not None else 0
-    with DeviceShard(ctx.num_topics, ctx.vocab_size, ctx.alpha, ctx.beta, seed=seed, device=device) as sh:
+    # the hybrid 16/32-bit phi columns follow the GLOBAL word frequencies (the
+    # column sums of the global phi), not the chunk's own: a chunk-light word
+    # may hold global cells above 65535 when C > 1
+    freq = np.asarray(phi.counts).sum(axis=0, dtype=np.int64)
+    with DeviceShard(ctx.num_topics, ctx.vocab_size, ctx.alpha, ctx.beta, seed=seed, device=device,
+                     global_word_freq=freq) as sh:
         sh.load(chunk)
         sh.set_phi(phi.counts.astype(np.uint32, copy=False), phi.topic_totals)
         sh.set_theta(*_local_theta(theta, chunk))

@@ -89,11 +89,20 @@ class DeviceShard:
         _lib.check(_lib.lib().gf_shard_set_stream(self._h, ctypes.c_void_p(int(handle))))
 
     def load(self, chunk):
+        """Upload a Chunk.  Its group directory may be in any order (e.g. the
+        heavy-first order of sort_word_groups_desc, corpus.py:290-302): the
+        token arrays are word-sorted, so ascending offsets are ascending words
+        and the device builds its own heavy-first schedule."""
         c = chunk
+        go = np.asarray(c.group_offsets, np.int64)
+        order = np.argsort(go, kind="stable") if go.size > 1 and np.any(go[1:] < go[:-1]) else None
+        gw, gs = c.group_words, c.group_sizes
+        if order is not None:
+            gw, go, gs = np.asarray(gw)[order], go[order], np.asarray(gs)[order]
         self._keep = [
             _lib.carr(c.doc_ids, np.int32), _lib.carr(c.word_ids, np.int32),
-            _lib.carr(c.assignments, np.uint16), _lib.carr(c.group_words, np.int32),
-            _lib.carr(c.group_offsets, np.int64), _lib.carr(c.group_sizes, np.int64),
+            _lib.carr(c.assignments, np.uint16), _lib.carr(gw, np.int32),
+            _lib.carr(go, np.int64), _lib.carr(gs, np.int64),
             _lib.carr(c.dw_ptr, np.int64), _lib.carr(c.dw_tok, np.int64),
         ]
         d, w, z, gw, go, gs, dp, dt = self._keep

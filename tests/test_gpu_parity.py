@@ -433,6 +433,39 @@ def test_sample_chunk_api():
     assert np.mean(z1 == want) > 0.998
 
 
+def test_sample_chunk_global_phi_and_heavy_first_directory():
+    """with C > 1 a word that is light in this chunk can hold a
+    GLOBAL phi cell above 65535 (sample_chunk must size the hybrid columns from
+    the global phi), and a chunk in the heavy-first directory order of
+    sort_word_groups_desc (corpus.py:290-302) is a valid input."""
+    K, V = 2, 6
+    r = np.random.default_rng(3)
+    docs, words = [], []
+    for d in range(100):                      # chunk 0: word 0 dominates (140K tokens)
+        docs += [d] * 1410
+        words += [0] * 1400 + list(r.integers(1, V, 10))
+    for d in range(100, 200):                 # chunk 1: word 0 is rare
+        docs += [d] * 30
+        words += [0] * 2 + list(r.integers(1, V, 28))
+    corp = cp.corpus_from_tokens(np.array(docs), np.array(words), V)
+    ch0, ch1 = cp.partition(corp, 2, K, 11)
+    assert ch1.doc_lo == 100
+    ph0 = md.rebuild_phi_replica(ch0, K, V)
+    ph1 = md.rebuild_phi_replica(ch1, K, V)
+    phi = engine.reduce_phi([ph0, ph1])
+    assert phi.counts[:, 0].max() > 65535
+    theta1 = md.rebuild_theta(ch1, K)
+    ctx = sampler.SamplerContext(50.0 / K, 0.01, K, V)
+    z1 = sampler.sample_chunk(ch1, phi, theta1, ctx, iteration=2, seed=5)
+    want = oracle.sample_tokens(K, V, 50.0 / K, 0.01, 5, 2, ch1.doc_ids, ch1.word_ids, ch1.assignments, ch1.doc_lo,
+                                theta1.row_ptr, theta1.topic_ids, theta1.counts, phi.counts, phi.topic_totals,
+                                mode="thin")
+    assert np.mean(z1 == want) > 0.998
+    z2 = sampler.sample_chunk(cp.sort_word_groups_desc(ch1), phi, theta1, ctx, iteration=2, seed=5)
+    np.testing.assert_array_equal(z1, z2)
+    np.testing.assert_array_equal(md.rebuild_theta(cp.sort_word_groups_desc(ch1), K).counts, theta1.counts)
+
+
 def test_two_device_shards_with_summed_sync_buffers_match_one_shard():
     """The multi-GPU protocol on one GPU: two shards (greedy_boundaries, C=2),
     replicas summed elementwise through their int32 sync-buffer views (what the
