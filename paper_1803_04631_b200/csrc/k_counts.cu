@@ -51,77 +51,85 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
     uint32_t* phi16w = sync + off16;                           // packed light columns (u32 words)
     const uint4* zv = reinterpret_cast<const uint4*>(z);
     if (warp < nwarps_per_cta) {
-        while (true) {
-            int it = 0;
-            if (lane == 0) it = (int)atomicAdd(next_item, 1u);
-            it = __shfl_sync(kFull, it, 0);
-            if (it >= n_items) break;
+        // the next item is claimed while the current one is counted
+        int mine = 0;
+        if (lane == 0) mine = (int)atomicAdd(next_item, 1u);
+        int it = __shfl_sync(kFull, mine, 0);
+        while (it < n_items) {
             const int4 w = __ldg(items + it);
+            if (lane == 0) mine = (int)atomicAdd(next_item, 1u);
             const int col = w.x;
-            const uint32_t t0 = (uint32_t)w.y, t1 = (uint32_t)w.z;
-            // ---- count: scalar head / tail, 16-byte body (8 topics per lane, two loads in flight) ----
-            const uint32_t a0 = min(t1, (t0 + 7u) & ~7u), a1 = max(a0, t1 & ~7u);
-            if (t0 + lane < a0) k2_count(bins, z[t0 + lane], K, t0 + lane, errs);
-            if (a1 + lane < t1) k2_count(bins, z[a1 + lane], K, a1 + lane, errs);
-            uint32_t q = (a0 >> 3) + lane;
-            const uint32_t qe = a1 >> 3;
-            for (; q + 32u < qe; q += 64u) {
-                const uint4 v0 = __ldg(zv + q), v1 = __ldg(zv + q + 32u);
-                const uint32_t e[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            // a heavy (32-bit column) item longer than 65535 tokens (one huge
+            // (doc, word) run) is counted and flushed in pieces so no packed
+            // 16-bit bin can carry; a light item is <= 65535 tokens by construction
+            for (uint32_t t0 = (uint32_t)w.y, tend = (uint32_t)w.z;;) {
+                const uint32_t t1 = col >= 0 ? tend : min(tend, t0 + 65528u);
+                // ---- count: scalar head / tail, 16-byte body; four 16-byte loads
+                // per lane in flight (32 topics), then their 32 shared atomics ----
+                const uint32_t a0 = min(t1, (t0 + 7u) & ~7u), a1 = max(a0, t1 & ~7u);
+                if (t0 + lane < a0) k2_count(bins, z[t0 + lane], K, t0 + lane, errs);
+                if (a1 + lane < t1) k2_count(bins, z[a1 + lane], K, a1 + lane, errs);
+                const uint32_t qe = a1 >> 3;
+                for (uint32_t q = (a0 >> 3) + lane; q < qe; q += 128u) {
+                    uint4 v[4];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const uint32_t tb = 8u * (i < 4 ? q : q + 32u) + 2u * (i & 3);
-                    k2_count(bins, e[i] & 0xffffu, K, tb, errs);
-                    k2_count(bins, e[i] >> 16, K, tb + 1u, errs);
+                    for (int i = 0; i < 4; ++i)
+                        if (q + 32u * i < qe) v[i] = __ldg(zv + q + 32u * i);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        if (q + 32u * i < qe) {
+                            const uint32_t e[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+                            const uint32_t tb = 8u * (q + 32u * i);
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                k2_count(bins, e[h] & 0xffffu, K, tb + 2u * h, errs);
+                                k2_count(bins, e[h] >> 16, K, tb + 2u * h + 1u, errs);
+                            }
+                        }
+                    }
                 }
-            }
-            if (q < qe) {
-                const uint4 v0 = __ldg(zv + q);
-                const uint32_t e[4] = {v0.x, v0.y, v0.z, v0.w};
+                __syncwarp();
+                // ---- flush: every packed word once (lane-strided), cleared behind ----
+                if (col >= 0) {
+                    uint32_t* dst = phi16w + (size_t)col * KW;
+                    if (vec_cols) {
+                        for (int j = lane; j < (KW >> 2); j += 32) {
+                            const uint4 b = reinterpret_cast<const uint4*>(bins)[j];
+                            reinterpret_cast<uint4*>(bins)[j] = make_uint4(0u, 0u, 0u, 0u);
+                            reinterpret_cast<uint4*>(dst)[j] = b;
+                            const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    k2_count(bins, e[i] & 0xffffu, K, 8u * q + 2u * i, errs);
-                    k2_count(bins, e[i] >> 16, K, 8u * q + 2u * i + 1u, errs);
-                }
-            }
-            __syncwarp();
-            // ---- flush: every packed word once (lane-strided), cleared behind ----
-            if (col >= 0) {
-                uint32_t* dst = phi16w + (size_t)col * KW;
-                if (vec_cols) {
-                    for (int j = lane; j < (KW >> 2); j += 32) {
-                        const uint4 b = reinterpret_cast<const uint4*>(bins)[j];
-                        reinterpret_cast<uint4*>(bins)[j] = make_uint4(0u, 0u, 0u, 0u);
-                        reinterpret_cast<uint4*>(dst)[j] = b;
-                        const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const uint32_t k = 8u * j + 2u * i;
-                            if (bw[i] & 0xffffu) atomicAdd(&nks[k], bw[i] & 0xffffu);
-                            if (bw[i] >> 16) atomicAdd(&nks[k + 1], bw[i] >> 16);
+                            for (int i = 0; i < 4; ++i) {
+                                const uint32_t k = 8u * j + 2u * i;
+                                if (bw[i] & 0xffffu) atomicAdd(&nks[k], bw[i] & 0xffffu);
+                                if (bw[i] >> 16) atomicAdd(&nks[k + 1], bw[i] >> 16);
+                            }
+                        }
+                    } else {
+                        for (int j = lane; j < KW; j += 32) {
+                            const uint32_t b = bins[j];
+                            bins[j] = 0u;
+                            dst[j] = b;
+                            if (b & 0xffffu) atomicAdd(&nks[2 * j], b & 0xffffu);
+                            if (b >> 16) atomicAdd(&nks[2 * j + 1], b >> 16);
                         }
                     }
                 } else {
+                    uint32_t* dst = sync + (size_t)(~col) * K;
                     for (int j = lane; j < KW; j += 32) {
                         const uint32_t b = bins[j];
+                        if (!b) continue;
                         bins[j] = 0u;
-                        dst[j] = b;
-                        if (b & 0xffffu) atomicAdd(&nks[2 * j], b & 0xffffu);
-                        if (b >> 16) atomicAdd(&nks[2 * j + 1], b >> 16);
+                        const uint32_t k = 2u * j, c0 = b & 0xffffu, c1 = b >> 16;
+                        if (c0) { atomicAdd(&nks[k], c0); atomicAdd(dst + k, c0); }
+                        if (c1) { atomicAdd(&nks[k + 1], c1); atomicAdd(dst + k + 1, c1); }
                     }
                 }
-            } else {
-                uint32_t* dst = sync + (size_t)(~col) * K;
-                for (int j = lane; j < KW; j += 32) {
-                    const uint32_t b = bins[j];
-                    if (!b) continue;
-                    bins[j] = 0u;
-                    const uint32_t k = 2u * j, c0 = b & 0xffffu, c1 = b >> 16;
-                    if (c0) { atomicAdd(&nks[k], c0); atomicAdd(dst + k, c0); }
-                    if (c1) { atomicAdd(&nks[k + 1], c1); atomicAdd(dst + k + 1, c1); }
-                }
+                __syncwarp();
+                if (t1 >= tend) break;
+                t0 = t1;
             }
-            __syncwarp();
+            it = __shfl_sync(kFull, mine, 0);
         }
     }
     __syncthreads();
@@ -245,29 +253,26 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
             }
             nnz = __popc(heads);
         } else if (L <= 128) {
-            // token-parallel emit (32 < L <= 128, the tokens stay in registers):
-            // the first occurrence of each topic (atomicAdd returned 0) writes
-            // its entry at its rank = distinct topics below it (word prefix +
-            // popc inside the word) -- no per-bitmap-word loop, no divergence.
-            // Only the ncol = ceil(L / 32) register columns the document fills
-            // are touched (warp-uniform).
+            // 32 < L <= 128, the tokens stay in registers (ncol = ceil(L / 32)
+            // columns, warp-uniform).  Count: every token adds to its bin and
+            // sets its bitmap bit (no returned values, no branches).  Emit: the
+            // rank of topic k = distinct topics below it = word prefix + popc
+            // inside the word; one token per topic wins atomicExch(bin, 0) (it
+            // gets the count and clears the bin) and writes the entry.
             const uint32_t ncol = (L + 31u) >> 5;
             uint32_t kk[4] = {zf, 0xffffu, 0xffffu, 0xffffu};
 #pragma unroll
             for (uint32_t j = 1; j < 4; ++j)
                 if (j < ncol && lane + 32u * j < L) kk[j] = zdoc[b + lane + 32u * j];
-            bool fst[4];
 #pragma unroll
             for (uint32_t j = 0; j < 4; ++j) {
-                fst[j] = false;
-                if (j < ncol) {
-                    const uint32_t k = kk[j];
-                    if (k < (uint32_t)K) {
-                        fst[j] = atomicAdd(&bins[k], 1u) == 0u;
-                        if (fst[j]) atomicOr(&bmp[k >> 5], 1u << (k & 31u));
-                    } else if ((uint32_t)lane + 32u * j < L) {
-                        atomicMin(errs + 2, (unsigned long long)d);
-                    }
+                const uint32_t k = kk[j];
+                if (j < ncol && k < (uint32_t)K) {
+                    atomicAdd(&bins[k], 1u);
+                    atomicOr(&bmp[k >> 5], 1u << (k & 31u));
+                } else if (j < ncol && k != 0xffffu) {
+                    atomicMin(errs + 2, (unsigned long long)d);
+                    kk[j] = 0xffffu;
                 }
             }
             __syncwarp();
@@ -290,15 +295,12 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
                     if (j < ncol) {
                         const uint32_t k = kk[j], w = (k >> 5) & 31u;
                         const uint32_t ww = __shfl_sync(kFull, word, w), pw = __shfl_sync(kFull, pre, w);
-                        if (fst[j])
+                        const uint32_t c = k < (uint32_t)K ? atomicExch(&bins[k], 0u) : 0u;
+                        if (c)
                             theta_ent[off + pw + __popc(ww & ((1u << (k & 31u)) - 1u))] =
-                                (tpos(k, tm) << 2) | (bins[k] << 16);     // <= 128: no overflow
+                                (tpos(k, tm) << 2) | (c << 16);               // <= 128: no overflow
                     }
                 }
-                __syncwarp();
-#pragma unroll
-                for (uint32_t j = 0; j < 4; ++j)
-                    if (j < ncol && fst[j]) bins[kk[j]] = 0u;
             } else {
                 uint32_t base = 0;
                 for (int c = 0; c < NW; c += 32) {
@@ -316,16 +318,19 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
                 nnz = base;
                 __syncwarp();
 #pragma unroll
-                for (uint32_t j = 0; j < 4; ++j)
-                    if (j < ncol && fst[j]) {
-                        const uint32_t k = kk[j], w = k >> 5;
-                        const uint32_t r = wpre[w] + __popc(bmp[w] & ((1u << (k & 31u)) - 1u));
-                        theta_ent[off + r] = (tpos(k, tm) << 2) | (bins[k] << 16);    // <= 128: no overflow
+                for (uint32_t j = 0; j < 4; ++j) {
+                    const uint32_t k = kk[j];
+                    const uint32_t c = (j < ncol && k < (uint32_t)K) ? atomicExch(&bins[k], 0u) : 0u;
+                    if (c) {
+                        const uint32_t w = k >> 5;
+                        theta_ent[off + wpre[w] + __popc(bmp[w] & ((1u << (k & 31u)) - 1u))] =
+                            (tpos(k, tm) << 2) | (c << 16);                 // <= 128: no overflow
                     }
+                }
                 __syncwarp();
 #pragma unroll
                 for (uint32_t j = 0; j < 4; ++j)
-                    if (j < ncol && fst[j]) { bins[kk[j]] = 0u; bmp[kk[j] >> 5] = 0u; }
+                    if (j < ncol && kk[j] < (uint32_t)K) bmp[kk[j] >> 5] = 0u;
             }
             __syncwarp();
         } else {

@@ -202,7 +202,7 @@ __device__ __forceinline__ bool keep_own(float ut, uint32_t cnt, float alpha, fl
 // call would copy the struct to local memory in every thread)
 // The uniform is word 3 of the last rejected proposal's Philox block, recomputed
 // here so the draw loop keeps no extra register live.
-__device__ __noinline__ uint32_t exact_excluded_draw(int K, float alpha, TPos tm, const float* pstar,
+__device__ __forceinline__ uint32_t exact_excluded_draw(int K, float alpha, TPos tm, const float* pstar,
                                                      const uint32_t* row, uint32_t nnz, uint32_t z, float pex_z,
                                                      uint4 ctr, uint2 key) {
     const float u = u24(philox4x32_10(ctr, key).w);
