@@ -234,9 +234,15 @@ int gf_shard_last_times(gf_shard* shard, float* ms, int num);
 /* ------------------------------------------------------ ptree primitive --
  * ptree.py:116-151 on the device: levels built from a prefix array exactly as
  * build() does (every fanout-th boundary), then a warp-ballot descent per u
- * returning the minimal index with prefix > u (ties go right). */
+ * returning the minimal index with prefix > u (ties go right): replaces
+ * PrefixTree.sample / sample_many / sample_with_stats (ptree.py:64-113).
+ * visited_out / widest_out (may be NULL) receive _descend's (levels visited,
+ * widest scan) per u (ptree.py:73-99).  _f64 is the fp64 tree mode
+ * (build(..., dtype=np.float64), ptree.py:119-121). */
 int gf_ptree_sample(int device, const float* prefix, int64_t n, int32_t fanout, const float* u,
-                    int64_t m, int64_t* idx_out);
+                    int64_t m, int64_t* idx_out, int32_t* visited_out, int32_t* widest_out);
+int gf_ptree_sample_f64(int device, const double* prefix, int64_t n, int32_t fanout, const double* u,
+                        int64_t m, int64_t* idx_out, int32_t* visited_out, int32_t* widest_out);
 
 /* ------------------------------------------------- synthetic corpora --
  * Not in the reference (no datasets offline): seeded LDA-generative corpora

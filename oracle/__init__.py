@@ -88,6 +88,37 @@ def _c(a, dtype):
 
 
 # ---------------------------------------------------------------- rng.py ----
+def ptree_levels(weights, fanout, dtype):
+    """ptree.py:116-136: level 0 = left-to-right cumsum in `dtype`, each level
+    above keeps every fanout-th boundary (clamped to the last)."""
+    levels = [np.cumsum(np.asarray(weights).astype(dtype, copy=False), dtype=dtype)]
+    while len(levels[-1]) > 1:
+        prev = levels[-1]
+        tails = np.minimum(np.arange(fanout - 1, len(prev) + fanout - 1, fanout), len(prev) - 1)
+        levels.append(prev[tails])
+    return levels
+
+
+def ptree_descend(levels, fanout, u):
+    """ptree.py:77-99 as a plain loop (small cases only): (index, levels
+    visited, widest scan) -- the first child whose boundary exceeds u, else
+    the last child."""
+    u = levels[0].dtype.type(u)
+    idx = visited = widest = 0
+    for level in range(len(levels) - 2, -1, -1):
+        bounds = levels[level]
+        lo = idx * fanout
+        hi = min(lo + fanout, len(bounds))
+        idx = hi - 1
+        for j in range(lo, hi):
+            if bounds[j] > u:
+                idx = j
+                break
+        visited += 1
+        widest = max(widest, hi - lo)
+    return idx, visited, widest
+
+
 def stream_key(*parts):
     """rng.py:45-53 (mix64 over uint64-masked parts)."""
     arr = np.array([p & 0xFFFFFFFFFFFFFFFF for p in parts], dtype=np.uint64)

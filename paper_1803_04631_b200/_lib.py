@@ -76,7 +76,8 @@ SIGNATURES = {
     "gf_shard_stats": (_int, [_p, _p, _int]),
     "gf_shard_reset_stats": (_int, [_p]),
     "gf_shard_last_times": (_int, [_p, _p, _int]),
-    "gf_ptree_sample": (_int, [_int, _p, _i64, _i32, _p, _i64, _p]),
+    "gf_ptree_sample": (_int, [_int, _p, _i64, _i32, _p, _i64, _p, _p, _p]),
+    "gf_ptree_sample_f64": (_int, [_int, _p, _i64, _i32, _p, _i64, _p, _p, _p]),
     "gf_uci_scan": (_int, [ctypes.c_char_p, _p, _p]),
     "gf_uci_tokens": (_int, [ctypes.c_char_p, _i64, _p, _p, _p]),
     "gf_synth_lengths": (_int, [_u64, _i64, _i64, _f64, _f64, _p]),

@@ -808,32 +808,56 @@ int gf_shard_reset_stats(gf_shard* s) {
 }
 
 // -------------------------------------------------------------- ptree ------
-int gf_ptree_sample(int device, const float* prefix, int64_t n, int32_t fanout, const float* u, int64_t m,
-                    int64_t* idx_out) {
-    if (fanout < 2 || fanout > 32) return fail(GF_ERR_VALUE, "fanout must be in [2, 32], got %d", fanout);
+}  // extern "C"
+
+namespace {
+template <typename T, typename Launch>
+int ptree_sample_any(int device, const T* prefix, int64_t n, int32_t fanout, const T* u, int64_t m,
+                     int64_t* idx_out, int32_t* visited_out, int32_t* widest_out, Launch launch) {
+    if (fanout < 2) return fail(GF_ERR_VALUE, "fanout must be >= 2, got %d", fanout);
     if (n < 1) return fail(GF_ERR_EMPTY, "weights must be a non-empty 1-d array");
-    const float total = prefix[n - 1];
-    if (!(total > 0.f)) return fail(GF_ERR_EMPTY, "cannot sample: total weight is zero");
+    const T total = prefix[n - 1];
+    if (!(total > T(0))) return fail(GF_ERR_EMPTY, "cannot sample: total weight is zero");
     for (int64_t i = 0; i < m; ++i)
-        if (!(u[i] >= 0.f) || !(u[i] < total)) return fail(GF_ERR_VALUE, "u values outside [0, total)");
+        if (!(u[i] >= T(0)) || !(u[i] < total)) return fail(GF_ERR_VALUE, "u values outside [0, total)");
     int ndev = 0;
     gf_device_count(&ndev);
     if (ndev == 0) return fail(GF_ERR_NODEVICE, "no CUDA device visible");
     CU(cudaSetDevice(device), "cudaSetDevice");
-    float *dp = nullptr, *du = nullptr;
+    const int64_t mm = std::max<int64_t>(m, 1);
+    T *dp = nullptr, *du = nullptr;
     int64_t* di = nullptr;
-    CU(cudaMalloc(&dp, n * 4), "ptree");
-    CU(cudaMalloc(&du, std::max<int64_t>(m, 1) * 4), "ptree");
-    CU(cudaMalloc(&di, std::max<int64_t>(m, 1) * 8), "ptree");
-    cudaMemcpy(dp, prefix, n * 4, cudaMemcpyHostToDevice);
-    if (m) cudaMemcpy(du, u, m * 4, cudaMemcpyHostToDevice);
-    cudaError_t e = gf::ptree_sample(dp, n, fanout, du, m, di, 0);
+    int32_t* ds = nullptr;  // [visited | widest]
+    cudaError_t e = cudaMalloc(&dp, n * sizeof(T));
+    if (e == cudaSuccess) e = cudaMalloc(&du, mm * sizeof(T));
+    if (e == cudaSuccess) e = cudaMalloc(&di, mm * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&ds, mm * 8);
+    if (e == cudaSuccess) e = cudaMemcpy(dp, prefix, n * sizeof(T), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && m) e = cudaMemcpy(du, u, m * sizeof(T), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch(dp, n, fanout, du, m, di, ds, ds + mm, (cudaStream_t)0);
     if (e == cudaSuccess && m) e = cudaMemcpy(idx_out, di, m * 8, cudaMemcpyDeviceToHost);
-    cudaFree(dp);
-    cudaFree(du);
-    cudaFree(di);
+    if (e == cudaSuccess && m && visited_out) e = cudaMemcpy(visited_out, ds, m * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && m && widest_out) e = cudaMemcpy(widest_out, ds + mm, m * 4, cudaMemcpyDeviceToHost);
+    if (dp) cudaFree(dp);
+    if (du) cudaFree(du);
+    if (di) cudaFree(di);
+    if (ds) cudaFree(ds);
     if (e != cudaSuccess) return cuda_fail(e, "ptree_sample");
     return GF_OK;
+}
+}  // namespace
+
+extern "C" {
+int gf_ptree_sample(int device, const float* prefix, int64_t n, int32_t fanout, const float* u, int64_t m,
+                    int64_t* idx_out, int32_t* visited_out, int32_t* widest_out) {
+    return ptree_sample_any<float>(device, prefix, n, fanout, u, m, idx_out, visited_out, widest_out,
+                                   gf::ptree_sample);
+}
+
+int gf_ptree_sample_f64(int device, const double* prefix, int64_t n, int32_t fanout, const double* u, int64_t m,
+                        int64_t* idx_out, int32_t* visited_out, int32_t* widest_out) {
+    return ptree_sample_any<double>(device, prefix, n, fanout, u, m, idx_out, visited_out, widest_out,
+                                    gf::ptree_sample_f64);
 }
 
 }  // extern "C"

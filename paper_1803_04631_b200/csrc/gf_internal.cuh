@@ -163,7 +163,7 @@ int partition_to_host(int device, const int32_t* doc_ids, const int32_t* word_id
                       int32_t* gw, int64_t* go, int64_t* gs, int64_t* ng_out, int64_t* dw_ptr, int64_t* dw_tok);
 }  // namespace gf
 
-// kernel launchers (k_sample.cu / k_counts.cu / k_ptree.cu)
+// kernel launchers (k_sample.cu / k_counts.cu)
 namespace gf {
 cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only = 0);
 cudaError_t launch_sample_range(gf_shard* s, uint32_t iteration, int eval_only, int64_t slice0, int64_t n);
@@ -183,5 +183,7 @@ cudaError_t launch_validate(gf_shard* s);
 size_t sample_smem_bytes(const gf_shard* s);
 size_t context_floats(const gf_shard* s);
 cudaError_t ptree_sample(const float* d_prefix, int64_t n, int fanout, const float* d_u, int64_t m,
-                         int64_t* d_idx, cudaStream_t st);
+                         int64_t* d_idx, int32_t* d_visited, int32_t* d_widest, cudaStream_t st);
+cudaError_t ptree_sample_f64(const double* d_prefix, int64_t n, int fanout, const double* d_u, int64_t m,
+                             int64_t* d_idx, int32_t* d_visited, int32_t* d_widest, cudaStream_t st);
 }  // namespace gf

@@ -634,32 +634,53 @@ cudaError_t launch_phi_import(gf_shard* s, const uint32_t* d_in, const int32_t* 
 }
 
 // ------------------------------------------------------ ptree primitive ------
-__global__ void ptree_level_kernel(const float* prev, long long prev_len, float* next, long long len, int F) {
+// ptree.py:116-136 levels (every F-th boundary of the level below) and the
+// _descend of ptree.py:77-99 as a warp ballot per u, in fp32 (the device
+// precision) or fp64 (the reference's oracle mode, ptree.py:119-121).  The
+// optional stats are sample_with_stats' (levels visited, widest scan).
+template <typename T>
+__global__ void ptree_level_kernel(const T* prev, long long prev_len, T* next, long long len, int F) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < len) next[i] = prev[min((long long)F * i + F - 1, prev_len - 1)];
 }
 
-__global__ void ptree_sample_kernel(const float* levels, const long long* off, const long long* len, int nlev, int F,
-                                    const float* __restrict__ u, long long m, int64_t* out) {
+template <typename T>
+__global__ void ptree_sample_kernel(const T* levels, const long long* off, const long long* len, int nlev, int F,
+                                    const T* __restrict__ u, long long m, int64_t* out, int32_t* visited,
+                                    int32_t* widest) {
     const int lane = threadIdx.x & 31;
     const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     for (long long q = w; q < m; q += nw) {
-        const float uu = u[q];
+        const T uu = u[q];
         long long idx = 0;
-        for (int l = nlev - 1; l >= 0; --l) {
+        int wide = 0;
+        for (int l = nlev - 2; l >= 0; --l) {            // the root level holds one entry: start below it
             const long long lo = idx * F;
             const int n = (int)min((long long)F, len[l] - lo);
-            const bool ok = lane < n && levels[off[l] + lo + lane] > uu;
-            const unsigned b = __ballot_sync(kFull, ok);
-            idx = b ? lo + __ffs(b) - 1 : lo + n - 1;   // last child bounds u from above
+            long long hit = lo + n - 1;                  // last child bounds u from above
+            for (int c = 0; c < n; c += 32) {            // fanouts above 32: one ballot per 32 children
+                const bool ok = c + lane < n && levels[off[l] + lo + c + lane] > uu;
+                const unsigned b = __ballot_sync(kFull, ok);
+                if (b) {
+                    hit = lo + c + __ffs(b) - 1;
+                    break;
+                }
+            }
+            idx = hit;
+            wide = max(wide, n);
         }
-        if (lane == 0) out[q] = idx;
+        if (lane == 0) {
+            out[q] = idx;
+            if (visited) visited[q] = nlev - 1;
+            if (widest) widest[q] = wide;
+        }
     }
 }
 
-cudaError_t ptree_sample(const float* d_prefix, int64_t n, int F, const float* d_u, int64_t m, int64_t* d_idx,
-                         cudaStream_t st) {
+template <typename T>
+cudaError_t ptree_sample_t(const T* d_prefix, int64_t n, int F, const T* d_u, int64_t m, int64_t* d_idx,
+                           int32_t* d_visited, int32_t* d_widest, cudaStream_t st) {
     std::vector<long long> off{0}, len{n};
     long long total = n;
     while (len.back() > 1) {
@@ -668,27 +689,46 @@ cudaError_t ptree_sample(const float* d_prefix, int64_t n, int F, const float* d
         len.push_back(l);
         total += l;
     }
-    float* lv = nullptr;
+    T* lv = nullptr;
     long long* dmeta = nullptr;
-    cudaError_t e = cudaMalloc(&lv, sizeof(float) * total);
+    cudaError_t e = cudaMalloc(&lv, sizeof(T) * total);
     if (e != cudaSuccess) return e;
     e = cudaMalloc(&dmeta, sizeof(long long) * 2 * off.size());
-    if (e != cudaSuccess) { cudaFree(lv); return e; }
-    cudaMemcpyAsync(lv, d_prefix, sizeof(float) * n, cudaMemcpyDeviceToDevice, st);
-    for (size_t l = 1; l < off.size(); ++l)
-        ptree_level_kernel<<<(unsigned)((len[l] + 255) / 256), 256, 0, st>>>(lv + off[l - 1], len[l - 1], lv + off[l],
-                                                                          len[l], F);
-    cudaMemcpyAsync(dmeta, off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(dmeta + off.size(), len.data(), sizeof(long long) * len.size(), cudaMemcpyHostToDevice, st);
-    const long long blocks = std::min<long long>((m + 7) / 8, 4096);
-    if (m > 0)
-        ptree_sample_kernel<<<(unsigned)blocks, 256, 0, st>>>(lv, dmeta, dmeta + off.size(), (int)off.size(), F, d_u, m,
-                                                            d_idx);
-    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(lv, d_prefix, sizeof(T) * n, cudaMemcpyDeviceToDevice, st);
+    for (size_t l = 1; e == cudaSuccess && l < off.size(); ++l) {
+        ptree_level_kernel<T><<<(unsigned)((len[l] + 255) / 256), 256, 0, st>>>(lv + off[l - 1], len[l - 1],
+                                                                               lv + off[l], len[l], F);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dmeta, off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dmeta + off.size(), len.data(), sizeof(long long) * len.size(), cudaMemcpyHostToDevice,
+                            st);
+    if (e == cudaSuccess && m > 0) {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const long long blocks = std::min<long long>((m + 7) / 8, 8LL * std::max(sms, 1));
+        ptree_sample_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(lv, dmeta, dmeta + off.size(), (int)off.size(), F,
+                                                                d_u, m, d_idx, d_visited, d_widest);
+        e = cudaGetLastError();
+    }
+    const cudaError_t es = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = es;
     cudaFree(lv);
-    cudaFree(dmeta);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    if (dmeta) cudaFree(dmeta);
+    return e;
+}
+
+cudaError_t ptree_sample(const float* d_prefix, int64_t n, int F, const float* d_u, int64_t m, int64_t* d_idx,
+                         int32_t* d_visited, int32_t* d_widest, cudaStream_t st) {
+    return ptree_sample_t<float>(d_prefix, n, F, d_u, m, d_idx, d_visited, d_widest, st);
+}
+
+cudaError_t ptree_sample_f64(const double* d_prefix, int64_t n, int F, const double* d_u, int64_t m, int64_t* d_idx,
+                             int32_t* d_visited, int32_t* d_widest, cudaStream_t st) {
+    return ptree_sample_t<double>(d_prefix, n, F, d_u, m, d_idx, d_visited, d_widest, st);
 }
 
 }  // namespace gf

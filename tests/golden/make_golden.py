@@ -15,6 +15,8 @@ What is captured (each block names the reference function it exercises):
   counts.npz     rebuild_theta / concat_theta / rebuild_phi_replica  model.py:109-161
   messages.json  CountOverflowError / ConservationReport texts       model.py:91-225
   ptree.npz      ptree.build levels + sample / sample_many indices   ptree.py:116-151
+  ptree_api.npz  sample_with_stats, fp64 trees, fanouts > 32,
+                 sample_total_and_draw in fp64                      ptree.py:54-151
 """
 
 import json
@@ -261,9 +263,49 @@ def main():
     pz["meta"] = json.dumps(pmeta)
     np.savez_compressed(os.path.join(HERE, "ptree.npz"), **pz)
 
+    ptree_api(pt, rng)
     stores(cp, md)
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))
+
+
+def ptree_api(pt=None, rng=None):
+    """The rest of the PrefixTree surface (ptree.py:54-151): per-u descent
+    stats, the fp64 oracle mode, fanouts wider than one warp ballot."""
+    if pt is None:
+        _, _, pt, rng, _ = import_reference()
+    r = np.random.default_rng(19)
+    pz, meta = {}, []
+    cases = [(np.float32, 2), (np.float32, 8), (np.float32, 32), (np.float32, 64), (np.float32, 100),
+             (np.float64, 2), (np.float64, 8), (np.float64, 32), (np.float64, 50)]
+    for i, (dt, fanout) in enumerate(cases):
+        nleaf = int(r.integers(1, 5000))
+        w = r.random(nleaf)
+        w[r.random(nleaf) < 0.25] = 0.0
+        if w.sum() == 0:
+            w[0] = 1.0
+        tree = pt.build(w, fanout=fanout, dtype=dt)
+        top = tree.levels[-1][0]
+        us = np.minimum((r.random(80) * tree.total).astype(dt), np.nextafter(top, dt(0)))
+        stats = [tree.sample_with_stats(u) for u in us]
+        pz[f"a{i}__w"] = w
+        pz[f"a{i}__u"] = us
+        pz[f"a{i}__idx"] = np.array([x[0] for x in stats], np.int64)
+        pz[f"a{i}__visited"] = np.array([x[1] for x in stats], np.int32)
+        pz[f"a{i}__widest"] = np.array([x[2] for x in stats], np.int32)
+        pz[f"a{i}__prefix_before"] = np.array([tree.prefix_before(j) for j in range(0, nleaf, 97)], dt)
+        for lvl in range(len(tree.levels)):
+            pz[f"a{i}__sums{lvl}"] = tree.level_sums(lvl)
+        meta.append({"i": i, "dtype": np.dtype(dt).name, "fanout": fanout, "height": tree.height, "n": nleaf})
+    w = r.random(300)
+    tree = pt.build(w, fanout=4, dtype=np.float64)
+    st = rng.Stream(77, 3)
+    draws = [pt.sample_total_and_draw(tree, st) for _ in range(200)]
+    pz["draw64__w"] = w
+    pz["draw64__idx"] = np.array([d[0] for d in draws], np.int64)
+    pz["draw64__u"] = np.array([d[1] for d in draws], np.float64)
+    pz["meta"] = json.dumps(meta)
+    np.savez_compressed(os.path.join(HERE, "ptree_api.npz"), **pz)
 
 
 def stores(cp=None, md=None):
@@ -307,5 +349,7 @@ def stores(cp=None, md=None):
 if __name__ == "__main__":
     if sys.argv[1:] == ["--stores-only"]:
         stores()
+    elif sys.argv[1:] == ["--ptree-api-only"]:
+        ptree_api()
     else:
         main()

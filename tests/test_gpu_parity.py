@@ -152,6 +152,38 @@ def test_device_tree_search_matches_reference():
             np.testing.assert_array_equal(a, b)
 
 
+def test_device_tree_api_matches_reference():
+    """sample_with_stats (index, visited, widest), fp64 trees and fanouts > 32
+    on the device against the reference's outputs (ptree_api.npz)."""
+    from paper_1803_04631_b200 import rng
+
+    g = np.load(os.path.join(GOLD, "ptree_api.npz"))
+    for m in json.loads(str(g["meta"])):
+        i = m["i"]
+        tree = ptree.build(g[f"a{i}__w"], fanout=m["fanout"], dtype=np.dtype(m["dtype"]))
+        us = g[f"a{i}__u"]
+        np.testing.assert_array_equal(tree.sample_many(us), g[f"a{i}__idx"])
+        for j in range(0, len(us), 9):
+            assert tree.sample_with_stats(us[j]) == (g[f"a{i}__idx"][j], g[f"a{i}__visited"][j],
+                                                     g[f"a{i}__widest"][j])
+    tree = ptree.build(g["draw64__w"], fanout=4, dtype=np.float64)
+    st = rng.Stream(77, 3)
+    draws = [ptree.sample_total_and_draw(tree, st) for _ in range(len(g["draw64__idx"]))]
+    np.testing.assert_array_equal([d[0] for d in draws], g["draw64__idx"])
+    np.testing.assert_array_equal([d[1] for d in draws], g["draw64__u"])
+    # fp32 replay of the reference's own Stream(2024) draws (ptree.npz)
+    g32 = np.load(os.path.join(GOLD, "ptree.npz"))
+    tree = ptree.build(g32["draw__w"], fanout=2)
+    st = rng.Stream(2024)
+    draws = [ptree.sample_total_and_draw(tree, st) for _ in range(len(g32["draw__idx"]))]
+    np.testing.assert_array_equal([d[0] for d in draws], g32["draw__idx"])
+    np.testing.assert_array_equal([d[1] for d in draws], g32["draw__u"])
+    with pytest.raises(errors.EmptyDistributionError):
+        ptree.sample_total_and_draw(ptree.build([0.0, 0.0], 2), rng.Stream(0))
+    with pytest.raises(ValueError):
+        ptree.build([1.0, 2.0], 2).sample(3.5)
+
+
 def test_device_tree_zero_leaves_never_drawn():
     tree = ptree.build(np.array([0.0, 1.0, 0.0, 2.0, 0.0], np.float32), fanout=2)
     us = (np.random.default_rng(1).random(20000) * tree.total).astype(np.float32)
@@ -444,7 +476,7 @@ def test_sample_chunk_global_phi_and_heavy_first_directory():
     for d in range(100):                      # chunk 0: word 0 dominates (140K tokens)
         docs += [d] * 1410
         words += [0] * 1400 + list(r.integers(1, V, 10))
-    for d in range(100, 200):                 # chunk 1: word 0 is rare
+    for d in range(100, 4800):                # chunk 1 (same token count): word 0 is rare
         docs += [d] * 30
         words += [0] * 2 + list(r.integers(1, V, 28))
     corp = cp.corpus_from_tokens(np.array(docs), np.array(words), V)

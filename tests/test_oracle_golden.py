@@ -201,6 +201,35 @@ def test_ptree_golden_is_sequential_scan():
         np.testing.assert_array_equal(idx, g[f"t{i}__idx_many"])
 
 
+def test_ptree_api_golden():
+    """ptree.py:54-151 (sample_with_stats, level_sums, prefix_before, fp64 mode,
+    fanouts > 32, sample_total_and_draw) against the reference's own outputs;
+    the host-side levels of the repo's build() match too."""
+    from paper_1803_04631_b200 import ptree
+
+    g = load("ptree_api.npz")
+    for m in json.loads(str(g["meta"])):
+        i, dt, F = m["i"], np.dtype(m["dtype"]), m["fanout"]
+        levels = oracle.ptree_levels(g[f"a{i}__w"], F, dt)
+        tree = ptree.build(g[f"a{i}__w"], fanout=F, dtype=dt)
+        assert tree.height == m["height"] == len(levels) - 1
+        for lvl in range(len(levels)):
+            np.testing.assert_array_equal(tree.level_sums(lvl), g[f"a{i}__sums{lvl}"])
+            np.testing.assert_array_equal(tree.levels[lvl], levels[lvl])
+        np.testing.assert_array_equal([tree.prefix_before(j) for j in range(0, m["n"], 97)],
+                                      g[f"a{i}__prefix_before"])
+        got = [oracle.ptree_descend(levels, F, u) for u in g[f"a{i}__u"]]
+        np.testing.assert_array_equal([x[0] for x in got], g[f"a{i}__idx"])
+        np.testing.assert_array_equal([x[1] for x in got], g[f"a{i}__visited"])
+        np.testing.assert_array_equal([x[2] for x in got], g[f"a{i}__widest"])
+    # fp64 sample_total_and_draw: u = Stream.uniform() * total (ptree.py:139-151)
+    w = g["draw64__w"]
+    levels = oracle.ptree_levels(w, 4, np.float64)
+    us = oracle.stream_uniforms((77, 3), len(g["draw64__u"])) * float(levels[0][-1])
+    np.testing.assert_array_equal(us, g["draw64__u"])
+    np.testing.assert_array_equal([oracle.ptree_descend(levels, 4, u)[0] for u in us], g["draw64__idx"])
+
+
 # ------------------------------------------------------------ sampler ------
 def test_spec_sample_dense_example():
     # SPEC.md:255: K=2, theta_d=[1,0], phi_.v=[1,1], totals=[2,2], a=0.5, b=0.1, V=3 -> [0.75, 0.25]
