@@ -100,6 +100,11 @@ int gf_shard_create(gf_shard** out, int device, int32_t num_topics, int32_t voca
 int gf_shard_destroy(gf_shard* shard);
 /* run every kernel / copy of this shard on `cuda_stream` (a cudaStream_t) */
 int gf_shard_set_stream(gf_shard* shard, void* cuda_stream);
+/* Change the Dirichlet hyper-parameters and the Philox key of a loaded shard
+ * (SamplerContext alpha / beta, TrainConfig.seed) without rebuilding it: the
+ * next sample recomputes the word contexts.  Lets a caller that hands the same
+ * Chunk to sampler.sample_chunk repeatedly keep one resident shard. */
+int gf_shard_set_params(gf_shard* shard, double alpha, double beta, uint64_t seed);
 /* global word frequencies (length V), identical on every rank: fixes the
  * hybrid phi layout so replicas can be summed elementwise.  Optional on one GPU
  * (defaults to the shard's own frequencies at load). */
@@ -215,6 +220,11 @@ int gf_shard_set_theta(gf_shard* shard, const int64_t* row_ptr, const uint16_t* 
  * from the sync buffer (replica after rebuild_phi, global after the sync). */
 int gf_shard_get_phi(gf_shard* shard, uint32_t* counts_kv, int64_t* topic_totals);
 int gf_shard_set_phi(gf_shard* shard, const uint32_t* counts_kv, const int64_t* topic_totals);
+/* the same for a PhiMatrix of either width (16: uint16 cells; the export
+ * raises the reference's 16-bit overflow text for the argmax cell first,
+ * model.py:152-157, and narrows on the device) */
+int gf_shard_get_phi_w(gf_shard* shard, void* counts_kv, int32_t phi_width, int64_t* topic_totals);
+int gf_shard_set_phi_w(gf_shard* shard, const void* counts_kv, int32_t phi_width, const int64_t* topic_totals);
 /* model.py:152-157: max cell count and its first (row-major K x V) position */
 int gf_shard_phi_argmax(gf_shard* shard, int64_t* max_count, int32_t* topic, int32_t* word);
 
@@ -230,6 +240,38 @@ int gf_shard_reset_stats(gf_shard* shard);
  * beside it on an internal stream), [2] prepare (+ word contexts), [3] theta
  * rebuild time not hidden behind [1] + [2]. */
 int gf_shard_last_times(gf_shard* shard, float* ms, int num);
+
+/* ------------------------------------------------- K5 conservation --
+ * check_conservation (model.py:180-225) as device reductions.
+ * report = {code, index, a, b}: 0 ok; 1 theta row `index` (global doc) sums
+ * to a, its document length is b; 2 topic `index`: theta column sum a != n_k
+ * b; 3 topic `index`: phi row sum a != n_k b; 4 totals sum to a, the corpus
+ * has b tokens.  The host turns the report into the reference's text.
+ * On a shard: stage 1 sums theta rows / columns and phi rows of the resident
+ * state and returns the row report; a multi-rank caller then sums the theta
+ * column sums over ranks in place (gf_shard_conservation_buffer: K uint64 on
+ * the device); stage 2 compares against n_k and num_tokens. */
+int gf_shard_conservation(gf_shard* shard, int stage, int64_t num_tokens, int64_t* report);
+int gf_shard_conservation_buffer(gf_shard* shard, void** theta_col_sums, int64_t* num_topics);
+/* The same check over the reference's exported arrays (ThetaRows CSR,
+ * PhiMatrix K x V of phi_width bits, corpus doc lengths) uploaded to `device`;
+ * report[0..3] is the row report, report[4..7] the column / phi / total one. */
+int gf_check_conservation(int device, int32_t K, int64_t V, int64_t D, const int64_t* row_ptr,
+                          const uint16_t* topic_ids, const uint16_t* counts, const int64_t* doc_lengths,
+                          const void* phi_counts, int32_t phi_width, const int64_t* topic_totals,
+                          int64_t num_tokens, int64_t* report);
+
+/* ------------------------------------------------------ GFSNAP1 store --
+ * save_snapshot / load_snapshot (model.py:228-296): native streaming writer
+ * and reader of the reference's byte layout (bad magic / width:
+ * GF_ERR_FORMAT with the reference's texts).  header: {K, V, D, NNZ,
+ * phi_width, metadata bytes}; read fills caller-sized arrays. */
+int gf_snapshot_write(const char* path, int64_t K, int64_t V, int64_t D, int64_t nnz, int32_t phi_width,
+                      const void* phi_counts, const int64_t* topic_totals, const int64_t* row_ptr,
+                      const uint16_t* topic_ids, const uint16_t* counts, const char* meta, int64_t meta_len);
+int gf_snapshot_header(const char* path, int64_t* header_out);
+int gf_snapshot_read(const char* path, void* phi_counts, int64_t* topic_totals, int64_t* row_ptr,
+                     uint16_t* topic_ids, uint16_t* counts, char* meta);
 
 /* ------------------------------------------------------ ptree primitive --
  * ptree.py:116-151 on the device: levels built from a prefix array exactly as

@@ -41,6 +41,7 @@ SIGNATURES = {
     "gf_shard_create": (_int, [_pp, _int, _i32, _i32, _f64, _f64, _u64, _u32]),
     "gf_shard_destroy": (_int, [_p]),
     "gf_shard_set_stream": (_int, [_p, _p]),
+    "gf_shard_set_params": (_int, [_p, _f64, _f64, _u64]),
     "gf_shard_set_vocab": (_int, [_p, _p]),
     "gf_shard_load": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _p]),
     "gf_shard_rebuild_phi": (_int, [_p]),
@@ -72,10 +73,19 @@ SIGNATURES = {
     "gf_shard_set_theta": (_int, [_p, _p, _p, _p]),
     "gf_shard_get_phi": (_int, [_p, _p, _p]),
     "gf_shard_set_phi": (_int, [_p, _p, _p]),
+    "gf_shard_get_phi_w": (_int, [_p, _p, _i32, _p]),
+    "gf_shard_set_phi_w": (_int, [_p, _p, _i32, _p]),
     "gf_shard_phi_argmax": (_int, [_p, _p, _p, _p]),
     "gf_shard_stats": (_int, [_p, _p, _int]),
     "gf_shard_reset_stats": (_int, [_p]),
     "gf_shard_last_times": (_int, [_p, _p, _int]),
+    "gf_shard_conservation": (_int, [_p, _int, _i64, _p]),
+    "gf_shard_conservation_buffer": (_int, [_p, _pp, _p]),
+    "gf_check_conservation": (_int, [_int, _i32, _i64, _i64] + [_p] * 5 + [_i32, _p, _i64, _p]),
+    "gf_snapshot_write": (_int, [ctypes.c_char_p, _i64, _i64, _i64, _i64, _i32] + [_p] * 5
+                          + [ctypes.c_char_p, _i64]),
+    "gf_snapshot_header": (_int, [ctypes.c_char_p, _p]),
+    "gf_snapshot_read": (_int, [ctypes.c_char_p] + [_p] * 6),
     "gf_ptree_sample": (_int, [_int, _p, _i64, _i32, _p, _i64, _p, _p, _p]),
     "gf_ptree_sample_f64": (_int, [_int, _p, _i64, _i32, _p, _i64, _p, _p, _p]),
     "gf_uci_scan": (_int, [ctypes.c_char_p, _p, _p]),

@@ -85,7 +85,7 @@ void free_dev(gf_shard* s) {
     auto& d = s->d;
     void* ptrs[] = {d.z, d.zstage, d.run_doc, d.run_start, d.slices, d.k2items, d.dw_ptr, d.zdoc, d.run_dwpos, d.run_rec, d.theta_ent,
                     d.theta_meta, d.sync, d.inv_den, d.ctx_tab, d.ctx_cols, d.slice_ctx, d.ll_part, d.ll_sum,
-                    d.errs, d.bytes, d.scratch};
+                    d.errs, d.bytes, d.scratch, d.k5};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     d = gf::ShardDev{};
@@ -307,6 +307,26 @@ int gf_shard_set_stream(gf_shard* s, void* st) {
     if (s->own_stream && s->stream) { cudaStreamSynchronize(s->stream); cudaStreamDestroy(s->stream); }
     s->stream = (cudaStream_t)st;
     s->own_stream = false;
+    return GF_OK;
+}
+
+int gf_shard_set_params(gf_shard* s, double alpha, double beta, uint64_t seed) {
+    if (!(alpha > 0) || !(beta > 0)) return fail(GF_ERR_VALUE, "alpha and beta must be > 0");
+    if (alpha != s->alpha || beta != s->beta) s->ctx_dirty = true;   // denominators and contexts follow
+    if (alpha != s->alpha && s->loaded && s->D > 0) {
+        // the loglik constant sum_d L_d log(L_d + K a) follows alpha
+        std::vector<uint32_t> dwp((size_t)s->D + 1);
+        CU(cudaMemcpy(dwp.data(), s->d.dw_ptr, dwp.size() * 4, cudaMemcpyDeviceToHost), "set_params");
+        double llc = 0.0;
+        for (int64_t d = 0; d < s->D; ++d) {
+            const double L = (double)(dwp[d + 1] - dwp[d]);
+            if (L > 0) llc += L * std::log(L + (double)s->K * alpha);
+        }
+        s->ll_const = llc;
+    }
+    s->alpha = alpha;
+    s->beta = beta;
+    s->seed = seed;
     return GF_OK;
 }
 
@@ -666,81 +686,156 @@ int gf_shard_get_theta(gf_shard* s, int64_t* row_ptr, uint16_t* ids, uint16_t* c
 }
 
 int gf_shard_set_theta(gf_shard* s, const int64_t* row_ptr, const uint16_t* ids, const uint16_t* cnts) {
+    // upload, then validate on the device (theta_validate_kernel: capacity,
+    // ids < K, nonzero counts, strictly increasing ids) before importing
     if (int rc = need_loaded(s)) return rc;
-    std::vector<uint2> meta;
-    if (int rc = fetch_meta(s, meta)) return rc;
-    for (int64_t d = 0; d < s->D; ++d) {
-        const int64_t n = row_ptr[d + 1] - row_ptr[d];
-        const uint32_t next = d + 1 < s->D ? meta[d + 1].x : (uint32_t)s->theta_cap;
-        if (n < 0 || n > (int64_t)(next - meta[d].x))
-            return fail(GF_ERR_SHAPE, "theta row %lld has %lld entries, capacity %u", (long long)d, (long long)n,
-                        next - meta[d].x);
-        for (int64_t j = row_ptr[d]; j < row_ptr[d + 1]; ++j) {
-            if (ids[j] >= s->K || cnts[j] == 0) return fail(GF_ERR_SHAPE, "theta row %lld: bad entry", (long long)d);
-            if (j > row_ptr[d] && ids[j] <= ids[j - 1])
-                return fail(GF_ERR_SHAPE, "theta row %lld: topic ids not strictly increasing", (long long)d);
-        }
-    }
     const int64_t nnz = row_ptr[s->D];
-    int64_t* drp = nullptr;
-    uint16_t* dids = nullptr;
-    CU(cudaMalloc(&drp, (s->D + 1) * 8), "set_theta");
-    CU(cudaMalloc(&dids, std::max<int64_t>(nnz, 1) * 4), "set_theta");
-    uint16_t* dcnt = dids + std::max<int64_t>(nnz, 1);
-    cudaMemcpyAsync(drp, row_ptr, (s->D + 1) * 8, cudaMemcpyHostToDevice, s->stream);
-    if (nnz) cudaMemcpyAsync(dids, ids, nnz * 2, cudaMemcpyHostToDevice, s->stream);
-    if (nnz) cudaMemcpyAsync(dcnt, cnts, nnz * 2, cudaMemcpyHostToDevice, s->stream);
-    cudaError_t e = gf::launch_theta_import(s, drp, dids, dcnt);
+    if (nnz < 0) return fail(GF_ERR_SHAPE, "theta row_ptr is not non-decreasing");
+    const int64_t nn = std::max<int64_t>(nnz, 1);
+    char* base = nullptr;
+    const size_t b_rp = ((s->D + 1) * 8 + 15) & ~(size_t)15, b_e = ((size_t)nn * 2 + 15) & ~(size_t)15;
+    CU(cudaMalloc(&base, b_rp + 2 * b_e + 16), "set_theta");
+    int64_t* drp = reinterpret_cast<int64_t*>(base);
+    uint16_t* dids = reinterpret_cast<uint16_t*>(base + b_rp);
+    uint16_t* dcnt = reinterpret_cast<uint16_t*>(base + b_rp + b_e);
+    unsigned long long* dfirst = reinterpret_cast<unsigned long long*>(base + b_rp + 2 * b_e);
+    unsigned long long first = ~0ull;
+    cudaError_t e = cudaMemcpyAsync(drp, row_ptr, (s->D + 1) * 8, cudaMemcpyHostToDevice, s->stream);
+    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(dids, ids, nnz * 2, cudaMemcpyHostToDevice, s->stream);
+    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(dcnt, cnts, nnz * 2, cudaMemcpyHostToDevice, s->stream);
+    if (e == cudaSuccess) e = gf::launch_theta_validate(s, drp, dids, dcnt, dfirst);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&first, dfirst, 8, cudaMemcpyDeviceToHost, s->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
-    cudaFree(drp);
-    cudaFree(dids);
+    if (e == cudaSuccess && first != ~0ull) {
+        cudaFree(base);
+        const long long d = (long long)(first >> 34);
+        const uint64_t low = first & ((1ull << 34) - 1);
+        if (low == 0) {
+            std::vector<uint2> meta;
+            if (int rc = fetch_meta(s, meta)) return rc;
+            const uint32_t next = d + 1 < s->D ? meta[d + 1].x : (uint32_t)s->theta_cap;
+            return fail(GF_ERR_SHAPE, "theta row %lld has %lld entries, capacity %u", d,
+                        (long long)(row_ptr[d + 1] - row_ptr[d]), next - meta[d].x);
+        }
+        if ((low & 1) == 0) return fail(GF_ERR_SHAPE, "theta row %lld: bad entry", d);
+        return fail(GF_ERR_SHAPE, "theta row %lld: topic ids not strictly increasing", d);
+    }
+    if (e == cudaSuccess) e = gf::launch_theta_import(s, drp, dids, dcnt);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    cudaFree(base);
     if (e != cudaSuccess) return cuda_fail(e, "set_theta");
     s->stale_theta = true;
     return GF_OK;
 }
 
-int gf_shard_get_phi(gf_shard* s, uint32_t* counts_kv, int64_t* totals) {
+// K x V export into a device buffer (u32) plus the device argmax: the phi
+// checks and the 16-bit narrowing run before anything crosses PCIe
+static int phi_export_device(gf_shard* s, uint32_t** dout, int32_t** dcol) {
+    const size_t cells = (size_t)s->K * s->V;
+    *dout = nullptr;
+    *dcol = nullptr;
+    CU(cudaMalloc(dout, cells * 4 + 16), "phi export");
+    cudaError_t e = cudaMalloc(dcol, (size_t)s->V * 4);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(*dcol, s->word_col.data(), (size_t)s->V * 4, cudaMemcpyHostToDevice, s->stream);
+    if (e == cudaSuccess) e = gf::launch_phi_export(s, *dout, 32, *dcol);
+    if (e != cudaSuccess) {
+        cudaFree(*dout);
+        if (*dcol) cudaFree(*dcol);
+        return cuda_fail(e, "phi export");
+    }
+    return GF_OK;
+}
+
+static int phi_argmax_device(gf_shard* s, uint32_t* dout, int64_t* max_count, int32_t* topic, int32_t* word) {
+    const size_t cells = (size_t)s->K * s->V;
+    unsigned int* dmax = reinterpret_cast<unsigned int*>(dout + cells);
+    unsigned long long* dfirst = reinterpret_cast<unsigned long long*>(dout + ((cells + 3) & ~(size_t)1));
+    unsigned int mx = 0;
+    unsigned long long first = 0;
+    CU(gf::launch_phi_argmax(dout, (int64_t)cells, dmax, dfirst, s->stream), "phi_argmax");
+    CU(cudaMemcpyAsync(&mx, dmax, 4, cudaMemcpyDeviceToHost, s->stream), "phi_argmax");
+    CU(cudaMemcpyAsync(&first, dfirst, 8, cudaMemcpyDeviceToHost, s->stream), "phi_argmax");
+    CU(cudaStreamSynchronize(s->stream), "phi_argmax");
+    if (cells == 0) first = 0;
+    *max_count = mx;
+    *topic = (int32_t)(first / s->V);
+    *word = (int32_t)(first % s->V);
+    return GF_OK;
+}
+
+int gf_shard_get_phi_w(gf_shard* s, void* counts_kv, int32_t width, int64_t* totals) {
     if (int rc = need_loaded(s)) return rc;
+    if (width != 16 && width != 32) return fail(GF_ERR_VALUE, "phi width must be 16 or 32, got %d", width);
     const size_t cells = (size_t)s->K * s->V;
     uint32_t* dout = nullptr;
     int32_t* dcol = nullptr;
-    CU(cudaMalloc(&dout, cells * 4), "get_phi");
-    CU(cudaMalloc(&dcol, (size_t)s->V * 4), "get_phi");
+    if (int rc = phi_export_device(s, &dout, &dcol)) return rc;
+    int rc = GF_OK;
+    if (width == 16) {                        // model.py:152-157: the argmax cell must fit 16 bits
+        int64_t m = 0;
+        int32_t k = 0, v = 0;
+        rc = phi_argmax_device(s, dout, &m, &k, &v);
+        if (rc == GF_OK && m > 65535)
+            rc = fail(GF_ERR_OVERFLOW, "phi cell (topic %d, word %d) count %lld exceeds 16-bit range", k, v,
+                      (long long)m);
+        if (rc == GF_OK) {                   // narrow on the device: half the PCIe bytes
+            cudaError_t e = gf::launch_phi_export(s, dout, 16, dcol);
+            if (e != cudaSuccess) rc = cuda_fail(e, "get_phi");
+        }
+    }
     std::vector<uint32_t> nk((size_t)s->K);
-    cudaMemcpyAsync(dcol, s->word_col.data(), (size_t)s->V * 4, cudaMemcpyHostToDevice, s->stream);
-    cudaError_t e = gf::launch_phi_export(s, dout, dcol);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(counts_kv, dout, cells * 4, cudaMemcpyDeviceToHost, s->stream);
-    if (e == cudaSuccess)
+    cudaError_t e = cudaSuccess;
+    if (rc == GF_OK) e = cudaMemcpyAsync(counts_kv, dout, cells * (width / 8), cudaMemcpyDeviceToHost, s->stream);
+    if (rc == GF_OK && e == cudaSuccess)
         e = cudaMemcpyAsync(nk.data(), s->d.sync + s->off_nk_u32, (size_t)s->K * 4, cudaMemcpyDeviceToHost, s->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    if (rc == GF_OK && e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     cudaFree(dout);
     cudaFree(dcol);
+    if (rc != GF_OK) return rc;
     if (e != cudaSuccess) return cuda_fail(e, "get_phi");
     for (int k = 0; k < s->K; ++k) totals[k] = nk[k];
     return GF_OK;
 }
 
-int gf_shard_set_phi(gf_shard* s, const uint32_t* counts_kv, const int64_t* totals) {
+int gf_shard_get_phi(gf_shard* s, uint32_t* counts_kv, int64_t* totals) {
+    return gf_shard_get_phi_w(s, counts_kv, 32, totals);
+}
+
+int gf_shard_set_phi_w(gf_shard* s, const void* counts_kv, int32_t width, const int64_t* totals) {
     if (int rc = need_loaded(s)) return rc;
-    for (int v = 0; v < s->V; ++v)
-        if (s->word_col[v] >= 0)
-            for (int k = 0; k < s->K; ++k)
-                if (counts_kv[(size_t)k * s->V + v] > 65535u)
-                    return fail(GF_ERR_OVERFLOW, "phi cell (topic %d, word %d) count %u exceeds its 16-bit column", k, v,
-                                counts_kv[(size_t)k * s->V + v]);
+    if (width != 16 && width != 32) return fail(GF_ERR_VALUE, "phi width must be 16 or 32, got %d", width);
     for (int k = 0; k < s->K; ++k)
         if (totals[k] < 0 || totals[k] > (int64_t)UINT32_MAX) return fail(GF_ERR_OVERFLOW, "topic total out of range");
     const size_t cells = (size_t)s->K * s->V;
-    uint32_t* din = nullptr;
+    void* din = nullptr;
     int32_t* dcol = nullptr;
-    CU(cudaMalloc(&din, cells * 4), "set_phi");
-    CU(cudaMalloc(&dcol, (size_t)s->V * 4), "set_phi");
+    CU(cudaMalloc(&din, cells * (width / 8) + 16), "set_phi");
+    cudaError_t e = cudaMalloc(&dcol, (size_t)s->V * 4 + 32);
+    if (e != cudaSuccess) { cudaFree(din); return cuda_fail(e, "set_phi"); }
+    unsigned long long* dfirst = reinterpret_cast<unsigned long long*>(dcol + ((s->V + 3) & ~3));
     std::vector<uint32_t> nk((size_t)s->K);
     for (int k = 0; k < s->K; ++k) nk[k] = (uint32_t)totals[k];
-    cudaMemsetAsync(s->d.sync, 0, s->sync_u32 * 4, s->stream);
-    cudaMemcpyAsync(dcol, s->word_col.data(), (size_t)s->V * 4, cudaMemcpyHostToDevice, s->stream);
-    cudaMemcpyAsync(din, counts_kv, cells * 4, cudaMemcpyHostToDevice, s->stream);
-    cudaError_t e = gf::launch_phi_import(s, din, dcol);
+    unsigned long long first = ~0ull;
+    e = cudaMemcpyAsync(dcol, s->word_col.data(), (size_t)s->V * 4, cudaMemcpyHostToDevice, s->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(din, counts_kv, cells * (width / 8), cudaMemcpyHostToDevice, s->stream);
+    // a light (16-bit) column must not receive a cell above 65535: checked on the
+    // device before anything is written (first cell in word-major order)
+    if (width == 32) {
+        if (e == cudaSuccess)
+            e = gf::launch_phi_u16_overflow((const uint32_t*)din, dcol, s->K, s->V, dfirst, s->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&first, dfirst, 8, cudaMemcpyDeviceToHost, s->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+        if (e == cudaSuccess && first != ~0ull) {
+            cudaFree(din);
+            cudaFree(dcol);
+            const int v = (int)(first / s->K), k = (int)(first % s->K);
+            return fail(GF_ERR_OVERFLOW, "phi cell (topic %d, word %d) count %u exceeds its 16-bit column", k, v,
+                        ((const uint32_t*)counts_kv)[(size_t)k * s->V + v]);
+        }
+    }
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->d.sync, 0, s->sync_u32 * 4, s->stream);
+    if (e == cudaSuccess) e = gf::launch_phi_import(s, din, width, dcol);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(s->d.sync + s->off_nk_u32, nk.data(), (size_t)s->K * 4, cudaMemcpyHostToDevice, s->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
@@ -752,17 +847,91 @@ int gf_shard_set_phi(gf_shard* s, const uint32_t* counts_kv, const int64_t* tota
     return GF_OK;
 }
 
+int gf_shard_set_phi(gf_shard* s, const uint32_t* counts_kv, const int64_t* totals) {
+    return gf_shard_set_phi_w(s, counts_kv, 32, totals);
+}
+
 int gf_shard_phi_argmax(gf_shard* s, int64_t* max_count, int32_t* topic, int32_t* word) {
+    // np.argmax of the exported K x V counts (model.py:152-157), reduced on the
+    // device: the export stays in HBM, 12 bytes come back
     if (int rc = need_loaded(s)) return rc;
-    std::vector<uint32_t> kv((size_t)s->K * s->V);
-    std::vector<int64_t> tot((size_t)s->K);
-    if (int rc = gf_shard_get_phi(s, kv.data(), tot.data())) return rc;
-    size_t best = 0;
-    for (size_t i = 1; i < kv.size(); ++i)
-        if (kv[i] > kv[best]) best = i;
-    *max_count = kv.empty() ? 0 : kv[best];
-    *topic = (int32_t)(best / s->V);
-    *word = (int32_t)(best % s->V);
+    uint32_t* dout = nullptr;
+    int32_t* dcol = nullptr;
+    if (int rc = phi_export_device(s, &dout, &dcol)) return rc;
+    const int rc = phi_argmax_device(s, dout, max_count, topic, word);
+    cudaFree(dout);
+    cudaFree(dcol);
+    return rc;
+}
+
+// ------------------------------------------------- K5 conservation ------
+static int k5_scratch(gf_shard* s) {
+    if (!s->d.k5) CU(cudaMalloc(&s->d.k5, (2 * (size_t)s->K + 1 + 8) * 8), "conservation");
+    return GF_OK;
+}
+
+int gf_shard_conservation(gf_shard* s, int stage, int64_t num_tokens, int64_t* report) {
+    if (int rc = need_loaded(s)) return rc;
+    if (stage != 1 && stage != 2) return fail(GF_ERR_VALUE, "conservation stage must be 1 or 2, got %d", stage);
+    if (int rc = k5_scratch(s)) return rc;
+    int64_t* drep = reinterpret_cast<int64_t*>(s->d.k5 + 2 * (size_t)s->K + 1);
+    if (stage == 1) CU(gf::launch_conservation_stage1(s, s->d.k5, drep), "conservation");
+    else CU(gf::launch_conservation_stage2(s, s->d.k5, num_tokens, drep), "conservation");
+    CU(cudaMemcpyAsync(report, drep, 32, cudaMemcpyDeviceToHost, s->stream), "conservation");
+    CU(cudaStreamSynchronize(s->stream), "conservation");
+    return GF_OK;
+}
+
+int gf_shard_conservation_buffer(gf_shard* s, void** theta_col, int64_t* n) {
+    if (int rc = need_loaded(s)) return rc;
+    if (int rc = k5_scratch(s)) return rc;
+    *theta_col = s->d.k5;
+    *n = s->K;
+    return GF_OK;
+}
+
+int gf_check_conservation(int device, int32_t K, int64_t V, int64_t D, const int64_t* row_ptr,
+                          const uint16_t* topic_ids, const uint16_t* counts, const int64_t* doc_lengths,
+                          const void* phi_counts, int32_t phi_width, const int64_t* topic_totals, int64_t num_tokens,
+                          int64_t* report) {
+    if (K < 1 || V < 0 || D < 0) return fail(GF_ERR_VALUE, "bad conservation dimensions");
+    if (phi_width != 16 && phi_width != 32) return fail(GF_ERR_VALUE, "phi width must be 16 or 32, got %d", phi_width);
+    int ndev = 0;
+    gf_device_count(&ndev);
+    if (ndev == 0) return fail(GF_ERR_NODEVICE, "no CUDA device visible");
+    CU(cudaSetDevice(device), "cudaSetDevice");
+    const int64_t nnz = row_ptr[D];
+    const size_t b_rp = (D + 1) * 8, b_ids = std::max<int64_t>(nnz, 1) * 2, b_len = std::max<int64_t>(D, 1) * 8;
+    const size_t b_phi = std::max<size_t>((size_t)K * V * (phi_width / 8), 4), b_tot = (size_t)K * 8;
+    const size_t b_k5 = (2 * (size_t)K + 1) * 8 + 64;
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t total = al(b_rp) + 2 * al(b_ids) + al(b_len) + al(b_phi) + al(b_tot) + al(b_k5);
+    char* base = nullptr;
+    CU(cudaMalloc(&base, total), "check_conservation");
+    char* p = base;
+    auto take = [&](size_t b) { char* q = p; p += al(b); return q; };
+    int64_t* drp = (int64_t*)take(b_rp);
+    uint16_t* dids = (uint16_t*)take(b_ids);
+    uint16_t* dcnt = (uint16_t*)take(b_ids);
+    int64_t* dlen = (int64_t*)take(b_len);
+    void* dphi = take(b_phi);
+    int64_t* dtot = (int64_t*)take(b_tot);
+    unsigned long long* dk5 = (unsigned long long*)take(b_k5);
+    int64_t* drep = reinterpret_cast<int64_t*>(dk5 + 2 * (size_t)K + 1);
+    cudaStream_t st = 0;
+    cudaError_t e = cudaMemcpyAsync(drp, row_ptr, b_rp, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(dids, topic_ids, nnz * 2, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(dcnt, counts, nnz * 2, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && D) e = cudaMemcpyAsync(dlen, doc_lengths, D * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && K * V)
+        e = cudaMemcpyAsync(dphi, phi_counts, (size_t)K * V * (phi_width / 8), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dtot, topic_totals, b_tot, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = gf::conservation_csr(K, V, D, drp, dids, dcnt, dlen, dphi, phi_width, dtot, num_tokens, dk5, drep, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(report, drep, 64, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(base);
+    if (e != cudaSuccess) return cuda_fail(e, "check_conservation");
     return GF_OK;
 }
 

@@ -65,6 +65,8 @@ struct ShardDev {
     unsigned long long* bytes = nullptr;     // [0] sum over runs of nnz (sampler bytes model), [1] import flag
     uint32_t* scratch = nullptr;             // export staging
     size_t scratch_bytes = 0;
+    unsigned long long* k5 = nullptr;        // K5 conservation: [K] theta column sums | [K] phi row sums |
+                                             // first bad doc | report (int64 x 4); allocated on first use
 };
 
 constexpr int kMaxPeers = 8;                 // ranks of one NVLink/NVSwitch node
@@ -137,6 +139,17 @@ inline bool attr_once(unsigned long long& done, int device) {
     return true;
 }
 int shard_fail(int code, const char* fmt, ...);
+// streaming multiprocessors of `device` (grid sizing; cached per device)
+inline int sm_count(int device) {
+    static int cache[64] = {0};
+    int& c = cache[device & 63];
+    if (!c) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n < 1) n = 1;
+        c = n;
+    }
+    return c;
+}
 int shard_cuda_fail(cudaError_t e, const char* what);
 int shard_set_layout(gf_shard* s);
 int64_t shard_env_int(const char* name, int64_t dflt);
@@ -177,11 +190,24 @@ cudaError_t launch_ll_reduce(gf_shard* s);
 cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt);
 cudaError_t launch_theta_import(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids,
                                 const uint16_t* d_cnt);
-cudaError_t launch_phi_export(gf_shard* s, uint32_t* d_out_kv, const int32_t* d_word_col);
-cudaError_t launch_phi_import(gf_shard* s, const uint32_t* d_in_kv, const int32_t* d_word_col);
+cudaError_t launch_theta_validate(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids, const uint16_t* d_cnt,
+                                  unsigned long long* d_first);
+cudaError_t launch_phi_export(gf_shard* s, void* d_out_kv, int width, const int32_t* d_word_col);
+cudaError_t launch_phi_import(gf_shard* s, const void* d_in_kv, int width, const int32_t* d_word_col);
 cudaError_t launch_validate(gf_shard* s);
 size_t sample_smem_bytes(const gf_shard* s);
 size_t context_floats(const gf_shard* s);
+// K5 + device phi checks (k_check.cu)
+cudaError_t launch_conservation_stage1(gf_shard* s, unsigned long long* scratch, int64_t* d_report);
+cudaError_t launch_conservation_stage2(gf_shard* s, const unsigned long long* scratch, int64_t T, int64_t* d_report);
+cudaError_t conservation_csr(int K, int64_t V, int64_t D, const int64_t* row_ptr, const uint16_t* ids,
+                             const uint16_t* cnt, const int64_t* doc_len, const void* phi, int width,
+                             const int64_t* totals, int64_t T, unsigned long long* scratch, int64_t* d_report,
+                             cudaStream_t st);
+cudaError_t launch_phi_u16_overflow(const uint32_t* d_kv, const int32_t* d_wcol, int K, int64_t V,
+                                    unsigned long long* d_first, cudaStream_t st);
+cudaError_t launch_phi_argmax(const uint32_t* d_kv, int64_t n, unsigned int* d_max, unsigned long long* d_first,
+                              cudaStream_t st);
 cudaError_t ptree_sample(const float* d_prefix, int64_t n, int fanout, const float* d_u, int64_t m,
                          int64_t* d_idx, int32_t* d_visited, int32_t* d_widest, cudaStream_t st);
 cudaError_t ptree_sample_f64(const double* d_prefix, int64_t n, int fanout, const double* d_u, int64_t m,

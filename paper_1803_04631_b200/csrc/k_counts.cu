@@ -44,7 +44,8 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
     uint32_t* nks = sh;                                       // [K] this CTA's n_k
     uint32_t* bins = sh + ((K + 3) & ~3) + (size_t)warp * ((KW + 3) & ~3);
     for (int i = threadIdx.x; i < K; i += blockDim.x) nks[i] = 0u;
-    for (int i = lane; i < KW; i += 32) bins[i] = 0u;
+    if (warp < nwarps_per_cta)                                // only these warps own a histogram
+        for (int i = lane; i < KW; i += 32) bins[i] = 0u;
     __syncthreads();
     // 16-byte column stores need a 16-byte aligned packed column
     const bool vec_cols = (KW & 3) == 0 && (off16 & 3) == 0;
@@ -151,8 +152,7 @@ cudaError_t launch_phi_rebuild(gf_shard* s) {
     if (e == cudaSuccess)
         e = cudaMemsetAsync(s->d.sync + s->off_nk_u32, 0, ((size_t)s->sync_u32 - s->off_nk_u32 + 1) * 4, s->stream);
     if (e != cudaSuccess || s->n_k2 == 0) return e;
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
+    const int nsm = sm_count(s->device);
     // 8 warps per CTA up to K = 8192 (16 KB histograms), 4 above
     const int warps = s->Kp > 8192 ? 4 : kK2Warps;
     const size_t smem = k2_smem(s->K, s->Kp, warps);
@@ -406,8 +406,8 @@ cudaError_t launch_theta_rebuild(gf_shard* s, cudaStream_t st) {
     // persistent grid (exactly the resident CTAs): the warps sweep the
     // documents as one contiguous moving window, so the word-major z sectors
     // they gather are shared by neighbouring documents while still in L2
-    int nsm = 148, per_sm = 1;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
+    const int nsm = sm_count(s->device);
+    int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, theta_rebuild_kernel, wpc * 32, smem);
     const long long need = (s->D + wpc - 1) / wpc;
     const long long grid = std::min<long long>(need, (long long)nsm * std::max(per_sm, 1));
@@ -477,15 +477,15 @@ cudaError_t launch_import_staged(gf_shard* s) {
     unsigned int* any = reinterpret_cast<unsigned int*>(s->d.bytes + 1);
     cudaError_t e = cudaMemsetAsync(any, 0, 4, s->stream);
     if (e != cudaSuccess) return e;
-    staged_diff_kernel<<<148 * 8, 256, 0, s->stream>>>((long long)s->T, s->d.zstage, s->d.z, any);
-    import_staged_gate<<<148 * 8, 256, 0, s->stream>>>((long long)s->R, s->d.run_start, s->d.run_dwpos, s->d.zstage,
+    staged_diff_kernel<<<sm_count(s->device) * 8, 256, 0, s->stream>>>((long long)s->T, s->d.zstage, s->d.z, any);
+    import_staged_gate<<<sm_count(s->device) * 8, 256, 0, s->stream>>>((long long)s->R, s->d.run_start, s->d.run_dwpos, s->d.zstage,
                                                        s->d.z, s->d.zdoc, any);
     return cudaGetLastError();
 }
 
 cudaError_t launch_zdoc_sync(gf_shard* s) {
     if (s->R == 0) return cudaSuccess;
-    zdoc_sync_kernel<<<148 * 8, 256, 0, s->stream>>>((long long)s->R, s->d.run_start, s->d.run_dwpos, s->d.z,
+    zdoc_sync_kernel<<<sm_count(s->device) * 8, 256, 0, s->stream>>>((long long)s->R, s->d.run_start, s->d.run_dwpos, s->d.z,
                                                      s->d.zdoc);
     return cudaGetLastError();
 }
@@ -562,24 +562,68 @@ __global__ void theta_import_kernel(int D, uint2* meta, uint32_t* ent, const int
     }
 }
 
+// set_theta's checks on the device, before anything is written: a row longer
+// than its fixed capacity, a topic id >= K or a zero count, topic ids not
+// strictly increasing.  first = min over failures of
+//   d << 34 | (capacity ? 0 : (j - row start + 1) << 1 | (kind: 0 bad entry, 1 order))
+// i.e. the first document, and inside it the first entry the host loop
+// (gf_shard_set_theta) would have stopped at.
+__global__ void theta_validate_kernel(int D, const uint2* __restrict__ meta, uint32_t cap,
+                                      const int64_t* __restrict__ rowptr, const uint16_t* __restrict__ ids,
+                                      const uint16_t* __restrict__ cnt, int K, unsigned long long* first) {
+    const int lane = threadIdx.x & 31;
+    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long d = w; d < D; d += nw) {
+        const int64_t o = rowptr[d], n = rowptr[d + 1] - o;
+        const uint32_t room = (d + 1 < D ? meta[d + 1].x : cap) - meta[d].x;
+        if (n < 0 || n > (int64_t)room) {
+            if (lane == 0) atomicMin(first, (unsigned long long)d << 34);
+            continue;
+        }
+        for (int64_t j = lane; j < n; j += 32) {
+            const uint32_t t = ids[o + j];
+            int kind = -1;
+            if (t >= (uint32_t)K || cnt[o + j] == 0) kind = 0;
+            else if (j > 0 && t <= ids[o + j - 1]) kind = 1;
+            if (kind >= 0)
+                atomicMin(first, ((unsigned long long)d << 34) | ((unsigned long long)(j + 1) << 1) | (unsigned)kind);
+        }
+    }
+}
+
+cudaError_t launch_theta_validate(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids, const uint16_t* d_cnt,
+                                  unsigned long long* d_first) {
+    cudaError_t e = cudaMemsetAsync(d_first, 0xff, 8, s->stream);
+    if (e != cudaSuccess || s->D == 0) return e;
+    const int nsm = sm_count(s->device);
+    theta_validate_kernel<<<8 * nsm, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, (uint32_t)s->theta_cap,
+                                                          d_rowptr, d_ids, d_cnt, s->K, d_first);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt) {
     if (s->D == 0) return cudaSuccess;
-    theta_export_kernel<<<1184, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, s->d.theta_ent, d_rowptr, d_ids,
+    const int nsm = sm_count(s->device);
+    theta_export_kernel<<<8 * nsm, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, s->d.theta_ent, d_rowptr, d_ids,
                                                      d_cnt, tpos_geom(s->K));
     return cudaGetLastError();
 }
 
 cudaError_t launch_theta_import(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids, const uint16_t* d_cnt) {
     if (s->D == 0) return cudaSuccess;
-    theta_import_kernel<<<1184, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, s->d.theta_ent, d_rowptr, d_ids,
+    const int nsm = sm_count(s->device);
+    theta_import_kernel<<<8 * nsm, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, s->d.theta_ent, d_rowptr, d_ids,
                                                      d_cnt, tpos_geom(s->K));
     return cudaGetLastError();
 }
 
 // ----------------------------------------------------------- phi export ------
-// word-major columns <-> reference K x V row-major, 32x32 tiles through smem
+// word-major columns <-> reference K x V row-major (u32, or u16 for a 16-bit
+// PhiMatrix), 32x32 tiles through smem
+template <typename T>
 __global__ void phi_export_kernel(const uint32_t* __restrict__ sync, long long off16, const int32_t* __restrict__ wcol,
-                                  int K, int Kp, int V, uint32_t* out) {
+                                  int K, int Kp, int V, T* out) {
     __shared__ uint32_t tile[32][33];
     const int v0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
     const uint16_t* phi16 = reinterpret_cast<const uint16_t*>(sync + off16);
@@ -595,18 +639,19 @@ __global__ void phi_export_kernel(const uint32_t* __restrict__ sync, long long o
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int k = k0 + r, v = v0 + threadIdx.x;
-        if (k < K && v < V) out[(size_t)k * V + v] = tile[threadIdx.x][r];
+        if (k < K && v < V) out[(size_t)k * V + v] = (T)tile[threadIdx.x][r];   // u16: checked <= 65535 first
     }
 }
 
+template <typename T>
 __global__ void phi_import_kernel(uint32_t* sync, long long off16, const int32_t* __restrict__ wcol, int K, int Kp,
-                                  int V, const uint32_t* __restrict__ in) {
+                                  int V, const T* __restrict__ in) {
     __shared__ uint32_t tile[32][33];
     const int v0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
     uint16_t* phi16 = reinterpret_cast<uint16_t*>(sync + off16);
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int k = k0 + r, v = v0 + threadIdx.x;
-        tile[threadIdx.x][r] = (k < K && v < V) ? in[(size_t)k * V + v] : 0u;
+        tile[threadIdx.x][r] = (k < K && v < V) ? (uint32_t)in[(size_t)k * V + v] : 0u;
     }
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -619,17 +664,25 @@ __global__ void phi_import_kernel(uint32_t* sync, long long off16, const int32_t
     }
 }
 
-cudaError_t launch_phi_export(gf_shard* s, uint32_t* d_out, const int32_t* d_wcol) {
+cudaError_t launch_phi_export(gf_shard* s, void* d_out, int width, const int32_t* d_wcol) {
     dim3 grid((s->V + 31) / 32, (s->K + 31) / 32);
-    phi_export_kernel<<<grid, dim3(32, 8), 0, s->stream>>>(s->d.sync, s->off_phi16_u32, d_wcol, s->K, s->Kp, s->V,
-                                                            d_out);
+    if (width == 16)
+        phi_export_kernel<uint16_t><<<grid, dim3(32, 8), 0, s->stream>>>(s->d.sync, s->off_phi16_u32, d_wcol, s->K,
+                                                                        s->Kp, s->V, (uint16_t*)d_out);
+    else
+        phi_export_kernel<uint32_t><<<grid, dim3(32, 8), 0, s->stream>>>(s->d.sync, s->off_phi16_u32, d_wcol, s->K,
+                                                                        s->Kp, s->V, (uint32_t*)d_out);
     return cudaGetLastError();
 }
 
-cudaError_t launch_phi_import(gf_shard* s, const uint32_t* d_in, const int32_t* d_wcol) {
+cudaError_t launch_phi_import(gf_shard* s, const void* d_in, int width, const int32_t* d_wcol) {
     dim3 grid((s->V + 31) / 32, (s->K + 31) / 32);
-    phi_import_kernel<<<grid, dim3(32, 8), 0, s->stream>>>(s->d.sync, s->off_phi16_u32, d_wcol, s->K, s->Kp, s->V,
-                                                            d_in);
+    if (width == 16)
+        phi_import_kernel<uint16_t><<<grid, dim3(32, 8), 0, s->stream>>>(s->d.sync, s->off_phi16_u32, d_wcol, s->K,
+                                                                        s->Kp, s->V, (const uint16_t*)d_in);
+    else
+        phi_import_kernel<uint32_t><<<grid, dim3(32, 8), 0, s->stream>>>(s->d.sync, s->off_phi16_u32, d_wcol, s->K,
+                                                                        s->Kp, s->V, (const uint32_t*)d_in);
     return cudaGetLastError();
 }
 

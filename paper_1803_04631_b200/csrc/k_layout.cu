@@ -707,7 +707,7 @@ int load_chunk(gf_shard* s, int64_t lo, int64_t hi, int64_t T, const int32_t* do
         CK(cudaMemcpyAsync(dgo, go, ng * 8, cudaMemcpyHostToDevice, st), "upload");
         CK(cudaMemcpyAsync(dgo + ng, gs, ng * 8, cudaMemcpyHostToDevice, st), "upload");
         int32_t* dgw = c.gw;
-        k_expand_groups<<<(unsigned)std::min<int64_t>(ng, 148 * 32), 256, 0, st>>>(ng, dgw, dgo, dgo + ng, expect);
+        k_expand_groups<<<(unsigned)std::min<int64_t>(ng, (int64_t)sm_count(s->device) * 32), 256, 0, st>>>(ng, dgw, dgo, dgo + ng, expect);
     } else {
         const uint32_t tn = (uint32_t)T;
         CK(cudaMemcpyAsync(c.go, &tn, 4, cudaMemcpyHostToDevice, st), "upload");

@@ -27,7 +27,7 @@ import numpy as np
 
 from .corpus import greedy_boundaries, make_chunk
 from .errors import ShapeMismatchError
-from .model import PhiMatrix, ThetaRows, check_conservation, concat_theta, phi_dtype
+from .model import PhiMatrix, ThetaRows, concat_theta, conservation_report, phi_dtype
 
 
 @dataclass
@@ -217,10 +217,27 @@ class Trainer:
         elapsed = time.perf_counter() - t0
         report = IterationReport(it, elapsed, self.num_tokens / elapsed if elapsed > 0 else float("inf"), ll)
         if self.cfg.check_conservation:
-            theta, phi = self.theta(gather=True), self.phi()
-            report.conservation = check_conservation(theta, phi, self.corpus).detail
+            report.conservation = self.conservation().detail
         self.iteration += 1
         return report
+
+    def conservation(self):
+        """check_conservation (model.py:180-225) of the resident model by K5,
+        nothing exported: each rank reduces its theta rows and the (global) phi;
+        the theta column sums are summed over ranks on the device and the first
+        bad document is the lowest-ranked report (shards are contiguous in
+        document order)."""
+        sh = self.shard
+        row = sh.conservation(1)
+        if self.world > 1:
+            rows = [None] * self.world
+            self.dist.all_gather_object(rows, row, group=self.group)
+            row = next((r for r in rows if r[0]), row)
+            cols = sh.conservation_columns()
+            self.dist.all_reduce(cols, group=self.group)
+        if row[0]:
+            return conservation_report(*row)
+        return conservation_report(*sh.conservation(2, self.num_tokens))
 
     def evaluate(self):
         """loglik_per_token of the current model."""

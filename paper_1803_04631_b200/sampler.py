@@ -45,21 +45,33 @@ def _local_theta(theta, chunk):
 def sample_chunk(chunk, phi, theta, ctx, cfg=None, iteration=0, seed=None, device=0):
     """Resample every assignment of `chunk` once; returns the new uint16 array.
     `phi` is the global PhiMatrix, `theta` the ThetaRows of the chunk's
-    documents (local rows or the whole corpus)."""
-    from .shard import DeviceShard
+    documents (local rows or the whole corpus).
+
+    The chunk's shard stays resident between calls (shard.RESIDENT): a chunk
+    sampled again -- the same Chunk, or a dataclasses.replace() of it with the
+    new assignments -- skips the K4 layout; its assignments go through the
+    staged import and theta / phi are uploaded as given (phi at its own width)
+    and validated on the device."""
+    from .errors import CountOverflowError
+    from .shard import RESIDENT, chunk_shard
 
     if seed is None:
         seed = getattr(cfg, "seed", 0) if cfg is not None else 0
-    # the hybrid 16/32-bit phi columns follow the GLOBAL word frequencies (the
-    # column sums of the global phi), not the chunk's own: a chunk-light word
-    # may hold global cells above 65535 when C > 1
-    freq = np.asarray(phi.counts).sum(axis=0, dtype=np.int64)
-    with DeviceShard(ctx.num_topics, ctx.vocab_size, ctx.alpha, ctx.beta, seed=seed, device=device,
-                     global_word_freq=freq) as sh:
-        sh.load(chunk)
-        sh.set_phi(phi.counts.astype(np.uint32, copy=False), phi.topic_totals)
-        sh.set_theta(*_local_theta(theta, chunk))
-        sh.prepare()
-        sh.sample(iteration)
-        sh.check_errors()
-        return sh.get_assignments()
+    args = (ctx.num_topics, ctx.vocab_size, ctx.alpha, ctx.beta, seed, device)
+    sh = chunk_shard(chunk, *args)
+    try:
+        sh.set_phi(phi.counts, phi.topic_totals)
+    except CountOverflowError:
+        # the hybrid 16/32-bit columns of the chunk's own word frequencies
+        # cannot hold this phi: a chunk-light word has a GLOBAL cell above
+        # 65535 (C > 1).  Lay the shard out by the global frequencies instead.
+        arrays = (chunk.word_ids, chunk.doc_ids, chunk.dw_tok, chunk.group_offsets)
+        RESIDENT.drop(arrays, (ctx.num_topics, ctx.vocab_size, device, chunk.doc_lo, chunk.doc_hi, "chunk"))
+        freq = np.asarray(phi.counts).sum(axis=0, dtype=np.int64)
+        sh = chunk_shard(chunk, *args, global_word_freq=freq, layout="global")
+        sh.set_phi(phi.counts, phi.topic_totals)
+    sh.set_theta(*_local_theta(theta, chunk))
+    sh.prepare()
+    sh.sample(iteration)
+    sh.check_errors()
+    return sh.get_assignments()

@@ -30,6 +30,101 @@ class _CudaArray:
         }
 
 
+class ResidentShards:
+    """Shards kept resident for the reference-facing one-call functions
+    (sampler.sample_chunk, model.rebuild_theta / rebuild_phi_replica,
+    eval.loglik_per_token): a chunk handed in again -- the same token arrays,
+    e.g. the same Chunk or a dataclasses.replace() of it with new assignments --
+    reuses its shard instead of repeating the K4 layout.  Only what the call
+    passes is uploaded: the assignments through the staged import (a device-side
+    diff rewrites only changed runs), theta / phi when given.  Least recently
+    used shards beyond `capacity` are closed (release() closes all)."""
+
+    def __init__(self, capacity=4):
+        from collections import OrderedDict
+
+        self.capacity = capacity
+        self._lru = OrderedDict()
+
+    @staticmethod
+    def _key(arrays, extra):
+        return tuple(id(a) for a in arrays) + tuple(extra)
+
+    def get(self, arrays, extra, build):
+        """The live shard for (token arrays, extra) or a new one from build()."""
+        import weakref
+
+        key = self._key(arrays, extra)
+        ent = self._lru.get(key)
+        if ent is not None and all(r() is a for r, a in zip(ent[0], arrays)):
+            self._lru.move_to_end(key)
+            return ent[1], False
+        if ent is not None:
+            ent[1].close()
+            del self._lru[key]
+        sh = build()
+        self._lru[key] = ([weakref.ref(a) for a in arrays], sh)
+        while len(self._lru) > self.capacity:
+            self._lru.popitem(last=False)[1][1].close()
+        return sh, True
+
+    def find(self, arrays, pred):
+        """The most recently used live shard of these arrays whose extra key
+        satisfies pred (or None)."""
+        ids = tuple(id(a) for a in arrays)
+        for key in reversed(list(self._lru)):
+            refs, sh = self._lru[key]
+            if key[: len(ids)] == ids and pred(key[len(ids):]) and all(r() is a for r, a in zip(refs, arrays)):
+                self._lru.move_to_end(key)
+                return sh
+        return None
+
+    def drop(self, arrays, extra):
+        ent = self._lru.pop(self._key(arrays, extra), None)
+        if ent is not None:
+            ent[1].close()
+
+    def release(self):
+        while self._lru:
+            self._lru.popitem()[1][1].close()
+
+
+RESIDENT = ResidentShards()
+
+
+def chunk_shard(chunk, num_topics, vocab_size, alpha=1.0, beta=1.0, seed=0, device=0, global_word_freq=None,
+                layout="chunk", any_vocab=False):
+    """The resident shard of `chunk` with its assignments current (staged
+    import: nothing is rewritten when they did not change).  any_vocab: any
+    resident shard of the chunk with this K will do (theta needs no phi layout)."""
+    arrays = (chunk.word_ids, chunk.doc_ids, chunk.dw_tok, chunk.group_offsets)
+    extra = (int(num_topics), int(vocab_size), int(device), int(chunk.doc_lo), int(chunk.doc_hi), layout)
+    if any_vocab:
+        sh = RESIDENT.find(arrays, lambda e: e[0] == extra[0] and e[2:5] == extra[2:5])
+        if sh is not None:
+            _import_assignments(sh, chunk)
+            return sh
+
+    def build():
+        sh = DeviceShard(num_topics, vocab_size, alpha, beta, seed=seed, device=device,
+                         global_word_freq=global_word_freq)
+        return sh.load(chunk)
+
+    sh, fresh = RESIDENT.get(arrays, extra, build)
+    if not fresh:
+        sh.set_params(alpha, beta, seed)
+        _import_assignments(sh, chunk)
+    return sh
+
+
+def _import_assignments(sh, chunk):
+    z = chunk.assignments
+    if not (isinstance(z, np.ndarray) and z.dtype == np.uint16 and z.flags.c_contiguous):
+        z = np.ascontiguousarray(z, dtype=np.uint16)
+    sh.copy_assignments_async(z, 0, len(z), True)
+    sh.assignments_imported()
+
+
 def sync_layout(global_word_freq, num_topics, heavy_threshold=65535):
     """gf_sync_layout: (word_col int32[V], (phi16 off, n_k off, total) in u32 words)."""
     freq = _lib.carr(global_word_freq, np.int64)
@@ -281,19 +376,30 @@ class DeviceShard:
             raise ValueError("theta row_ptr must have num_local_docs + 1 entries")
         _lib.check(_lib.lib().gf_shard_set_theta(self._h, _lib.ptr(rp), _lib.ptr(ids), _lib.ptr(cn)))
 
-    def get_phi(self):
-        """(counts uint32[K, V] row-major, topic_totals int64[K]) from the sync buffer."""
-        kv = np.empty((self.K, self.V), np.uint32)
+    def get_phi(self, width=32):
+        """(counts [K, V] row-major, uint32 -- or uint16 for width 16, which
+        raises the reference's overflow text for a cell above 65535 --,
+        topic_totals int64[K]) from the sync buffer."""
+        kv = np.empty((self.K, self.V), np.uint16 if width == 16 else np.uint32)
         tot = np.empty(self.K, np.int64)
-        _lib.check(_lib.lib().gf_shard_get_phi(self._h, _lib.ptr(kv), _lib.ptr(tot)))
+        _lib.check(_lib.lib().gf_shard_get_phi_w(self._h, _lib.ptr(kv), int(width), _lib.ptr(tot)))
         return kv, tot
 
     def set_phi(self, counts, totals):
-        kv = _lib.carr(counts, np.uint32)
+        """Import a K x V PhiMatrix (uint16 or uint32 cells, as given)."""
+        kv = np.ascontiguousarray(counts)
+        if kv.dtype not in (np.uint16, np.uint32):
+            kv = kv.astype(np.uint32)
         tot = _lib.carr(totals, np.int64)
         if kv.shape != (self.K, self.V):
             raise ValueError(f"phi must be {self.K} x {self.V}")
-        _lib.check(_lib.lib().gf_shard_set_phi(self._h, _lib.ptr(kv), _lib.ptr(tot)))
+        _lib.check(_lib.lib().gf_shard_set_phi_w(self._h, _lib.ptr(kv), kv.dtype.itemsize * 8, _lib.ptr(tot)))
+
+    def set_params(self, alpha, beta, seed):
+        """gf_shard_set_params: new hyper-parameters / Philox key, same shard."""
+        _lib.check(_lib.lib().gf_shard_set_params(self._h, float(alpha), float(beta),
+                                                  int(seed) & 0xFFFFFFFFFFFFFFFF))
+        self.alpha, self.beta = float(alpha), float(beta)
 
     def phi_argmax(self):
         m = ctypes.c_int64()
@@ -308,6 +414,26 @@ class DeviceShard:
             m, k, v = self.phi_argmax()
             if m > 65535:
                 raise CountOverflowError(f"phi cell (topic {k}, word {v}) count {m} exceeds 16-bit range")
+
+    # ---------------------------------------------------- K5 conservation --
+    def conservation(self, stage, num_tokens=0):
+        """gf_shard_conservation: stage 1 reduces the resident theta / phi and
+        returns the row report (code, global doc, row sum, length); stage 2
+        compares the (possibly rank-summed) theta column sums, the phi row sums
+        and sum n_k with n_k / num_tokens.  Reports: model.conservation_report."""
+        rep = np.zeros(4, np.int64)
+        _lib.check(_lib.lib().gf_shard_conservation(self._h, int(stage), int(num_tokens), _lib.ptr(rep)))
+        return tuple(int(x) for x in rep)
+
+    def conservation_columns(self):
+        """The K theta column sums of stage 1 as a torch int64 CUDA tensor
+        (zero-copy) for a cross-rank allreduce before stage 2."""
+        import torch
+
+        p = ctypes.c_void_p()
+        n = ctypes.c_int64()
+        _lib.check(_lib.lib().gf_shard_conservation_buffer(self._h, ctypes.byref(p), ctypes.byref(n)))
+        return torch.as_tensor(_CudaArray(p.value, n.value, "<i8", self), device=f"cuda:{self.device}")
 
     # ------------------------------------------------------------ counters --
     def stats(self):

@@ -117,3 +117,30 @@ class OracleShard:
 
     def check_phi_width(self, width):
         pass
+
+    # --- K5 stand-in: the oracle's reductions in the device report layout
+    def conservation(self, stage, num_tokens=0):
+        rp, ids, cn = self.theta
+        if stage == 1:
+            D = len(rp) - 1
+            sums = np.bincount(np.repeat(np.arange(D), np.diff(rp)), weights=cn, minlength=D).astype(np.int64)
+            bad = np.flatnonzero(sums != self.doc_len)
+            self._cols = torch.as_tensor(np.bincount(ids.astype(np.int64), weights=cn, minlength=self.K)
+                                         .astype(np.int64))
+            if bad.size:
+                d = int(bad[0])
+                return (1, self.chunk.doc_lo + d, int(sums[d]), int(self.doc_len[d]))
+            return (0, 0, 0, 0)
+        counts, totals = self._unpack()
+        cols = self._cols.numpy()
+        for code, val in ((2, cols), (3, counts.sum(axis=1, dtype=np.int64))):
+            bad = np.flatnonzero(val != totals)
+            if bad.size:
+                k = int(bad[0])
+                return (code, k, int(val[k]), int(totals[k]))
+        if int(totals.sum()) != num_tokens:
+            return (4, 0, int(totals.sum()), int(num_tokens))
+        return (0, 0, 0, 0)
+
+    def conservation_columns(self):
+        return self._cols

@@ -44,15 +44,35 @@ def _run_rank(rank, world, port, out):
     from paper_1803_04631_b200 import engine
 
     corp = _corpus()
-    tr = engine.Trainer(corp, engine.TrainConfig(workers=world, **CFG), shard_factory=OracleShard)
-    lls = [tr.step().loglik_per_token for _ in range(CFG["iterations"])]
+    tr = engine.Trainer(corp, engine.TrainConfig(workers=world, check_conservation=True, **CFG),
+                        shard_factory=OracleShard)
+    reps = [tr.step() for _ in range(CFG["iterations"])]
+    lls = [r.loglik_per_token for r in reps]
     theta = tr.theta(gather=True)
     phi = tr.phi()
     z = [None] * world
     dist.all_gather_object(z, (tr.chunk.doc_lo, tr.chunk.doc_hi, tr.assignments()))
+    # K5 across ranks: rank 1 corrupts its first theta row -> every rank reports
+    # that document by its global index; the rank-summed columns catch a
+    # column fault that no single rank sees
+    rp, ids, cn = tr.shard.theta
+    if rank == 1:
+        cn = cn.copy()
+        cn[0] += 1
+        tr.shard.theta = (rp, ids, cn)
+    row_fault = tr.conservation().detail
+    if rank == 1:
+        cn = cn.copy()
+        cn[0] -= 1
+        k0, k1 = int(ids[0]), int(ids[1])
+        ids = ids.copy()
+        ids[0], ids[1] = ids[1], ids[0]                  # moves counts between topics k0 and k1
+        tr.shard.theta = (rp, ids, cn)
+    col_fault = tr.conservation().detail
     if rank == 0:
         np.savez(out, lls=np.array(lls), phi=phi.counts, tot=phi.topic_totals, rp=theta.row_ptr,
-                 ids=theta.topic_ids, cn=theta.counts, bounds=np.array([(a, b) for a, b, _ in z]))
+                 ids=theta.topic_ids, cn=theta.counts, bounds=np.array([(a, b) for a, b, _ in z]),
+                 cons=np.array([r.conservation for r in reps] + [row_fault, col_fault]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -94,6 +114,21 @@ def test_two_ranks_train_the_same_model_as_one(two_rank_result):
     np.testing.assert_allclose(r["lls"], lls, rtol=1e-12)
     # shards are greedy_boundaries(C = G) (corpus.py:210-237)
     assert [tuple(b) for b in r["bounds"]] == cp.greedy_boundaries(corp.doc_lengths, 2)
+
+
+def test_two_rank_conservation_reports(two_rank_result):
+    """Trainer.conservation (K5 protocol: local row check, rank-summed theta
+    columns) over 2 gloo ranks: ok every iteration, and the reference's texts
+    (model.py:180-225) for an injected row fault and column fault."""
+    from paper_1803_04631_b200 import corpus as cp
+
+    corp = _corpus()
+    cons = [str(c) for c in two_rank_result["cons"]]
+    assert cons[:-2] == ["ok"] * CFG["iterations"]
+    lo1 = cp.greedy_boundaries(corp.doc_lengths, 2)[1][0]
+    assert cons[-2].startswith(f"theta row {lo1} sums to ") and cons[-2].endswith(
+        f"document length is {int(corp.doc_lengths[lo1])}")
+    assert cons[-1].startswith("topic ") and ": theta column sum " in cons[-1] and "!= phi total" in cons[-1]
 
 
 def test_packed_phi_allreduce_is_exact(two_rank_result):

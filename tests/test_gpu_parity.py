@@ -829,3 +829,178 @@ def test_async_chunked_assignment_copies():
         np.testing.assert_array_equal(gphi, phi)
         with pytest.raises(errors.ShapeMismatchError):
             sh.copy_assignments_async(host, T - 1, 5, True)
+
+
+# ---------------------------------------------------------- K5 conservation --
+def test_conservation_kernel_fault_injection():
+    """K5 (gf_shard_conservation on the resident state, gf_check_conservation on
+    exported arrays) reports the first violated invariant of model.py:180-225
+    with the reference's text: the same answer as the oracle for a clean model
+    and for an injected fault of each kind, in the reference's check order."""
+    K = 24
+    corp = synth.generate(300, 500, 40.0, seed=13)
+    ch = cp.partition(corp, 1, K, 4)[0]
+    rp, ids, cn = oracle_theta(ch, K)
+    phi, tot = oracle.rebuild_phi(ch.assignments, ch.word_ids, K, corp.vocab_size)
+    phi = phi.astype(np.uint32)
+    L, T = corp.doc_lengths, corp.num_tokens
+    freq = np.bincount(corp.word_ids, minlength=corp.vocab_size)
+
+    def want(rp_, ids_, cn_, phi_, tot_):
+        return oracle.check_conservation(rp_, ids_, cn_, phi_, tot_, L, T)[1]
+
+    def exported(rp_, ids_, cn_, phi_, tot_):
+        return md.check_conservation(md.ThetaRows(rp_, ids_, cn_, K), md.PhiMatrix(phi_, tot_), corp).detail
+
+    with DeviceShard(K, corp.vocab_size, 0.5, 0.01, global_word_freq=freq) as sh:
+        sh.load(ch)
+        sh.initialize()
+
+        def resident():
+            row = sh.conservation(1)
+            return md.conservation_report(*(row if row[0] else sh.conservation(2, T))).detail
+
+        assert resident() == exported(rp, ids, cn, phi, tot) == want(rp, ids, cn, phi, tot) == "ok"
+        # 1. a theta row off by one
+        cn1 = cn.copy()
+        cn1[rp[37]] += 1
+        sh.set_theta(rp, ids, cn1)
+        assert resident() == exported(rp, ids, cn1, phi, tot) == want(rp, ids, cn1, phi, tot)
+        assert resident().startswith("theta row 37 sums to")
+        # 2. one count moved between two topics of a row (row sums still right)
+        d = int(np.flatnonzero((np.diff(rp) >= 2))[0])
+        j = int(rp[d])
+        cn2 = cn.copy()
+        cn2[j] += 1
+        cn2[j + 1] -= 1
+        if cn2[j + 1] == 0:                  # keep the row a valid CSR row
+            cn2[j + 1] += 1
+            cn2[j] -= 1
+            cn2[j] -= 1 if cn2[j] > 1 else 0
+            cn2[j + 1] += 1 if cn[j] > 1 else 0
+        sh.set_theta(rp, ids, cn2)
+        w2 = want(rp, ids, cn2, phi, tot)
+        assert w2 != "ok"
+        assert resident() == exported(rp, ids, cn2, phi, tot) == w2
+        sh.set_theta(rp, ids, cn)
+        # 3. one phi cell moved to another topic (phi row sums off, totals stored)
+        phi3 = phi.copy()
+        v = int(np.flatnonzero(phi3[2])[0])
+        phi3[2, v] -= 1
+        phi3[9, v] += 1
+        sh.set_phi(phi3, tot)
+        w3 = want(rp, ids, cn, phi3, tot)
+        assert w3.startswith("topic 2: phi row sum")
+        assert resident() == exported(rp, ids, cn, phi3, tot) == w3
+        # 4. stored totals moved with phi but not with theta
+        tot4 = tot.copy()
+        tot4[3] += 1
+        phi4 = phi.copy()
+        phi4[3, v] += 1
+        sh.set_phi(phi4, tot4)
+        w4 = want(rp, ids, cn, phi4, tot4)
+        assert w4.startswith("topic 3: theta column sum")
+        assert resident() == exported(rp, ids, cn, phi4, tot4) == w4
+    # 5. the total check (exported arrays: empty model of a non-empty corpus)
+    Lz = np.zeros_like(L)
+    rpz = np.zeros(len(L) + 1, np.int64)
+    e16 = np.zeros(0, np.uint16)
+    phz, totz = np.zeros((K, corp.vocab_size), np.uint16), np.zeros(K, np.int64)
+    want5 = oracle.check_conservation(rpz, e16, e16, phz, totz, Lz, T)[1]
+    assert want5 == f"totals sum to 0, corpus has {T} tokens"
+    from paper_1803_04631_b200 import _lib
+
+    rep = np.zeros(8, np.int64)
+    _lib.check(_lib.lib().gf_check_conservation(0, K, corp.vocab_size, len(L), _lib.ptr(rpz), _lib.ptr(e16),
+                                                _lib.ptr(e16), _lib.ptr(Lz), _lib.ptr(phz), 16, _lib.ptr(totz), T,
+                                                _lib.ptr(rep)))
+    assert rep[0] == 0 and md.conservation_report(*rep[4:]).detail == want5
+
+
+def test_conservation_golden_texts_on_device():
+    """The reference's own ConservationReport texts (tests/golden/messages.json,
+    written by gibbsflow.model.check_conservation) from the device check."""
+    import test_oracle_golden as tog
+
+    msgs = json.load(open(os.path.join(GOLD, "messages.json")))
+    for name, corp, rp, ids, cn, phi, tot in tog.conservation_cases():
+        c = cp.corpus_from_tokens(corp["doc_ids"], corp["word_ids"], corp["V"])
+        th = md.ThetaRows(rp, ids.astype(np.uint16), cn.astype(np.uint16), phi.shape[0])
+        got = md.check_conservation(th, md.PhiMatrix(phi.astype(np.uint32), tot), c)
+        assert got.detail == msgs[name], name
+        assert got.ok == (name == "conservation_ok")
+
+
+def test_set_phi_rejects_light_column_overflow_on_device():
+    """gf_shard_set_phi checks the 16-bit (light) columns on the device and names
+    the first offending cell in word-major order; heavy columns take any u32."""
+    K, V = 4, 6
+    corp = synth.generate(40, V, 20.0, seed=3)
+    ch = cp.partition(corp, 1, K, 1)[0]
+    freq = np.bincount(corp.word_ids, minlength=V)
+    with DeviceShard(K, V, 0.5, 0.01, global_word_freq=freq, heavy_threshold=int(freq.max()) - 1) as sh:
+        sh.load(ch)
+        sh.initialize()
+        phi, tot = sh.get_phi()
+        heavy = int(np.argmax(freq))
+        light = [v for v in range(V) if v != heavy]
+        big = phi.copy()
+        big[1, heavy] = 100000                      # heavy (u32) column: accepted
+        sh.set_phi(big, tot + np.eye(K, dtype=np.int64)[1] * (100000 - int(phi[1, heavy])))
+        bad = phi.copy()
+        bad[2, light[3]] = 70000
+        bad[0, light[4]] = 80000
+        with pytest.raises(errors.CountOverflowError) as ei:
+            sh.set_phi(bad, tot)
+        assert str(ei.value) == f"phi cell (topic 2, word {light[3]}) count 70000 exceeds its 16-bit column"
+
+
+def test_drop_in_api_keeps_the_chunk_resident():
+    """sample_chunk / rebuild_theta / rebuild_phi_replica reuse one resident
+    shard per chunk (shard.RESIDENT): the K4 layout runs once, a
+    dataclasses.replace() of the chunk with new assignments hits the same
+    shard, and every result equals a cold call's."""
+    from dataclasses import replace
+
+    from paper_1803_04631_b200.shard import RESIDENT
+
+    K = 16
+    corp = synth.generate(300, 400, 50.0, seed=12)
+    ch = cp.partition(corp, 1, K, 9)[0]
+    ctx = sampler.SamplerContext(50.0 / K, 0.01, K, corp.vocab_size)
+    RESIDENT.release()
+
+    def one_iteration(c, it):
+        th = md.rebuild_theta(c, K)
+        ph = md.rebuild_phi_replica(c, K, corp.vocab_size, width=16)
+        z = sampler.sample_chunk(c, ph, th, ctx, iteration=it, seed=3)
+        return th, ph, z
+
+    warm, c = [], ch
+    for it in range(3):
+        th, ph, z = one_iteration(c, it)
+        warm.append((th, ph, z))
+        c = replace(c, assignments=z)
+    assert len(RESIDENT._lru) == 1                 # one shard served all nine calls
+    cold, c = [], ch
+    for it in range(3):
+        RESIDENT.release()
+        th, ph, z = one_iteration(c, it)
+        cold.append((th, ph, z))
+        c = replace(c, assignments=z)
+    for (t1, p1, z1), (t2, p2, z2) in zip(warm, cold):
+        np.testing.assert_array_equal(t1.counts, t2.counts)
+        np.testing.assert_array_equal(t1.topic_ids, t2.topic_ids)
+        assert p1.counts.dtype == np.uint16
+        np.testing.assert_array_equal(p1.counts, p2.counts)
+        np.testing.assert_array_equal(z1, z2)
+    # the oracle agrees with the warm path's draws (thin form)
+    th, ph, z = warm[1]
+    want = oracle.sample_tokens(K, corp.vocab_size, 50.0 / K, 0.01, 3, 1, ch.doc_ids, ch.word_ids, warm[0][2], 0,
+                                th.row_ptr, th.topic_ids, th.counts, ph.counts, ph.topic_totals, mode="thin")
+    assert np.mean(z == want) > 0.998
+    # loglik through the resident corpus shard: twice, same value
+    l1 = ev.loglik_per_token(th, ph, corp, 50.0 / K, 0.01)
+    l2 = ev.loglik_per_token(th, ph, corp, 50.0 / K, 0.01)
+    assert l1 == l2
+    RESIDENT.release()

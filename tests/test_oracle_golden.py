@@ -152,9 +152,9 @@ def test_overflow_messages_match_reference():
     assert f"document {d}: topic count {c} exceeds 16-bit range" == msgs["theta_overflow_doc3"]
 
 
-def test_conservation_texts_match_reference():
-    with open(os.path.join(GOLD, "messages.json")) as fh:
-        msgs = json.load(fh)
+def conservation_cases():
+    """The four states make_golden.py hands to the reference's
+    check_conservation (model.py:180-225) for messages.json."""
 
     def model(lengths, V, K, seed):
         r = np.random.default_rng(seed)
@@ -171,19 +171,27 @@ def test_conservation_texts_match_reference():
             tot += pt
         return corp, rp, ids, cn, phi, tot
 
-    corp, rp, ids, cn, phi, tot = model([5, 8, 3, 9], 7, 3, 1)
-    assert oracle.check_conservation(rp, ids, cn, phi, tot, corp["doc_lengths"], corp["T"])[1] == msgs["conservation_ok"]
+    out = [("conservation_ok",) + model([5, 8, 3, 9], 7, 3, 1)]
     corp, rp, ids, cn, phi, tot = model([5, 8, 3, 9], 7, 3, 2)
     phi[1, 0] += 1
     tot[1] += 1
-    assert oracle.check_conservation(rp, ids, cn, phi, tot, corp["doc_lengths"], corp["T"])[1] == msgs["conservation_phi_fault"]
+    out.append(("conservation_phi_fault", corp, rp, ids, cn, phi, tot))
     corp, rp, ids, cn, phi, tot = model([5, 8, 3], 7, 3, 4)
     phi[2, 1] += 1
-    assert oracle.check_conservation(rp, ids, cn, phi, tot, corp["doc_lengths"], corp["T"])[1] == msgs["conservation_stale_totals"]
+    out.append(("conservation_stale_totals", corp, rp, ids, cn, phi, tot))
     corp, rp, ids, cn, phi, tot = model([5, 8, 3], 7, 3, 5)
     cn = cn.copy()
     cn[rp[1]] += 1
-    assert oracle.check_conservation(rp, ids, cn, phi, tot, corp["doc_lengths"], corp["T"])[1] == msgs["conservation_theta_row"]
+    out.append(("conservation_theta_row", corp, rp, ids, cn, phi, tot))
+    return out
+
+
+def test_conservation_texts_match_reference():
+    with open(os.path.join(GOLD, "messages.json")) as fh:
+        msgs = json.load(fh)
+    for name, corp, rp, ids, cn, phi, tot in conservation_cases():
+        got = oracle.check_conservation(rp, ids, cn, phi, tot, corp["doc_lengths"], corp["T"])[1]
+        assert got == msgs[name], name
 
 
 # -------------------------------------------------------------- ptree ------
