@@ -137,10 +137,14 @@ class Trainer:
 
             shard_factory = DeviceShard
         stream = None
-        if self.world > 1 and self._backend() == "nccl":
+        if self.world > 1:
             import torch
 
-            stream = torch.cuda.current_stream(device)
+            # the shard runs on torch's current stream so the phi all_reduce
+            # (NCCL, or gloo on the CUDA sync tensor) is ordered after K2 and
+            # before prepare / the next K1 without host synchronisation
+            if self._backend() == "nccl" or torch.cuda.is_available():
+                stream = torch.cuda.current_stream(device)
         self.shard = shard_factory(K, V, cfg.alpha, cfg.beta, seed=cfg.seed, device=device,
                                    heavy_threshold=cfg.heavy_threshold, global_word_freq=self.global_freq,
                                    stream=stream)
