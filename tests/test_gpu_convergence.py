@@ -58,9 +58,12 @@ def test_device_trajectory_inside_independent_seed_band():
     assert gpu[-1] > gpu[0] + 0.05
 
 
-def planted_corpus(seed, D=200, V=50, K=5, mean_len=50, alpha=0.5):
-    """K topics with disjoint 10-word supports; per document theta ~ Dir(alpha),
-    length ~ Poisson(mean_len) (>= 1), z ~ theta, w uniform over topic z's words."""
+def planted_corpus(seed, D=200, V=50, K=5, mean_len=50, alpha=0.1):
+    """K topics with disjoint 10-word supports; per document theta ~ Dir(alpha)
+    (sparse: documents are mostly about one topic -- SPEC #7 leaves the mixing
+    open; with Dir(0.5) mixtures the attainable gain at alpha = 50/K is ~0.4
+    nats, measured on both the device and the oracle), length ~ Poisson(mean_len)
+    (>= 1), z ~ theta, w uniform over topic z's words."""
     r = np.random.default_rng(seed)
     per = V // K
     docs, words = [], []
@@ -86,5 +89,8 @@ def test_planted_topic_convergence_spec7():
         last = tr.evaluate()                               # the model after the 100th iteration
         tr.close()
         gains.append(last - first)
+        if seed < 3:                                       # the oracle's direct sampler gets the same gain
+            ref = oracle_direct_trajectory(corp, 5, seed, 99 + seed, 101)
+            assert abs((ref[-1] - ref[0]) - gains[-1]) < 0.05 * abs(ref[-1] - ref[0]), (ref[-1] - ref[0], gains[-1])
     gains = np.array(gains)
     assert np.mean(gains >= 0.5) >= 0.95, gains
