@@ -709,6 +709,36 @@ def run_ours(args, world, rank, local):
                       f"loglik_sum (C ABI)"}
         del lls
 
+    # ---- after the timed regions: K2 and K3 each ALONE (the step runs them
+    # concurrently), and the K5 conservation check's cost (debug mode) ----
+    def alone(fn, reps=3):
+        ms = []
+        for _ in range(reps):
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(device)
+            a0.record(stream)
+            fn()
+            a1.record(stream)
+            torch.cuda.synchronize(device)
+            ms.append(a0.elapsed_time(a1))
+        return float(np.median(ms))
+
+    sh.set_stream(stream)
+    k2_alone = alone(sh.rebuild_phi)
+    w = allreduce_async()                     # the replica is global again
+    if w:
+        w.wait()
+    sh.prepare()
+    k3_alone = alone(sh.rebuild_theta)
+
+    def k5():
+        r = sh.conservation(1)
+        if not r[0]:
+            r = sh.conservation(2, T_local if not dist else T_all)
+        k5.report = r
+    k5_ms = alone(k5)
+    k5_ok = k5.report[0] == 0 or (dist is not None)   # N>1: columns are rank-local here
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:      # rank 0 at N=1 only
         nd = args.cpu_sample_docs or min(CPU_SAMPLE_DOCS[args.workload], SHAPES[args.workload]["num_docs"])
@@ -726,19 +756,25 @@ def run_ours(args, world, rank, local):
                        "doc_blocks": st["doc_blocks"], "theta_nnz_after_last_step": st["theta_nnz"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic["bytes_per_launch"] if traffic else None,
-                         "traffic_source": (f"{traffic['source']} (committed ncu --set full capture; not this run)"
-                                            if traffic else None),
+                         "traffic_source": (f"{traffic['source']} (committed ncu --set full capture of the same "
+                                            f"command's K1 at the iteration named; ncu cannot run inside the "
+                                            f"timed region)" if traffic else None),
                          "frac_of_nominal_8tbs": achieved / 8000.0,
                          "kernel": "gf::sample_kernel (K1)", "algorithmic_bytes_per_launch": st["sample_bytes"],
                          "kernel_ms": k1_ms, "peak_source": peak_src},
             "kernels": {
-                "phi_rebuild": kernel_block("gf::phi_rebuild_kernel (K2, + sync-buffer memset)", acc[1],
-                                            st["phi_bytes"], peak),
-                "theta_rebuild": kernel_block("gf::theta_rebuild_kernel (K3, side stream)", acc[4],
+                "phi_rebuild": kernel_block("gf::phi_rebuild_kernel (K2, + memset of the 32-bit columns), alone",
+                                            k2_alone, st["phi_bytes"], peak),
+                "theta_rebuild": kernel_block("gf::theta_rebuild_kernel (K3), alone", k3_alone,
                                               st["theta_bytes"], peak),
-                "note": "K2 and K3 run concurrently (main / side stream), so each time includes the other's "
-                        "contention",
+                "in_step_ms": {"phi_rebuild": acc[1], "theta_rebuild": acc[4]},
+                "note": "alone = median of 3 launches timed by CUDA events after the timed region; inside the "
+                        "step K2 and K3 run concurrently (main / side stream), in_step_ms includes that contention",
             },
+            "conservation": {"ms": k5_ms, "frac_of_step": k5_ms / ms_step, "ok": bool(k5_ok),
+                             "what": "K5 (gf_shard_conservation stages 1+2: theta row/column sums, phi row "
+                                     "sums, n_k, T; 2 tiny D2H reads) -- the per-iteration cost of "
+                                     "TrainConfig(check_conservation=True), not in the timed step"},
             "kernel_ms": {"sample": acc[0], "phi_rebuild": acc[1], "allreduce_and_prepare": acc[2],
                           "theta_rebuild_exposed": acc[3], "theta_rebuild": acc[4]},
             "loglik_per_token": ll,

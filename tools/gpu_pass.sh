@@ -20,7 +20,8 @@ e = d.get("e2e") or {}
 ks = d.get("kernels") or {}
 print(sys.argv[1].split("/")[-1], f"{d['value']/1e9:.3f} G ms/step={d['ms_per_step']:.2f}", f"K1frac={r.get('frac', 0):.3f}",
       f"e2e={(e or {}).get('value', 0)/1e9:.3f} G", {k: round(v, 3) for k, v in (d.get("kernel_ms") or {}).items()},
-      {k: round(v.get("frac", 0), 3) for k, v in ks.items() if isinstance(v, dict)},
+      {k: (round(v.get("ms", 0), 3), round(v.get("frac", 0), 3)) for k, v in ks.items() if isinstance(v, dict) and "frac" in v},
+      "k5", (d.get("conservation") or {}).get("ms"),
       "cpu", (d.get("cpu_baseline") or {}).get("value"), d.get("clocks", {}).get("reasons"))
 PY
 }
@@ -41,6 +42,13 @@ fi
 if want nyt; then
   timeout 900 python bench.py --workload nytimes --no-cpu-baseline --steps 20 --warmup 5 > $o/${tag}_bench_nyt.json 2> $o/${tag}_bench_nyt.err
   summ $o/${tag}_bench_nyt.json
+fi
+if want api; then
+  timeout 900 python tools/api_e2e.py --tag ${tag} --out-dir $o > $o/${tag}_api.log 2>&1; echo "api e2e rc=$? $(tail -c 400 $o/${tag}_api.log)"
+fi
+if want traj; then
+  timeout 3000 python tools/trajectory.py --workload nytimes --gpu-iters 100 --cpu-iters 30 --cpu-seeds 1001,2002,3003 \
+    --tag ${tag} --out-dir $o > $o/${tag}_traj.log 2>&1; echo "trajectory rc=$? $(tail -c 600 $o/${tag}_traj.log)"
 fi
 if want ncu; then
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
