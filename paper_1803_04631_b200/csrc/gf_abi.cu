@@ -396,6 +396,23 @@ static int need_loaded(gf_shard* s) {
     return GF_OK;
 }
 
+// the shard's grow-only device scratch for import / export staging (one call
+// at a time per shard; every user synchronises before returning)
+static int dev_scratch(gf_shard* s, size_t bytes, char** out) {
+    if (s->d.scratch_bytes < bytes) {
+        if (s->d.scratch) { cudaStreamSynchronize(s->stream); cudaFree(s->d.scratch); }
+        s->d.scratch = nullptr;
+        s->d.scratch_bytes = 0;
+        const size_t want = bytes + bytes / 4;
+        CU(cudaMalloc((void**)&s->d.scratch, want), "device scratch");
+        s->d.scratch_bytes = want;
+    }
+    *out = reinterpret_cast<char*>(s->d.scratch);
+    return GF_OK;
+}
+
+static inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
+
 int gf_shard_rebuild_phi(gf_shard* s) {
     if (int rc = need_loaded(s)) return rc;
     CU(gf::launch_phi_rebuild(s), "rebuild_phi");
@@ -605,15 +622,14 @@ int gf_shard_peer_close(gf_shard* s) {
 
 int gf_shard_get_assignments(gf_shard* s, uint16_t* out) {
     if (int rc = need_loaded(s)) return rc;
-    CU(cudaMemcpyAsync(out, s->d.z, s->T * 2, cudaMemcpyDeviceToHost, s->stream), "get_assignments");
-    CU(cudaStreamSynchronize(s->stream), "get_assignments");
+    CU(gf::xfer_d2h(out, s->d.z, s->T * 2, s->stream), "get_assignments");
     return GF_OK;
 }
 
 int gf_shard_set_assignments(gf_shard* s, const uint16_t* in) {
     if (int rc = need_loaded(s)) return rc;
     // range is checked on the device (K1/K2/K3 flag z >= K as a consistency error)
-    CU(cudaMemcpyAsync(s->d.z, in, s->T * 2, cudaMemcpyHostToDevice, s->stream), "set_assignments");
+    CU(gf::xfer_h2d(s->d.z, in, s->T * 2, s->stream), "set_assignments");
     CU(gf::launch_zdoc_sync(s), "set_assignments");
     CU(cudaStreamSynchronize(s->stream), "set_assignments");
     s->stale_theta = s->stale_phi = true;
@@ -631,8 +647,10 @@ int gf_shard_copy_assignments_async(gf_shard* s, void* host, int64_t offset, int
     }
     uint16_t* dev = (to_device ? s->d.zstage : s->d.z) + offset;
     uint16_t* h = static_cast<uint16_t*>(host) + offset;
-    if (to_device) CU(cudaMemcpyAsync(dev, h, count * 2, cudaMemcpyHostToDevice, st), "copy_assignments");
-    else CU(cudaMemcpyAsync(h, dev, count * 2, cudaMemcpyDeviceToHost, st), "copy_assignments");
+    // pinned host buffers: a plain async copy; pageable ones go through the
+    // pinned bounce buffers (the host side then completes before returning)
+    if (to_device) CU(gf::xfer_h2d(dev, h, count * 2, st), "copy_assignments");
+    else CU(gf::xfer_d2h(h, dev, count * 2, st), "copy_assignments");
     return GF_OK;
 }
 
@@ -652,35 +670,54 @@ static int fetch_meta(gf_shard* s, std::vector<uint2>& meta) {
     return GF_OK;
 }
 
+// the exported CSR's row_ptr, scanned on the device into the scratch
+static int theta_rowptr_dev(gf_shard* s, int64_t** d_rowptr, char** after) {
+    size_t tmp = 0;
+    CU(gf::theta_rowptr(s, nullptr, nullptr, &tmp), "theta row_ptr");
+    const size_t b_rp = al256((s->D + 1) * 8);
+    char* base = nullptr;
+    if (int rc = dev_scratch(s, b_rp + al256(tmp), &base)) return rc;
+    *d_rowptr = reinterpret_cast<int64_t*>(base);
+    CU(gf::theta_rowptr(s, *d_rowptr, base + b_rp, &tmp), "theta row_ptr");
+    if (after) *after = base + b_rp;
+    return GF_OK;
+}
+
 int gf_shard_theta_nnz(gf_shard* s, int64_t* nnz) {
     if (int rc = need_loaded(s)) return rc;
-    std::vector<uint2> meta;
-    if (int rc = fetch_meta(s, meta)) return rc;
-    int64_t n = 0;
-    for (auto& m : meta) n += m.y;
-    *nnz = n;
+    int64_t* drp = nullptr;
+    if (int rc = theta_rowptr_dev(s, &drp, nullptr)) return rc;
+    CU(cudaMemcpyAsync(nnz, drp + s->D, 8, cudaMemcpyDeviceToHost, s->stream), "theta nnz");
+    CU(cudaStreamSynchronize(s->stream), "theta nnz");
     return GF_OK;
 }
 
 int gf_shard_get_theta(gf_shard* s, int64_t* row_ptr, uint16_t* ids, uint16_t* cnts) {
+    // row_ptr by a device scan, the entries by the export kernel, all three
+    // arrays back through the staged copies (no host loop over documents)
     if (int rc = need_loaded(s)) return rc;
-    std::vector<uint2> meta;
-    if (int rc = fetch_meta(s, meta)) return rc;
-    row_ptr[0] = 0;
-    for (int64_t d = 0; d < s->D; ++d) row_ptr[d + 1] = row_ptr[d] + meta[d].y;
-    const int64_t nnz = row_ptr[s->D];
-    int64_t* drp = nullptr;
-    uint16_t* dids = nullptr;
-    CU(cudaMalloc(&drp, (s->D + 1) * 8), "get_theta");
-    CU(cudaMalloc(&dids, std::max<int64_t>(nnz, 1) * 4), "get_theta");
-    uint16_t* dcnt = dids + std::max<int64_t>(nnz, 1);
-    cudaMemcpyAsync(drp, row_ptr, (s->D + 1) * 8, cudaMemcpyHostToDevice, s->stream);
+    int64_t nnz = 0;
+    if (int rc = gf_shard_theta_nnz(s, &nnz)) return rc;
+    const size_t b_rp = al256((s->D + 1) * 8), b_e = al256((size_t)std::max<int64_t>(nnz, 1) * 2);
+    char* base = nullptr;
+    if (int rc = dev_scratch(s, b_rp + 2 * b_e, &base)) return rc;
+    int64_t* drp = reinterpret_cast<int64_t*>(base);
+    uint16_t* dids = reinterpret_cast<uint16_t*>(base + b_rp);
+    uint16_t* dcnt = reinterpret_cast<uint16_t*>(base + b_rp + b_e);
+    size_t tmp = 0;
+    CU(gf::theta_rowptr(s, nullptr, nullptr, &tmp), "get_theta");
+    if (tmp > b_e) {                          // scan temp space: reuse the counts slot only if it fits
+        if (int rc = dev_scratch(s, b_rp + 2 * b_e + al256(tmp), &base)) return rc;
+        drp = reinterpret_cast<int64_t*>(base);
+        dids = reinterpret_cast<uint16_t*>(base + b_rp);
+        dcnt = reinterpret_cast<uint16_t*>(base + b_rp + b_e);
+    }
+    void* tmpp = tmp > b_e ? (void*)(base + b_rp + 2 * b_e) : (void*)dcnt;
+    CU(gf::theta_rowptr(s, drp, tmpp, &tmp), "get_theta");
     cudaError_t e = gf::launch_theta_export(s, drp, dids, dcnt);
-    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(ids, dids, nnz * 2, cudaMemcpyDeviceToHost, s->stream);
-    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(cnts, dcnt, nnz * 2, cudaMemcpyDeviceToHost, s->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
-    cudaFree(drp);
-    cudaFree(dids);
+    if (e == cudaSuccess) e = gf::xfer_d2h(row_ptr, drp, (s->D + 1) * 8, s->stream);
+    if (e == cudaSuccess && nnz) e = gf::xfer_d2h(ids, dids, nnz * 2, s->stream);
+    if (e == cudaSuccess && nnz) e = gf::xfer_d2h(cnts, dcnt, nnz * 2, s->stream);
     if (e != cudaSuccess) return cuda_fail(e, "get_theta");
     return GF_OK;
 }
@@ -693,21 +730,20 @@ int gf_shard_set_theta(gf_shard* s, const int64_t* row_ptr, const uint16_t* ids,
     if (nnz < 0) return fail(GF_ERR_SHAPE, "theta row_ptr is not non-decreasing");
     const int64_t nn = std::max<int64_t>(nnz, 1);
     char* base = nullptr;
-    const size_t b_rp = ((s->D + 1) * 8 + 15) & ~(size_t)15, b_e = ((size_t)nn * 2 + 15) & ~(size_t)15;
-    CU(cudaMalloc(&base, b_rp + 2 * b_e + 16), "set_theta");
+    const size_t b_rp = al256((s->D + 1) * 8), b_e = al256((size_t)nn * 2);
+    if (int rc = dev_scratch(s, b_rp + 2 * b_e + 16, &base)) return rc;
     int64_t* drp = reinterpret_cast<int64_t*>(base);
     uint16_t* dids = reinterpret_cast<uint16_t*>(base + b_rp);
     uint16_t* dcnt = reinterpret_cast<uint16_t*>(base + b_rp + b_e);
     unsigned long long* dfirst = reinterpret_cast<unsigned long long*>(base + b_rp + 2 * b_e);
     unsigned long long first = ~0ull;
-    cudaError_t e = cudaMemcpyAsync(drp, row_ptr, (s->D + 1) * 8, cudaMemcpyHostToDevice, s->stream);
-    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(dids, ids, nnz * 2, cudaMemcpyHostToDevice, s->stream);
-    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(dcnt, cnts, nnz * 2, cudaMemcpyHostToDevice, s->stream);
+    cudaError_t e = gf::xfer_h2d(drp, row_ptr, (s->D + 1) * 8, s->stream);
+    if (e == cudaSuccess && nnz) e = gf::xfer_h2d(dids, ids, nnz * 2, s->stream);
+    if (e == cudaSuccess && nnz) e = gf::xfer_h2d(dcnt, cnts, nnz * 2, s->stream);
     if (e == cudaSuccess) e = gf::launch_theta_validate(s, drp, dids, dcnt, dfirst);
     if (e == cudaSuccess) e = cudaMemcpyAsync(&first, dfirst, 8, cudaMemcpyDeviceToHost, s->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e == cudaSuccess && first != ~0ull) {
-        cudaFree(base);
         const long long d = (long long)(first >> 34);
         const uint64_t low = first & ((1ull << 34) - 1);
         if (low == 0) {
@@ -722,7 +758,6 @@ int gf_shard_set_theta(gf_shard* s, const int64_t* row_ptr, const uint16_t* ids,
     }
     if (e == cudaSuccess) e = gf::launch_theta_import(s, drp, dids, dcnt);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
-    cudaFree(base);
     if (e != cudaSuccess) return cuda_fail(e, "set_theta");
     s->stale_theta = true;
     return GF_OK;
@@ -732,18 +767,12 @@ int gf_shard_set_theta(gf_shard* s, const int64_t* row_ptr, const uint16_t* ids,
 // checks and the 16-bit narrowing run before anything crosses PCIe
 static int phi_export_device(gf_shard* s, uint32_t** dout, int32_t** dcol) {
     const size_t cells = (size_t)s->K * s->V;
-    *dout = nullptr;
-    *dcol = nullptr;
-    CU(cudaMalloc(dout, cells * 4 + 16), "phi export");
-    cudaError_t e = cudaMalloc(dcol, (size_t)s->V * 4);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(*dcol, s->word_col.data(), (size_t)s->V * 4, cudaMemcpyHostToDevice, s->stream);
-    if (e == cudaSuccess) e = gf::launch_phi_export(s, *dout, 32, *dcol);
-    if (e != cudaSuccess) {
-        cudaFree(*dout);
-        if (*dcol) cudaFree(*dcol);
-        return cuda_fail(e, "phi export");
-    }
+    char* base = nullptr;
+    if (int rc = dev_scratch(s, al256(cells * 4 + 16) + al256((size_t)s->V * 4), &base)) return rc;
+    *dout = reinterpret_cast<uint32_t*>(base);
+    *dcol = reinterpret_cast<int32_t*>(base + al256(cells * 4 + 16));
+    CU(cudaMemcpyAsync(*dcol, s->word_col.data(), (size_t)s->V * 4, cudaMemcpyHostToDevice, s->stream), "phi export");
+    CU(gf::launch_phi_export(s, *dout, 32, *dcol), "phi export");
     return GF_OK;
 }
 
@@ -786,12 +815,10 @@ int gf_shard_get_phi_w(gf_shard* s, void* counts_kv, int32_t width, int64_t* tot
     }
     std::vector<uint32_t> nk((size_t)s->K);
     cudaError_t e = cudaSuccess;
-    if (rc == GF_OK) e = cudaMemcpyAsync(counts_kv, dout, cells * (width / 8), cudaMemcpyDeviceToHost, s->stream);
+    if (rc == GF_OK) e = gf::xfer_d2h(counts_kv, dout, cells * (width / 8), s->stream);
     if (rc == GF_OK && e == cudaSuccess)
         e = cudaMemcpyAsync(nk.data(), s->d.sync + s->off_nk_u32, (size_t)s->K * 4, cudaMemcpyDeviceToHost, s->stream);
     if (rc == GF_OK && e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
-    cudaFree(dout);
-    cudaFree(dcol);
     if (rc != GF_OK) return rc;
     if (e != cudaSuccess) return cuda_fail(e, "get_phi");
     for (int k = 0; k < s->K; ++k) totals[k] = nk[k];
@@ -808,17 +835,18 @@ int gf_shard_set_phi_w(gf_shard* s, const void* counts_kv, int32_t width, const 
     for (int k = 0; k < s->K; ++k)
         if (totals[k] < 0 || totals[k] > (int64_t)UINT32_MAX) return fail(GF_ERR_OVERFLOW, "topic total out of range");
     const size_t cells = (size_t)s->K * s->V;
-    void* din = nullptr;
-    int32_t* dcol = nullptr;
-    CU(cudaMalloc(&din, cells * (width / 8) + 16), "set_phi");
-    cudaError_t e = cudaMalloc(&dcol, (size_t)s->V * 4 + 32);
-    if (e != cudaSuccess) { cudaFree(din); return cuda_fail(e, "set_phi"); }
+    char* base = nullptr;
+    const size_t b_in = al256(cells * (width / 8) + 16);
+    if (int rc = dev_scratch(s, b_in + al256((size_t)s->V * 4 + 32), &base)) return rc;
+    void* din = base;
+    int32_t* dcol = reinterpret_cast<int32_t*>(base + b_in);
+    cudaError_t e = cudaSuccess;
     unsigned long long* dfirst = reinterpret_cast<unsigned long long*>(dcol + ((s->V + 3) & ~3));
     std::vector<uint32_t> nk((size_t)s->K);
     for (int k = 0; k < s->K; ++k) nk[k] = (uint32_t)totals[k];
     unsigned long long first = ~0ull;
     e = cudaMemcpyAsync(dcol, s->word_col.data(), (size_t)s->V * 4, cudaMemcpyHostToDevice, s->stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(din, counts_kv, cells * (width / 8), cudaMemcpyHostToDevice, s->stream);
+    if (e == cudaSuccess) e = gf::xfer_h2d(din, counts_kv, cells * (width / 8), s->stream);
     // a light (16-bit) column must not receive a cell above 65535: checked on the
     // device before anything is written (first cell in word-major order)
     if (width == 32) {
@@ -827,8 +855,6 @@ int gf_shard_set_phi_w(gf_shard* s, const void* counts_kv, int32_t width, const 
         if (e == cudaSuccess) e = cudaMemcpyAsync(&first, dfirst, 8, cudaMemcpyDeviceToHost, s->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
         if (e == cudaSuccess && first != ~0ull) {
-            cudaFree(din);
-            cudaFree(dcol);
             const int v = (int)(first / s->K), k = (int)(first % s->K);
             return fail(GF_ERR_OVERFLOW, "phi cell (topic %d, word %d) count %u exceeds its 16-bit column", k, v,
                         ((const uint32_t*)counts_kv)[(size_t)k * s->V + v]);
@@ -839,8 +865,6 @@ int gf_shard_set_phi_w(gf_shard* s, const void* counts_kv, int32_t width, const 
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(s->d.sync + s->off_nk_u32, nk.data(), (size_t)s->K * 4, cudaMemcpyHostToDevice, s->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
-    cudaFree(din);
-    cudaFree(dcol);
     if (e != cudaSuccess) return cuda_fail(e, "set_phi");
     s->stale_phi = true;
     s->ctx_dirty = true;                     // denominators and word contexts follow the new phi
@@ -858,10 +882,7 @@ int gf_shard_phi_argmax(gf_shard* s, int64_t* max_count, int32_t* topic, int32_t
     uint32_t* dout = nullptr;
     int32_t* dcol = nullptr;
     if (int rc = phi_export_device(s, &dout, &dcol)) return rc;
-    const int rc = phi_argmax_device(s, dout, max_count, topic, word);
-    cudaFree(dout);
-    cudaFree(dcol);
-    return rc;
+    return phi_argmax_device(s, dout, max_count, topic, word);
 }
 
 // ------------------------------------------------- K5 conservation ------

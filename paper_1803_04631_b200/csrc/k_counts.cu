@@ -8,6 +8,9 @@
 #include "gf_internal.cuh"
 #include "gf_device.cuh"
 
+#include <cub/cub.cuh>
+#include <thrust/iterator/transform_iterator.h>
+
 namespace gf {
 
 // ---------------------------------------------------------------- K2 ------
@@ -600,6 +603,20 @@ cudaError_t launch_theta_validate(gf_shard* s, const int64_t* d_rowptr, const ui
     theta_validate_kernel<<<8 * nsm, 256, 0, s->stream>>>((int)s->D, s->d.theta_meta, (uint32_t)s->theta_cap,
                                                           d_rowptr, d_ids, d_cnt, s->K, d_first);
     return cudaGetLastError();
+}
+
+// row_ptr of the exported CSR on the device: d_rowptr[0] = 0, d_rowptr[d+1] =
+// sum of nnz over rows <= d (an inclusive scan of theta_meta[].y)
+struct MetaNnz {
+    __device__ int64_t operator()(const uint2& m) const { return (int64_t)m.y; }
+};
+
+cudaError_t theta_rowptr(gf_shard* s, int64_t* d_rowptr, void* tmp, size_t* tmp_bytes) {
+    const auto in = thrust::make_transform_iterator(s->d.theta_meta, MetaNnz());
+    if (!tmp) return cub::DeviceScan::InclusiveSum(nullptr, *tmp_bytes, in, d_rowptr + 1, (int)s->D, s->stream);
+    cudaError_t e = cudaMemsetAsync(d_rowptr, 0, 8, s->stream);
+    if (e != cudaSuccess || s->D == 0) return e;
+    return cub::DeviceScan::InclusiveSum(tmp, *tmp_bytes, in, d_rowptr + 1, (int)s->D, s->stream);
 }
 
 cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt) {

@@ -362,11 +362,10 @@ class DeviceShard:
         nnz = ctypes.c_int64()
         _lib.check(_lib.lib().gf_shard_theta_nnz(self._h, ctypes.byref(nnz)))
         rp = np.empty(self.num_docs + 1, np.int64)
-        ids = np.empty(max(nnz.value, 1), np.uint16)
-        cn = np.empty(max(nnz.value, 1), np.uint16)
+        ids = np.empty(nnz.value, np.uint16)
+        cn = np.empty(nnz.value, np.uint16)
         _lib.check(_lib.lib().gf_shard_get_theta(self._h, _lib.ptr(rp), _lib.ptr(ids), _lib.ptr(cn)))
-        n = int(rp[-1])
-        return rp, ids[:n].copy(), cn[:n].copy()
+        return rp, ids, cn
 
     def set_theta(self, row_ptr, topic_ids, counts):
         rp = _lib.carr(row_ptr, np.int64)
