@@ -88,6 +88,94 @@ __global__ void __launch_bounds__(256) k5_theta_kernel(Rows rows, int64_t D, int
     }
 }
 
+// The resident rows, one THREAD per document: a row starts on a 32-byte
+// boundary and is zero-padded to whole 8-entry granules (K3 / theta import),
+// so it is read as ceil(nnz / 8) pairs of 16-byte loads; the zero pads add
+// nothing.  Column sums: shared K-bin histogram (per-CTA u32, flushed as u64).
+__global__ void __launch_bounds__(256) k5_theta_shard_kernel(const uint2* __restrict__ meta,
+                                                             const uint32_t* __restrict__ ent,
+                                                             const uint32_t* __restrict__ dw_ptr, int64_t D, int K,
+                                                             TPos tm, bool smem_hist, unsigned long long* col,
+                                                             unsigned long long* bad_doc) {
+    extern __shared__ uint32_t hist[];
+    if (smem_hist) {
+        for (int k = threadIdx.x; k < K; k += blockDim.x) hist[k] = 0u;
+        __syncthreads();
+    }
+    for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x) {
+        const uint2 m = meta[d];
+        const uint4* row = reinterpret_cast<const uint4*>(ent + m.x);
+        unsigned long long sum = 0;
+        for (uint32_t g = 0; g < (m.y + 7u) >> 3; ++g) {
+            const uint4 a = __ldg(row + 2 * g), b = __ldg(row + 2 * g + 1);
+            const uint32_t e[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t c = e[i] >> 16;
+                if (c) {
+                    sum += c;
+                    const uint32_t k = tpos_inv((e[i] & 0xffffu) >> 2, tm);
+                    if (k < (uint32_t)K) {
+                        if (smem_hist) atomicAdd(hist + k, c);
+                        else atomicAdd(col + k, (unsigned long long)c);
+                    }
+                }
+            }
+        }
+        if ((int64_t)sum != (int64_t)(dw_ptr[d + 1] - dw_ptr[d])) atomicMin(bad_doc, (unsigned long long)d);
+    }
+    if (smem_hist) {
+        __syncthreads();
+        for (int k = threadIdx.x; k < K; k += blockDim.x)
+            if (hist[k]) atomicAdd(col + k, (unsigned long long)hist[k]);
+    }
+}
+
+// phi row sums, vectorised: every column is a contiguous K-vector starting on
+// a 16-byte boundary; thread j of the CTA owns 16-byte slot j (+ SPT-1 more
+// slots blockDim apart) of every column the CTA visits and sums it in u32
+// registers (a topic's sum over any set of columns is <= n_k < 2^32), flushed
+// once per CTA with u64 atomics.
+template <typename T, int SPT>
+__global__ void __launch_bounds__(256) k5_phi_vec_kernel(const uint4* __restrict__ cols, int64_t ncol, int slots,
+                                                         int K, unsigned long long* row) {
+    constexpr int E = 16 / sizeof(T);
+    uint32_t acc[SPT][E];
+#pragma unroll
+    for (int s = 0; s < SPT; ++s)
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[s][e] = 0u;
+    for (int64_t c = blockIdx.x; c < ncol; c += gridDim.x) {
+        const uint4* p = cols + c * (int64_t)slots;
+#pragma unroll
+        for (int s = 0; s < SPT; ++s) {
+            const int j = threadIdx.x + s * blockDim.x;
+            if (j < slots) {
+                const uint4 v = __ldg(p + j);
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (E == 8) {
+                        acc[s][2 * q] += w[q] & 0xffffu;
+                        acc[s][2 * q + 1] += w[q] >> 16;
+                    } else {
+                        acc[s][q] += w[q];
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < SPT; ++s) {
+        const int j = threadIdx.x + s * blockDim.x;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int k = j * E + e;
+            if (j < slots && k < K && acc[s][e]) atomicAdd(row + k, (unsigned long long)acc[s][e]);
+        }
+    }
+}
+
 // phi row sums over the shard's word-major hybrid columns: heavy u32 columns
 // (stride K) then light u16 columns (stride Kp); thread t owns topics t + i*NT
 template <typename T>
@@ -197,6 +285,20 @@ template <typename T>
 static cudaError_t phi_cols_pass(const T* cols, int64_t ncol, int stride, int K, unsigned long long* row,
                                  cudaStream_t st) {
     if (ncol == 0) return cudaSuccess;
+    constexpr int E = 16 / sizeof(T);
+    const int slots = (stride + E - 1) / E;
+    const bool vec = stride % E == 0 && (reinterpret_cast<uintptr_t>(cols) & 15) == 0 && slots <= 8 * 256;
+    if (vec) {
+        const int nt = std::min(256, (slots + 31) / 32 * 32);
+        const int spt = (slots + nt - 1) / nt;
+        const int64_t blocks = std::min<int64_t>(ncol, 4LL * sm_count());
+        const uint4* c4 = reinterpret_cast<const uint4*>(cols);
+        if (spt == 1) k5_phi_vec_kernel<T, 1><<<(unsigned)blocks, nt, 0, st>>>(c4, ncol, slots, K, row);
+        else if (spt == 2) k5_phi_vec_kernel<T, 2><<<(unsigned)blocks, nt, 0, st>>>(c4, ncol, slots, K, row);
+        else if (spt <= 4) k5_phi_vec_kernel<T, 4><<<(unsigned)blocks, nt, 0, st>>>(c4, ncol, slots, K, row);
+        else k5_phi_vec_kernel<T, 8><<<(unsigned)blocks, nt, 0, st>>>(c4, ncol, slots, K, row);
+        return cudaGetLastError();
+    }
     const size_t smem = (size_t)K * 8;
     static unsigned long long attr = 0;
     int dev = 0;
@@ -206,7 +308,7 @@ static cudaError_t phi_cols_pass(const T* cols, int64_t ncol, int stride, int K,
                                              200 * 1024);
         if (e != cudaSuccess) return e;
     }
-    if (smem > 200 * 1024) return cudaErrorInvalidValue;   // K > 25600: rejected by the caller
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;   // K > 25600 (the shard caps K at 16384)
     const int64_t blocks = std::min<int64_t>(ncol, 2LL * sm_count());
     k5_phi_cols_kernel<T><<<(unsigned)blocks, 256, smem, st>>>(cols, ncol, stride, K, row);
     return cudaGetLastError();
@@ -222,7 +324,13 @@ cudaError_t launch_conservation_stage1(gf_shard* s, unsigned long long* scratch,
     cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(unsigned long long) * 2 * K, s->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0xff, 8, s->stream);
     const ShardRows rows{s->d.theta_meta, s->d.theta_ent, s->d.dw_ptr, tpos_geom(K)};
-    if (e == cudaSuccess) e = theta_pass(rows, s->D, K, col, bad, s->stream);
+    if (e == cudaSuccess && s->D > 0) {
+        const bool smem_hist = (size_t)K * 4 <= 48 * 1024;
+        const int64_t blocks = std::min<int64_t>((s->D + 255) / 256, 8LL * sm_count());
+        k5_theta_shard_kernel<<<(unsigned)blocks, 256, smem_hist ? (size_t)K * 4 : 0, s->stream>>>(
+            s->d.theta_meta, s->d.theta_ent, s->d.dw_ptr, s->D, K, tpos_geom(K), smem_hist, col, bad);
+        e = cudaGetLastError();
+    }
     if (e == cudaSuccess) e = phi_cols_pass(s->d.sync, s->n_heavy, K, K, row, s->stream);
     if (e == cudaSuccess)
         e = phi_cols_pass(reinterpret_cast<const uint16_t*>(s->d.sync + s->off_phi16_u32), s->n_light,
