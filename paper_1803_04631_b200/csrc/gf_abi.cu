@@ -85,7 +85,7 @@ void free_dev(gf_shard* s) {
     auto& d = s->d;
     void* ptrs[] = {d.z, d.zstage, d.run_doc, d.run_start, d.slices, d.k2items, d.dw_ptr, d.zdoc, d.run_dwpos, d.run_rec, d.theta_ent,
                     d.theta_meta, d.sync, d.inv_den, d.ctx_tab, d.ctx_cols, d.slice_ctx, d.ll_part, d.ll_sum,
-                    d.errs, d.bytes, d.scratch, d.k5, d.bigdocs};
+                    d.errs, d.bytes, d.scratch, d.k5};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     d = gf::ShardDev{};

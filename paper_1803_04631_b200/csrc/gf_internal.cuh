@@ -65,7 +65,6 @@ struct ShardDev {
     unsigned long long* bytes = nullptr;     // [0] sum over runs of nnz (sampler bytes model), [1] import flag
     uint32_t* scratch = nullptr;             // export staging
     size_t scratch_bytes = 0;
-    uint32_t* bigdocs = nullptr;             // local docs longer than 65535 tokens (K3's 32-bit side path)
     unsigned long long* k5 = nullptr;        // K5 conservation: [K] theta column sums | [K] phi row sums |
                                              // first bad doc | report (int64 x 4); allocated on first use
 };
@@ -102,7 +101,6 @@ struct gf_shard {
     int64_t off_phi16_u32 = 0, off_nk_u32 = 0, sync_u32 = 0;
     int64_t doc_lo = 0, doc_hi = 0, D = 0, T = 0, R = 0, n_slices = 0, n_k2 = 0;
     int64_t theta_cap = 0;
-    int64_t n_big = 0;                       // documents longer than 65535 tokens
     int64_t n_doc_blocks = 1;
     // sampling phases (gf_shard_set_phases): the slice schedule is phase-major;
     // phase p owns the word groups whose tokens are z[phase_tok0[p], phase_tok0[p+1])

@@ -194,56 +194,35 @@ cudaError_t launch_prepare(gf_shard* s) {
 }
 
 // ---------------------------------------------------------------- K3 ------
-// One warp per document, persistent grid (the warps sweep the documents as
-// one moving window).  The warp's shared slice holds a K-bin histogram of
-// PACKED 16-bit bins (two per u32 word: a document of <= 65535 tokens cannot
-// carry into its neighbour; longer documents go to theta_big_kernel with
-// 32-bit bins), a K-bit presence bitmap and, for K > 1024, the distinct-topic
-// prefix of every bitmap word (section 6.2: "generate a dense array
-// ... then CSR").  Bins and bitmap are zero between documents: each document
-// clears exactly what it touched.
-//  <= 128 tokens: the topics stay in registers (ncol = ceil(L / 32) columns,
-//    warp-uniform).  Count: every token adds to its bin and sets its bitmap
-//    bit.  Emit: the rank of topic k = distinct topics below it = bitmap-word
-//    prefix + popc inside the word; exactly one token per topic wins the
-//    atomicAnd that clears its half-word (it gets the count) and writes the
-//    entry.
-//  longer: the count streams zdoc; each lane then emits the topics of its
-//    bitmap word in ascending order at the word's prefix -- O(L + K/32) per
-//    document instead of O(K).
-// Output rows: (count << 16 | tpos(topic) << 2) (the topic pre-scaled to a
-// byte offset into K1's shared p* table), ascending topic, in the
-// fixed-capacity row, zero-padded to 8 entries; nnz into meta.y.  Topics come
-// from zdoc (contiguous per document), not a gather through the dw-map.
+// One warp per document.  Short documents (<= 32 tokens): the topics are
+// gathered through the doc-word map into one register per lane, bitonic-sorted
+// across the warp and run-length encoded with ballots (no K-sized state).
+// Longer documents: K-bin histogram plus a K-bit presence bitmap in the warp's
+// shared-memory slice (section 6.2 "generate a dense array ... then
+// CSR"); the output rank of topic k is popc of the bitmap below k (one warp
+// scan over the K/32 bitmap words), so each lane emits the topics of its
+// bitmap word in ascending order and clears exactly the bins it touched --
+// O(L + K/32) per document instead of O(K).  Bins and bitmap are zeroed once
+// per CTA and kept zero between documents.  Output rows: (count << 16 |
+// topic << 2) (the topic pre-scaled to a byte offset into K1's shared p*
+// table), ascending topic, in the fixed-capacity row; nnz into meta.y.
 __host__ __device__ inline int k3_words(int K) { return (K + 31) >> 5; }
-__host__ __device__ inline int k3_bins(int K) { return (K + 1) >> 1; }
-__host__ __device__ inline int k3_warp_u32(int K) { return k3_bins(K) + 2 * k3_words(K); }   // bins | bitmap | prefixes
+__host__ __device__ inline int k3_warp_u32(int K) { return K + 2 * k3_words(K); }   // bins | bitmap | word ranks
 
-__device__ __forceinline__ void k3_count(uint32_t* bins, uint32_t* bmp, uint32_t k) {
-    atomicAdd(&bins[k >> 1], 1u << ((k & 1u) << 4));
-    atomicOr(&bmp[k >> 5], 1u << (k & 31u));
-}
-
-// take topic k's count and clear its half-word (one caller per topic gets it)
-__device__ __forceinline__ uint32_t k3_take(uint32_t* bins, uint32_t k) {
-    const uint32_t sh = (k & 1u) << 4;
-    return (atomicAnd(&bins[k >> 1], ~(0xffffu << sh)) >> sh) & 0xffffu;
-}
-
-template <int MINB>
-__global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
-                                                                  const uint16_t* __restrict__ zdoc,
-                                                                  uint32_t* theta_ent, uint2* theta_meta, int K,
-                                                                  int warps_per_cta, unsigned long long* errs) {
+__global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
+                                                            const uint16_t* __restrict__ zdoc, uint32_t* theta_ent,
+                                                            uint2* theta_meta, int K, int warps_per_cta,
+                                                            unsigned long long* errs) {
     extern __shared__ uint32_t sh[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int NW = k3_words(K);
     const TPos tm = tpos_geom(K);
     uint32_t* bins = sh + (size_t)warp * k3_warp_u32(K);
-    uint32_t* bmp = bins + k3_bins(K);
+    uint32_t* bmp = bins + K;
     uint32_t* wpre = bmp + NW;                     // distinct topics below each bitmap word
-    for (int i = lane; i < k3_bins(K) + NW; i += 32) bins[i] = 0u;
+    for (int i = lane; i < K + NW; i += 32) bins[i] = 0u;
     __syncwarp();
+    const unsigned lt = (1u << lane) - 1u;
     // software pipeline over this warp's documents d, d+s, d+2s: the next
     // document's first 32 topics and the one after's (dw_ptr, meta) are in
     // flight while the current one is counted
@@ -261,13 +240,30 @@ __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const u
         uint32_t b2, L2, o2;
         meta_of(d + 2 * s, b2, L2, o2);
         const uint32_t zn = (d + s < D && (uint32_t)lane < L1) ? zdoc[b1 + lane] : 0xffffu;
-        uint32_t nnz = 0;
-        bool own = true;
-        if (L > 65535u) {
-            own = false;                           // theta_big_kernel writes this row
+        uint32_t nnz;
+        if (L <= 32) {
+            uint32_t key = 0xffffu;
+            if (lane < (int)L) key = zf;
+            if (key >= (uint32_t)K && lane < (int)L) { atomicMin(errs + 2, (unsigned long long)d); key = 0xffffu; }
+            key = warp_bitonic_sort(key, lane);
+            const uint32_t prev = __shfl_up_sync(kFull, key, 1);
+            const bool head = key != 0xffffu && (lane == 0 || key != prev);
+            const unsigned heads = __ballot_sync(kFull, head);
+            if (head) {
+                const unsigned later = heads & ~((2u << lane) - 1u);
+                const uint32_t next = later ? (uint32_t)(__ffs(later) - 1) : L;
+                theta_ent[off + __popc(heads & lt)] = (tpos(key, tm) << 2) | ((next - lane) << 16);
+            }
+            nnz = __popc(heads);
         } else if (L <= 128) {
+            // 32 < L <= 128, the tokens stay in registers (ncol = ceil(L / 32)
+            // columns, warp-uniform).  Count: every token adds to its bin and
+            // sets its bitmap bit (no returned values, no branches).  Emit: the
+            // rank of topic k = distinct topics below it = word prefix + popc
+            // inside the word; one token per topic wins atomicExch(bin, 0) (it
+            // gets the count and clears the bin) and writes the entry.
             const uint32_t ncol = (L + 31u) >> 5;
-            uint32_t kk[4] = {(uint32_t)lane < L ? zf : 0xffffu, 0xffffu, 0xffffu, 0xffffu};
+            uint32_t kk[4] = {zf, 0xffffu, 0xffffu, 0xffffu};
 #pragma unroll
             for (uint32_t j = 1; j < 4; ++j)
                 if (j < ncol && lane + 32u * j < L) kk[j] = zdoc[b + lane + 32u * j];
@@ -275,7 +271,8 @@ __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const u
             for (uint32_t j = 0; j < 4; ++j) {
                 const uint32_t k = kk[j];
                 if (j < ncol && k < (uint32_t)K) {
-                    k3_count(bins, bmp, k);
+                    atomicAdd(&bins[k], 1u);
+                    atomicOr(&bmp[k >> 5], 1u << (k & 31u));
                 } else if (j < ncol && k != 0xffffu) {
                     atomicMin(errs + 2, (unsigned long long)d);
                     kk[j] = 0xffffu;
@@ -301,7 +298,7 @@ __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const u
                     if (j < ncol) {
                         const uint32_t k = kk[j], w = (k >> 5) & 31u;
                         const uint32_t ww = __shfl_sync(kFull, word, w), pw = __shfl_sync(kFull, pre, w);
-                        const uint32_t c = k < (uint32_t)K ? k3_take(bins, k) : 0u;
+                        const uint32_t c = k < (uint32_t)K ? atomicExch(&bins[k], 0u) : 0u;
                         if (c)
                             theta_ent[off + pw + __popc(ww & ((1u << (k & 31u)) - 1u))] =
                                 (tpos(k, tm) << 2) | (c << 16);               // <= 128: no overflow
@@ -326,7 +323,7 @@ __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const u
 #pragma unroll
                 for (uint32_t j = 0; j < 4; ++j) {
                     const uint32_t k = kk[j];
-                    const uint32_t c = (j < ncol && k < (uint32_t)K) ? k3_take(bins, k) : 0u;
+                    const uint32_t c = (j < ncol && k < (uint32_t)K) ? atomicExch(&bins[k], 0u) : 0u;
                     if (c) {
                         const uint32_t w = k >> 5;
                         theta_ent[off + wpre[w] + __popc(bmp[w] & ((1u << (k & 31u)) - 1u))] =
@@ -341,20 +338,24 @@ __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const u
             __syncwarp();
         } else {
             auto count = [&](uint32_t k) {
-                if (k < (uint32_t)K) k3_count(bins, bmp, k);
-                else atomicMin(errs + 2, (unsigned long long)d);
+                if (k < (uint32_t)K) {
+                    atomicAdd(&bins[k], 1u);
+                    atomicOr(&bmp[k >> 5], 1u << (k & 31u));
+                } else {
+                    atomicMin(errs + 2, (unsigned long long)d);
+                }
             };
             // the next 96 topics load together (independent), then count
             const uint32_t i1 = lane + 32u, i2 = lane + 64u, i3 = lane + 96u;
             const uint32_t k1 = i1 < L ? zdoc[b + i1] : 0u, k2 = i2 < L ? zdoc[b + i2] : 0u,
                            k3 = i3 < L ? zdoc[b + i3] : 0u;
-            count(zf);                                          // L > 128: every lane has one
-            count(k1);
-            count(k2);
-            count(k3);
+            count(zf);                                          // L > 32: every lane has one
+            if (i1 < L) count(k1);
+            if (i2 < L) count(k2);
+            if (i3 < L) count(k3);
             for (uint32_t i = lane + 128u; i < L; i += 32) count(zdoc[b + i]);
             __syncwarp();
-            uint32_t base = 0;
+            uint32_t base = 0, mx = 0;
             for (int c = 0; c < NW; c += 32) {
                 const int w = c + lane;
                 uint32_t word = w < NW ? bmp[w] : 0u;
@@ -367,95 +368,29 @@ __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const u
                 }
                 uint32_t pos = off + base + incl - pc;
                 if (w < NW) bmp[w] = 0u;
-                // this lane owns topics [32w, 32w + 32): bins words [16w, 16w + 16)
                 while (word) {
                     const uint32_t k = ((uint32_t)w << 5) + (uint32_t)(__ffs(word) - 1);
                     word &= word - 1u;
-                    const uint32_t pair = bins[k >> 1];
-                    const uint32_t v = (pair >> ((k & 1u) << 4)) & 0xffffu;
-                    // clear the pair once both halves are read (k odd, or k + 1 absent)
-                    if ((k & 1u) || !((word >> ((k + 1u) & 31u)) & 1u)) bins[k >> 1] = 0u;
-                    theta_ent[pos++] = (tpos(k, tm) << 2) | (v << 16);     // L <= 65535: v fits
+                    const uint32_t v = bins[k];
+                    bins[k] = 0u;
+                    theta_ent[pos++] = (tpos(k, tm) << 2) | (min(v, 65535u) << 16);
+                    mx = max(mx, v);
                 }
                 base += __shfl_sync(kFull, incl, 31);
             }
             nnz = base;
+            mx = warp_max_u32(mx);
+            if (mx > 65535u && lane == 0) atomicMin(errs + 1, ((unsigned long long)d << 32) | mx);
             __syncwarp();
         }
-        if (own) {
-            // zero the row's padding up to a multiple of 8 entries: K1 reads rows
-            // as 32-byte granules and relies on (count 0) pads contributing nothing
-            if ((uint32_t)lane < ((8u - (nnz & 7u)) & 7u)) theta_ent[off + nnz + lane] = 0u;
-            if (lane == 0) theta_meta[d].y = nnz;
-        }
+        // zero the row's padding up to a multiple of 8 entries: K1 reads rows
+        // as 32-byte granules and relies on (count 0) pads contributing nothing
+        if ((uint32_t)lane < ((8u - (nnz & 7u)) & 7u)) theta_ent[off + nnz + lane] = 0u;
+        if (lane == 0) theta_meta[d].y = nnz;
         b = b1; L = L1; off = o1;
         b1 = b2; L1 = L2; o1 = o2;
         zf = zn;
     }
-}
-
-// Documents longer than 65535 tokens (rare; a 16-bit bin could overflow):
-// one CTA per document, 32-bit shared bins, warp 0 emits the nonzero bins in
-// topic order by ballot and reports a count above 65535 (model.py:91-106's
-// CountOverflowError) as errs[1] = d << 32 | max count.
-__global__ void __launch_bounds__(256) theta_big_kernel(const uint32_t* __restrict__ big, int nbig,
-                                                        const uint32_t* __restrict__ dw_ptr,
-                                                        const uint16_t* __restrict__ zdoc, uint32_t* theta_ent,
-                                                        uint2* theta_meta, int K, unsigned long long* errs) {
-    extern __shared__ uint32_t bins32[];
-    const TPos tm = tpos_geom(K);
-    for (int i = blockIdx.x; i < nbig; i += gridDim.x) {
-        const uint32_t d = big[i];
-        for (int k = threadIdx.x; k < K; k += blockDim.x) bins32[k] = 0u;
-        __syncthreads();
-        const uint32_t b = dw_ptr[d], L = dw_ptr[d + 1] - b;
-        for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
-            const uint32_t k = zdoc[b + t];
-            if (k < (uint32_t)K) atomicAdd(&bins32[k], 1u);
-            else atomicMin(errs + 2, (unsigned long long)d);
-        }
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            const int lane = threadIdx.x;
-            const uint32_t off = theta_meta[d].x;
-            uint32_t n = 0, mx = 0;
-            for (int k0 = 0; k0 < K; k0 += 32) {
-                const uint32_t k = (uint32_t)(k0 + lane);
-                const uint32_t v = k < (uint32_t)K ? bins32[k] : 0u;
-                const unsigned m = __ballot_sync(kFull, v != 0u);
-                if (v) theta_ent[off + n + __popc(m & ((1u << lane) - 1u))] = (tpos(k, tm) << 2) | (min(v, 65535u) << 16);
-                n += __popc(m);
-                mx = max(mx, v);
-            }
-            mx = warp_max_u32(mx);
-            if ((uint32_t)lane < ((8u - (n & 7u)) & 7u)) theta_ent[off + n + lane] = 0u;
-            if (lane == 0) {
-                theta_meta[d].y = n;
-                if (mx > 65535u) atomicMin(errs + 1, ((unsigned long long)d << 32) | mx);
-            }
-        }
-        __syncthreads();
-    }
-}
-
-template <int MINB>
-static cudaError_t theta_rebuild_variant(gf_shard* s, cudaStream_t st, int wpc, size_t smem) {
-    static unsigned long long attr = 0;
-    if (attr_once(attr, s->device)) {
-        cudaError_t e = cudaFuncSetAttribute(theta_rebuild_kernel<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             200 * 1024);
-        if (e != cudaSuccess) return e;
-    }
-    // persistent grid (exactly the resident CTAs): the warps sweep the
-    // documents as one contiguous moving window, so the word-major z sectors
-    // they gather are shared by neighbouring documents while still in L2
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, theta_rebuild_kernel<MINB>, wpc * 32, smem);
-    const long long need = (s->D + wpc - 1) / wpc;
-    const long long grid = std::min<long long>(need, (long long)sm_count(s->device) * std::max(per_sm, 1));
-    theta_rebuild_kernel<MINB><<<(unsigned)grid, wpc * 32, smem, st>>>(
-        (int)s->D, s->d.dw_ptr, s->d.zdoc, s->d.theta_ent, s->d.theta_meta, s->K, wpc, s->d.errs);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_theta_rebuild(gf_shard* s, cudaStream_t st) {
@@ -465,22 +400,24 @@ cudaError_t launch_theta_rebuild(gf_shard* s, cudaStream_t st) {
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * per_warp > 96 * 1024) wpc >>= 1;
     const size_t smem = (size_t)wpc * per_warp;
-    static int minb = -1;                       // tuning knob GF_K3_MINB (A/B runs)
-    if (minb < 0) minb = (int)shard_env_int("GF_K3_MINB", 5);
-    cudaError_t e = minb >= 8 ? theta_rebuild_variant<8>(s, st, wpc, smem)
-                  : minb >= 6 ? theta_rebuild_variant<6>(s, st, wpc, smem)
-                              : theta_rebuild_variant<5>(s, st, wpc, smem);
-    if (e == cudaSuccess && s->n_big > 0) {
-        static unsigned long long attr = 0;
-        if (attr_once(attr, s->device)) {
-            e = cudaFuncSetAttribute(theta_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            if (e != cudaSuccess) return e;
-        }
-        theta_big_kernel<<<(unsigned)std::min<int64_t>(s->n_big, sm_count(s->device)), 256, (size_t)s->K * 4, st>>>(
-            s->d.bigdocs, (int)s->n_big, s->d.dw_ptr, s->d.zdoc, s->d.theta_ent, s->d.theta_meta, s->K, s->d.errs);
-        e = cudaGetLastError();
+    static unsigned long long attr = 0;
+    if (attr_once(attr, s->device)) {
+        cudaError_t e = cudaFuncSetAttribute(theta_rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024);
+        if (e != cudaSuccess) return e;
     }
-    return e;
+    // persistent grid (exactly the resident CTAs): the warps sweep the
+    // documents as one contiguous moving window, so the word-major z sectors
+    // they gather are shared by neighbouring documents while still in L2
+    const int nsm = sm_count(s->device);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, theta_rebuild_kernel, wpc * 32, smem);
+    const long long need = (s->D + wpc - 1) / wpc;
+    const long long grid = std::min<long long>(need, (long long)nsm * std::max(per_sm, 1));
+    theta_rebuild_kernel<<<(unsigned)grid, wpc * 32, smem, st>>>((int)s->D, s->d.dw_ptr, s->d.zdoc,
+                                                                         s->d.theta_ent, s->d.theta_meta, s->K, wpc,
+                                                                         s->d.errs);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ zdoc sync ------

@@ -414,7 +414,6 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
     uint64_t cap = 0;
     double llc = 0.0;
     int32_t nblk = 0;
-    std::vector<uint32_t> big;                   // docs whose counts need 32-bit bins in K3
     {
         int64_t acc = 0;
         for (int64_t d = 0; d < D; ++d) {
@@ -427,7 +426,6 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
             doc_blk[d] = nblk;
             acc += 4 * ent;
             if (L > 0) llc += (double)L * std::log((double)L + (double)K * s->alpha);
-            if (L > 65535) big.push_back((uint32_t)d);
         }
         ++nblk;
     }
@@ -441,10 +439,8 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
         (rc = shard_alloc(&dv.theta_ent, cap + 8, "theta")) || (rc = shard_alloc(&dv.theta_meta, D, "theta")) ||
         (rc = shard_alloc(&dv.sync, s->sync_u32 + 1, "phi")) || (rc = shard_alloc(&dv.inv_den, 2 * K, "inv_den")) ||
         (rc = shard_alloc(&dv.ll_sum, kLlSlots, "ll")) || (rc = shard_alloc(&dv.errs, 4, "errs")) ||
-        (rc = shard_alloc(&dv.bytes, 2, "bytes")) || (rc = shard_alloc(&dv.bigdocs, big.size(), "theta")))
+        (rc = shard_alloc(&dv.bytes, 2, "bytes")))
         return rc;
-    if (!big.empty())
-        CK(cudaMemcpyAsync(dv.bigdocs, big.data(), big.size() * 4, cudaMemcpyHostToDevice, st), "layout");
     if (T > 0) {
         k_run_scatter<<<blocks_for(T), 256, 0, st>>>(c.doc, flag, rid, T, dv.run_start, dv.run_doc);
         CK(cudaMemcpyAsync(dv.z, c.z, T * 2, cudaMemcpyDeviceToDevice, st), "layout");
@@ -647,7 +643,6 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
     s->n_k2 = M;
     s->n_ctx = (int64_t)ctx_cols.size();
     s->n_doc_blocks = nblk;
-    s->n_big = (int64_t)big.size();
     s->ctx_dirty = true;
     s->theta_cap = (int64_t)cap;
     s->ll_const = llc;
