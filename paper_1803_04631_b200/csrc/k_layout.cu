@@ -294,10 +294,22 @@ struct DevChunk {
     uint32_t* go = nullptr;                   // [ng+1] group offsets (+ T)
 };
 
-int64_t read_u32(cudaStream_t st, const uint32_t* p) {
+// checked async calls: cudaError_t-returning helpers propagate, the ABI-facing
+// loaders turn a failure into the shard error text
+#define GF_TRY(call)                                         \
+    do {                                                     \
+        const cudaError_t _e = (call);                       \
+        if (_e != cudaSuccess) return _e;                    \
+    } while (0)
+#define GF_TRY_RC(call, what)                                \
+    do {                                                     \
+        const cudaError_t _e = (call);                       \
+        if (_e != cudaSuccess) return shard_cuda_fail(_e, what); \
+    } while (0)
+
+int64_t read_u32(cudaStream_t st, const uint32_t* p) {   // a failure leaves 0 and resurfaces at the next check
     uint32_t v = 0;
-    cudaMemcpyAsync(&v, p, 4, cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
+    if (cudaMemcpyAsync(&v, p, 4, cudaMemcpyDeviceToHost, st) == cudaSuccess) cudaStreamSynchronize(st);
     return v;
 }
 
@@ -341,9 +353,9 @@ cudaError_t partition_device(Scratch& sc, cudaStream_t st, const int32_t* d_doc,
     if (sc.err != cudaSuccess) return sc.err;
     if (n > 0) k_group_scatter<<<blocks_for(n), 256, 0, st>>>(c.word, ta, tb, n, c.gw, c.go);
     const uint32_t tn = (uint32_t)n;
-    cudaMemcpyAsync(c.go + c.ng, &tn, 4, cudaMemcpyHostToDevice, st);
+    GF_TRY(cudaMemcpyAsync(c.go + c.ng, &tn, 4, cudaMemcpyHostToDevice, st));
     // doc-word map: histogram -> dw_ptr; stable sort of positions by local doc -> dw_tok
-    cudaMemsetAsync(ta, 0, (size_t)(D + 1) * 4, st);
+    GF_TRY(cudaMemsetAsync(ta, 0, (size_t)(D + 1) * 4, st));
     if (n > 0) k_doc_hist<<<blocks_for(n), 256, 0, st>>>(c.doc, n, ta);
     e = cub_call(sc, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, ta, c.dw_ptr, D + 1, st); });
     if (e != cudaSuccess) return e;
@@ -719,7 +731,7 @@ int load_chunk(gf_shard* s, int64_t lo, int64_t hi, int64_t T, const int32_t* do
     CK(cudaStreamSynchronize(st), "load");
     if (e[0] != ~0ULL) {
         uint16_t zz = 0;
-        cudaMemcpy(&zz, c.z + e[0], 2, cudaMemcpyDeviceToHost);
+        CK(cudaMemcpy(&zz, c.z + e[0], 2, cudaMemcpyDeviceToHost), "load");
         return shard_fail(GF_ERR_SHAPE, "assignment %d at token %lld >= K=%d", (int)zz, (long long)e[0], s->K);
     }
     if (e[1] != ~0ULL)
@@ -740,16 +752,16 @@ int load_tokens(gf_shard* s, int64_t lo, int64_t hi, int64_t T, const int32_t* d
     int32_t* d_word = reinterpret_cast<int32_t*>(sc.u32(T));
     unsigned long long* errs = static_cast<unsigned long long*>(sc.get(16));
     if (sc.err != cudaSuccess) return shard_cuda_fail(sc.err, "load_tokens");
-    cudaMemsetAsync(errs, 0xff, 16, st);
+    GF_TRY_RC(cudaMemsetAsync(errs, 0xff, 16, st), "partition");
     if (T > 0) {
-        cudaMemcpyAsync(d_doc, doc_ids, T * 4, cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(d_word, word_ids, T * 4, cudaMemcpyHostToDevice, st);
+        GF_TRY_RC(cudaMemcpyAsync(d_doc, doc_ids, T * 4, cudaMemcpyHostToDevice, st), "partition");
+        GF_TRY_RC(cudaMemcpyAsync(d_word, word_ids, T * 4, cudaMemcpyHostToDevice, st), "partition");
     }
     DevChunk c;
     cudaError_t e = partition_device(sc, st, d_doc, d_word, T, lo, hi, s->V, s->K, zkey, c, errs);
     if (e != cudaSuccess) return shard_cuda_fail(e, "partition");
     unsigned long long he[2];
-    cudaMemcpyAsync(he, errs, 16, cudaMemcpyDeviceToHost, st);
+    GF_TRY_RC(cudaMemcpyAsync(he, errs, 16, cudaMemcpyDeviceToHost, st), "partition");
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return shard_cuda_fail(e, "partition");
     if (he[0] != ~0ULL) return shard_fail(GF_ERR_VALUE, "word id outside [0, vocab_size)");
     if (he[1] != ~0ULL) return shard_fail(GF_ERR_VALUE, "doc id %d outside chunk range", doc_ids[he[1]]);
@@ -769,16 +781,16 @@ int partition_to_host(int device, const int32_t* doc_ids, const int32_t* word_id
     int32_t* d_word = reinterpret_cast<int32_t*>(sc.u32(n));
     unsigned long long* errs = static_cast<unsigned long long*>(sc.get(16));
     if (sc.err != cudaSuccess) return shard_cuda_fail(sc.err, "partition");
-    cudaMemsetAsync(errs, 0xff, 16, st);
+    GF_TRY_RC(cudaMemsetAsync(errs, 0xff, 16, st), "partition");
     if (n > 0) {
-        cudaMemcpyAsync(d_doc, doc_ids, n * 4, cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(d_word, word_ids, n * 4, cudaMemcpyHostToDevice, st);
+        GF_TRY_RC(cudaMemcpyAsync(d_doc, doc_ids, n * 4, cudaMemcpyHostToDevice, st), "partition");
+        GF_TRY_RC(cudaMemcpyAsync(d_word, word_ids, n * 4, cudaMemcpyHostToDevice, st), "partition");
     }
     DevChunk c;
     cudaError_t e = partition_device(sc, st, d_doc, d_word, n, lo, hi, V, K, zkey, c, errs);
     if (e != cudaSuccess) return shard_cuda_fail(e, "partition");
     unsigned long long he[2];
-    cudaMemcpyAsync(he, errs, 16, cudaMemcpyDeviceToHost, st);
+    GF_TRY_RC(cudaMemcpyAsync(he, errs, 16, cudaMemcpyDeviceToHost, st), "partition");
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return shard_cuda_fail(e, "partition");
     if (he[0] != ~0ULL) return shard_fail(GF_ERR_VALUE, "word id outside [0, vocab_size)");
     if (he[1] != ~0ULL) return shard_fail(GF_ERR_VALUE, "doc id %d outside chunk range", doc_ids[he[1]]);
@@ -787,18 +799,18 @@ int partition_to_host(int device, const int32_t* doc_ids, const int32_t* word_id
     if (sc.err != cudaSuccess) return shard_cuda_fail(sc.err, "partition");
     if (n > 0) {
         k_u32_to_i32<<<blocks_for(n), 256, 0, st>>>(n, c.doc, d32, lo);
-        cudaMemcpyAsync(out_doc, d32, n * 4, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(out_word, c.word, n * 4, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(out_z, c.z, n * 2, cudaMemcpyDeviceToHost, st);
+        GF_TRY_RC(cudaMemcpyAsync(out_doc, d32, n * 4, cudaMemcpyDeviceToHost, st), "partition");
+        GF_TRY_RC(cudaMemcpyAsync(out_word, c.word, n * 4, cudaMemcpyDeviceToHost, st), "partition");
+        GF_TRY_RC(cudaMemcpyAsync(out_z, c.z, n * 2, cudaMemcpyDeviceToHost, st), "partition");
         k_u32_to_i64<<<blocks_for(n), 256, 0, st>>>(n, c.dw_tok, d64, 0);
-        cudaMemcpyAsync(dw_tok, d64, n * 8, cudaMemcpyDeviceToHost, st);
+        GF_TRY_RC(cudaMemcpyAsync(dw_tok, d64, n * 8, cudaMemcpyDeviceToHost, st), "partition");
     }
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return shard_cuda_fail(e, "partition");
     k_u32_to_i64<<<blocks_for(D + 1), 256, 0, st>>>(D + 1, c.dw_ptr, d64, 0);
-    cudaMemcpyAsync(dw_ptr, d64, (D + 1) * 8, cudaMemcpyDeviceToHost, st);
+    GF_TRY_RC(cudaMemcpyAsync(dw_ptr, d64, (D + 1) * 8, cudaMemcpyDeviceToHost, st), "partition");
     std::vector<uint32_t> go32((size_t)c.ng + 1);
     if (c.ng) cudaMemcpyAsync(gw, c.gw, c.ng * 4, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(go32.data(), c.go, (c.ng + 1) * 4, cudaMemcpyDeviceToHost, st);
+    GF_TRY_RC(cudaMemcpyAsync(go32.data(), c.go, (c.ng + 1) * 4, cudaMemcpyDeviceToHost, st), "partition");
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return shard_cuda_fail(e, "partition");
     for (int64_t g = 0; g < c.ng; ++g) {
         go[g] = go32[g];
