@@ -11,18 +11,19 @@ tag = sys.argv[1]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 O, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
 
-for w in ["nyt", "pm", "z4", "k128", "k256", "k4096", "ref"]:
+for w in ["pm", "ref", "shard0of8", "shard7of8", "nyt", "z4", "k128", "k256", "k4096"]:
     src = os.path.join(O, f"{tag}_bench_{w}.json")
     lines = [l for l in open(src) if l.startswith("{")] if os.path.exists(src) else []
     if lines:
         open(os.path.join(P, f"{tag}_bench_{w}.json"), "w").write(lines[-1])
 summ = os.path.join(P, "ncu_summary.py")
 for rep, out, top in [(f"{tag}_k1_nyt.ncu-rep", f"{tag}_nyt_sample_kernel_ncu.txt", "30"),
-                      (f"{tag}_pm.ncu-rep", f"{tag}_pubmed_k1_k2_k3_ncu.txt", "25")]:
+                      (f"{tag}_pm.ncu-rep", f"{tag}_pubmed_k1_k2_k3_ncu.txt", "25"),
+                      (f"{tag}_k5_pm.ncu-rep", f"{tag}_pubmed_k5_ncu.txt", "15")]:
     if os.path.exists(os.path.join(O, rep)):
         with open(os.path.join(P, out), "w") as fh:
             subprocess.run([sys.executable, summ, os.path.join(O, rep), top], stdout=fh, stderr=subprocess.STDOUT)
-lst = os.path.join(O, f"{tag}_launches_nyt.csv")
+lst = os.path.join(O, f"{tag}_launches_pm.csv")
 if os.path.exists(lst):
     shutil.copy(lst, P)
     rows = [r for r in csv.reader(open(lst)) if len(r) > 10]
@@ -41,7 +42,7 @@ if os.path.exists(lst):
         elif r[mi].startswith("dram__bytes_write"):
             d["wr"] = v * sc[u] / 1e9
     out = ["ncu launch list (iteration kernels only): python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e",
-           "(NYTimes-shape, K=1024, 1 B200), launches 6..41; per-launch times are cold-cache and serialised",
+           "(PubMed-shape, K=1024, 1 B200: the bench default), launches 6..41; per-launch times are cold-cache and serialised",
            "(compare shares, not absolutes); bench.py runs K3 on a side stream beside K2, ncu serialises them", "",
            f"{'id':>3} {'kernel':42s} {'ms':>8} {'dram_read_GB':>12} {'dram_write_GB':>13}"]
     tot = {}

@@ -8,5 +8,5 @@ for tool in memcheck racecheck synccheck initcheck; do
   echo "$tool rc=$? $(grep -m1 'ERROR SUMMARY' gpurun_out/san_$tool.log)"
 done
 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py -m gpu -x -q \
-  -k "load_tokens or partition_gpu_matches_host or checkpoint or large_k" > gpurun_out/san_memcheck_tests.log 2>&1
+  -k "load_tokens or partition_gpu_matches_host or checkpoint or large_k or conservation or resident or set_phi or tree_api" > gpurun_out/san_memcheck_tests.log 2>&1
 echo "memcheck(tests) rc=$? $(grep -m1 'ERROR SUMMARY' gpurun_out/san_memcheck_tests.log) $(tail -1 gpurun_out/san_memcheck_tests.log)"
