@@ -190,6 +190,12 @@ int gf_shard_sync_buffer(gf_shard* shard, void** device_ptr, int64_t* num_u32);
 int gf_shard_peer_handle(gf_shard* shard, void* handle_out);
 int gf_shard_peer_open(gf_shard* shard, int rank, int world, const void* handles);
 int gf_shard_peer_allreduce(gf_shard* shard);
+/* K2X: rebuild the phi replica (K2) and sum it over the peer group in ONE
+ * kernel, pipelined by stripes of the sync buffer (work items sorted by
+ * buffer position at gf_shard_peer_open; a stripe is exchanged as soon as
+ * every rank has completed it).  gf_shard_iterate uses it whenever a peer
+ * group is open (GF_PEER_FUSED=0: K2 then the two-shot exchange kernel). */
+int gf_shard_rebuild_phi_exchange(gf_shard* shard);
 int gf_shard_peer_close(gf_shard* shard);
 /* Host-only: the sync-buffer layout a shard derives from the global word
  * frequencies.  word_col_out[v] >= 0: 16-bit column index; < 0: ~(32-bit

@@ -63,6 +63,7 @@ SIGNATURES = {
     "gf_shard_peer_open": (_int, [_p, _int, _int, _p]),
     "gf_shard_peer_allreduce": (_int, [_p]),
     "gf_shard_peer_close": (_int, [_p]),
+    "gf_shard_rebuild_phi_exchange": (_int, [_p]),
     "gf_sync_layout": (_int, [_p, _i32, _i32, _u32, _p, _p]),
     "gf_shard_get_assignments": (_int, [_p, _p]),
     "gf_shard_set_assignments": (_int, [_p, _p]),

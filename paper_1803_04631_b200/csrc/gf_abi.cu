@@ -524,8 +524,12 @@ int gf_shard_iterate(gf_shard* s, uint32_t iteration) {
     CU(cudaStreamWaitEvent(s->aux, s->fork, 0), "iterate");
     CU(gf::launch_theta_rebuild(s, s->aux), "rebuild_theta");
     CU(cudaEventRecord(s->join, s->aux), "iterate");
-    CU(gf::launch_phi_rebuild(s), "rebuild_phi");
-    if (s->peer.world > 1) CU(gf::launch_peer_allreduce(s, st), "peer_allreduce");
+    if (s->peer.world > 1 && env_int("GF_PEER_FUSED", 1)) {
+        CU(gf::launch_phi_rebuild_exchange(s), "rebuild_phi_exchange");   // K2X: K2 + exchange in one kernel
+    } else {
+        CU(gf::launch_phi_rebuild(s), "rebuild_phi");
+        if (s->peer.world > 1) CU(gf::launch_peer_allreduce(s, st), "peer_allreduce");
+    }
     if (s->timing) cudaEventRecord(s->ev[2], st);
     CU(gf::launch_prepare(s), "prepare");
     if (s->timing) cudaEventRecord(s->ev[3], st);
@@ -610,6 +614,16 @@ int gf_shard_peer_allreduce(gf_shard* s) {
         return fail(GF_ERR_VALUE, "no peer group open on this shard's current sync buffer");
     cudaSetDevice(s->device);
     if (s->peer.world > 1) CU(gf::launch_peer_allreduce(s, s->stream), "peer_allreduce");
+    return GF_OK;
+}
+
+int gf_shard_rebuild_phi_exchange(gf_shard* s) {
+    if (int rc = need_loaded(s)) return rc;
+    if (s->peer.world < 1) return fail(GF_ERR_VALUE, "no peer group: gf_shard_peer_open first");
+    if (s->peer.sync != s->d.sync)
+        return fail(GF_ERR_VALUE, "peer group opened before the last load: exchange handles and reopen");
+    CU(gf::launch_phi_rebuild_exchange(s), "rebuild_phi_exchange");
+    s->stale_phi = false;
     return GF_OK;
 }
 

@@ -80,4 +80,19 @@ __device__ __forceinline__ uint32_t tpos_inv(uint32_t p, TPos g) { return (p & 3
 
 __device__ __forceinline__ float prev_float(float x) { return __int_as_float(__float_as_int(x) - 1); }
 
+// system-scope signalling between the GPUs of one node (peer-mapped memory)
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long now_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 }  // namespace gf

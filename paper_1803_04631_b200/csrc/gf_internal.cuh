@@ -81,6 +81,11 @@ struct PeerGroup {
     uint32_t* own_sig = nullptr;             // this rank's signal slots (cudaMalloc, exported)
     uint32_t* sync = nullptr;                // the sync buffer the group was opened on
     uint32_t epoch = 0;
+    // fused K2 + exchange (k_counts.cu K2X): stripes of the sync buffer
+    size_t sig_fused = 0;                    // offset (u32) of the fused kernel's slots in every sig array
+    int nstripe = 0;
+    long long stripe_words = 0;
+    unsigned* xdev = nullptr;                // [nstripe] items per stripe | [nstripe + 2] counters
 };
 
 }  // namespace gf
@@ -181,6 +186,7 @@ namespace gf {
 cudaError_t launch_sample(gf_shard* s, uint32_t iteration, int eval_only = 0);
 cudaError_t launch_sample_range(gf_shard* s, uint32_t iteration, int eval_only, int64_t slice0, int64_t n);
 cudaError_t launch_phi_rebuild(gf_shard* s);
+cudaError_t launch_phi_rebuild_exchange(gf_shard* s);   // K2X: K2 fused with the peer exchange
 cudaError_t launch_prepare(gf_shard* s);
 cudaError_t launch_contexts(gf_shard* s);
 cudaError_t launch_theta_rebuild(gf_shard* s, cudaStream_t st = nullptr);

@@ -29,18 +29,102 @@ namespace gf {
 // and clears the histogram it read.  n_k accumulates per CTA in shared memory
 // (nonzero cells only) and is flushed with K atomics at the end.  No block
 // barrier inside the item loop: each warp keeps its own loads in flight.
+//
+// K2X (X = true): the same kernel fused with
+// the peer-memory phi exchange of a node (k_peer.cu maps the ranks' sync
+// buffers), pipelined by STRIPES of the sync buffer.  The items are sorted by
+// the first buffer word they write (gf::peer_open), so the stripes fill in
+// order; the warp that completes the last item of stripe s (per-stripe
+// counters, fenced) release-stores the iteration's epoch into stripe s's flag
+// on every rank.  A CTA with no items left flushes its n_k (the last CTA to do
+// so signals the n_k stripe) and turns to the exchange: for each stripe in
+// order it waits until every rank has signalled it, then sums this rank's
+// 1/G of the stripe over the G replicas (16-byte peer loads) and stores the
+// sum into all G replicas -- the two-shot allreduce of the round-1 exchange
+// kernel, overlapped with the tail of the count.  The last CTA to finish
+// signals "done" to every rank and waits for every rank's "done", so the
+// kernel returns only when no peer will touch this buffer again this
+// iteration.  The grid is the resident persistent grid (every CTA that waits
+// is co-resident with the ones still counting); a wait beyond the timeout
+// sets errs[3] (a dead peer reports TrainingError, no hang).
 constexpr int kK2Warps = 8;
+constexpr unsigned long long kK2XTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+struct K2XArgs {
+    uint32_t* buf[kMaxPeers];      // every rank's sync buffer (own included)
+    uint32_t* sig[kMaxPeers];      // every rank's fused-kernel signal slots
+    int rank = 0, world = 1;
+    uint32_t epoch = 0;
+    int nstripe = 0;               // stripes over [0, off_nk); stripe nstripe = n_k
+    long long stripe_words = 0;
+    long long n = 0;               // u32 words of the exchanged buffer (phi + n_k)
+    const unsigned* need = nullptr;  // [nstripe] items touching each stripe
+    unsigned* done = nullptr;        // [nstripe] + [2] CTA counters (zeroed per launch)
+    unsigned long long* err = nullptr;
+};
 
 __device__ __forceinline__ void k2_count(uint32_t* bins, uint32_t k, int K, uint32_t t, unsigned long long* errs) {
     if (k < (uint32_t)K) atomicAdd(&bins[k >> 1], 1u << ((k & 1u) << 4));
     else atomicMin(errs, (unsigned long long)t);
 }
 
+// signal stripe s complete to every rank (slot s * kMaxPeers + this rank)
+__device__ __forceinline__ void k2x_signal(const K2XArgs& x, int s) {
+    __threadfence_system();
+    for (int p = 0; p < x.world; ++p) st_release_sys(x.sig[p] + (size_t)s * kMaxPeers + x.rank, x.epoch);
+}
+
+// block-wide wait for slot s of every rank; false on timeout
+__device__ bool k2x_wait(const K2XArgs& x, int s) {
+    bool ok = true;
+    if ((int)threadIdx.x < x.world) {
+        const uint32_t* f = x.sig[x.rank] + (size_t)s * kMaxPeers + threadIdx.x;
+        const unsigned long long t0 = now_ns();
+        while ((int32_t)(ld_acquire_sys(f) - x.epoch) < 0) {
+            if (now_ns() - t0 > kK2XTimeoutNs) {
+                atomicMin(x.err, (unsigned long long)s);
+                ok = false;
+                break;
+            }
+            __nanosleep(128);
+        }
+    }
+    return __syncthreads_and(ok);
+}
+
+// this rank's 1/G of words [lo, hi): sum over the replicas, store everywhere
+__device__ __forceinline__ void k2x_reduce(const K2XArgs& x, long long lo, long long hi) {
+    const long long plo = lo + (hi - lo) * x.rank / x.world, phi = lo + (hi - lo) * (x.rank + 1) / x.world;
+    const long long v0 = (plo + 3) >> 2, v1 = phi >> 2;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (long long v = v0 + gid; v < v1; v += stride) {
+        uint4 s = make_uint4(0, 0, 0, 0);
+        for (int p = 0; p < x.world; ++p) {
+            const uint4 q = __ldcg(reinterpret_cast<const uint4*>(x.buf[p]) + v);
+            s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
+        }
+        for (int p = 0; p < x.world; ++p) __stcg(reinterpret_cast<uint4*>(x.buf[p]) + v, s);
+    }
+    const long long h1 = min(v0 * 4, phi), t0 = max(max(v1 * 4, plo), h1);
+    for (long long i = plo + gid; i < h1; i += stride) {            // head words before the first vector
+        uint32_t s = 0;
+        for (int p = 0; p < x.world; ++p) s += __ldcg(x.buf[p] + i);
+        for (int p = 0; p < x.world; ++p) __stcg(x.buf[p] + i, s);
+    }
+    for (long long i = t0 + gid; i < phi; i += stride) {            // tail words
+        uint32_t s = 0;
+        for (int p = 0; p < x.world; ++p) s += __ldcg(x.buf[p] + i);
+        for (int p = 0; p < x.world; ++p) __stcg(x.buf[p] + i, s);
+    }
+}
+
+template <bool X>
 __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* __restrict__ items, int n_items,
                                                                     const uint16_t* __restrict__ z, uint32_t* sync,
                                                                     int K, int Kp, long long off16, long long offnk,
                                                                     int nwarps_per_cta, unsigned int* next_item,
-                                                                    unsigned long long* errs) {
+                                                                    unsigned long long* errs, K2XArgs x) {
     extern __shared__ uint32_t sh[];
     const int KW = Kp >> 1;                                   // packed words per histogram
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -49,6 +133,9 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
     for (int i = threadIdx.x; i < K; i += blockDim.x) nks[i] = 0u;
     if (warp < nwarps_per_cta)                                // only these warps own a histogram
         for (int i = lane; i < KW; i += 32) bins[i] = 0u;
+    if (X && blockIdx.x == 0 && threadIdx.x == 0)             // stripes no item writes (all-zero columns)
+        for (int s = 0; s < x.nstripe; ++s)
+            if (x.need[s] == 0u) k2x_signal(x, s);
     __syncthreads();
     // 16-byte column stores need a 16-byte aligned packed column
     const bool vec_cols = (KW & 3) == 0 && (off16 & 3) == 0;
@@ -133,6 +220,20 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
                 if (t1 >= tend) break;
                 t0 = t1;
             }
+            if (X) {
+                // the item's column is final: count it against the stripes it
+                // touches, and publish any stripe it completes
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) {
+                    const long long fw = col >= 0 ? off16 + (long long)col * KW : (long long)(~col) * K;
+                    const long long lw = fw + (col >= 0 ? KW : K) - 1;
+                    const int s0 = (int)(fw / x.stripe_words);
+                    const int s1 = (int)min((long long)x.nstripe - 1, lw / x.stripe_words);
+                    for (int s = s0; s <= s1; ++s)
+                        if (atomicAdd(&x.done[s], 1u) + 1u == x.need[s]) k2x_signal(x, s);
+                }
+            }
             it = __shfl_sync(kFull, mine, 0);
         }
     }
@@ -140,6 +241,25 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
     uint32_t* nk = sync + offnk;
     for (int k = threadIdx.x; k < K; k += blockDim.x)
         if (nks[k]) atomicAdd(&nk[k], nks[k]);
+    if (!X) return;
+    // ---- fused exchange ----
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&x.done[x.nstripe], 1u) + 1u == gridDim.x) k2x_signal(x, x.nstripe);
+    for (int s = 0; s <= x.nstripe; ++s) {
+        if (!k2x_wait(x, s)) return;
+        const long long lo = s < x.nstripe ? (long long)s * x.stripe_words : offnk;
+        const long long hi = s < x.nstripe ? min((long long)(s + 1) * x.stripe_words, offnk) : x.n;
+        k2x_reduce(x, lo, hi);
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&x.done[x.nstripe + 1], 1u) + 1u == gridDim.x) {
+        // every CTA of this rank has written its share everywhere: tell every
+        // rank, then wait until every rank has done the same
+        for (int p = 0; p < x.world; ++p) st_release_sys(x.sig[p] + (size_t)(x.nstripe + 1) * kMaxPeers + x.rank, x.epoch);
+    }
+    if (blockIdx.x == 0) k2x_wait(x, x.nstripe + 1);
 }
 
 // bytes of the K2 shared memory: the CTA's n_k plus one packed histogram per warp
@@ -147,31 +267,56 @@ static size_t k2_smem(int K, int Kp, int warps) {
     return ((size_t)((K + 3) & ~3) + (size_t)warps * (((Kp >> 1) + 3) & ~3)) * sizeof(uint32_t);
 }
 
-cudaError_t launch_phi_rebuild(gf_shard* s) {
+template <bool X>
+static cudaError_t launch_k2(gf_shard* s, const K2XArgs& x) {
     s->ctx_dirty = true;
     // only the 32-bit columns (atomic adds) and n_k need zeroing: every 16-bit
     // column is rewritten whole by its item; the last word is the item counter
     cudaError_t e = cudaMemsetAsync(s->d.sync, 0, (size_t)s->off_phi16_u32 * 4, s->stream);
     if (e == cudaSuccess)
         e = cudaMemsetAsync(s->d.sync + s->off_nk_u32, 0, ((size_t)s->sync_u32 - s->off_nk_u32 + 1) * 4, s->stream);
-    if (e != cudaSuccess || s->n_k2 == 0) return e;
+    if (e == cudaSuccess && X) e = cudaMemsetAsync(x.done, 0, (size_t)(x.nstripe + 2) * 4, s->stream);
+    if (e != cudaSuccess || (s->n_k2 == 0 && !X)) return e;
     const int nsm = sm_count(s->device);
     // 8 warps per CTA up to K = 8192 (16 KB histograms), 4 above
     const int warps = s->Kp > 8192 ? 4 : kK2Warps;
     const size_t smem = k2_smem(s->K, s->Kp, warps);
     static unsigned long long attr = 0;
     if (attr_once(attr, s->device)) {
-        e = cudaFuncSetAttribute(phi_rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        e = cudaFuncSetAttribute(phi_rebuild_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
     }
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_rebuild_kernel, kK2Warps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_rebuild_kernel<X>, kK2Warps * 32, smem);
     const long long need = (s->n_k2 + warps - 1) / warps;
-    const long long grid = std::max<long long>(1, std::min<long long>(need, (long long)nsm * std::max(per_sm, 1)));
-    phi_rebuild_kernel<<<(unsigned)grid, kK2Warps * 32, smem, s->stream>>>(
+    // K2X: the resident grid, so every waiting CTA is co-resident with the counting ones
+    const long long cap = (long long)nsm * std::max(per_sm, 1);
+    const long long grid = X ? cap : std::max<long long>(1, std::min<long long>(need, cap));
+    phi_rebuild_kernel<X><<<(unsigned)grid, kK2Warps * 32, smem, s->stream>>>(
         s->d.k2items, (int)s->n_k2, s->d.z, s->d.sync, s->K, s->Kp, s->off_phi16_u32, s->off_nk_u32, warps,
-        s->d.sync + s->sync_u32, s->d.errs);
+        s->d.sync + s->sync_u32, s->d.errs, x);
     return cudaGetLastError();
+}
+
+cudaError_t launch_phi_rebuild(gf_shard* s) { return launch_k2<false>(s, K2XArgs{}); }
+
+cudaError_t launch_phi_rebuild_exchange(gf_shard* s) {
+    const PeerGroup& g = s->peer;
+    K2XArgs x;
+    for (int p = 0; p < g.world; ++p) {
+        x.buf[p] = g.buf[p];
+        x.sig[p] = g.sig[p] + g.sig_fused;
+    }
+    x.rank = g.rank;
+    x.world = g.world;
+    x.epoch = ++s->peer.epoch;
+    x.nstripe = g.nstripe;
+    x.stripe_words = g.stripe_words;
+    x.n = s->sync_u32;
+    x.need = g.xdev;
+    x.done = g.xdev + g.nstripe;
+    x.err = s->d.errs + 3;
+    return launch_k2<true>(s, x);
 }
 
 // ------------------------------------------------------------- prepare ------

@@ -26,9 +26,12 @@
 // co-residency is needed on a device; a wait that exceeds the timeout sets an
 // error word and the host reports it (no hang on a dead peer).
 #include "gf_internal.cuh"
+#include "gf_device.cuh"
 #include "../../include/gibbsflow_b200.h"
 
+#include <algorithm>
 #include <cstring>
+#include <vector>
 
 namespace gf {
 
@@ -47,19 +50,6 @@ struct PeerArgs {
     unsigned long long* err;      // own errs[3]: block that timed out (min)
 };
 
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ unsigned long long now_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 
 // block-level barrier with the same-index block of every rank; phase 0/1
 __device__ bool peer_barrier(const PeerArgs& a, int phase) {
@@ -115,7 +105,9 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(PeerArgs a
 
 }  // namespace
 
-size_t peer_signal_bytes() { return (size_t)2 * kPeerBlocks * kMaxPeers * sizeof(uint32_t); }
+// [barrier phase 0 | barrier phase 1] of the two-shot kernel, then the fused
+// K2X kernel's stripe / done flags (k_counts.cu)
+size_t peer_signal_bytes() { return (size_t)3 * kPeerBlocks * kMaxPeers * sizeof(uint32_t); }
 
 void peer_close(gf_shard* s) {
     PeerGroup& g = s->peer;
@@ -125,6 +117,7 @@ void peer_close(gf_shard* s) {
         if (g.sig[p]) cudaIpcCloseMemHandle(g.sig[p]);
     }
     if (g.own_sig) cudaFree(g.own_sig);
+    if (g.xdev) cudaFree(g.xdev);
     g = PeerGroup{};
 }
 
@@ -141,6 +134,38 @@ int peer_handle(gf_shard* s, void* out) {
     if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[1], g.own_sig);
     if (e != cudaSuccess) return shard_cuda_fail(e, "peer_handle");
     std::memcpy(out, h, sizeof h);
+    return 0;
+}
+
+// K2X set-up: stripes of ~1 MiB (<= 32) over the phi region, the work items
+// re-ordered by the first buffer word they write (the stripes then complete in
+// order while K2 runs), and the number of items touching each stripe
+static int fused_setup(gf_shard* s) {
+    PeerGroup& g = s->peer;
+    g.sig_fused = (size_t)2 * kPeerBlocks * kMaxPeers;
+    const long long nphi = s->off_nk_u32;
+    g.nstripe = (int)std::max<long long>(1, std::min<long long>(32, nphi / (1 << 18)));
+    g.stripe_words = std::max<long long>(1, (nphi + g.nstripe - 1) / g.nstripe);
+    const int KW = s->Kp >> 1;
+    auto first_word = [&](const int4& w) {
+        return w.x >= 0 ? (long long)s->off_phi16_u32 + (long long)w.x * KW : (long long)(~w.x) * s->K;
+    };
+    std::vector<int4> items((size_t)s->n_k2);
+    cudaError_t e = cudaSuccess;
+    if (s->n_k2) e = cudaMemcpy(items.data(), s->d.k2items, items.size() * sizeof(int4), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return shard_cuda_fail(e, "peer_open (items)");
+    std::stable_sort(items.begin(), items.end(),
+                     [&](const int4& a, const int4& b) { return first_word(a) < first_word(b); });
+    std::vector<unsigned> need((size_t)g.nstripe, 0u);
+    for (const int4& w : items) {
+        const long long fw = first_word(w), lw = fw + (w.x >= 0 ? KW : s->K) - 1;
+        const long long s0 = fw / g.stripe_words, s1 = std::min<long long>(g.nstripe - 1, lw / g.stripe_words);
+        for (long long q = s0; q <= s1; ++q) ++need[(size_t)q];
+    }
+    if (s->n_k2) e = cudaMemcpy(s->d.k2items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !g.xdev) e = cudaMalloc((void**)&g.xdev, (size_t)(2 * 32 + 2) * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemcpy(g.xdev, need.data(), need.size() * sizeof(unsigned), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return shard_cuda_fail(e, "peer_open (stripes)");
     return 0;
 }
 
@@ -177,7 +202,7 @@ int peer_open(gf_shard* s, int rank, int world, const void* handles) {
         g.buf[p] = static_cast<uint32_t*>(b);
         g.sig[p] = static_cast<uint32_t*>(q);
     }
-    return 0;
+    return fused_setup(s);
 }
 
 cudaError_t launch_peer_allreduce(gf_shard* s, cudaStream_t st) {

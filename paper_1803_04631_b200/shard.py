@@ -312,6 +312,10 @@ class DeviceShard:
         """Sum the sync buffers of the peer group in place (stream-ordered)."""
         _lib.check(_lib.lib().gf_shard_peer_allreduce(self._h))
 
+    def rebuild_phi_exchange(self):
+        """K2X: rebuild the replica and sum it over the peer group in one kernel."""
+        _lib.check(_lib.lib().gf_shard_rebuild_phi_exchange(self._h))
+
     def peer_close(self):
         _lib.check(_lib.lib().gf_shard_peer_close(self._h))
 

@@ -8,6 +8,8 @@ carries the IPC handles and the reference sums.
 
 Checks: one exchange == the elementwise uint32 sum of the two replicas (the
 all_reduce it replaces), bit-exact; repeated exchanges (epochs) stay exact;
+the fused K2 + exchange kernel (K2X, what gf_shard_iterate runs with a peer
+group) gives the same sum;
 a Trainer with phi_sync="peer" keeps phi/n_k conserved against the gathered
 assignments every iteration and tracks the one-rank loglik.
 """
@@ -90,6 +92,14 @@ def _rank_main(rank, world, port, out):
         ok &= bool(torch.equal(sh.sync_tensor().cpu(), expect))
     sh.check_errors()
     res["epochs_exact"] = ok
+    # K2X: the replica rebuild fused with the stripe-pipelined exchange
+    ok = True
+    for _ in range(3):
+        sh.rebuild_phi_exchange()
+        sh.synchronize()
+        ok &= bool(torch.equal(sh.sync_tensor().cpu(), expect))
+    sh.check_errors()
+    res["fused_exact"] = ok
     sh.peer_close()
     sh.close()
 
@@ -174,6 +184,13 @@ def test_peer_exchange_equals_replica_sum(peer_result):
 
 def test_peer_exchange_repeated_epochs(peer_result):
     assert peer_result["epochs_exact"]
+
+
+def test_fused_k2_exchange_equals_replica_sum(peer_result):
+    """K2X (gf_shard_rebuild_phi_exchange): rebuilding the replica and summing it
+    over the group in one stripe-pipelined kernel gives the all_reduce result,
+    bit-exact, epoch after epoch."""
+    assert peer_result["fused_exact"]
 
 
 def test_trainer_peer_sync_conserves_counts(peer_result):
