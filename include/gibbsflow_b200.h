@@ -204,6 +204,17 @@ int gf_shard_peer_close(gf_shard* shard);
 int gf_sync_layout(const int64_t* global_word_freq, int32_t vocab_size, int32_t num_topics,
                    uint32_t heavy_threshold, int32_t* word_col_out, int64_t* layout_out);
 
+/* Pinned host blocks for arrays that cross PCIe every call (not in the
+ * reference: its arrays never leave the host).  The Python mirror allocates
+ * the one-call API's results here (get_theta / get_phi / get_assignments) and
+ * frees them when the array is collected; a freed block is cached for the
+ * next allocation of a similar size, so results are DMA'd directly, without
+ * bounce copies or first-touch page faults, and an array handed back as the
+ * next call's input uploads at full PCIe speed.  gf_host_free takes the
+ * size passed to gf_host_alloc. */
+int gf_host_alloc(int64_t bytes, void** out);
+int gf_host_free(void* p, int64_t bytes);
+
 /* import / export (host buffers, caller-allocated) */
 int gf_shard_get_assignments(gf_shard* shard, uint16_t* out);      /* word-group order */
 int gf_shard_set_assignments(gf_shard* shard, const uint16_t* in);

@@ -65,6 +65,8 @@ SIGNATURES = {
     "gf_shard_peer_close": (_int, [_p]),
     "gf_shard_rebuild_phi_exchange": (_int, [_p]),
     "gf_sync_layout": (_int, [_p, _i32, _i32, _u32, _p, _p]),
+    "gf_host_alloc": (_int, [_i64, _pp]),
+    "gf_host_free": (_int, [_p, _i64]),
     "gf_shard_get_assignments": (_int, [_p, _p]),
     "gf_shard_set_assignments": (_int, [_p, _p]),
     "gf_shard_copy_assignments_async": (_int, [_p, _p, _i64, _i64, _int, _p]),
@@ -140,6 +142,39 @@ def ptr(a):
 
 def carr(a, dtype):
     return np.ascontiguousarray(a, dtype=dtype)
+
+
+class _PinnedBlock:
+    """A gf_host_alloc block exposed to numpy (`__array_interface__`); it goes
+    back to the library's cache when the last array viewing it is collected."""
+
+    def __init__(self, nbytes):
+        import weakref
+
+        p = ctypes.c_void_p()
+        check(lib().gf_host_alloc(nbytes, ctypes.byref(p)))
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (p.value, False), "version": 3}
+        fin = weakref.finalize(self, lib().gf_host_free, ctypes.c_void_p(p.value), nbytes)
+        fin.atexit = False                       # the driver releases pinned memory at exit
+
+
+_PINNED_MIN = 1 << 20
+
+
+def pinned_empty(shape, dtype):
+    """np.empty in a cached pinned block (results of the one-call API: DMA'd
+    directly, no first-touch page faults, full-speed upload when handed back);
+    small arrays, or a failed pinned allocation, get ordinary memory."""
+    dtype = np.dtype(dtype)
+    shape = tuple(int(x) for x in np.atleast_1d(shape))
+    n = int(np.prod(shape)) * dtype.itemsize
+    if n < _PINNED_MIN:
+        return np.empty(shape, dtype)
+    try:
+        blk = _PinnedBlock(n)
+    except errors.GibbsflowError:
+        return np.empty(shape, dtype)
+    return np.asarray(blk).view(dtype).reshape(shape)
 
 
 def device_count():

@@ -634,6 +634,19 @@ int gf_shard_peer_close(gf_shard* s) {
     return GF_OK;
 }
 
+// pinned result blocks of the one-call API (gf_xfer.cpp host_alloc)
+int gf_host_alloc(int64_t bytes, void** out) {
+    if (bytes < 0 || !out) return fail(GF_ERR_VALUE, "host_alloc: bad arguments");
+    *out = nullptr;
+    CU(gf::host_alloc((size_t)bytes, out), "host_alloc");
+    return GF_OK;
+}
+
+int gf_host_free(void* p, int64_t bytes) {
+    CU(gf::host_free(p, (size_t)bytes), "host_free");
+    return GF_OK;
+}
+
 int gf_shard_get_assignments(gf_shard* s, uint16_t* out) {
     if (int rc = need_loaded(s)) return rc;
     CU(gf::xfer_d2h(out, s->d.z, s->T * 2, s->stream), "get_assignments");
@@ -661,10 +674,18 @@ int gf_shard_copy_assignments_async(gf_shard* s, void* host, int64_t offset, int
     }
     uint16_t* dev = (to_device ? s->d.zstage : s->d.z) + offset;
     uint16_t* h = static_cast<uint16_t*>(host) + offset;
-    // pinned host buffers: a plain async copy; pageable ones go through the
-    // pinned bounce buffers (the host side then completes before returning)
-    if (to_device) CU(gf::xfer_h2d(dev, h, count * 2, st), "copy_assignments");
-    else CU(gf::xfer_d2h(h, dev, count * 2, st), "copy_assignments");
+    // pinned host buffers: a plain async copy in both directions (the call
+    // returns at once; stream order is the caller's); pageable ones go through
+    // the pinned bounce buffers (the host side then completes before returning)
+    if (gf::host_is_pinned(h)) {
+        CU(cudaMemcpyAsync(to_device ? (void*)dev : (void*)h, to_device ? (const void*)h : (const void*)dev, count * 2,
+                           to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
+           "copy_assignments");
+    } else if (to_device) {
+        CU(gf::xfer_h2d(dev, h, count * 2, st), "copy_assignments");
+    } else {
+        CU(gf::xfer_d2h(h, dev, count * 2, st), "copy_assignments");
+    }
     return GF_OK;
 }
 

@@ -95,4 +95,9 @@ __device__ __forceinline__ unsigned long long now_ns() {
     return t;
 }
 
+// TMA bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, bytes % 16 == 0)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 }  // namespace gf

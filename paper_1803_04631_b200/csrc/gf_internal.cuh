@@ -200,6 +200,10 @@ cudaError_t theta_rowptr(gf_shard* s, int64_t* d_rowptr, void* tmp, size_t* tmp_
 // host <-> device copies of pageable arrays through pinned bounce buffers (gf_xfer.cpp)
 cudaError_t xfer_h2d(void* dst, const void* src, size_t n, cudaStream_t st);
 cudaError_t xfer_d2h(void* dst, const void* src, size_t n, cudaStream_t st);
+// cached pinned host blocks for the one-call API's result arrays (gf_host_alloc)
+cudaError_t host_alloc(size_t n, void** out);
+cudaError_t host_free(void* p, size_t n);
+bool host_is_pinned(const void* p);
 cudaError_t launch_theta_validate(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids, const uint16_t* d_cnt,
                                   unsigned long long* d_first);
 cudaError_t launch_phi_export(gf_shard* s, void* d_out_kv, int width, const int32_t* d_word_col);

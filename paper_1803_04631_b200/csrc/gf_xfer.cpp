@@ -17,6 +17,8 @@
 #include <cstdint>
 #include <cstring>
 #include <functional>
+#include <iterator>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -150,7 +152,77 @@ bool is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
+// Pinned blocks for the result arrays of the one-call API (host_alloc /
+// host_free, gf_host_alloc in the ABI).  A numpy result array in pageable
+// memory costs a first-touch page fault per 4 KB page on every call (the
+// array is new each time) plus the bounce copy; a pinned block is DMA'd
+// into directly, and a freed block is kept for the next call of a similar
+// size (best fit within 1.5x), so a training loop through the API stops
+// faulting after its first iteration.  The cache holds at most kCacheCap
+// bytes of free blocks; larger frees go back to the driver.
+constexpr size_t kHostGrain = 2u << 20;
+constexpr size_t kCacheCap = 16ull << 30;
+
+struct HostCache {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_blocks;   // rounded size -> block
+    size_t cached = 0;
+};
+
+HostCache& host_cache() {
+    static HostCache* c = new HostCache();      // process lifetime
+    return *c;
+}
+
 }  // namespace
+
+bool host_is_pinned(const void* p) { return is_pinned(p); }
+
+size_t host_block_bytes(size_t n) { return std::max<size_t>(kHostGrain, (n + kHostGrain - 1) / kHostGrain * kHostGrain); }
+
+cudaError_t host_alloc(size_t n, void** out) {
+    const size_t want = host_block_bytes(n);
+    HostCache& C = host_cache();
+    {
+        std::lock_guard<std::mutex> g(C.mu);
+        auto it = C.free_blocks.lower_bound(want);
+        if (it != C.free_blocks.end() && it->first <= want + want / 2) {
+            *out = it->second;
+            C.cached -= it->first;
+            C.free_blocks.erase(it);
+            return cudaSuccess;
+        }
+    }
+    return cudaHostAlloc(out, want, cudaHostAllocPortable);
+}
+
+// `n` is the size passed to host_alloc for this block
+cudaError_t host_free(void* p, size_t n) {
+    if (!p) return cudaSuccess;
+    const size_t sz = host_block_bytes(n);
+    HostCache& C = host_cache();
+    std::vector<void*> drop;
+    {
+        std::lock_guard<std::mutex> g(C.mu);
+        // a block reused from the cache may be larger than host_block_bytes(n):
+        // it is filed under the size it was looked up with, which only under-
+        // states it (best fit keeps working)
+        C.free_blocks.emplace(sz, p);
+        C.cached += sz;
+        while (C.cached > kCacheCap && !C.free_blocks.empty()) {   // evict the largest
+            auto it = std::prev(C.free_blocks.end());
+            C.cached -= it->first;
+            drop.push_back(it->second);
+            C.free_blocks.erase(it);
+        }
+    }
+    cudaError_t e = cudaSuccess;
+    for (void* q : drop) {
+        cudaError_t r = cudaFreeHost(q);
+        if (r != cudaSuccess) e = r;
+    }
+    return e;
+}
 
 // host -> device; returns when the host buffer may be reused (the DMA of the
 // last piece may still be in flight on `st`, ordered before later work on it)

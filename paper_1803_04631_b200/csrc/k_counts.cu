@@ -142,32 +142,51 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
     uint32_t* phi16w = sync + off16;                           // packed light columns (u32 words)
     const uint4* zv = reinterpret_cast<const uint4*>(z);
     if (warp < nwarps_per_cta) {
-        // the next item is claimed while the current one is counted
+        // the next item is claimed while the current one is counted, and its
+        // z range is bulk-prefetched into L2 right away (TMA prefetch, one
+        // instruction), so the item after this one starts on L2 hits instead of
+        // a cold DRAM round trip per 2 KB batch
         int mine = 0;
-        if (lane == 0) mine = (int)atomicAdd(next_item, 1u);
+        auto claim = [&]() {
+            if (lane == 0) {
+                mine = (int)atomicAdd(next_item, 1u);
+                if (mine < n_items) {
+                    const int4 nw = __ldg(items + mine);
+                    const uint32_t p0 = (uint32_t)nw.y & ~7u, p1 = min(((uint32_t)nw.z + 7u) & ~7u, p0 + 32768u);
+                    if (p1 > p0) prefetch_l2_bulk(z + p0, (p1 - p0) * 2u);
+                }
+            }
+        };
+        claim();
         int it = __shfl_sync(kFull, mine, 0);
         while (it < n_items) {
             const int4 w = __ldg(items + it);
-            if (lane == 0) mine = (int)atomicAdd(next_item, 1u);
+            claim();
             const int col = w.x;
             // a heavy (32-bit column) item longer than 65535 tokens (one huge
             // (doc, word) run) is counted and flushed in pieces so no packed
             // 16-bit bin can carry; a light item is <= 65535 tokens by construction
             for (uint32_t t0 = (uint32_t)w.y, tend = (uint32_t)w.z;;) {
                 const uint32_t t1 = col >= 0 ? tend : min(tend, t0 + 65528u);
-                // ---- count: scalar head / tail, 16-byte body; four 16-byte loads
-                // per lane in flight (32 topics), then their 32 shared atomics ----
+                // ---- count: scalar head / tail, 16-byte body, double-buffered:
+                // the next two 16-byte loads per lane are in flight while the
+                // current two (16 topics) are counted by shared atomics ----
                 const uint32_t a0 = min(t1, (t0 + 7u) & ~7u), a1 = max(a0, t1 & ~7u);
                 if (t0 + lane < a0) k2_count(bins, z[t0 + lane], K, t0 + lane, errs);
                 if (a1 + lane < t1) k2_count(bins, z[a1 + lane], K, a1 + lane, errs);
                 const uint32_t qe = a1 >> 3;
-                for (uint32_t q = (a0 >> 3) + lane; q < qe; q += 128u) {
-                    uint4 v[4];
+                uint32_t q = (a0 >> 3) + lane;
+                uint4 v[2];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (q + 32u * i < qe) v[i] = __ldg(zv + q + 32u * i);
+                for (int i = 0; i < 2; ++i)
+                    if (q + 32u * i < qe) v[i] = __ldg(zv + q + 32u * i);
+                for (; q < qe; q += 64u) {
+                    uint4 nx[2];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
+                    for (int i = 0; i < 2; ++i)
+                        if (q + 64u + 32u * i < qe) nx[i] = __ldg(zv + q + 64u + 32u * i);
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
                         if (q + 32u * i < qe) {
                             const uint32_t e[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
                             const uint32_t tb = 8u * (q + 32u * i);
@@ -178,6 +197,8 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
                             }
                         }
                     }
+                    v[0] = nx[0];
+                    v[1] = nx[1];
                 }
                 __syncwarp();
                 // ---- flush: every packed word once (lane-strided), cleared behind ----
@@ -357,7 +378,7 @@ __host__ __device__ inline int k3_warp_u32(int K) { return K + 2 * k3_words(K); 
 __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
                                                             const uint16_t* __restrict__ zdoc, uint32_t* theta_ent,
                                                             uint2* theta_meta, int K, int warps_per_cta,
-                                                            unsigned long long* errs) {
+                                                            int gsz, unsigned long long* errs) {
     extern __shared__ uint32_t sh[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int NW = k3_words(K);
@@ -368,173 +389,196 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
     for (int i = lane; i < K + NW; i += 32) bins[i] = 0u;
     __syncwarp();
     const unsigned lt = (1u << lane) - 1u;
-    // software pipeline over this warp's documents d, d+s, d+2s: the next
-    // document's first 32 topics and the one after's (dw_ptr, meta) are in
-    // flight while the current one is counted
-    const int s = gridDim.x * warps_per_cta;
-    auto meta_of = [&](int dd, uint32_t& mb, uint32_t& mL, uint32_t& mo) {
+    // The warp takes GROUPS of gsz <= 32 consecutive documents (group g, then
+    // g + the number of warps; gsz keeps >= 4 groups per warp): lane j holds
+    // document j's {zdoc begin, length, theta row offset} (three coalesced
+    // loads per group instead of three per document), and the next group's
+    // are loaded while this one is processed.  Halfway through a group, lane 0 bulk-prefetches the next
+    // group's topics into L2 (one contiguous zdoc range), so the next group's
+    // loads hit L2; the next document's first 32 topics are always in flight
+    // (registers) while the current one is counted.
+    const int ngroups = (D + gsz - 1) / gsz;
+    const int gstride = gridDim.x * warps_per_cta;
+    auto group_meta = [&](int g, uint32_t& mb, uint32_t& mL, uint32_t& mo) {
+        const int dd = g * gsz + lane;
         mb = mL = mo = 0u;
-        if (dd < D) { mb = dw_ptr[dd]; mL = dw_ptr[dd + 1] - mb; mo = theta_meta[dd].x; }
+        if (g < ngroups && lane < gsz && dd < D) { mb = dw_ptr[dd]; mL = dw_ptr[dd + 1] - mb; mo = theta_meta[dd].x; }
     };
-    int d = blockIdx.x * warps_per_cta + warp;
-    uint32_t b, L, off, b1, L1, o1;
-    meta_of(d, b, L, off);
-    meta_of(d + s, b1, L1, o1);
-    uint32_t zf = (d < D && (uint32_t)lane < L) ? zdoc[b + lane] : 0xffffu;   // first 32 topics of d
-    for (; d < D; d += s) {
-        uint32_t b2, L2, o2;
-        meta_of(d + 2 * s, b2, L2, o2);
-        const uint32_t zn = (d + s < D && (uint32_t)lane < L1) ? zdoc[b1 + lane] : 0xffffu;
-        uint32_t nnz;
-        if (L <= 32) {
-            uint32_t key = 0xffffu;
-            if (lane < (int)L) key = zf;
-            if (key >= (uint32_t)K && lane < (int)L) { atomicMin(errs + 2, (unsigned long long)d); key = 0xffffu; }
-            key = warp_bitonic_sort(key, lane);
-            const uint32_t prev = __shfl_up_sync(kFull, key, 1);
-            const bool head = key != 0xffffu && (lane == 0 || key != prev);
-            const unsigned heads = __ballot_sync(kFull, head);
-            if (head) {
-                const unsigned later = heads & ~((2u << lane) - 1u);
-                const uint32_t next = later ? (uint32_t)(__ffs(later) - 1) : L;
-                theta_ent[off + __popc(heads & lt)] = (tpos(key, tm) << 2) | ((next - lane) << 16);
-            }
-            nnz = __popc(heads);
-        } else if (L <= 128) {
-            // 32 < L <= 128, the tokens stay in registers (ncol = ceil(L / 32)
-            // columns, warp-uniform).  Count: every token adds to its bin and
-            // sets its bitmap bit (no returned values, no branches).  Emit: the
-            // rank of topic k = distinct topics below it = word prefix + popc
-            // inside the word; one token per topic wins atomicExch(bin, 0) (it
-            // gets the count and clears the bin) and writes the entry.
-            const uint32_t ncol = (L + 31u) >> 5;
-            uint32_t kk[4] = {zf, 0xffffu, 0xffffu, 0xffffu};
-#pragma unroll
-            for (uint32_t j = 1; j < 4; ++j)
-                if (j < ncol && lane + 32u * j < L) kk[j] = zdoc[b + lane + 32u * j];
-#pragma unroll
-            for (uint32_t j = 0; j < 4; ++j) {
-                const uint32_t k = kk[j];
-                if (j < ncol && k < (uint32_t)K) {
-                    atomicAdd(&bins[k], 1u);
-                    atomicOr(&bmp[k >> 5], 1u << (k & 31u));
-                } else if (j < ncol && k != 0xffffu) {
-                    atomicMin(errs + 2, (unsigned long long)d);
-                    kk[j] = 0xffffu;
+    int g = blockIdx.x * warps_per_cta + warp;
+    uint32_t gb, gL, go;
+    group_meta(g, gb, gL, go);
+    const uint32_t b00 = __shfl_sync(kFull, gb, 0), L00 = __shfl_sync(kFull, gL, 0);   // all lanes shuffle
+    uint32_t zf = (uint32_t)lane < L00 ? zdoc[b00 + lane] : 0xffffu;
+    for (; g < ngroups; g += gstride) {
+        uint32_t nb, nL, no;
+        group_meta(g + gstride, nb, nL, no);
+        const int nd = min(gsz, D - g * gsz);
+        for (int i = 0; i < nd; ++i) {
+            const int d = g * gsz + i;
+            const uint32_t b = __shfl_sync(kFull, gb, i), L = __shfl_sync(kFull, gL, i), off = __shfl_sync(kFull, go, i);
+            const bool last = i + 1 == nd;
+            const uint32_t b1 = __shfl_sync(kFull, last ? nb : gb, last ? 0 : i + 1);
+            const uint32_t L1 = __shfl_sync(kFull, last ? nL : gL, last ? 0 : i + 1);
+            const uint32_t zn = (uint32_t)lane < L1 ? zdoc[b1 + lane] : 0xffffu;        // L1 = 0 past the end
+            if (i == (gsz >> 1)) {
+                const uint32_t b0 = __shfl_sync(kFull, nb, 0), end = __reduce_max_sync(kFull, nL ? nb + nL : 0u);
+                if (lane == 0 && end > b0) {
+                    const uint32_t p0 = b0 & ~7u, p1 = (end + 7u) & ~7u;
+                    prefetch_l2_bulk(zdoc + p0, (p1 - p0) * 2u);
                 }
             }
-            __syncwarp();
-            if (NW <= 32) {
-                // K <= 1024: lane w holds bitmap word w and the distinct topics
-                // below it in registers; the emit fetches both by shuffle
-                const uint32_t word = lane < NW ? bmp[lane] : 0u;
-                if (lane < NW) bmp[lane] = 0u;
-                const uint32_t pc = __popc(word);
-                uint32_t incl = pc;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o) incl += y;
+            uint32_t nnz;
+            if (L <= 32) {
+                uint32_t key = 0xffffu;
+                if (lane < (int)L) key = zf;
+                if (key >= (uint32_t)K && lane < (int)L) { atomicMin(errs + 2, (unsigned long long)d); key = 0xffffu; }
+                key = warp_bitonic_sort(key, lane);
+                const uint32_t prev = __shfl_up_sync(kFull, key, 1);
+                const bool head = key != 0xffffu && (lane == 0 || key != prev);
+                const unsigned heads = __ballot_sync(kFull, head);
+                if (head) {
+                    const unsigned later = heads & ~((2u << lane) - 1u);
+                    const uint32_t next = later ? (uint32_t)(__ffs(later) - 1) : L;
+                    theta_ent[off + __popc(heads & lt)] = (tpos(key, tm) << 2) | ((next - lane) << 16);
                 }
-                nnz = __shfl_sync(kFull, incl, 31);
-                const uint32_t pre = incl - pc;
-#pragma unroll
+                nnz = __popc(heads);
+            } else if (L <= 128) {
+                // 32 < L <= 128, the tokens stay in registers (ncol = ceil(L / 32)
+                // columns, warp-uniform).  Count: every token adds to its bin and
+                // sets its bitmap bit (no returned values, no branches).  Emit: the
+                // rank of topic k = distinct topics below it = word prefix + popc
+                // inside the word; one token per topic wins atomicExch(bin, 0) (it
+                // gets the count and clears the bin) and writes the entry.
+                const uint32_t ncol = (L + 31u) >> 5;
+                uint32_t kk[4] = {zf, 0xffffu, 0xffffu, 0xffffu};
+    #pragma unroll
+                for (uint32_t j = 1; j < 4; ++j)
+                    if (j < ncol && lane + 32u * j < L) kk[j] = zdoc[b + lane + 32u * j];
+    #pragma unroll
                 for (uint32_t j = 0; j < 4; ++j) {
-                    if (j < ncol) {
-                        const uint32_t k = kk[j], w = (k >> 5) & 31u;
-                        const uint32_t ww = __shfl_sync(kFull, word, w), pw = __shfl_sync(kFull, pre, w);
-                        const uint32_t c = k < (uint32_t)K ? atomicExch(&bins[k], 0u) : 0u;
-                        if (c)
-                            theta_ent[off + pw + __popc(ww & ((1u << (k & 31u)) - 1u))] =
-                                (tpos(k, tm) << 2) | (c << 16);               // <= 128: no overflow
+                    const uint32_t k = kk[j];
+                    if (j < ncol && k < (uint32_t)K) {
+                        atomicAdd(&bins[k], 1u);
+                        atomicOr(&bmp[k >> 5], 1u << (k & 31u));
+                    } else if (j < ncol && k != 0xffffu) {
+                        atomicMin(errs + 2, (unsigned long long)d);
+                        kk[j] = 0xffffu;
                     }
                 }
-            } else {
-                uint32_t base = 0;
-                for (int c = 0; c < NW; c += 32) {
-                    const int w = c + lane;
-                    const uint32_t pc = w < NW ? __popc(bmp[w]) : 0u;
+                __syncwarp();
+                if (NW <= 32) {
+                    // K <= 1024: lane w holds bitmap word w and the distinct topics
+                    // below it in registers; the emit fetches both by shuffle
+                    const uint32_t word = lane < NW ? bmp[lane] : 0u;
+                    if (lane < NW) bmp[lane] = 0u;
+                    const uint32_t pc = __popc(word);
                     uint32_t incl = pc;
-#pragma unroll
+    #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
                         const uint32_t y = __shfl_up_sync(kFull, incl, o);
                         if (lane >= o) incl += y;
                     }
-                    if (w < NW) wpre[w] = base + incl - pc;
+                    nnz = __shfl_sync(kFull, incl, 31);
+                    const uint32_t pre = incl - pc;
+    #pragma unroll
+                    for (uint32_t j = 0; j < 4; ++j) {
+                        if (j < ncol) {
+                            const uint32_t k = kk[j], w = (k >> 5) & 31u;
+                            const uint32_t ww = __shfl_sync(kFull, word, w), pw = __shfl_sync(kFull, pre, w);
+                            const uint32_t c = k < (uint32_t)K ? atomicExch(&bins[k], 0u) : 0u;
+                            if (c)
+                                theta_ent[off + pw + __popc(ww & ((1u << (k & 31u)) - 1u))] =
+                                    (tpos(k, tm) << 2) | (c << 16);               // <= 128: no overflow
+                        }
+                    }
+                } else {
+                    uint32_t base = 0;
+                    for (int c = 0; c < NW; c += 32) {
+                        const int w = c + lane;
+                        const uint32_t pc = w < NW ? __popc(bmp[w]) : 0u;
+                        uint32_t incl = pc;
+    #pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                            if (lane >= o) incl += y;
+                        }
+                        if (w < NW) wpre[w] = base + incl - pc;
+                        base += __shfl_sync(kFull, incl, 31);
+                    }
+                    nnz = base;
+                    __syncwarp();
+    #pragma unroll
+                    for (uint32_t j = 0; j < 4; ++j) {
+                        const uint32_t k = kk[j];
+                        const uint32_t c = (j < ncol && k < (uint32_t)K) ? atomicExch(&bins[k], 0u) : 0u;
+                        if (c) {
+                            const uint32_t w = k >> 5;
+                            theta_ent[off + wpre[w] + __popc(bmp[w] & ((1u << (k & 31u)) - 1u))] =
+                                (tpos(k, tm) << 2) | (c << 16);                 // <= 128: no overflow
+                        }
+                    }
+                    __syncwarp();
+    #pragma unroll
+                    for (uint32_t j = 0; j < 4; ++j)
+                        if (j < ncol && kk[j] < (uint32_t)K) bmp[kk[j] >> 5] = 0u;
+                }
+                __syncwarp();
+            } else {
+                auto count = [&](uint32_t k) {
+                    if (k < (uint32_t)K) {
+                        atomicAdd(&bins[k], 1u);
+                        atomicOr(&bmp[k >> 5], 1u << (k & 31u));
+                    } else {
+                        atomicMin(errs + 2, (unsigned long long)d);
+                    }
+                };
+                // the next 96 topics load together (independent), then count
+                const uint32_t i1 = lane + 32u, i2 = lane + 64u, i3 = lane + 96u;
+                const uint32_t k1 = i1 < L ? zdoc[b + i1] : 0u, k2 = i2 < L ? zdoc[b + i2] : 0u,
+                               k3 = i3 < L ? zdoc[b + i3] : 0u;
+                count(zf);                                          // L > 32: every lane has one
+                if (i1 < L) count(k1);
+                if (i2 < L) count(k2);
+                if (i3 < L) count(k3);
+                for (uint32_t i = lane + 128u; i < L; i += 32) count(zdoc[b + i]);
+                __syncwarp();
+                uint32_t base = 0, mx = 0;
+                for (int c = 0; c < NW; c += 32) {
+                    const int w = c + lane;
+                    uint32_t word = w < NW ? bmp[w] : 0u;
+                    const uint32_t pc = __popc(word);
+                    uint32_t incl = pc;
+    #pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    uint32_t pos = off + base + incl - pc;
+                    if (w < NW) bmp[w] = 0u;
+                    while (word) {
+                        const uint32_t k = ((uint32_t)w << 5) + (uint32_t)(__ffs(word) - 1);
+                        word &= word - 1u;
+                        const uint32_t v = bins[k];
+                        bins[k] = 0u;
+                        theta_ent[pos++] = (tpos(k, tm) << 2) | (min(v, 65535u) << 16);
+                        mx = max(mx, v);
+                    }
                     base += __shfl_sync(kFull, incl, 31);
                 }
                 nnz = base;
+                mx = warp_max_u32(mx);
+                if (mx > 65535u && lane == 0) atomicMin(errs + 1, ((unsigned long long)d << 32) | mx);
                 __syncwarp();
-#pragma unroll
-                for (uint32_t j = 0; j < 4; ++j) {
-                    const uint32_t k = kk[j];
-                    const uint32_t c = (j < ncol && k < (uint32_t)K) ? atomicExch(&bins[k], 0u) : 0u;
-                    if (c) {
-                        const uint32_t w = k >> 5;
-                        theta_ent[off + wpre[w] + __popc(bmp[w] & ((1u << (k & 31u)) - 1u))] =
-                            (tpos(k, tm) << 2) | (c << 16);                 // <= 128: no overflow
-                    }
-                }
-                __syncwarp();
-#pragma unroll
-                for (uint32_t j = 0; j < 4; ++j)
-                    if (j < ncol && kk[j] < (uint32_t)K) bmp[kk[j] >> 5] = 0u;
             }
-            __syncwarp();
-        } else {
-            auto count = [&](uint32_t k) {
-                if (k < (uint32_t)K) {
-                    atomicAdd(&bins[k], 1u);
-                    atomicOr(&bmp[k >> 5], 1u << (k & 31u));
-                } else {
-                    atomicMin(errs + 2, (unsigned long long)d);
-                }
-            };
-            // the next 96 topics load together (independent), then count
-            const uint32_t i1 = lane + 32u, i2 = lane + 64u, i3 = lane + 96u;
-            const uint32_t k1 = i1 < L ? zdoc[b + i1] : 0u, k2 = i2 < L ? zdoc[b + i2] : 0u,
-                           k3 = i3 < L ? zdoc[b + i3] : 0u;
-            count(zf);                                          // L > 32: every lane has one
-            if (i1 < L) count(k1);
-            if (i2 < L) count(k2);
-            if (i3 < L) count(k3);
-            for (uint32_t i = lane + 128u; i < L; i += 32) count(zdoc[b + i]);
-            __syncwarp();
-            uint32_t base = 0, mx = 0;
-            for (int c = 0; c < NW; c += 32) {
-                const int w = c + lane;
-                uint32_t word = w < NW ? bmp[w] : 0u;
-                const uint32_t pc = __popc(word);
-                uint32_t incl = pc;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                uint32_t pos = off + base + incl - pc;
-                if (w < NW) bmp[w] = 0u;
-                while (word) {
-                    const uint32_t k = ((uint32_t)w << 5) + (uint32_t)(__ffs(word) - 1);
-                    word &= word - 1u;
-                    const uint32_t v = bins[k];
-                    bins[k] = 0u;
-                    theta_ent[pos++] = (tpos(k, tm) << 2) | (min(v, 65535u) << 16);
-                    mx = max(mx, v);
-                }
-                base += __shfl_sync(kFull, incl, 31);
-            }
-            nnz = base;
-            mx = warp_max_u32(mx);
-            if (mx > 65535u && lane == 0) atomicMin(errs + 1, ((unsigned long long)d << 32) | mx);
-            __syncwarp();
+            // zero the row's padding up to a multiple of 8 entries: K1 reads rows
+            // as 32-byte granules and relies on (count 0) pads contributing nothing
+            if ((uint32_t)lane < ((8u - (nnz & 7u)) & 7u)) theta_ent[off + nnz + lane] = 0u;
+            if (lane == 0) theta_meta[d].y = nnz;
+            zf = zn;
         }
-        // zero the row's padding up to a multiple of 8 entries: K1 reads rows
-        // as 32-byte granules and relies on (count 0) pads contributing nothing
-        if ((uint32_t)lane < ((8u - (nnz & 7u)) & 7u)) theta_ent[off + nnz + lane] = 0u;
-        if (lane == 0) theta_meta[d].y = nnz;
-        b = b1; L = L1; off = o1;
-        b1 = b2; L1 = L2; o1 = o2;
-        zf = zn;
+        gb = nb;
+        gL = nL;
+        go = no;
     }
 }
 
@@ -559,9 +603,11 @@ cudaError_t launch_theta_rebuild(gf_shard* s, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, theta_rebuild_kernel, wpc * 32, smem);
     const long long need = (s->D + wpc - 1) / wpc;
     const long long grid = std::min<long long>(need, (long long)nsm * std::max(per_sm, 1));
+    // documents per warp group: 32, unless that leaves fewer than 4 groups per warp
+    const int gsz = (int)std::max<long long>(1, std::min<long long>(32, s->D / (4 * grid * wpc)));
     theta_rebuild_kernel<<<(unsigned)grid, wpc * 32, smem, st>>>((int)s->D, s->d.dw_ptr, s->d.zdoc,
                                                                          s->d.theta_ent, s->d.theta_meta, s->K, wpc,
-                                                                         s->d.errs);
+                                                                         gsz, s->d.errs);
     return cudaGetLastError();
 }
 

@@ -167,35 +167,6 @@ __global__ void k_slice_emit(int64_t N, int64_t R, const uint32_t* order, const 
     }
 }
 
-// K2 work items (unsorted slice order): one per slice of a u32-column word
-// (atomic when the word has several slices), one per u16-column group, plus
-// (appended on the host) an empty item per absent u16-column word
-__global__ void k_items_flags(int64_t N, int64_t R, int64_t ng, const uint32_t* srb, const uint32_t* run_group,
-                              const int32_t* g_col, uint32_t* flag) {
-    GRID_STRIDE(i, N + ng) {
-        if (i < N) flag[i] = g_col[run_group[srb[i]]] < 0 ? 1u : 0u;
-        else flag[i] = g_col[i - N] >= 0 ? 1u : 0u;
-    }
-}
-
-__global__ void k_items_emit(int64_t N, int64_t R, int64_t ng, int64_t T, const uint32_t* srb, const uint32_t* run_group,
-                             const uint32_t* run_start, const int32_t* g_col, const uint32_t* g_nslices,
-                             const uint32_t* go, const uint32_t* flag, const uint32_t* pos, int4* items) {
-    GRID_STRIDE(i, N + ng) {
-        if (!flag[i]) continue;
-        if (i < N) {
-            const uint32_t r0 = srb[i], r1 = i + 1 < N ? srb[i + 1] : (uint32_t)R, g = run_group[r0];
-            const uint32_t t1 = r1 < (uint32_t)R ? run_start[r1] : (uint32_t)T;
-            items[pos[i]] = make_int4(g_col[g], (int)run_start[r0], (int)t1, g_nslices[g] > 1 ? 1 : 0);
-        } else {
-            const int64_t g = i - N;
-            const uint32_t t1 = g + 1 < ng ? go[g + 1] : (uint32_t)T;
-            items[pos[i]] = make_int4(g_col[g], (int)go[g], (int)t1, 0);
-        }
-    }
-}
-
-
 // zdoc positions (heavy-first inside each document)
 __global__ void k_inverse(int64_t T, const uint32_t* dw_tok, uint32_t* inv) { GRID_STRIDE(q, T) inv[dw_tok[q]] = (uint32_t)q; }
 
@@ -445,9 +416,10 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
     shard_free_device(s);
     auto& dv = s->d;
     int rc;
-    if ((rc = shard_alloc(&dv.z, T, "z")) || (rc = shard_alloc(&dv.run_doc, R, "runs")) ||
+    // z, zdoc: + 8 tokens, K2 / K3 bulk-prefetch whole 16-byte vectors of a range
+    if ((rc = shard_alloc(&dv.z, T + 8, "z")) || (rc = shard_alloc(&dv.run_doc, R, "runs")) ||
         (rc = shard_alloc(&dv.run_start, R + 1, "runs")) || (rc = shard_alloc(&dv.run_dwpos, R, "runs")) || (rc = shard_alloc(&dv.run_rec, R, "runs")) ||
-        (rc = shard_alloc(&dv.dw_ptr, D + 1, "dw_ptr")) || (rc = shard_alloc(&dv.zdoc, T, "zdoc")) ||
+        (rc = shard_alloc(&dv.dw_ptr, D + 1, "dw_ptr")) || (rc = shard_alloc(&dv.zdoc, T + 8, "zdoc")) ||
         (rc = shard_alloc(&dv.theta_ent, cap + 8, "theta")) || (rc = shard_alloc(&dv.theta_meta, D, "theta")) ||
         (rc = shard_alloc(&dv.sync, s->sync_u32 + 1, "phi")) || (rc = shard_alloc(&dv.inv_den, 2 * K, "inv_den")) ||
         (rc = shard_alloc(&dv.ll_sum, kLlSlots, "ll")) || (rc = shard_alloc(&dv.errs, 4, "errs")) ||
@@ -597,36 +569,40 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
         k_slice_emit<<<blocks_for(N), 256, 0, st>>>(N, R, sorder, srb, run_group, c.gw, d_gcol, d_gctx, dv.slices,
                                                     dv.slice_ctx);
     }
-    // ---- K2 work items ----
-    uint32_t* iflag = sc.u32(N + ng + 1);
-    uint32_t* ipos = sc.u32(N + ng + 1);
-    CK(sc.err, "layout scratch");
-    int64_t M = 0;
-    if (N + ng > 0) {
-        k_items_flags<<<blocks_for(N + ng), 256, 0, st>>>(N, R, ng, srb, run_group, d_gcol, iflag);
-        CK(cub_call(sc, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, iflag, ipos, N + ng, st); }),
-           "items");
-        M = read_u32(st, iflag + N + ng - 1) + read_u32(st, ipos + N + ng - 1);
-    }
-    // light words absent from this shard still own a 16-bit column: K2 writes
-    // every light column densely (no memset of the light region), so each
-    // absent one gets an empty item that writes its zeros
-    std::vector<int4> zero_items;
+    // ---- K2 work items (host, O(groups)): one per u16-column (light) group,
+    // whose packed column the item writes densely (<= 65535 tokens); a
+    // u32-column (heavy) group is cut into pieces of <= kK2Piece tokens, each
+    // flushed with global atomics into its pre-zeroed column -- few enough
+    // atomics (K per piece) and pieces small enough to balance the warps.
+    // Independent of K1's slices.  Longest first, so no long item starts last;
+    // light words absent from this shard still own a 16-bit column (K2 writes
+    // every light column densely, no memset of the light region), so each
+    // absent one gets an empty item that writes its zeros. ----
+    const int64_t piece = std::max<int64_t>(1024, shard_env_int("GF_K2_PIECE", 16384));
+    std::vector<int4> items;
+    items.reserve((size_t)ng + (size_t)(T / piece) + 16);
     {
         std::vector<uint8_t> present((size_t)V, 0);
-        for (int64_t g = 0; g < ng; ++g) present[gw[g]] = 1;
+        for (int64_t g = 0; g < ng; ++g) {
+            present[gw[g]] = 1;
+            const int32_t col = s->word_col[gw[g]];
+            const int64_t t0 = go[g], t1 = go[g + 1];
+            if (col >= 0) {
+                items.push_back(make_int4(col, (int)t0, (int)t1, 0));
+            } else {
+                for (int64_t a = t0; a < t1; a += piece)
+                    items.push_back(make_int4(col, (int)a, (int)std::min(t1, a + piece), 1));
+            }
+        }
+        std::stable_sort(items.begin(), items.end(), [](const int4& a, const int4& b) { return a.z - a.y > b.z - b.y; });
         for (int32_t v = 0; v < V; ++v)
-            if (!present[v] && s->word_col[v] >= 0) zero_items.push_back(make_int4(s->word_col[v], 0, 0, 0));
+            if (!present[v] && s->word_col[v] >= 0) items.push_back(make_int4(s->word_col[v], 0, 0, 0));
     }
-    if ((rc = shard_alloc(&dv.k2items, M + (int64_t)zero_items.size(), "items"))) return rc;
-    if (M > 0)
-        k_items_emit<<<blocks_for(N + ng), 256, 0, st>>>(N, R, ng, T, srb, run_group, dv.run_start, d_gcol, d_gnsl,
-                                                         c.go, iflag, ipos, dv.k2items);
-    if (!zero_items.empty())
-        CK(cudaMemcpyAsync(dv.k2items + M, zero_items.data(), zero_items.size() * sizeof(int4), cudaMemcpyHostToDevice,
-                           st),
-           "items");
-    M += (int64_t)zero_items.size();
+    const int64_t M0 = (int64_t)items.size();
+    if ((rc = shard_alloc(&dv.k2items, M0, "items"))) return rc;
+    if (M0) CK(cudaMemcpyAsync(dv.k2items, items.data(), M0 * sizeof(int4), cudaMemcpyHostToDevice, st), "items");
+    CK(cudaStreamSynchronize(st), "items");            // `items` is freed at scope end
+    int64_t M = M0;
     // ---- zdoc positions: heavy-first inside each document ----
     if (T > 0) {
         uint32_t* inv = flag;                 // reuse: [T]

@@ -52,11 +52,6 @@ __device__ __forceinline__ void ldg256(const uint32_t* p, uint4& lo, uint4& hi) 
                  : "l"(p));
 }
 
-// TMA bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, bytes % 16 == 0)
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
 struct SampleArgs {
     int K, Kp;
     float alpha, beta, vbeta;

@@ -96,14 +96,18 @@ def chunk_shard(chunk, num_topics, vocab_size, alpha=1.0, beta=1.0, seed=0, devi
                 layout="chunk", any_vocab=False):
     """The resident shard of `chunk` with its assignments current (staged
     import: nothing is rewritten when they did not change).  any_vocab: any
-    resident shard of the chunk with this K will do (theta needs no phi layout)."""
+    resident shard of the chunk with this K will do (theta needs no phi
+    layout).  vocab_size may be a callable, evaluated only for a new shard."""
     arrays = (chunk.word_ids, chunk.doc_ids, chunk.dw_tok, chunk.group_offsets)
-    extra = (int(num_topics), int(vocab_size), int(device), int(chunk.doc_lo), int(chunk.doc_hi), layout)
     if any_vocab:
-        sh = RESIDENT.find(arrays, lambda e: e[0] == extra[0] and e[2:5] == extra[2:5])
+        want = (int(num_topics), int(device), int(chunk.doc_lo), int(chunk.doc_hi))
+        sh = RESIDENT.find(arrays, lambda e: (e[0],) + tuple(e[2:5]) == want)
         if sh is not None:
             _import_assignments(sh, chunk)
             return sh
+    if callable(vocab_size):          # only needed for a new shard (an O(T) scan for some callers)
+        vocab_size = vocab_size()
+    extra = (int(num_topics), int(vocab_size), int(device), int(chunk.doc_lo), int(chunk.doc_hi), layout)
 
     def build():
         sh = DeviceShard(num_topics, vocab_size, alpha, beta, seed=seed, device=device,
@@ -329,7 +333,7 @@ class DeviceShard:
         return self._shape[1]
 
     def get_assignments(self):
-        out = np.empty(self.num_tokens, np.uint16)
+        out = _lib.pinned_empty(self.num_tokens, np.uint16)
         _lib.check(_lib.lib().gf_shard_get_assignments(self._h, _lib.ptr(out)))
         return out
 
@@ -365,9 +369,9 @@ class DeviceShard:
         """(row_ptr int64[D_s+1], topic_ids uint16, counts uint16) of local rows."""
         nnz = ctypes.c_int64()
         _lib.check(_lib.lib().gf_shard_theta_nnz(self._h, ctypes.byref(nnz)))
-        rp = np.empty(self.num_docs + 1, np.int64)
-        ids = np.empty(nnz.value, np.uint16)
-        cn = np.empty(nnz.value, np.uint16)
+        rp = _lib.pinned_empty(self.num_docs + 1, np.int64)
+        ids = _lib.pinned_empty(nnz.value, np.uint16)
+        cn = _lib.pinned_empty(nnz.value, np.uint16)
         _lib.check(_lib.lib().gf_shard_get_theta(self._h, _lib.ptr(rp), _lib.ptr(ids), _lib.ptr(cn)))
         return rp, ids, cn
 
@@ -383,7 +387,7 @@ class DeviceShard:
         """(counts [K, V] row-major, uint32 -- or uint16 for width 16, which
         raises the reference's overflow text for a cell above 65535 --,
         topic_totals int64[K]) from the sync buffer."""
-        kv = np.empty((self.K, self.V), np.uint16 if width == 16 else np.uint32)
+        kv = _lib.pinned_empty((self.K, self.V), np.uint16 if width == 16 else np.uint32)
         tot = np.empty(self.K, np.int64)
         _lib.check(_lib.lib().gf_shard_get_phi_w(self._h, _lib.ptr(kv), int(width), _lib.ptr(tot)))
         return kv, tot

@@ -1004,3 +1004,46 @@ def test_drop_in_api_keeps_the_chunk_resident():
     l2 = ev.loglik_per_token(th, ph, corp, 50.0 / K, 0.01)
     assert l1 == l2
     RESIDENT.release()
+
+
+def test_api_results_live_in_cached_pinned_blocks():
+    """The one-call API returns its large arrays in pinned blocks
+    (_lib.pinned_empty / gf_host_alloc): ordinary writeable numpy arrays,
+    private to each call (a freed block is reused only after its last array
+    is gone), and an edit made in place -- the reference's own fault-injection
+    pattern (test_model.py:169-184) -- is what the next call sees."""
+    from paper_1803_04631_b200 import _lib
+    from paper_1803_04631_b200.shard import RESIDENT
+
+    def pinned(a):
+        while a is not None and not isinstance(a, _lib._PinnedBlock):
+            a = a.base
+        return a is not None
+
+    K = 64
+    corp = synth.generate(30000, 6000, 80.0, seed=21)         # ~2.4M tokens, K x V: every result array >= 1 MiB
+    ch = cp.partition(corp, 1, K, 5)[0]
+    RESIDENT.release()
+    th1 = md.rebuild_theta(ch, K)
+    ph1 = md.rebuild_phi_replica(ch, K, corp.vocab_size, width=32)
+    assert pinned(th1.topic_ids) and pinned(th1.counts) and pinned(ph1.counts)
+    assert th1.counts.flags.writeable and ph1.counts.flags.writeable
+    keep = th1.counts.copy()
+    th2 = md.rebuild_theta(ch, K)
+    assert not np.shares_memory(th1.counts, th2.counts)
+    np.testing.assert_array_equal(th2.counts, keep)
+    del th1
+    th3 = md.rebuild_theta(ch, K)                              # may reuse th1's block
+    np.testing.assert_array_equal(th2.counts, keep)            # th2 untouched
+    np.testing.assert_array_equal(th3.counts, keep)
+    assert md.check_conservation(th3, ph1, corp).ok
+    th3.counts[th3.row_ptr[1]] += 1                            # reference test_model.py:184
+    rep = md.check_conservation(th3, ph1, corp)
+    assert not rep.ok and "row 1" in rep.detail
+    ph1.counts[1, 0] += 1                                      # reference test_model.py:169-170
+    ph1.topic_totals[1] += 1
+    th4 = md.rebuild_theta(ch, K)
+    ctx = sampler.SamplerContext(50.0 / K, 0.01, K, corp.vocab_size)
+    z = sampler.sample_chunk(ch, md.rebuild_phi_replica(ch, K, corp.vocab_size), th4, ctx, iteration=1, seed=3)
+    assert pinned(z) and z.dtype == np.uint16 and len(z) == corp.num_tokens
+    RESIDENT.release()
