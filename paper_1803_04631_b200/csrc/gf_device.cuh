@@ -100,4 +100,31 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// Shared-memory accesses on 32-bit shared-window addresses.  Through a
+// generic pointer (e.g. a per-warp slice of an extern __shared__ array used
+// with atomicAdd) the compiler re-derives the CTA's shared window at every
+// access (S2UR SR_CgaCtaId + 4 uniform ops + LEA: ~6 extra issue slots per
+// atomic, measured in K3's SASS); with the address converted once these are
+// one LEA + the ATOMS / LDS.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void sh_red_add(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sh_red_or(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t sh_exch(uint32_t a, uint32_t v) {
+    uint32_t r;
+    asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
+    return r;
+}
+__device__ __forceinline__ uint32_t sh_ld(uint32_t a) {
+    uint32_t r;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a) : "memory");
+    return r;
+}
+__device__ __forceinline__ void sh_st(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 }  // namespace gf

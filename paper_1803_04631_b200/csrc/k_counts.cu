@@ -63,8 +63,9 @@ struct K2XArgs {
     unsigned long long* err = nullptr;
 };
 
-__device__ __forceinline__ void k2_count(uint32_t* bins, uint32_t k, int K, uint32_t t, unsigned long long* errs) {
-    if (k < (uint32_t)K) atomicAdd(&bins[k >> 1], 1u << ((k & 1u) << 4));
+// s_bins: 32-bit shared address of the warp's packed histogram
+__device__ __forceinline__ void k2_count(uint32_t s_bins, uint32_t k, int K, uint32_t t, unsigned long long* errs) {
+    if (k < (uint32_t)K) sh_red_add(s_bins + ((k >> 1) << 2), 1u << ((k & 1u) << 4));
     else atomicMin(errs, (unsigned long long)t);
 }
 
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
     for (int i = threadIdx.x; i < K; i += blockDim.x) nks[i] = 0u;
     if (warp < nwarps_per_cta)                                // only these warps own a histogram
         for (int i = lane; i < KW; i += 32) bins[i] = 0u;
+    const uint32_t s_bins = smem_addr(bins), s_nks = smem_addr(nks);
     if (X && blockIdx.x == 0 && threadIdx.x == 0)             // stripes no item writes (all-zero columns)
         for (int s = 0; s < x.nstripe; ++s)
             if (x.need[s] == 0u) k2x_signal(x, s);
@@ -172,8 +174,8 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
                 // the next two 16-byte loads per lane are in flight while the
                 // current two (16 topics) are counted by shared atomics ----
                 const uint32_t a0 = min(t1, (t0 + 7u) & ~7u), a1 = max(a0, t1 & ~7u);
-                if (t0 + lane < a0) k2_count(bins, z[t0 + lane], K, t0 + lane, errs);
-                if (a1 + lane < t1) k2_count(bins, z[a1 + lane], K, a1 + lane, errs);
+                if (t0 + lane < a0) k2_count(s_bins, z[t0 + lane], K, t0 + lane, errs);
+                if (a1 + lane < t1) k2_count(s_bins, z[a1 + lane], K, a1 + lane, errs);
                 const uint32_t qe = a1 >> 3;
                 uint32_t q = (a0 >> 3) + lane;
                 uint4 v[2];
@@ -192,8 +194,8 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
                             const uint32_t tb = 8u * (q + 32u * i);
 #pragma unroll
                             for (int h = 0; h < 4; ++h) {
-                                k2_count(bins, e[h] & 0xffffu, K, tb + 2u * h, errs);
-                                k2_count(bins, e[h] >> 16, K, tb + 2u * h + 1u, errs);
+                                k2_count(s_bins, e[h] & 0xffffu, K, tb + 2u * h, errs);
+                                k2_count(s_bins, e[h] >> 16, K, tb + 2u * h + 1u, errs);
                             }
                         }
                     }
@@ -213,8 +215,8 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
 #pragma unroll
                             for (int i = 0; i < 4; ++i) {
                                 const uint32_t k = 8u * j + 2u * i;
-                                if (bw[i] & 0xffffu) atomicAdd(&nks[k], bw[i] & 0xffffu);
-                                if (bw[i] >> 16) atomicAdd(&nks[k + 1], bw[i] >> 16);
+                                if (bw[i] & 0xffffu) sh_red_add(s_nks + 4u * k, bw[i] & 0xffffu);
+                                if (bw[i] >> 16) sh_red_add(s_nks + 4u * (k + 1), bw[i] >> 16);
                             }
                         }
                     } else {
@@ -222,8 +224,8 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
                             const uint32_t b = bins[j];
                             bins[j] = 0u;
                             dst[j] = b;
-                            if (b & 0xffffu) atomicAdd(&nks[2 * j], b & 0xffffu);
-                            if (b >> 16) atomicAdd(&nks[2 * j + 1], b >> 16);
+                            if (b & 0xffffu) sh_red_add(s_nks + 8u * j, b & 0xffffu);
+                            if (b >> 16) sh_red_add(s_nks + 8u * j + 4u, b >> 16);
                         }
                     }
                 } else {
@@ -233,8 +235,8 @@ __global__ void __launch_bounds__(kK2Warps * 32) phi_rebuild_kernel(const int4* 
                         if (!b) continue;
                         bins[j] = 0u;
                         const uint32_t k = 2u * j, c0 = b & 0xffffu, c1 = b >> 16;
-                        if (c0) { atomicAdd(&nks[k], c0); atomicAdd(dst + k, c0); }
-                        if (c1) { atomicAdd(&nks[k + 1], c1); atomicAdd(dst + k + 1, c1); }
+                        if (c0) { sh_red_add(s_nks + 4u * k, c0); atomicAdd(dst + k, c0); }
+                        if (c1) { sh_red_add(s_nks + 4u * (k + 1), c1); atomicAdd(dst + k + 1, c1); }
                     }
                 }
                 __syncwarp();
@@ -388,15 +390,18 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
     uint32_t* wpre = bmp + NW;                     // distinct topics below each bitmap word
     for (int i = lane; i < K + NW; i += 32) bins[i] = 0u;
     __syncwarp();
+    // 32-bit shared addresses of the warp's bins / bitmap / word ranks (sh_*)
+    const uint32_t s_bins = smem_addr(bins), s_bmp = smem_addr(bmp), s_wpre = smem_addr(wpre);
+    (void)wpre;
     const unsigned lt = (1u << lane) - 1u;
     // The warp takes GROUPS of gsz <= 32 consecutive documents (group g, then
     // g + the number of warps; gsz keeps >= 4 groups per warp): lane j holds
     // document j's {zdoc begin, length, theta row offset} (three coalesced
     // loads per group instead of three per document), and the next group's
-    // are loaded while this one is processed.  Halfway through a group, lane 0 bulk-prefetches the next
-    // group's topics into L2 (one contiguous zdoc range), so the next group's
-    // loads hit L2; the next document's first 32 topics are always in flight
-    // (registers) while the current one is counted.
+    // are loaded while this one is processed.  Halfway through a group, lane
+    // 0 bulk-prefetches the next group's topics into L2 (one contiguous zdoc
+    // range), so the next group's loads hit L2; the next document's first 32
+    // topics are always in flight (registers) while the current one is counted.
     const int ngroups = (D + gsz - 1) / gsz;
     const int gstride = gridDim.x * warps_per_cta;
     auto group_meta = [&](int g, uint32_t& mb, uint32_t& mL, uint32_t& mo) {
@@ -451,15 +456,15 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
                 // gets the count and clears the bin) and writes the entry.
                 const uint32_t ncol = (L + 31u) >> 5;
                 uint32_t kk[4] = {zf, 0xffffu, 0xffffu, 0xffffu};
-    #pragma unroll
+#pragma unroll
                 for (uint32_t j = 1; j < 4; ++j)
                     if (j < ncol && lane + 32u * j < L) kk[j] = zdoc[b + lane + 32u * j];
-    #pragma unroll
+#pragma unroll
                 for (uint32_t j = 0; j < 4; ++j) {
                     const uint32_t k = kk[j];
                     if (j < ncol && k < (uint32_t)K) {
-                        atomicAdd(&bins[k], 1u);
-                        atomicOr(&bmp[k >> 5], 1u << (k & 31u));
+                        sh_red_add(s_bins + 4u * k, 1u);
+                        sh_red_or(s_bmp + ((k >> 3) & ~3u), 1u << (k & 31u));
                     } else if (j < ncol && k != 0xffffu) {
                         atomicMin(errs + 2, (unsigned long long)d);
                         kk[j] = 0xffffu;
@@ -469,23 +474,23 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
                 if (NW <= 32) {
                     // K <= 1024: lane w holds bitmap word w and the distinct topics
                     // below it in registers; the emit fetches both by shuffle
-                    const uint32_t word = lane < NW ? bmp[lane] : 0u;
-                    if (lane < NW) bmp[lane] = 0u;
+                    const uint32_t word = lane < NW ? sh_ld(s_bmp + 4u * lane) : 0u;
+                    if (lane < NW) sh_st(s_bmp + 4u * lane, 0u);
                     const uint32_t pc = __popc(word);
                     uint32_t incl = pc;
-    #pragma unroll
+#pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
                         const uint32_t y = __shfl_up_sync(kFull, incl, o);
                         if (lane >= o) incl += y;
                     }
                     nnz = __shfl_sync(kFull, incl, 31);
                     const uint32_t pre = incl - pc;
-    #pragma unroll
+#pragma unroll
                     for (uint32_t j = 0; j < 4; ++j) {
                         if (j < ncol) {
                             const uint32_t k = kk[j], w = (k >> 5) & 31u;
                             const uint32_t ww = __shfl_sync(kFull, word, w), pw = __shfl_sync(kFull, pre, w);
-                            const uint32_t c = k < (uint32_t)K ? atomicExch(&bins[k], 0u) : 0u;
+                            const uint32_t c = k < (uint32_t)K ? sh_exch(s_bins + 4u * k, 0u) : 0u;
                             if (c)
                                 theta_ent[off + pw + __popc(ww & ((1u << (k & 31u)) - 1u))] =
                                     (tpos(k, tm) << 2) | (c << 16);               // <= 128: no overflow
@@ -495,39 +500,39 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
                     uint32_t base = 0;
                     for (int c = 0; c < NW; c += 32) {
                         const int w = c + lane;
-                        const uint32_t pc = w < NW ? __popc(bmp[w]) : 0u;
+                        const uint32_t pc = w < NW ? __popc(sh_ld(s_bmp + 4u * w)) : 0u;
                         uint32_t incl = pc;
-    #pragma unroll
+#pragma unroll
                         for (int o = 1; o < 32; o <<= 1) {
                             const uint32_t y = __shfl_up_sync(kFull, incl, o);
                             if (lane >= o) incl += y;
                         }
-                        if (w < NW) wpre[w] = base + incl - pc;
+                        if (w < NW) sh_st(s_wpre + 4u * w, base + incl - pc);
                         base += __shfl_sync(kFull, incl, 31);
                     }
                     nnz = base;
                     __syncwarp();
-    #pragma unroll
+#pragma unroll
                     for (uint32_t j = 0; j < 4; ++j) {
                         const uint32_t k = kk[j];
-                        const uint32_t c = (j < ncol && k < (uint32_t)K) ? atomicExch(&bins[k], 0u) : 0u;
+                        const uint32_t c = (j < ncol && k < (uint32_t)K) ? sh_exch(s_bins + 4u * k, 0u) : 0u;
                         if (c) {
                             const uint32_t w = k >> 5;
-                            theta_ent[off + wpre[w] + __popc(bmp[w] & ((1u << (k & 31u)) - 1u))] =
+                            theta_ent[off + sh_ld(s_wpre + 4u * w) + __popc(sh_ld(s_bmp + 4u * w) & ((1u << (k & 31u)) - 1u))] =
                                 (tpos(k, tm) << 2) | (c << 16);                 // <= 128: no overflow
                         }
                     }
                     __syncwarp();
-    #pragma unroll
+#pragma unroll
                     for (uint32_t j = 0; j < 4; ++j)
-                        if (j < ncol && kk[j] < (uint32_t)K) bmp[kk[j] >> 5] = 0u;
+                        if (j < ncol && kk[j] < (uint32_t)K) sh_st(s_bmp + ((kk[j] >> 3) & ~3u), 0u);
                 }
                 __syncwarp();
             } else {
                 auto count = [&](uint32_t k) {
                     if (k < (uint32_t)K) {
-                        atomicAdd(&bins[k], 1u);
-                        atomicOr(&bmp[k >> 5], 1u << (k & 31u));
+                        sh_red_add(s_bins + 4u * k, 1u);
+                        sh_red_or(s_bmp + ((k >> 3) & ~3u), 1u << (k & 31u));
                     } else {
                         atomicMin(errs + 2, (unsigned long long)d);
                     }
@@ -545,21 +550,21 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
                 uint32_t base = 0, mx = 0;
                 for (int c = 0; c < NW; c += 32) {
                     const int w = c + lane;
-                    uint32_t word = w < NW ? bmp[w] : 0u;
+                    uint32_t word = w < NW ? sh_ld(s_bmp + 4u * w) : 0u;
                     const uint32_t pc = __popc(word);
                     uint32_t incl = pc;
-    #pragma unroll
+#pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
                         const uint32_t y = __shfl_up_sync(kFull, incl, o);
                         if (lane >= o) incl += y;
                     }
                     uint32_t pos = off + base + incl - pc;
-                    if (w < NW) bmp[w] = 0u;
+                    if (w < NW) sh_st(s_bmp + 4u * w, 0u);
                     while (word) {
                         const uint32_t k = ((uint32_t)w << 5) + (uint32_t)(__ffs(word) - 1);
                         word &= word - 1u;
-                        const uint32_t v = bins[k];
-                        bins[k] = 0u;
+                        const uint32_t v = sh_ld(s_bins + 4u * k);
+                        sh_st(s_bins + 4u * k, 0u);
                         theta_ent[pos++] = (tpos(k, tm) << 2) | (min(v, 65535u) << 16);
                         mx = max(mx, v);
                     }
