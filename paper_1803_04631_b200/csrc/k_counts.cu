@@ -377,14 +377,23 @@ cudaError_t launch_prepare(gf_shard* s) {
 __host__ __device__ inline int k3_words(int K) { return (K + 31) >> 5; }
 __host__ __device__ inline int k3_warp_u32(int K) { return K + 2 * k3_words(K); }   // bins | bitmap | word ranks
 
-__global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
-                                                            const uint16_t* __restrict__ zdoc, uint32_t* theta_ent,
-                                                            uint2* theta_meta, int K, int warps_per_cta,
-                                                            int gsz, unsigned long long* errs) {
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
+                                                               const uint16_t* __restrict__ zdoc, uint32_t* theta_ent,
+                                                               uint2* theta_meta, int K, int warps_per_cta, int gsz,
+                                                               int pf_back, unsigned long long* errs) {
     extern __shared__ uint32_t sh[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int NW = k3_words(K);
-    const TPos tm = tpos_geom(K);
+    // CTA table of the entries' topic fields, tpos(k) << 2 (a lookup instead of
+    // the multiply-high / remainder per emitted entry)
+    uint32_t* tpo = sh + (size_t)warps_per_cta * k3_warp_u32(K);
+    {
+        const TPos tm = tpos_geom(K);
+        for (int k = threadIdx.x; k < K; k += blockDim.x) tpo[k] = tpos((uint32_t)k, tm) << 2;
+        __syncthreads();
+    }
+    const uint32_t s_tpo = smem_addr(tpo);
     uint32_t* bins = sh + (size_t)warp * k3_warp_u32(K);
     uint32_t* bmp = bins + K;
     uint32_t* wpre = bmp + NW;                     // distinct topics below each bitmap word
@@ -425,7 +434,7 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
             const uint32_t b1 = __shfl_sync(kFull, last ? nb : gb, last ? 0 : i + 1);
             const uint32_t L1 = __shfl_sync(kFull, last ? nL : gL, last ? 0 : i + 1);
             const uint32_t zn = (uint32_t)lane < L1 ? zdoc[b1 + lane] : 0xffffu;        // L1 = 0 past the end
-            if (i == (gsz >> 1)) {
+            if (i == max(nd - pf_back, 0) && pf_back > 0) {
                 const uint32_t b0 = __shfl_sync(kFull, nb, 0), end = __reduce_max_sync(kFull, nL ? nb + nL : 0u);
                 if (lane == 0 && end > b0) {
                     const uint32_t p0 = b0 & ~7u, p1 = (end + 7u) & ~7u;
@@ -444,7 +453,7 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
                 if (head) {
                     const unsigned later = heads & ~((2u << lane) - 1u);
                     const uint32_t next = later ? (uint32_t)(__ffs(later) - 1) : L;
-                    theta_ent[off + __popc(heads & lt)] = (tpos(key, tm) << 2) | ((next - lane) << 16);
+                    theta_ent[off + __popc(heads & lt)] = sh_ld(s_tpo + 4u * key) | ((next - lane) << 16);
                 }
                 nnz = __popc(heads);
             } else if (L <= 128) {
@@ -493,7 +502,7 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
                             const uint32_t c = k < (uint32_t)K ? sh_exch(s_bins + 4u * k, 0u) : 0u;
                             if (c)
                                 theta_ent[off + pw + __popc(ww & ((1u << (k & 31u)) - 1u))] =
-                                    (tpos(k, tm) << 2) | (c << 16);               // <= 128: no overflow
+                                    sh_ld(s_tpo + 4u * k) | (c << 16);               // <= 128: no overflow
                         }
                     }
                 } else {
@@ -519,7 +528,7 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
                         if (c) {
                             const uint32_t w = k >> 5;
                             theta_ent[off + sh_ld(s_wpre + 4u * w) + __popc(sh_ld(s_bmp + 4u * w) & ((1u << (k & 31u)) - 1u))] =
-                                (tpos(k, tm) << 2) | (c << 16);                 // <= 128: no overflow
+                                sh_ld(s_tpo + 4u * k) | (c << 16);                 // <= 128: no overflow
                         }
                     }
                     __syncwarp();
@@ -565,7 +574,7 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
                         word &= word - 1u;
                         const uint32_t v = sh_ld(s_bins + 4u * k);
                         sh_st(s_bins + 4u * k, 0u);
-                        theta_ent[pos++] = (tpos(k, tm) << 2) | (min(v, 65535u) << 16);
+                        theta_ent[pos++] = sh_ld(s_tpo + 4u * k) | (min(v, 65535u) << 16);
                         mx = max(mx, v);
                     }
                     base += __shfl_sync(kFull, incl, 31);
@@ -587,33 +596,41 @@ __global__ void __launch_bounds__(256, 5) theta_rebuild_kernel(int D, const uint
     }
 }
 
-cudaError_t launch_theta_rebuild(gf_shard* s, cudaStream_t st) {
-    if (s->D == 0) return cudaSuccess;
-    if (!st) st = s->stream;
+template <int MINB>
+static cudaError_t launch_k3(gf_shard* s, cudaStream_t st) {
     const size_t per_warp = (size_t)k3_warp_u32(s->K) * 4;
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * per_warp > 96 * 1024) wpc >>= 1;
-    const size_t smem = (size_t)wpc * per_warp;
+    const size_t smem = (size_t)wpc * per_warp + (size_t)s->K * 4;     // + the tpos table
     static unsigned long long attr = 0;
     if (attr_once(attr, s->device)) {
-        cudaError_t e = cudaFuncSetAttribute(theta_rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(theta_rebuild_kernel<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              200 * 1024);
         if (e != cudaSuccess) return e;
     }
-    // persistent grid (exactly the resident CTAs): the warps sweep the
-    // documents as one contiguous moving window, so the word-major z sectors
-    // they gather are shared by neighbouring documents while still in L2
+    // persistent grid (exactly the resident CTAs)
     const int nsm = sm_count(s->device);
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, theta_rebuild_kernel, wpc * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, theta_rebuild_kernel<MINB>, wpc * 32, smem);
     const long long need = (s->D + wpc - 1) / wpc;
     const long long grid = std::min<long long>(need, (long long)nsm * std::max(per_sm, 1));
     // documents per warp group: 32, unless that leaves fewer than 4 groups per warp
     const int gsz = (int)std::max<long long>(1, std::min<long long>(32, s->D / (4 * grid * wpc)));
-    theta_rebuild_kernel<<<(unsigned)grid, wpc * 32, smem, st>>>((int)s->D, s->d.dw_ptr, s->d.zdoc,
-                                                                         s->d.theta_ent, s->d.theta_meta, s->K, wpc,
-                                                                         gsz, s->d.errs);
+    // the next group's topics are bulk-prefetched into L2 this many documents
+    // before the group ends (0: off)
+    static const int pf_back = (int)shard_env_int("GF_K3_PF", 8);
+    theta_rebuild_kernel<MINB><<<(unsigned)grid, wpc * 32, smem, st>>>((int)s->D, s->d.dw_ptr, s->d.zdoc,
+                                                                       s->d.theta_ent, s->d.theta_meta, s->K, wpc, gsz,
+                                                                       pf_back, s->d.errs);
     return cudaGetLastError();
+}
+
+cudaError_t launch_theta_rebuild(gf_shard* s, cudaStream_t st) {
+    if (s->D == 0) return cudaSuccess;
+    if (!st) st = s->stream;
+    // GF_K3_MINB (A/B): CTAs per SM the register budget is sized for
+    static const int minb = (int)shard_env_int("GF_K3_MINB", 5);
+    return minb == 4 ? launch_k3<4>(s, st) : launch_k3<5>(s, st);
 }
 
 // ------------------------------------------------------------ zdoc sync ------
