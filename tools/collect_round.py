@@ -59,8 +59,46 @@ for ext in ("csv", "json"):
     if os.path.exists(f):
         shutil.copy(f, P)
 with open(os.path.join(P, f"{tag}_sanitizer.txt"), "w") as fh:
-    for t in ["memcheck", "racecheck", "synccheck", "initcheck", "memcheck_tests"]:
+    for t in ["memcheck", "racecheck", "synccheck", "initcheck", "memcheck_tests", "memcheck_k23"]:
         f = os.path.join(O, f"san_{t}.log")
         if os.path.exists(f):
             fh.write(f"== {t}\n" + "".join(open(f).readlines()[-3:]))
 print("collected", tag)
+
+# roofline.traffic lookup for bench.py: DRAM bytes of the captured K1 launch
+# (iteration 6, inside the default timed range) per workload
+import io
+import json
+
+
+def k1_dram(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "-k", "regex:sample_kernel"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        return None
+    h, u, v = rows[0], rows[1], rows[2]
+    sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    get = lambda m: float(v[h.index(m)].replace(",", "")) * sc.get(u[h.index(m)], 1)
+    return {"kernel": v[h.index("Kernel Name")].split("(")[0], "dram_read_bytes": int(get("dram__bytes_read.sum")),
+            "dram_write_bytes": int(get("dram__bytes_write.sum")),
+            "bytes_per_launch": int(get("dram__bytes_read.sum") + get("dram__bytes_write.sum")),
+            "lts_hit_rate_pct": float(v[h.index("lts__t_sector_hit_rate.pct")])}
+
+
+tf = os.path.join(P, "sample_kernel_traffic.json")
+traffic = json.load(open(tf)) if os.path.exists(tf) else {}
+for key, rep, what in [("pubmed-1024", f"{tag}_pm.ncu-rep", "bench.py --steps 2 --warmup 5 (default workload)"),
+                       ("nytimes-1024", f"{tag}_k1_nyt.ncu-rep", "bench.py --workload nytimes --steps 2 --warmup 5")]:
+    r = os.path.join(O, rep)
+    if os.path.exists(r):
+        d = k1_dram(r)
+        if d:
+            d["source"] = f"profiles/{tag}_* (ncu --set full of `{what}`, the K1 launch of iteration 6)"
+            d["iteration"] = 6
+            traffic[key] = d
+traffic["note"] = ("dram__bytes_read.sum + dram__bytes_write.sum of one K1 launch (ncu --set full at iteration 6, "
+                   "inside bench.py's default timed range of iterations 3..12); bench.py reports the entry matching its "
+                   "--workload and K as roofline.traffic.  Algorithmic bytes per launch are reported live by bench.py.")
+json.dump(traffic, open(tf, "w"), indent=2)
+print("traffic entries", sorted(k for k in traffic if k != "note"))

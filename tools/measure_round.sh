@@ -40,14 +40,17 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   -k regex:"sample_kernel|phi_rebuild|theta_rebuild|prepare_kernel|context_kernel|ll_reduce" -s 6 -c 36 --csv \
   --log-file $o/${tag}_launches_pm.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 echo "launch list rc=$?"
-# full captures: K1 / K2 / K3 of iteration 3 (default workload), K5, K1 on NYTimes-shape
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"sample_kernel|theta_rebuild|phi_rebuild" -s 9 -c 3 \
-  -o $o/${tag}_pm python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+# full captures at ITERATION 6 (inside bench.py's default timed range,
+# iterations 3..12): K1 / K2 / K3 of the default workload, K5, K1 on
+# NYTimes-shape.  Matched launches: K2, K3 (initial counts), then per
+# iteration K1, K3, K2 -- so -s 20 is iteration 6 (--warmup 5).
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"sample_kernel|theta_rebuild|phi_rebuild" -s 20 -c 3 \
+  -o $o/${tag}_pm python bench.py --steps 2 --warmup 5 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 echo "pubmed capture rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k5_" -c 6 \
   -o $o/${tag}_k5_pm python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 echo "k5 capture rc=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"sample_kernel" -s 3 -c 1 \
-  -o $o/${tag}_k1_nyt python bench.py --workload nytimes --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"sample_kernel" -s 6 -c 1 \
+  -o $o/${tag}_k1_nyt python bench.py --workload nytimes --steps 2 --warmup 5 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 echo "k1 nyt capture rc=$?"
-bash tools/sanitize.sh
+[ "${SANITIZE:-1}" = 1 ] && bash tools/sanitize.sh
