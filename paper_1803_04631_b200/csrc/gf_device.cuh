@@ -127,4 +127,27 @@ __device__ __forceinline__ void sh_st(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
+// One-shot TMA bulk copy global -> this CTA's shared memory (16-byte
+// aligned, bytes % 16 == 0) completing on an mbarrier: thread 0 arms the
+// barrier and issues the copy, every thread waits on phase 0.  The caller
+// passes a fresh __shared__ 8-byte barrier and synchronises the block between
+// bulk_copy_issue and bulk_copy_wait (the barrier's init must be visible).
+__device__ __forceinline__ void bulk_copy_issue(uint32_t bar, uint32_t dst, const void* src, uint32_t bytes) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_copy_wait(uint32_t bar) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar)
+        : "memory");
+}
+
 }  // namespace gf

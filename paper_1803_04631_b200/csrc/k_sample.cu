@@ -61,6 +61,7 @@ struct SampleArgs {
     int eval_only;                            // loglik of the current model only
     int prefetch;                             // bulk-prefetch each batch's theta rows into L2
     int guide_min_tokens;                     // slices below this build no Q guide
+    int ctx_tma;                              // copy precomputed contexts by TMA bulk copy
     TreeGeom tree;
     const int4* slices;
     const uint32_t* run_doc;
@@ -412,10 +413,23 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     const int ctx = a.slice_ctx[blockIdx.x];
     // the Q guide pays off only for slices with many tokens (contexts always have one)
     bool guided = __ldg(a.run_start + sl.z) - __ldg(a.run_start + sl.y) >= (uint32_t)a.guide_min_tokens;
-    if (ctx >= 0) {                                  // word split into several slices: copy (L2)
-        const float4* src = reinterpret_cast<const float4*>(a.ctx_tab + (size_t)ctx * a.ctx_stride);
-        for (int i = tid; i < a.ctx_stride / 4; i += NT) reinterpret_cast<float4*>(smem)[i] = __ldg(src + i);
-        __syncthreads();
+    if (ctx >= 0) {
+        // word split into several slices: its context (built once per
+        // iteration by context_kernel) arrives by one TMA bulk copy from L2
+        // instead of ~7 dependent 2 KB load/store rounds of the whole CTA
+        if (a.ctx_tma) {
+            __shared__ __align__(8) unsigned long long ctx_bar;
+            const uint32_t bar = smem_addr(&ctx_bar);
+            if (tid == 0)
+                bulk_copy_issue(bar, smem_addr(smem), a.ctx_tab + (size_t)ctx * a.ctx_stride,
+                                (uint32_t)a.ctx_stride * 4u);
+            __syncthreads();
+            bulk_copy_wait(bar);
+        } else {                                     // (A/B: GF_CTX_TMA=0) thread copy
+            const float4* src = reinterpret_cast<const float4*>(a.ctx_tab + (size_t)ctx * a.ctx_stride);
+            for (int i = tid; i < a.ctx_stride / 4; i += NT) reinterpret_cast<float4*>(smem)[i] = __ldg(src + i);
+            __syncthreads();
+        }
         guided = true;
     } else {
         build_context<NT>(a, col, smem, tid, guided);
@@ -735,6 +749,7 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     a.prefetch = (int)env_flag("GF_PREFETCH", 1);
     a.zero_ent = (uint32_t)s->theta_cap;
     a.guide_min_tokens = (int)env_flag("GF_GUIDE_MIN", 512);
+    a.ctx_tma = (int)env_flag("GF_CTX_TMA", 1);
     a.tree = s->tree;
     a.slices = s->d.slices;
     a.run_doc = s->d.run_doc;
