@@ -62,6 +62,7 @@ struct SampleArgs {
     int prefetch;                             // bulk-prefetch each batch's theta rows into L2
     int guide_min_tokens;                     // slices below this build no Q guide
     int ctx_tma;                              // copy precomputed contexts by TMA bulk copy
+    int rec_prefetch;                         // bulk-prefetch each slice's run records into L2
     TreeGeom tree;
     const int4* slices;
     const uint32_t* run_doc;
@@ -409,7 +410,12 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     const int col = sl.w;
 
     // ---------------- prologue: the word context (p*, p*_ex, Q-tree) ----------------
-    if (tid == 0) next_run = sl.y;
+    if (tid == 0) {
+        next_run = sl.y;
+        // the slice's run records (16 B each, streamed once per iteration) into
+        // L2 now, so each batch's record load is an L2 hit, not a DRAM round trip
+        if (a.rec_prefetch && sl.z > sl.y) prefetch_l2_bulk(a.run_rec + sl.y, (uint32_t)(sl.z - sl.y) * 16u);
+    }
     const int ctx = a.slice_ctx[blockIdx.x];
     // the Q guide pays off only for slices with many tokens (contexts always have one)
     bool guided = __ldg(a.run_start + sl.z) - __ldg(a.run_start + sl.y) >= (uint32_t)a.guide_min_tokens;
@@ -750,6 +756,7 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     a.zero_ent = (uint32_t)s->theta_cap;
     a.guide_min_tokens = (int)env_flag("GF_GUIDE_MIN", 512);
     a.ctx_tma = (int)env_flag("GF_CTX_TMA", 1);
+    a.rec_prefetch = (int)env_flag("GF_REC_PF", 0);       // measured: PubMed +0.2%, NYTimes -0.2%
     a.tree = s->tree;
     a.slices = s->d.slices;
     a.run_doc = s->d.run_doc;

@@ -26,7 +26,7 @@ from typing import Optional
 import numpy as np
 
 from .corpus import greedy_boundaries, make_chunk
-from .errors import ShapeMismatchError
+from .errors import CapacityError, ShapeMismatchError
 from .model import PhiMatrix, ThetaRows, concat_theta, conservation_report, phi_dtype
 
 
@@ -130,6 +130,9 @@ class Trainer:
             import torch
 
             torch.cuda.set_device(device)          # before the first NCCL collective (one GPU per rank)
+        if corpus.num_tokens >= 2**32:
+            # n_k (sync buffer) and the theta / phi cells it bounds are 32-bit words
+            raise CapacityError(f"corpus has {corpus.num_tokens} tokens; topic totals are 32-bit (at most 2^32 - 1)")
         freq = np.bincount(self.chunk.word_ids, minlength=V).astype(np.int64)
         self.global_freq = self._allreduce_np(freq)
         if shard_factory is None:
