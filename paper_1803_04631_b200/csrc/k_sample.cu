@@ -59,7 +59,7 @@ struct SampleArgs {
     uint32_t iteration;
     uint32_t doc_lo;
     int eval_only;                            // loglik of the current model only
-    int prefetch;                             // bulk-prefetch each batch's theta rows into L2
+    int prefetch;                             // prefetch each batch's theta rows into L2 (1 lines, 2 bulk)
     int guide_min_tokens;                     // slices below this build no Q guide
     int ctx_tma;                              // copy precomputed contexts by TMA bulk copy
     int rec_prefetch;                         // bulk-prefetch each slice's run records into L2
@@ -470,8 +470,16 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
             nbytes += nnz;
             // the whole row (32-byte granules) into L2 now: the pass then streams
             // the batch's rows with every line already requested, instead of one
-            // 1 KB warp step in flight at a time
-            if (a.prefetch && nnz) prefetch_l2_bulk(a.theta_ent + off, ((nnz + 7u) & ~7u) * 4u);
+            // 1 KB warp step in flight at a time.  One per-thread line prefetch
+            // per 128 B of the row (GF_PREFETCH=2: the TMA bulk prefetch, which
+            // the compiler serialises over the lanes: uniform operands)
+            if (a.prefetch == 1 && nnz) {
+                const uint32_t* row = a.theta_ent + off;
+                const uint32_t lines = (((off & 31u) + ((nnz + 7u) & ~7u)) + 31u) >> 5;   // 32 entries per line
+                for (uint32_t l = 0; l < lines; ++l) prefetch_l2_line(row - (off & 31u) + 32u * l);
+            } else if (a.prefetch == 2 && nnz) {
+                prefetch_l2_bulk(a.theta_ent + off, ((nnz + 7u) & ~7u) * 4u);
+            }
         }
         t1 = __shfl_down_sync(kFull, t0, 1);                        // the next run's first token
         if (lane == nval - 1) t1 = __ldg(a.run_start + r + 1);
@@ -752,7 +760,7 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     a.iteration = iteration;
     a.doc_lo = (uint32_t)s->doc_lo;
     a.eval_only = eval_only;
-    a.prefetch = (int)env_flag("GF_PREFETCH", 1);
+    a.prefetch = (int)env_flag("GF_PREFETCH", 1);          // 1 line prefetches, 2 TMA bulk, 0 none
     a.zero_ent = (uint32_t)s->theta_cap;
     a.guide_min_tokens = (int)env_flag("GF_GUIDE_MIN", 512);
     a.ctx_tma = (int)env_flag("GF_CTX_TMA", 1);
