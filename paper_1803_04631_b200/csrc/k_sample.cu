@@ -63,6 +63,7 @@ struct SampleArgs {
     int guide_min_tokens;                     // slices below this build no Q guide
     int ctx_tma;                              // copy precomputed contexts by TMA bulk copy
     int rec_prefetch;                         // bulk-prefetch each slice's run records into L2
+    int grab_tokens;                          // > 0: target tokens per grab (runs per grab from the slice average)
     TreeGeom tree;
     const int4* slices;
     const uint32_t* run_doc;
@@ -418,7 +419,8 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     }
     const int ctx = a.slice_ctx[blockIdx.x];
     // the Q guide pays off only for slices with many tokens (contexts always have one)
-    bool guided = __ldg(a.run_start + sl.z) - __ldg(a.run_start + sl.y) >= (uint32_t)a.guide_min_tokens;
+    const uint32_t slice_tokens = __ldg(a.run_start + sl.z) - __ldg(a.run_start + sl.y);
+    bool guided = slice_tokens >= (uint32_t)a.guide_min_tokens;
     if (ctx >= 0) {
         // word split into several slices: its context (built once per
         // iteration by context_kernel) arrives by one TMA bulk copy from L2
@@ -446,7 +448,13 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     float* buf = wbuf + warp * CAPV;
     // runs per grab: 32 (one per lane) unless the slice is too small to give
     // every warp at least two grabs -- then smaller grabs keep all 8 warps busy
-    const int batch = min(32, max(1, (sl.z - sl.y + 2 * kWarps - 1) / (2 * kWarps)));
+    // GF_GRAB_TOKENS > 0 (A/B): runs per grab sized so a grab holds about that
+    // many tokens on this slice's average (fewer half-empty draw rounds)
+    const int nruns = sl.z - sl.y;
+    const int tok_cap = a.grab_tokens > 0 && slice_tokens > 0
+                            ? max(1, (int)((unsigned long long)a.grab_tokens * (unsigned)nruns / slice_tokens))
+                            : 32;
+    const int batch = min(min(32, tok_cap), max(1, (nruns + 2 * kWarps - 1) / (2 * kWarps)));
     double ll = 0.0;
     unsigned long long nbytes = 0;
 
@@ -765,6 +773,7 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     a.guide_min_tokens = (int)env_flag("GF_GUIDE_MIN", 512);
     a.ctx_tma = (int)env_flag("GF_CTX_TMA", 1);
     a.rec_prefetch = (int)env_flag("GF_REC_PF", 0);       // measured: PubMed +0.2%, NYTimes -0.2%
+    a.grab_tokens = (int)env_flag("GF_GRAB_TOKENS", 0);
     a.tree = s->tree;
     a.slices = s->d.slices;
     a.run_doc = s->d.run_doc;
