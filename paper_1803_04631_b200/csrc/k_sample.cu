@@ -61,9 +61,6 @@ struct SampleArgs {
     int eval_only;                            // loglik of the current model only
     int prefetch;                             // prefetch each batch's theta rows into L2 (1 lines, 2 bulk)
     int guide_min_tokens;                     // slices below this build no Q guide
-    int ctx_tma;                              // copy precomputed contexts by TMA bulk copy
-    int rec_prefetch;                         // bulk-prefetch each slice's run records into L2
-    int grab_tokens;                          // > 0: target tokens per grab (runs per grab from the slice average)
     TreeGeom tree;
     const int4* slices;
     const uint32_t* run_doc;
@@ -411,33 +408,20 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     const int col = sl.w;
 
     // ---------------- prologue: the word context (p*, p*_ex, Q-tree) ----------------
-    if (tid == 0) {
-        next_run = sl.y;
-        // the slice's run records (16 B each, streamed once per iteration) into
-        // L2 now, so each batch's record load is an L2 hit, not a DRAM round trip
-        if (a.rec_prefetch && sl.z > sl.y) prefetch_l2_bulk(a.run_rec + sl.y, (uint32_t)(sl.z - sl.y) * 16u);
-    }
+    if (tid == 0) next_run = sl.y;
     const int ctx = a.slice_ctx[blockIdx.x];
     // the Q guide pays off only for slices with many tokens (contexts always have one)
-    const uint32_t slice_tokens = __ldg(a.run_start + sl.z) - __ldg(a.run_start + sl.y);
-    bool guided = slice_tokens >= (uint32_t)a.guide_min_tokens;
+    bool guided = __ldg(a.run_start + sl.z) - __ldg(a.run_start + sl.y) >= (uint32_t)a.guide_min_tokens;
     if (ctx >= 0) {
         // word split into several slices: its context (built once per
         // iteration by context_kernel) arrives by one TMA bulk copy from L2
         // instead of ~7 dependent 2 KB load/store rounds of the whole CTA
-        if (a.ctx_tma) {
-            __shared__ __align__(8) unsigned long long ctx_bar;
-            const uint32_t bar = smem_addr(&ctx_bar);
-            if (tid == 0)
-                bulk_copy_issue(bar, smem_addr(smem), a.ctx_tab + (size_t)ctx * a.ctx_stride,
-                                (uint32_t)a.ctx_stride * 4u);
-            __syncthreads();
-            bulk_copy_wait(bar);
-        } else {                                     // (A/B: GF_CTX_TMA=0) thread copy
-            const float4* src = reinterpret_cast<const float4*>(a.ctx_tab + (size_t)ctx * a.ctx_stride);
-            for (int i = tid; i < a.ctx_stride / 4; i += NT) reinterpret_cast<float4*>(smem)[i] = __ldg(src + i);
-            __syncthreads();
-        }
+        __shared__ __align__(8) unsigned long long ctx_bar;
+        const uint32_t bar = smem_addr(&ctx_bar);
+        if (tid == 0)
+            bulk_copy_issue(bar, smem_addr(smem), a.ctx_tab + (size_t)ctx * a.ctx_stride, (uint32_t)a.ctx_stride * 4u);
+        __syncthreads();
+        bulk_copy_wait(bar);
         guided = true;
     } else {
         build_context<NT>(a, col, smem, tid, guided);
@@ -448,13 +432,7 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     float* buf = wbuf + warp * CAPV;
     // runs per grab: 32 (one per lane) unless the slice is too small to give
     // every warp at least two grabs -- then smaller grabs keep all 8 warps busy
-    // GF_GRAB_TOKENS > 0 (A/B): runs per grab sized so a grab holds about that
-    // many tokens on this slice's average (fewer half-empty draw rounds)
-    const int nruns = sl.z - sl.y;
-    const int tok_cap = a.grab_tokens > 0 && slice_tokens > 0
-                            ? max(1, (int)((unsigned long long)a.grab_tokens * (unsigned)nruns / slice_tokens))
-                            : 32;
-    const int batch = min(min(32, tok_cap), max(1, (nruns + 2 * kWarps - 1) / (2 * kWarps)));
+    const int batch = min(32, max(1, (sl.z - sl.y + 2 * kWarps - 1) / (2 * kWarps)));
     double ll = 0.0;
     unsigned long long nbytes = 0;
 
@@ -479,12 +457,19 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
             // the whole row (32-byte granules) into L2 now: the pass then streams
             // the batch's rows with every line already requested, instead of one
             // 1 KB warp step in flight at a time.  One per-thread line prefetch
-            // per 128 B of the row (GF_PREFETCH=2: the TMA bulk prefetch, which
-            // the compiler serialises over the lanes: uniform operands)
+            // per 128 B of the row, at most 8 (a fixed, predicated sequence: a
+            // variable-trip loop here made the compiler rematerialise the shared
+            // base and lane id inside the pass loop, 103 -> 127 instructions per
+            // step).  GF_PREFETCH=2: cp.async.bulk.prefetch, whose uniform
+            // operands the compiler serialises over the 32 lanes (13% of K1's
+            // instructions, measured).
             if (a.prefetch == 1 && nnz) {
-                const uint32_t* row = a.theta_ent + off;
+                const uint32_t* line = a.theta_ent + (off & ~31u);
                 const uint32_t lines = (((off & 31u) + ((nnz + 7u) & ~7u)) + 31u) >> 5;   // 32 entries per line
-                for (uint32_t l = 0; l < lines; ++l) prefetch_l2_line(row - (off & 31u) + 32u * l);
+                prefetch_l2_line(line);
+#pragma unroll
+                for (uint32_t l = 1; l < 8; ++l)
+                    if (l < lines) prefetch_l2_line(line + 32u * l);
             } else if (a.prefetch == 2 && nnz) {
                 prefetch_l2_bulk(a.theta_ent + off, ((nnz + 7u) & ~7u) * 4u);
             }
@@ -771,9 +756,6 @@ static SampleArgs make_args(gf_shard* s, uint32_t iteration, int eval_only) {
     a.prefetch = (int)env_flag("GF_PREFETCH", 1);          // 1 line prefetches, 2 TMA bulk, 0 none
     a.zero_ent = (uint32_t)s->theta_cap;
     a.guide_min_tokens = (int)env_flag("GF_GUIDE_MIN", 512);
-    a.ctx_tma = (int)env_flag("GF_CTX_TMA", 1);
-    a.rec_prefetch = (int)env_flag("GF_REC_PF", 0);       // measured: PubMed +0.2%, NYTimes -0.2%
-    a.grab_tokens = (int)env_flag("GF_GRAB_TOKENS", 0);
     a.tree = s->tree;
     a.slices = s->d.slices;
     a.run_doc = s->d.run_doc;
