@@ -832,10 +832,15 @@ cudaError_t launch_sample_range(gf_shard* s, uint32_t iteration, int eval_only, 
     if (s->K > 2048) return launch_variant<256, kCapV, 3, true, false>(s, a, n);    // p*_ex on demand: 3 x 8 warps/SM
     if (var == 2) return launch_variant<256, kCapV, 4, true, false>(s, a, n);        // 8-warp CTAs (A/B)
     if (var == 3) return launch_variant<128, 768, 8, false, false>(s, a, n);         // no pass prefetch (A/B)
-    // 4-warp CTAs, 8 per SM: a slice's tail (warps idle at the final barrier
-    // while the last batch finishes) strands half as many warps; the pass keeps
-    // its next 1 KB step in flight
-    return launch_variant<128, 768, 8, true, false>(s, a, n);
+    if (var == 1) return launch_variant<128, 768, 8, true, false>(s, a, n);          // 8 CTAs/SM (A/B)
+    if (var == 5) return launch_variant<128, 512, 10, true, false>(s, a, n);         // 10 CTAs/SM (A/B)
+    // 4-warp CTAs, 9 per SM (52 registers, 640-vector staging: rows <= 2560
+    // entries, i.e. any K <= 2048): a slice's tail (warps idle at the final
+    // barrier while the last batch finishes) strands few warps, the pass keeps
+    // its next 1 KB step in flight.  Measured against 8 CTAs/SM (768-vector
+    // staging, 63 registers): PubMed-shape equal, the 8-way shard proxy 2.3%
+    // faster (smaller slices: more prologue latency to hide); 10 CTAs/SM slower.
+    return launch_variant<128, 640, 9, true, false>(s, a, n);
 }
 
 }  // namespace gf
