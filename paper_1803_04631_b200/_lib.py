@@ -15,7 +15,8 @@ import numpy as np
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "_lib", "libgfb200.so")
+# GF_LIB: another build of the same library (A/B of kernel variants on one box)
+SO_PATH = os.environ.get("GF_LIB") or os.path.join(_HERE, "_lib", "libgfb200.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "gibbsflow_b200.h")
 
 _p = ctypes.c_void_p
