@@ -612,6 +612,10 @@ static cudaError_t launch_k3(gf_shard* s, cudaStream_t st) {
     const int nsm = sm_count(s->device);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, theta_rebuild_kernel<MINB>, wpc * 32, smem);
+    // GF_K3_CTAS (A/B): fewer resident CTAs per SM, leaving room for K2's CTAs
+    // beside it in the step (K3 alone fills the register file at 5 per SM)
+    static const int cap_sm = (int)shard_env_int("GF_K3_CTAS", 0);
+    if (cap_sm > 0) per_sm = std::min(per_sm, cap_sm);
     const long long need = (s->D + wpc - 1) / wpc;
     const long long grid = std::min<long long>(need, (long long)nsm * std::max(per_sm, 1));
     // documents per warp group: 32, unless that leaves fewer than 4 groups per warp
