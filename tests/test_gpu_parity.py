@@ -139,6 +139,47 @@ def test_heavy_words_split_across_slices_vs_oracle():
     np.testing.assert_array_equal(ph.topic_totals, ot)
 
 
+@pytest.mark.parametrize("piece", [1024, 200000])
+def test_heavy_word_pieces_vs_oracle(piece, monkeypatch):
+    """K2 items of a heavy (32-bit column) word: many small pieces flushed with
+    global atomics (GF_K2_PIECE=1024), or one item longer than 65535 tokens,
+    counted in <= 65528-token rounds inside the kernel (GF_K2_PIECE=200000)."""
+    from paper_1803_04631_b200.shard import RESIDENT
+
+    monkeypatch.setenv("GF_K2_PIECE", str(piece))
+    RESIDENT.release()
+    r = np.random.default_rng(40)
+    n = 400000
+    docs = np.repeat(np.arange(4000), 100)
+    words = np.where(r.random(n) < 0.45, 7, np.where(r.random(n) < 0.3, 3, r.integers(0, 30, n)))
+    ch = build_chunk(docs, words, r.integers(0, 24, n))
+    ph = md.rebuild_phi_replica(ch, 24, 30)
+    oc, ot = oracle.rebuild_phi(ch.assignments, ch.word_ids, 24, 30)
+    np.testing.assert_array_equal(ph.counts, oc)
+    np.testing.assert_array_equal(ph.topic_totals, ot)
+    RESIDENT.release()
+
+
+def test_theta_rebuild_document_groups_vs_oracle():
+    """K3 on enough documents that every warp takes groups of 32 (the
+    batched-metadata / L2-prefetch path; small tests run groups of 1)."""
+    from paper_1803_04631_b200.shard import RESIDENT
+
+    RESIDENT.release()
+    r = np.random.default_rng(41)
+    K = 1024
+    lengths = r.choice([1, 3, 17, 32, 33, 70, 128, 129, 400], size=900000,
+                       p=[0.2, 0.2, 0.2, 0.1, 0.1, 0.1, 0.05, 0.04, 0.01])
+    docs = np.repeat(np.arange(len(lengths)), lengths)
+    ch = build_chunk(docs, r.integers(0, 5000, len(docs)), r.integers(0, K, len(docs)))
+    th = md.rebuild_theta(ch, K)
+    rp, ids, cn = oracle_theta(ch, K)
+    np.testing.assert_array_equal(th.row_ptr, rp)
+    np.testing.assert_array_equal(th.topic_ids, ids)
+    np.testing.assert_array_equal(th.counts, cn)
+    RESIDENT.release()
+
+
 # --------------------------------------------------------------- ptree -------
 def test_device_tree_search_matches_reference():
     g = np.load(os.path.join(GOLD, "ptree.npz"))
