@@ -606,31 +606,48 @@ def run_ours(args, world, rank, local):
         # c of the next step's input, so the two PCIe directions run concurrently.
         z_in = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
         z_io = torch.empty(T_local, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
-        z_in[:] = sh.get_assignments()
-        # streamed sampling: the schedule is split into P word-group phases, so
-        # phase p's assignments travel back (and out again as the next step's
-        # input) while phases p+1.. sample; only the last phase's round trip is
-        # exposed.  Reload the same tokens with a phase-major schedule; the state
-        # carries over through z (the counts are rebuilt from it every step).
+        # streamed sampling: the schedule is split into phases, so phase p's
+        # assignments travel back (and out again as the next step's input)
+        # while phases p+1.. sample; only the last phase's round trip is
+        # exposed.  Word-group phases (halving sizes) and the word-group (chunk)
+        # order by default; GF_E2E_ORDER=doc: document-block phases and the
+        # shard's document-major order (no theta row streamed twice, but phase
+        # 0 -- the words not cut at block boundaries, ~46% of K1 on
+        # PubMed-shape -- must finish before any document range is final, so
+        # the round trip starts too late: measured 8.9 vs 11.1 G).  Reload the
+        # same tokens with the phased schedule; the state carries over through
+        # z (the counts are rebuilt from it every step).
+        order = os.environ.get("GF_E2E_ORDER", "word")
+        doc = order == "doc"
         spec = os.environ.get("GF_E2E_PHASES", "geo:9")
         if spec.startswith("geo:"):       # halving phase sizes: 1/2, 1/4, ..., last two equal
             n = int(spec[4:])
             cuts = [1.0 - 0.5 ** (p + 1) for p in range(n - 1)] + [1.0]
-            nphase, phase_arg = n, cuts
         else:
-            nphase = int(spec)
-            phase_arg = nphase
-        if nphase > 1:
-            sh.set_phases(phase_arg)
-            sh.load_tokens(lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, seed=TRAIN_SEED,
-                           chunk_id=chunk_id)
-            if peer:
-                handles = [None] * world
-                dist.all_gather_object(handles, sh.peer_handle())
-                sh.peer_open(rank, world, handles)
-            sync_t = sh.sync_tensor() if dist else None
+            n = int(spec)
+            cuts = [(p + 1) / n for p in range(n)]
+        cuts[-1] = 1.0
+        z_now = sh.get_assignments()
+        if doc:
+            sh.set_block_phases(cuts)
+        elif n > 1:
+            sh.set_phases(cuts)
+        sh.load_tokens(lo, lo + corp.num_docs, corp.doc_ids + lo, corp.word_ids, seed=TRAIN_SEED, chunk_id=chunk_id)
+        sh.set_assignments(z_now)
+        if peer:
+            handles = [None] * world
+            dist.all_gather_object(handles, sh.peer_handle())
+            sh.peer_open(rank, world, handles)
+        sync_t = sh.sync_tensor() if dist else None
+        copy = sh.copy_doc_assignments_async if doc else sh.copy_assignments_async
+        imported = sh.doc_assignments_imported if doc else sh.assignments_imported
+        if doc:
+            copy(z_in, 0, T_local, False)
+            sh.synchronize()
+        else:
+            z_in[:] = z_now
         nphase = sh.num_phases
-        ranges = [sh.phase_range(p) for p in range(nphase)]
+        ranges = [sh.phase_doc_range(p) if doc else sh.phase_range(p) for p in range(nphase)]
         nchunk = max(nphase, int(os.environ.get("GF_E2E_CHUNKS", "16")))
         target = max(1, T_local // nchunk)          # pieces of ~T/nchunk tokens inside each phase
         pieces = []
@@ -643,7 +660,7 @@ def run_ours(args, world, rank, local):
         def upload(host):
             for ps in pieces:
                 for x, y in ps:
-                    sh.copy_assignments_async(host, x, y - x, True, h2d_s)
+                    copy(host, x, y - x, True, h2d_s)
             return h2d_s.record_event()
 
         def counts_from_z():
@@ -660,14 +677,14 @@ def run_ours(args, world, rank, local):
             sh.prepare()
             stream.wait_stream(side)
 
-        sh.copy_assignments_async(z_in, 0, 1, True, h2d_s)   # allocates the import staging buffer
+        copy(z_in, 0, 1, True, h2d_s)            # allocates the import staging buffer
         torch.cuda.synchronize(device)
         barrier()
         t0 = time.perf_counter()
         ev_in = upload(z_in)
         for i in range(args.steps):
             stream.wait_event(ev_in)
-            sh.assignments_imported()
+            imported()
             counts_from_z()
             last = i + 1 == args.steps
             ready = stream.record_event()
@@ -683,12 +700,16 @@ def run_ours(args, world, rank, local):
                 sh.set_stream(ps)
                 sh.sample_phase(it, p)
                 done[p % 2] = ps.record_event()
+                if doc and p == 0:
+                    continue                  # document ranges are final from phase 1 on
                 d2h_s.wait_event(done[p % 2])
+                if doc:                       # ... and need phase 0 too (other stream)
+                    d2h_s.wait_event(done[0])
                 for x, y in pieces[p]:
-                    sh.copy_assignments_async(z_io, x, y - x, False, d2h_s)
+                    copy(z_io, x, y - x, False, d2h_s)
                     if not last:             # out again as the next step's input once it landed
                         h2d_s.wait_event(d2h_s.record_event())
-                        sh.copy_assignments_async(z_io, x, y - x, True, h2d_s)
+                        copy(z_io, x, y - x, True, h2d_s)
             sh.set_stream(stream)
             stream.wait_stream(alt)
             it += 1
@@ -701,12 +722,14 @@ def run_ours(args, world, rank, local):
             t = torch.tensor([el], dtype=torch.float64, device="cuda")
             ar(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
+        fn = "copy_doc_assignments_async" if doc else "copy_assignments_async"
         e2e = {"value": T_step * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": 2 * T_local,
                "d2h_bytes_per_step": 2 * T_local + 8,
-               "api": f"DeviceShard.copy_assignments_async (pinned host buffers, two copy streams) + "
-                      f"assignments_imported, rebuild_phi/prepare/rebuild_theta, sample_phase x {nphase} "
-                      f"(each phase's assignments copied back and out while later phases sample), "
-                      f"loglik_sum (C ABI)"}
+               "api": f"DeviceShard.{fn} (pinned host buffers, two copy streams; assignments in "
+                      f"{'document-major' if doc else 'word-group'} order) + "
+                      f"{'doc_' if doc else ''}assignments_imported, rebuild_phi/prepare/rebuild_theta, "
+                      f"sample_phase x {nphase} ({'document-block' if doc else 'word-group'} phases; each "
+                      f"phase's assignments copied back and out while later phases sample), loglik_sum (C ABI)"}
         del lls
 
     # ---- after the timed regions: K2 and K3 each ALONE (the step runs them

@@ -160,6 +160,16 @@ int gf_shard_set_phase_cuts(gf_shard* shard, const double* cuts, int num_phases)
 int gf_shard_num_phases(gf_shard* shard, int* num_phases_out);
 int gf_shard_phase_range(gf_shard* shard, int phase, int64_t* tok_begin, int64_t* tok_end);
 int gf_shard_sample_phase(gf_shard* shard, uint32_t iteration, int phase);
+/* Document-block phases (applies at the next load): phase 0 holds the slices of
+ * the words that are not cut at document-block boundaries (they touch every
+ * block), phase p >= 1 the block-scheduled slices of the document blocks whose
+ * first document starts below cut[p-1] of the doc-major tokens (cumulative
+ * fractions, strictly increasing, ending at 1.0).  Unlike word phases, no
+ * theta row is streamed by two phases.  gf_shard_phase_doc_range gives the
+ * doc-major token range [begin, end) that is final once phases 0..p have run
+ * (empty for phase 0). */
+int gf_shard_set_block_phases(gf_shard* shard, const double* cuts, int num_block_phases);
+int gf_shard_phase_doc_range(gf_shard* shard, int phase, int64_t* tok_begin, int64_t* tok_end);
 /* One deferred iteration: sample -> rebuild_phi [-> peer phi
  * exchange when a peer group is open] -> prepare, with rebuild_theta on an
  * internal stream beside everything after the sample. */
@@ -228,6 +238,14 @@ int gf_shard_set_assignments(gf_shard* shard, const uint16_t* in);
 int gf_shard_copy_assignments_async(gf_shard* shard, void* host, int64_t offset, int64_t count, int to_device,
                                     void* stream);
 int gf_shard_assignments_imported(gf_shard* shard);
+/* The same two calls in the shard's DOCUMENT-MAJOR order (the doc-major copy
+ * K1 keeps, zdoc: per document its tokens by word group, heavy words first;
+ * offsets index that order).  With document-block phases (below) a range of
+ * documents is final as soon as its phase has run, so a step's assignments can
+ * stream back per document range while later ranges sample. */
+int gf_shard_copy_doc_assignments_async(gf_shard* shard, void* host, int64_t offset, int64_t count, int to_device,
+                                        void* stream);
+int gf_shard_doc_assignments_imported(gf_shard* shard);
 int gf_shard_theta_nnz(gf_shard* shard, int64_t* nnz_out);
 /* ThetaRows (model.py:20-47) of the shard's docs: row_ptr[D_s+1] (local), ids, counts */
 int gf_shard_get_theta(gf_shard* shard, int64_t* row_ptr, uint16_t* topic_ids, uint16_t* counts);

@@ -72,6 +72,10 @@ SIGNATURES = {
     "gf_shard_set_assignments": (_int, [_p, _p]),
     "gf_shard_copy_assignments_async": (_int, [_p, _p, _i64, _i64, _int, _p]),
     "gf_shard_assignments_imported": (_int, [_p]),
+    "gf_shard_copy_doc_assignments_async": (_int, [_p, _p, _i64, _i64, _int, _p]),
+    "gf_shard_doc_assignments_imported": (_int, [_p]),
+    "gf_shard_set_block_phases": (_int, [_p, _p, _int]),
+    "gf_shard_phase_doc_range": (_int, [_p, _int, _p, _p]),
     "gf_shard_theta_nnz": (_int, [_p, _p]),
     "gf_shard_get_theta": (_int, [_p, _p, _p, _p]),
     "gf_shard_set_theta": (_int, [_p, _p, _p, _p]),

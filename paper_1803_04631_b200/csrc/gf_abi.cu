@@ -453,6 +453,7 @@ int gf_shard_sample(gf_shard* s, uint32_t iteration) {
 int gf_shard_set_phases(gf_shard* s, int num_phases) {
     if (num_phases < 1 || num_phases > 255) return fail(GF_ERR_VALUE, "phases must be in [1, 255]");
     s->n_phases = num_phases;     // applies at the next load (the slice schedule is built there)
+    s->block_phases = false;
     s->phase_cuts.clear();
     return GF_OK;
 }
@@ -463,7 +464,28 @@ int gf_shard_set_phase_cuts(gf_shard* s, const double* cuts, int num_phases) {
         if (!(cuts[p] > (p ? cuts[p - 1] : 0.0)) || cuts[p] > 1.0 || (p == num_phases - 1 && cuts[p] != 1.0))
             return fail(GF_ERR_VALUE, "phase cuts must increase strictly and end at 1.0");
     s->n_phases = num_phases;
+    s->block_phases = false;
     s->phase_cuts.assign(cuts, cuts + num_phases);
+    return GF_OK;
+}
+
+int gf_shard_set_block_phases(gf_shard* s, const double* cuts, int num_block_phases) {
+    if (num_block_phases < 1 || num_block_phases > 254) return fail(GF_ERR_VALUE, "block phases must be in [1, 254]");
+    for (int p = 0; p < num_block_phases; ++p)
+        if (!(cuts[p] > (p ? cuts[p - 1] : 0.0)) || cuts[p] > 1.0 || (p == num_block_phases - 1 && cuts[p] != 1.0))
+            return fail(GF_ERR_VALUE, "phase cuts must increase strictly and end at 1.0");
+    s->n_phases = num_block_phases + 1;   // + phase 0: the words not cut at block boundaries
+    s->block_phases = true;
+    s->phase_cuts.assign(cuts, cuts + num_block_phases);
+    return GF_OK;
+}
+
+int gf_shard_phase_doc_range(gf_shard* s, int phase, int64_t* tok_begin, int64_t* tok_end) {
+    if (int rc = need_loaded(s)) return rc;
+    if (!s->block_phases) return fail(GF_ERR_VALUE, "no document-block phases: gf_shard_set_block_phases, then load");
+    if (phase < 0 || phase + 1 >= (int)s->phase_doctok0.size()) return fail(GF_ERR_VALUE, "phase %d out of range", phase);
+    *tok_begin = s->phase_doctok0[phase];
+    *tok_end = s->phase_doctok0[phase + 1];
     return GF_OK;
 }
 
@@ -686,6 +708,40 @@ int gf_shard_copy_assignments_async(gf_shard* s, void* host, int64_t offset, int
     } else {
         CU(gf::xfer_d2h(h, dev, count * 2, st), "copy_assignments");
     }
+    return GF_OK;
+}
+
+// the same in the shard's document-major order (zdoc: per document, its tokens
+// by word group, heavy words first) -- the order in which document-block
+// phases complete
+int gf_shard_copy_doc_assignments_async(gf_shard* s, void* host, int64_t offset, int64_t count, int to_device,
+                                        void* stream) {
+    if (int rc = need_loaded(s)) return rc;
+    if (offset < 0 || count < 0 || offset + count > s->T) return fail(GF_ERR_SHAPE, "assignment range out of bounds");
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    if (to_device && !s->d.zstage) {
+        cudaSetDevice(s->device);
+        CU(cudaMalloc((void**)&s->d.zstage, std::max<int64_t>(s->T, 1) * 2), "copy_doc_assignments (staging)");
+    }
+    uint16_t* dev = (to_device ? s->d.zstage : s->d.zdoc) + offset;
+    uint16_t* h = static_cast<uint16_t*>(host) + offset;
+    if (gf::host_is_pinned(h)) {
+        CU(cudaMemcpyAsync(to_device ? (void*)dev : (void*)h, to_device ? (const void*)h : (const void*)dev, count * 2,
+                           to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
+           "copy_doc_assignments");
+    } else if (to_device) {
+        CU(gf::xfer_h2d(dev, h, count * 2, st), "copy_doc_assignments");
+    } else {
+        CU(gf::xfer_d2h(h, dev, count * 2, st), "copy_doc_assignments");
+    }
+    return GF_OK;
+}
+
+int gf_shard_doc_assignments_imported(gf_shard* s) {
+    if (int rc = need_loaded(s)) return rc;
+    if (!s->d.zstage) return fail(GF_ERR_VALUE, "no staged assignments: gf_shard_copy_doc_assignments_async(to_device=1) first");
+    CU(gf::launch_import_staged(s, true), "doc_assignments_imported");
+    s->stale_theta = s->stale_phi = true;
     return GF_OK;
 }
 

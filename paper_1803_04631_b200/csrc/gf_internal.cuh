@@ -113,6 +113,13 @@ struct gf_shard {
     int n_phases = 1;
     std::vector<double> phase_cuts;          // optional cumulative token fractions (gf_shard_set_phase_cuts)
     std::vector<int64_t> phase_slice0{0, 0}, phase_tok0{0, 0};
+    // document-block phases (gf_shard_set_block_phases): phase 0 = the slices
+    // of words not cut at block boundaries (they touch every block), phase
+    // p >= 1 = the block-scheduled slices of a range of document blocks; the
+    // doc-major (zdoc) tokens [phase_doctok0[p], phase_doctok0[p+1]) are final
+    // once phases 0..p have run (phase 0's range is empty)
+    bool block_phases = false;
+    std::vector<int64_t> phase_doctok0{0, 0};
     int64_t n_ctx = 0;
     bool ctx_dirty = true;                   // phi / n_k changed since the last prepare
     double ll_const = 0.0;                    // sum_d L_d log(L_d + K alpha)
@@ -191,7 +198,7 @@ cudaError_t launch_prepare(gf_shard* s);
 cudaError_t launch_contexts(gf_shard* s);
 cudaError_t launch_theta_rebuild(gf_shard* s, cudaStream_t st = nullptr);
 cudaError_t launch_zdoc_sync(gf_shard* s);
-cudaError_t launch_import_staged(gf_shard* s);
+cudaError_t launch_import_staged(gf_shard* s, bool doc_order = false);
 cudaError_t launch_ll_reduce(gf_shard* s);
 cudaError_t launch_theta_export(gf_shard* s, const int64_t* d_rowptr, uint16_t* d_ids, uint16_t* d_cnt);
 cudaError_t launch_theta_import(gf_shard* s, const int64_t* d_rowptr, const uint16_t* d_ids,

@@ -674,16 +674,17 @@ __global__ void staged_diff_kernel(long long T, const uint16_t* __restrict__ zin
 
 __global__ void import_staged_gate(long long R, const uint32_t* __restrict__ run_start,
                                    const uint32_t* __restrict__ dwpos, const uint16_t* __restrict__ zin, uint16_t* z,
-                                   uint16_t* zdoc, const unsigned int* any) {
+                                   uint16_t* zdoc, const unsigned int* any, bool doc_order) {
     if (*any == 0u) return;                   // nothing changed
     for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (long long)gridDim.x * blockDim.x) {
-        const uint32_t t0 = run_start[r], t1 = run_start[r + 1];
+        const uint32_t t0 = run_start[r], t1 = run_start[r + 1], p = dwpos[r];
+        // the staged array is in chunk order (zin[t]) or doc-major order (zin[p + i])
+        const uint32_t i0 = doc_order ? p : t0;
         bool diff = false;
-        for (uint32_t t = t0; t < t1; ++t) diff |= zin[t] != z[t];
+        for (uint32_t t = t0; t < t1; ++t) diff |= zin[i0 + (t - t0)] != z[t];
         if (diff) {
-            const uint32_t p = dwpos[r];
             for (uint32_t t = t0; t < t1; ++t) {
-                const uint16_t k = zin[t];
+                const uint16_t k = zin[i0 + (t - t0)];
                 z[t] = k;
                 zdoc[p + (t - t0)] = k;
             }
@@ -691,15 +692,17 @@ __global__ void import_staged_gate(long long R, const uint32_t* __restrict__ run
     }
 }
 
-cudaError_t launch_import_staged(gf_shard* s) {
+cudaError_t launch_import_staged(gf_shard* s, bool doc_order) {
     if (s->R == 0) return cudaSuccess;
     // bytes[1]: the "any staged topic differs" flag
     unsigned int* any = reinterpret_cast<unsigned int*>(s->d.bytes + 1);
     cudaError_t e = cudaMemsetAsync(any, 0, 4, s->stream);
     if (e != cudaSuccess) return e;
-    staged_diff_kernel<<<sm_count(s->device) * 8, 256, 0, s->stream>>>((long long)s->T, s->d.zstage, s->d.z, any);
-    import_staged_gate<<<sm_count(s->device) * 8, 256, 0, s->stream>>>((long long)s->R, s->d.run_start, s->d.run_dwpos, s->d.zstage,
-                                                       s->d.z, s->d.zdoc, any);
+    // the whole-array compare runs against the resident array of the same order
+    staged_diff_kernel<<<sm_count(s->device) * 8, 256, 0, s->stream>>>((long long)s->T, s->d.zstage,
+                                                                        doc_order ? s->d.zdoc : s->d.z, any);
+    import_staged_gate<<<sm_count(s->device) * 8, 256, 0, s->stream>>>((long long)s->R, s->d.run_start, s->d.run_dwpos,
+                                                                        s->d.zstage, s->d.z, s->d.zdoc, any, doc_order);
     return cudaGetLastError();
 }
 

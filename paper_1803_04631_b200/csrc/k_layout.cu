@@ -143,13 +143,16 @@ __global__ void k_slice_begin(int64_t R, const uint32_t* flag, const uint32_t* s
 // (sampling phase << 56 on top when the schedule is split into phases)
 __global__ void k_slice_keys(int64_t N, int64_t R, const uint32_t* srb, const uint32_t* run_group,
                              const uint32_t* run_doc, const int32_t* doc_blk, const uint32_t* g_info,
-                             const uint32_t* g_slice0, const uint8_t* g_phase, int nblk, unsigned long long* key,
-                             uint32_t* val) {
+                             const uint32_t* g_slice0, const uint8_t* g_phase, const uint8_t* blk_phase, int nblk,
+                             unsigned long long* key, uint32_t* val) {
     GRID_STRIDE(s, N) {
         const uint32_t r = srb[s], g = run_group[r];
         const bool blocked = (g_info[g] >> 31) != 0u;
         const uint64_t b = blocked ? (uint64_t)doc_blk[run_doc[r]] : (uint64_t)(s % nblk);
-        const uint64_t ph = g_phase ? (uint64_t)g_phase[g] : 0ull;
+        // word phases: the group's phase; document-block phases: 0 for words
+        // not cut at block boundaries, else the phase of the slice's block
+        const uint64_t ph = blk_phase ? (blocked ? (uint64_t)blk_phase[b] : 0ull)
+                                      : (g_phase ? (uint64_t)g_phase[g] : 0ull);
         key[s] = (ph << 56) | (b << 40) | ((uint64_t)(g_info[g] & 0xFFFFFu) << 20) | (uint64_t)((uint32_t)s - g_slice0[g]);
         val[s] = (uint32_t)s;
     }
@@ -165,6 +168,11 @@ __global__ void k_slice_emit(int64_t N, int64_t R, const uint32_t* order, const 
         slices[i] = make_int4(gw[g], (int)r0, (int)r1, g_col[g]);
         slice_ctx[i] = g_ctx[g];
     }
+}
+
+// slices per phase of the sorted schedule (document-block phases)
+__global__ void k_phase_counts(int64_t N, const unsigned long long* key, unsigned int* cnt) {
+    GRID_STRIDE(i, N) atomicAdd(cnt + (key[i] >> 56), 1u);
 }
 
 // zdoc positions (heavy-first inside each document)
@@ -535,8 +543,35 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
         for (int64_t g = 0; g < ng; ++g)
             if (gphase[g] >= p) { s->phase_tok0[p] = go[g]; break; }
     for (int p = 0; p < P; ++p) s->phase_slice0[p + 1] += s->phase_slice0[p];
+    // document-block phases: block b joins phase 1 + (the first cut above the
+    // doc-major token fraction at its first document); phase 0 holds the
+    // words that are not cut at block boundaries
+    const bool bphase = s->block_phases && P > 1;
+    std::vector<uint8_t> blkphase((size_t)nblk, 0);
+    s->phase_doctok0.assign((size_t)P + 1, T);
+    s->phase_doctok0[0] = 0;
+    s->phase_doctok0[1] = 0;
+    if (bphase) {
+        std::vector<int64_t> blk_tok0((size_t)nblk + 1, T);
+        for (int64_t d = D - 1; d >= 0; --d) blk_tok0[doc_blk[d]] = dwp[d];
+        for (int32_t b = 0; b < nblk; ++b) {
+            int ph = 1;
+            const double f = T > 0 ? (double)blk_tok0[b] / (double)T : 0.0;
+            while (ph < P - 1 && f >= s->phase_cuts[ph - 1]) ++ph;
+            blkphase[b] = (uint8_t)ph;
+        }
+        for (int p = P - 1; p >= 2; --p)   // first doc-major token of phase p
+            for (int32_t b = 0; b < nblk; ++b)
+                if (blkphase[b] >= p) { s->phase_doctok0[p] = blk_tok0[b]; break; }
+        gphase.assign(gphase.size(), 0);
+    }
     uint8_t* d_gphase = nullptr;
-    if (P > 1) {
+    uint8_t* d_blkphase = nullptr;
+    if (bphase) {
+        d_blkphase = static_cast<uint8_t*>(sc.get((size_t)std::max<int32_t>(nblk, 1)));
+        CK(sc.err, "layout scratch");
+        CK(cudaMemcpyAsync(d_blkphase, blkphase.data(), nblk, cudaMemcpyHostToDevice, st), "layout");
+    } else if (P > 1) {
         d_gphase = static_cast<uint8_t*>(sc.get((size_t)std::max<int64_t>(ng, 1)));
         CK(sc.err, "layout scratch");
         if (ng) CK(cudaMemcpyAsync(d_gphase, gphase.data(), ng, cudaMemcpyHostToDevice, st), "layout");
@@ -561,11 +596,22 @@ static int build_layout(gf_shard* s, Scratch& sc, DevChunk& c, int64_t lo, int64
     if (N > 0) {
         // block-major, heavy-first inside a block, slice order inside a word
         k_slice_keys<<<blocks_for(N), 256, 0, st>>>(N, R, srb, run_group, dv.run_doc, d_docblk, d_ginfo, d_gslice0,
-                                                   d_gphase, nblk, skey, sval);
+                                                   d_gphase, d_blkphase, nblk, skey, sval);
         CK(cub_call(sc, [&](void* t, size_t& b) {
                return cub::DeviceRadixSort::SortPairs(t, b, skey, skey2, sval, sorder, N, 0, 64, st);
            }),
            "slices");
+        if (bphase) {                           // slices per phase from the sorted keys
+            unsigned int* pc = sc.u32(P);
+            CK(sc.err, "layout scratch");
+            CK(cudaMemsetAsync(pc, 0, (size_t)P * 4, st), "layout");
+            k_phase_counts<<<blocks_for(N), 256, 0, st>>>(N, skey2, pc);
+            std::vector<unsigned int> cnt((size_t)P);
+            CK(cudaMemcpyAsync(cnt.data(), pc, (size_t)P * 4, cudaMemcpyDeviceToHost, st), "layout");
+            CK(cudaStreamSynchronize(st), "layout");
+            s->phase_slice0.assign((size_t)P + 1, 0);
+            for (int p = 0; p < P; ++p) s->phase_slice0[p + 1] = s->phase_slice0[p] + cnt[p];
+        }
         k_slice_emit<<<blocks_for(N), 256, 0, st>>>(N, R, sorder, srb, run_group, c.gw, d_gcol, d_gctx, dv.slices,
                                                     dv.slice_ctx);
     }

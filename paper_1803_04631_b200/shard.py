@@ -251,6 +251,20 @@ class DeviceShard:
             cuts = np.ascontiguousarray(num_phases, dtype=np.float64)
             _lib.check(_lib.lib().gf_shard_set_phase_cuts(self._h, _lib.ptr(cuts), len(cuts)))
 
+    def set_block_phases(self, cuts):
+        """Document-block phases (applies at the next load): phase 0 = the words
+        not cut at document-block boundaries, phase p >= 1 = the document blocks
+        starting below cuts[p-1] of the doc-major tokens (cumulative fractions,
+        strictly increasing, ending at 1.0).  No theta row is streamed twice."""
+        cuts = np.ascontiguousarray(cuts, dtype=np.float64)
+        _lib.check(_lib.lib().gf_shard_set_block_phases(self._h, _lib.ptr(cuts), len(cuts)))
+
+    def phase_doc_range(self, phase):
+        """(tok_begin, tok_end) in doc-major order: final once phases 0..phase ran."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib().gf_shard_phase_doc_range(self._h, int(phase), ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
     @property
     def num_phases(self):
         n = ctypes.c_int()
@@ -364,6 +378,20 @@ class DeviceShard:
         """After a complete host -> device import by copy_assignments_async
         (stream-ordered after it): refresh the doc-major copy, counts go stale."""
         _lib.check(_lib.lib().gf_shard_assignments_imported(self._h))
+
+    def copy_doc_assignments_async(self, host, offset, count, to_device, stream=None):
+        """copy_assignments_async in the shard's document-major order (per
+        document its tokens by word group, heavy words first)."""
+        if host.dtype != np.uint16 or not host.flags.c_contiguous or len(host) != self.num_tokens:
+            raise ValueError("host must be a contiguous uint16 array of num_tokens entries")
+        handle = getattr(stream, "cuda_stream", stream)
+        _lib.check(_lib.lib().gf_shard_copy_doc_assignments_async(
+            self._h, _lib.ptr(host), int(offset), int(count), 1 if to_device else 0,
+            ctypes.c_void_p(int(handle)) if handle else None))
+
+    def doc_assignments_imported(self):
+        """After a complete doc-major host -> device import (stream-ordered)."""
+        _lib.check(_lib.lib().gf_shard_doc_assignments_imported(self._h))
 
     def get_theta(self):
         """(row_ptr int64[D_s+1], topic_ids uint16, counts uint16) of local rows."""
