@@ -623,6 +623,9 @@ def run_ours(args, world, rank, local):
         if spec.startswith("geo:"):       # halving phase sizes: 1/2, 1/4, ..., last two equal
             n = int(spec[4:])
             cuts = [1.0 - 0.5 ** (p + 1) for p in range(n - 1)] + [1.0]
+        elif spec.startswith("r"):        # "r0.4:7": each phase `ratio` of the previous one, n phases
+            ratio, n = float(spec[1:].split(":")[0]), int(spec.split(":")[1])
+            cuts = [1.0 - ratio ** (p + 1) for p in range(n - 1)] + [1.0]
         else:
             n = int(spec)
             cuts = [(p + 1) / n for p in range(n)]
