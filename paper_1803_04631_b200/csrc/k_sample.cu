@@ -379,7 +379,7 @@ __device__ __forceinline__ void build_context(const SampleArgs& a, int col, floa
 template <int NT>
 __global__ void __launch_bounds__(NT) context_kernel(SampleArgs a, const int32_t* __restrict__ cols,
                                                                   float* out) {
-    extern __shared__ float smem[];
+    extern __shared__ __align__(128) float smem[];
     build_context<NT>(a, cols[blockIdx.x], smem, threadIdx.x);
     float4* dst = reinterpret_cast<float4*>(out + (size_t)blockIdx.x * a.ctx_stride);
     for (int i = threadIdx.x; i < a.ctx_stride / 4; i += NT) dst[i] = reinterpret_cast<const float4*>(smem)[i];
@@ -392,7 +392,7 @@ constexpr uint32_t VEC = 2;                  // 16-byte vectors per lane per pas
 template <int NT, uint32_t CAPV, int MINB, bool PF, bool HUGE>
 __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     constexpr int kWarps = NT / 32;
-    extern __shared__ float smem[];
+    extern __shared__ __align__(128) float smem[];   // TMA bulk-copy destination: 16-byte aligned
     const int K = a.K;
     float* pstar = smem;                            // p*(tpos(k))  (byte offset = theta topic field)
     float* pex = smem + lay_pex(K);                 // p*_ex(k)

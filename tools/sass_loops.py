@@ -1,5 +1,14 @@
+"""Static check of K1's loop bodies in a cubin / .so (cuobjdump): the loops that
+contain the pass's 256-bit theta load, their length and how many special-register
+reads / constant loads / moves the compiler put inside (register-pressure
+rematerialisation shows up here first).  Usage: python tools/sass_loops.py lib.so"""
 import re,subprocess,sys
-def loops(obj, fn="_ZN2gf13sample_kernelILi128ELj768ELi8ELb1ELb0EEEvNS_10SampleArgsE"):
+# the default K1 variant (K <= 2048: 4 warps, 640-vector staging, 9 CTAs/SM);
+# its entry-parallel pass loop should stay ~104 SASS per step
+DEFAULT_FN = "_ZN2gf13sample_kernelILi128ELj640ELi9ELb1ELb0EEEvNS_10SampleArgsE"
+
+
+def loops(obj, fn=DEFAULT_FN):
     sass=subprocess.run(f"cuobjdump -sass {obj}",shell=True,capture_output=True,text=True).stdout
     i=sass.find("Function : "+fn); f=sass[i:sass.find("Function :",i+10)]
     ins=[]
