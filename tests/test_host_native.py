@@ -26,6 +26,26 @@ def test_abi_exports_every_header_symbol():
     assert L.gf_abi_version() == 1
 
 
+def test_k1_pass_loop_stays_tight():
+    """Static SASS guard (cuobjdump, no GPU): the default K1 variant's
+    entry-parallel pass loop is ~104 instructions per 256-entry step with no
+    special-register reads inside; register pressure from code added elsewhere
+    in the kernel once pushed it to 127 (the shared base and lane id were
+    rematerialised every step) and cost K1 4%."""
+    import shutil
+    import subprocess
+    import sys
+
+    if not shutil.which("cuobjdump") or not os.path.exists(_lib.SO_PATH):
+        pytest.skip("cuobjdump or the built library is missing")
+    tool = os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools", "sass_loops.py")
+    out = subprocess.run([sys.executable, tool, _lib.SO_PATH], capture_output=True, text=True, timeout=300).stdout
+    lens = [int(m.group(1)) for m in re.finditer(r"len=(\d+) S2R=(\d+)", out)]
+    s2r = [int(m.group(2)) for m in re.finditer(r"len=(\d+) S2R=(\d+)", out)]
+    assert lens, out
+    assert lens[0] <= 110 and s2r[0] <= 1, out
+
+
 def test_no_device_fails_loudly():
     if _lib.device_count() > 0:
         pytest.skip("a GPU is visible")
