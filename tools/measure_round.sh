@@ -53,4 +53,4 @@ echo "k5 capture rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"sample_kernel" -s 6 -c 1 \
   -o $o/${tag}_k1_nyt python bench.py --workload nytimes --steps 2 --warmup 5 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 echo "k1 nyt capture rc=$?"
-[ "${SANITIZE:-1}" = 1 ] && bash tools/sanitize.sh
+if [ "${SANITIZE:-1}" = 1 ]; then bash tools/sanitize.sh; fi
