@@ -619,7 +619,10 @@ def run_ours(args, world, rank, local):
         # z (the counts are rebuilt from it every step).
         order = os.environ.get("GF_E2E_ORDER", "word")
         doc = order == "doc"
-        spec = os.environ.get("GF_E2E_PHASES", "r0.45:8")   # measured: r0.45:8 11.22, r0.4:7 11.21, geo:9 11.08 G
+        # phase sizes (measured): PubMed-shape (1.48 GB of z per step) r0.45:8
+        # 11.22 / geo:9 11.08 G; NYTimes-shape (199 MB) geo:9 8.65 / r0.45:8
+        # 8.15 G -- large steps prefer fewer, faster-shrinking phases
+        spec = os.environ.get("GF_E2E_PHASES", "r0.45:8" if T_local >= 300_000_000 else "geo:9")
         if spec.startswith("geo:"):       # halving phase sizes: 1/2, 1/4, ..., last two equal
             n = int(spec[4:])
             cuts = [1.0 - 0.5 ** (p + 1) for p in range(n - 1)] + [1.0]
