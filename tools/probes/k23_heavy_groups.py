@@ -1,3 +1,5 @@
+"""K2 on heavy-word pieces and K3 on document groups, small corpora with heavy
+words (run under compute-sanitizer memcheck by tools/sanitize.sh)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np

@@ -11,5 +11,5 @@ timeout 900 compute-sanitizer --tool memcheck --error-exitcode 99 python -m pyte
   -k "load_tokens or partition_gpu_matches_host or checkpoint or large_k or conservation or resident or set_phi or tree_api or pinned or heavy_words" > gpurun_out/san_memcheck_tests.log 2>&1
 echo "memcheck(tests) rc=$? $(grep -m1 'ERROR SUMMARY' gpurun_out/san_memcheck_tests.log) $(tail -1 gpurun_out/san_memcheck_tests.log)"
 # K2 heavy-word pieces + K3 document groups on corpora with heavy words
-timeout 600 compute-sanitizer --tool memcheck --error-exitcode 99 python tools/scratch/repro_iam.py > gpurun_out/san_memcheck_k23.log 2>&1
+timeout 600 compute-sanitizer --tool memcheck --error-exitcode 99 python tools/probes/k23_heavy_groups.py > gpurun_out/san_memcheck_k23.log 2>&1
 echo "memcheck(k2/k3) rc=$? $(grep -m1 'ERROR SUMMARY' gpurun_out/san_memcheck_k23.log)"
