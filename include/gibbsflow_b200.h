@@ -160,6 +160,11 @@ int gf_shard_set_phase_cuts(gf_shard* shard, const double* cuts, int num_phases)
 int gf_shard_num_phases(gf_shard* shard, int* num_phases_out);
 int gf_shard_phase_range(gf_shard* shard, int phase, int64_t* tok_begin, int64_t* tok_end);
 int gf_shard_sample_phase(gf_shard* shard, uint32_t iteration, int phase);
+/* sample_chunk's device half: K1 over every phase, each phase's new
+ * assignments (word-group order) copied into `out` while the later phases
+ * sample (overlapped when `out` is pinned and the shard has word phases);
+ * returns with `out` complete. */
+int gf_shard_sample_export(gf_shard* shard, uint32_t iteration, uint16_t* out);
 /* Document-block phases (applies at the next load): phase 0 holds the slices of
  * the words that are not cut at document-block boundaries (they touch every
  * block), phase p >= 1 the block-scheduled slices of the document blocks whose

@@ -51,6 +51,7 @@ SIGNATURES = {
     "gf_shard_sample": (_int, [_p, _u32]),
     "gf_shard_iterate": (_int, [_p, _u32]),
     "gf_shard_evaluate": (_int, [_p]),
+    "gf_shard_sample_export": (_int, [_p, _u32, _p]),
     "gf_shard_set_phases": (_int, [_p, _int]),
     "gf_shard_set_phase_cuts": (_int, [_p, _p, _int]),
     "gf_shard_num_phases": (_int, [_p, _p]),

@@ -518,6 +518,46 @@ int gf_shard_sample_phase(gf_shard* s, uint32_t iteration, int phase) {
     return GF_OK;
 }
 
+// K1 over every phase of the schedule, each phase's new assignments copied to
+// the host (word-group order) on the aux stream while the phases after it
+// sample; returns with `out` complete.  One-phase shards: sample, then copy.
+int gf_shard_sample_export(gf_shard* s, uint32_t iteration, uint16_t* out) {
+    if (int rc = need_loaded(s)) return rc;
+    if (int rc = validate_if_dirty(s)) return rc;
+    cudaSetDevice(s->device);
+    if (!s->aux) {
+        CU(cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking), "sample_export");
+        CU(cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming), "sample_export");
+        CU(cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming), "sample_export");
+    }
+    const int P = (int)s->phase_slice0.size() - 1;
+    const bool async = gf::host_is_pinned(out) && P > 1 && !s->block_phases;
+    if (!async) {
+        CU(gf::launch_sample(s, iteration), "sample");
+        CU(gf::launch_ll_reduce(s), "loglik");
+        s->stat_sample_launches++;
+        CU(gf::xfer_d2h(out, s->d.z, s->T * 2, s->stream), "sample_export");
+        return GF_OK;
+    }
+    for (int p = 0; p < P; ++p) {
+        const int64_t a = s->phase_slice0[p], b = s->phase_slice0[p + 1];
+        CU(gf::launch_sample_range(s, iteration, 0, a, b - a), "sample");
+        if (p == P - 1) CU(gf::launch_ll_reduce(s), "loglik");
+        const int64_t t0 = s->phase_tok0[p], t1 = s->phase_tok0[p + 1];
+        if (t1 > t0) {
+            // phase p alone writes z[t0, t1): copy it out behind the later phases
+            CU(cudaEventRecord(s->fork, s->stream), "sample_export");
+            CU(cudaStreamWaitEvent(s->aux, s->fork, 0), "sample_export");
+            CU(cudaMemcpyAsync(out + t0, s->d.z + t0, (size_t)(t1 - t0) * 2, cudaMemcpyDeviceToHost, s->aux),
+               "sample_export");
+        }
+    }
+    s->stat_sample_launches++;
+    CU(cudaStreamSynchronize(s->aux), "sample_export");
+    CU(cudaStreamSynchronize(s->stream), "sample_export");
+    return GF_OK;
+}
+
 int gf_shard_evaluate(gf_shard* s) {
     if (int rc = need_loaded(s)) return rc;
     CU(gf::launch_sample(s, 0, 1), "evaluate");

@@ -72,6 +72,6 @@ def sample_chunk(chunk, phi, theta, ctx, cfg=None, iteration=0, seed=None, devic
         sh.set_phi(phi.counts, phi.topic_totals)
     sh.set_theta(*_local_theta(theta, chunk))
     sh.prepare()
-    sh.sample(iteration)
+    z = sh.sample_export(iteration)       # K1, the result copied back phase by phase
     sh.check_errors()
-    return sh.get_assignments()
+    return z

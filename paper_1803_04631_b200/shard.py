@@ -90,6 +90,7 @@ class ResidentShards:
 
 
 RESIDENT = ResidentShards()
+API_PHASES = [0.5, 0.75, 0.875, 0.9375, 1.0]
 
 
 def chunk_shard(chunk, num_topics, vocab_size, alpha=1.0, beta=1.0, seed=0, device=0, global_word_freq=None,
@@ -110,8 +111,10 @@ def chunk_shard(chunk, num_topics, vocab_size, alpha=1.0, beta=1.0, seed=0, devi
     extra = (int(num_topics), int(vocab_size), int(device), int(chunk.doc_lo), int(chunk.doc_hi), layout)
 
     def build():
+        # word phases (halving sizes): sample_chunk's result streams back while
+        # the later phases sample (gf_shard_sample_export)
         sh = DeviceShard(num_topics, vocab_size, alpha, beta, seed=seed, device=device,
-                         global_word_freq=global_word_freq)
+                         global_word_freq=global_word_freq, phases=API_PHASES)
         return sh.load(chunk)
 
     sh, fresh = RESIDENT.get(arrays, extra, build)
@@ -279,6 +282,14 @@ class DeviceShard:
 
     def sample_phase(self, iteration, phase):
         _lib.check(_lib.lib().gf_shard_sample_phase(self._h, int(iteration), int(phase)))
+
+    def sample_export(self, iteration):
+        """K1 over every phase with each phase's new assignments copied back
+        while the later phases sample (gf_shard_sample_export); returns them
+        (word-group order) in a pinned block."""
+        out = _lib.pinned_empty(self.num_tokens, np.uint16)
+        _lib.check(_lib.lib().gf_shard_sample_export(self._h, int(iteration), _lib.ptr(out)))
+        return out
 
     def iterate(self, iteration):
         _lib.check(_lib.lib().gf_shard_iterate(self._h, int(iteration)))

@@ -158,3 +158,26 @@ def test_uneven_phase_cuts():
             sh.set_phases(bad)
     one.close()
     sh.close()
+
+
+@pytest.mark.parametrize("P", [1, 5])
+def test_sample_export_equals_sample_then_copy(chunk, P, monkeypatch):
+    """gf_shard_sample_export (sample_chunk's device half: each phase's
+    assignments copied back while the later phases sample) returns exactly
+    what sample + get_assignments gives, and leaves the same device state."""
+    from paper_1803_04631_b200 import _lib
+
+    monkeypatch.setattr(_lib, "_PINNED_MIN", 0)      # a pinned result: the overlapped path
+    corp, ch = chunk
+    a, b = _shard(corp, ch, P), _shard(corp, ch, P)
+    for it in range(3):
+        a.sample(it)
+        za = a.get_assignments()
+        zb = b.sample_export(it)
+        np.testing.assert_array_equal(za, zb)
+        np.testing.assert_array_equal(b.get_assignments(), zb)
+        assert a.loglik_sum() == b.loglik_sum()
+        _counts(a)
+        _counts(b)
+    a.close()
+    b.close()
