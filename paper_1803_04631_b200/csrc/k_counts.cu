@@ -15,14 +15,16 @@ namespace gf {
 
 // ---------------------------------------------------------------- K2 ------
 // One WARP per work item, items claimed dynamically (one global atomic per
-// item).  An item is (phi column, token range): a light word's whole group
-// (<= heavy_threshold <= 65535 tokens, 16-bit column), a slice of a heavy word
-// (<= 4096 tokens, 32-bit column, global atomics when the word has several
-// slices), or an empty item for a light word absent from the shard.  Tokens
-// are word-grouped, so an item is one contiguous z range: the warp streams it
-// with 16-byte loads and counts into its private PACKED histogram in shared
-// memory (two 16-bit bins per u32 word; an item has <= 65535 tokens, so a bin
-// cannot carry into its neighbour), then
+// item; the next item's z range is bulk-prefetched into L2 when claimed).  An
+// item is (phi column, token range), built on the host by k_layout.cu: a light
+// word's whole group (<= heavy_threshold <= 65535 tokens, 16-bit column), a
+// piece of <= GF_K2_PIECE (16384) tokens of a heavy word (32-bit column,
+// global atomics), or an empty item for a light word absent from the shard;
+// longest first.  Tokens are word-grouped, so an item is one contiguous z
+// range: the warp streams it with double-buffered 16-byte loads and counts
+// into its private PACKED histogram in shared memory (two 16-bit bins per u32
+// word; at most 65528 tokens are counted between flushes, so a bin cannot
+// carry into its neighbour), then
 //   light: writes the whole packed column densely (16-byte stores, zeros
 //          included) -- the light region needs no memset;
 //   heavy: adds its nonzero cells to the pre-zeroed 32-bit column;
