@@ -684,6 +684,9 @@ def run_ours(args, world, rank, local):
             stream.wait_stream(side)
 
         copy(z_in, 0, 1, True, h2d_s)            # allocates the import staging buffer
+        # each step's loglik is read back (D2H) without blocking the host, so
+        # the host never waits for a step before enqueueing the next one
+        ll_host = torch.zeros(2 * args.steps, dtype=torch.float64).pin_memory().numpy()
         torch.cuda.synchronize(device)
         barrier()
         t0 = time.perf_counter()
@@ -720,10 +723,13 @@ def run_ours(args, world, rank, local):
             stream.wait_stream(alt)
             it += 1
             ev_in = h2d_s.record_event()
-            lls = sh.loglik_sum()             # D2H of the step's loglik
+            sh.loglik_sum_async(ll_host[2 * i: 2 * i + 2], stream)   # D2H of the step's loglik
         torch.cuda.synchronize(device)
         barrier()
         el = time.perf_counter() - t0
+        lls = ll_host[0::2] - ll_host[1::2]
+        if not np.all(np.isfinite(lls)) or not np.all(lls < 0):
+            raise RuntimeError(f"e2e step logliks not finite / negative: {lls}")
         if dist:
             t = torch.tensor([el], dtype=torch.float64, device="cuda")
             ar(t, op=dist.ReduceOp.MAX)
@@ -735,7 +741,8 @@ def run_ours(args, world, rank, local):
                       f"{'document-major' if doc else 'word-group'} order) + "
                       f"{'doc_' if doc else ''}assignments_imported, rebuild_phi/prepare/rebuild_theta, "
                       f"sample_phase x {nphase} ({'document-block' if doc else 'word-group'} phases; each "
-                      f"phase's assignments copied back and out while later phases sample), loglik_sum (C ABI)"}
+                      f"phase's assignments copied back and out while later phases sample), "
+                      f"loglik_sum_async (C ABI; every step's loglik read back, the host never blocks on a step)"}
         del lls
 
     # ---- after the timed regions: K2 and K3 each ALONE (the step runs them

@@ -182,6 +182,9 @@ int gf_shard_iterate(gf_shard* shard, uint32_t iteration);
 /* Sum over this shard's tokens of log p(w | d) for the model the last
  * gf_shard_sample started from (synchronises the stream). */
 int gf_shard_loglik_sum(gf_shard* shard, double* sum_out);
+/* non-blocking: out[0] = raw device sum (async copy on `stream`, NULL: the
+ * shard's stream; `out` pinned), out[1] = the constant to subtract */
+int gf_shard_loglik_sum_async(gf_shard* shard, double* out, void* stream);
 /* Raise deferred device-side errors (overflow / consistency); synchronises. */
 int gf_shard_check_errors(gf_shard* shard);
 int gf_shard_synchronize(gf_shard* shard);

@@ -58,6 +58,7 @@ SIGNATURES = {
     "gf_shard_phase_range": (_int, [_p, _int, _p, _p]),
     "gf_shard_sample_phase": (_int, [_p, _u32, _int]),
     "gf_shard_loglik_sum": (_int, [_p, _p]),
+    "gf_shard_loglik_sum_async": (_int, [_p, _p, _p]),
     "gf_shard_check_errors": (_int, [_p]),
     "gf_shard_synchronize": (_int, [_p]),
     "gf_shard_sync_buffer": (_int, [_p, _pp, _p]),

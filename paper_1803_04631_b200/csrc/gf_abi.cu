@@ -613,6 +613,18 @@ int gf_shard_last_times(gf_shard* s, float* ms, int num) {
     return GF_OK;
 }
 
+// the same value without blocking the host: out[0] receives the raw device
+// sum (stream-ordered copy; `out` should be pinned) and out[1] the constant
+// to subtract, so the log-likelihood sum is out[0] - out[1] once the stream
+// has reached the copy
+int gf_shard_loglik_sum_async(gf_shard* s, double* out, void* stream) {
+    if (int rc = need_loaded(s)) return rc;
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    out[1] = s->ll_const;
+    CU(cudaMemcpyAsync(out, s->d.ll_sum, 8, cudaMemcpyDeviceToHost, st), "loglik");
+    return GF_OK;
+}
+
 int gf_shard_loglik_sum(gf_shard* s, double* out) {
     if (int rc = need_loaded(s)) return rc;
     double v = 0.0;

@@ -301,6 +301,16 @@ class DeviceShard:
         self.rebuild_theta()
         self.check_errors()
 
+    def loglik_sum_async(self, out, stream=None):
+        """Enqueue the loglik read without blocking: `out` is a pinned float64
+        array of 2; after the stream reaches the copy, out[0] - out[1] is the
+        value loglik_sum() returns."""
+        if out.dtype != np.float64 or len(out) < 2 or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous float64 array of >= 2 entries")
+        handle = getattr(stream, "cuda_stream", stream)
+        _lib.check(_lib.lib().gf_shard_loglik_sum_async(self._h, _lib.ptr(out),
+                                                        ctypes.c_void_p(int(handle)) if handle else None))
+
     def loglik_sum(self):
         v = ctypes.c_double()
         _lib.check(_lib.lib().gf_shard_loglik_sum(self._h, ctypes.byref(v)))
