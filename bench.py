@@ -556,6 +556,11 @@ def run_ours(args, world, rank, local):
             dist.barrier()
             torch.cuda.synchronize(device)
 
+    # the e2e leg below replays the SAME iterations from the same state (the
+    # sampler gets faster as theta sparsifies, so later iterations would
+    # flatter it): keep the state the timed region starts from
+    it_start = it
+    z_start = sh.get_assignments() if not args.no_e2e else None
     clocks = ClockSampler(device)
     barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -633,7 +638,8 @@ def run_ours(args, world, rank, local):
             n = int(spec)
             cuts = [(p + 1) / n for p in range(n)]
         cuts[-1] = 1.0
-        z_now = sh.get_assignments()
+        z_now = z_start                          # the timed region's starting state ...
+        it = it_start                            # ... and iterations
         if doc:
             sh.set_block_phases(cuts)
         elif n > 1:
