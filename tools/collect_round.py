@@ -59,7 +59,7 @@ for ext in ("csv", "json"):
     if os.path.exists(f):
         shutil.copy(f, P)
 with open(os.path.join(P, f"{tag}_sanitizer.txt"), "w") as fh:
-    for t in ["memcheck", "racecheck", "synccheck", "initcheck", "memcheck_tests", "memcheck_k23"]:
+    for t in ["memcheck", "racecheck", "synccheck", "initcheck", "memcheck_tests", "memcheck_k23", "memcheck_phases"]:
         f = os.path.join(O, f"san_{t}.log")
         if os.path.exists(f):
             fh.write(f"== {t}\n" + "".join(open(f).readlines()[-3:]))
