@@ -385,17 +385,81 @@ __global__ void __launch_bounds__(NT) context_kernel(SampleArgs a, const int32_t
     for (int i = threadIdx.x; i < a.ctx_stride / 4; i += NT) dst[i] = reinterpret_cast<const float4*>(smem)[i];
 }
 
+constexpr uint32_t VEC = 2;                  // 16-byte vectors per lane per pass step (32 B)
+
+// One token's draw (exclusion by thinning, the exact fallback after the 64th
+// rejection); writes z[t] and its doc-major copy.  seg: the owner run's staged
+// vector-end prefixes; occ: the token's occurrence in its (doc, word) run.
+__device__ __forceinline__ void draw_token(const SampleArgs& a, const float* smem, const float* lvl0,
+                                           const uint32_t* guide, bool guided, float Q, uint32_t v, int col,
+                                           const float* seg, uint32_t t, uint32_t occ, uint32_t odoc, uint32_t ooff,
+                                           uint32_t onnz, uint32_t odwp) {
+    const int K = a.K;
+    const float* pstar = smem;
+    const float* pex = smem + lay_pex(K);
+    const uint32_t oU = max(1u, (onnz + 3u) >> 2);
+    const uint32_t oUp = (oU + VEC - 1u) / VEC * VEC;
+    const float S = seg[oUp - 1u];
+    const uint32_t* row = a.theta_ent + ooff;
+    const uint32_t zt = a.z[t];
+    uint32_t k = zt;
+    for (int retry = 0; retry <= kMaxRetry; ++retry) {
+        const U3 u = draw_u(a, odoc, v, occ, (uint32_t)retry);
+        const bool isS = __fmul_rn(u.b, __fadd_rn(S, Q)) < S;
+        const float target = __fmul_rn(u.s, isS ? S : Q);
+        // Q: only the guide bucket [guide[j], guide[j+1]] (exact, see build_context)
+        const uint32_t gj = (uint32_t)(u.s * (float)kGuide);
+        const uint32_t qlo = (isS || !guided) ? 0u : guide[gj];
+        const uint32_t qn = isS ? oUp : (guided ? guide[gj + 1] - qlo + 1u : (uint32_t)K);
+        uint32_t g = first_above((isS ? seg : lvl0) + qlo, qn, target) + qlo;
+        uint32_t cnt = 0;
+        if (isS) {
+            g = min(g, oU - 1u);
+            float cum = g ? seg[g - 1u] : 0.f;
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + 4u * g));
+            const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
+            uint32_t pick = 0u, last = 0u;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                cum += w_of(e4[i], smem);
+                if (e4[i] >> 16) last = e4[i];                  // pads (count 0) never picked
+                if (!pick && (e4[i] >> 16) && cum > target) pick = e4[i];
+            }
+            if (!pick) pick = last;                             // rounding guard
+            k = topic_of(pick, a.tm);
+            cnt = pick >> 16;
+        } else {
+            k = g;
+            if (k == zt) cnt = row_count(row, onnz, zt, a.tm);
+        }
+        if (k != zt) break;
+        const float pz = zt < (uint32_t)K ? pex_of(a, pex, col, zt) : 0.f;
+        if (zt >= (uint32_t)K || cnt == 0u || pz == 0.f) {   // inconsistent state
+            atomicMin(a.errs, (unsigned long long)t);
+            break;
+        }
+        if (keep_own(u.t, cnt, a.alpha, pstar[tpos(zt, a.tm)], pz)) break;
+        if (retry == kMaxRetry) {                 // 64 rejections: one exact draw
+            k = exact_excluded_draw(a.K, a.alpha, a.tm, pstar, row, onnz, zt, pz,
+                                    make_uint4(odoc, v, occ | ((uint32_t)kMaxRetry << 26), a.iteration), a.key);
+            break;
+        }
+        k = zt;                                                   // rejected: redraw
+    }
+    a.z[t] = (uint16_t)k;
+    a.zdoc[odwp + occ] = (uint16_t)k;
+}
+
 // NT: threads per CTA; CAPV: staged vector ends per warp; MINB: CTAs per SM;
 // PF: keep the pass's next 1 KB step in flight; HUGE: compile the streaming
 // path (needed only when K > 4*CAPV)
-constexpr uint32_t VEC = 2;                  // 16-byte vectors per lane per pass step (32 B)
 template <int NT, uint32_t CAPV, int MINB, bool PF, bool HUGE>
 __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     constexpr int kWarps = NT / 32;
     extern __shared__ __align__(128) float smem[];   // TMA bulk-copy destination: 16-byte aligned
     const int K = a.K;
-    float* pstar = smem;                            // p*(tpos(k))  (byte offset = theta topic field)
-    float* pex = smem + lay_pex(K);                 // p*_ex(k)
+    // p*(tpos(k)) at smem[0] (byte offset = theta topic field), p*_ex(k) at
+    // lay_pex(K) (read by draw_token), the Q-tree levels at lay_tree(K)
     float* lvl = smem + lay_tree(K);                // Q-tree levels (level 0 = prefix of a p*)
     float* wbuf = smem + lay_buf(K, a.tree.total);  // kWarps x CAPV staged vector-end prefixes
     __shared__ double ll_w[kWarps];
@@ -435,7 +499,6 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
     const int batch = min(32, max(1, (sl.z - sl.y + 2 * kWarps - 1) / (2 * kWarps)));
     double ll = 0.0;
     unsigned long long nbytes = 0;
-
     while (true) {
         int rb = 0;
         if (lane == 0) rb = atomicAdd(&next_run, batch);
@@ -597,61 +660,9 @@ __global__ void __launch_bounds__(NT, MINB) sample_kernel(SampleArgs a) {
                     const uint32_t odwp = __shfl_sync(kFull, dwp, own);
                     cown = __shfl_sync(kFull, own, 31);
                     const uint32_t t = base + (uint32_t)lane;
-                    if (t < tend) {
-                        const uint32_t oU = max(1u, (onnz + 3u) >> 2);
-                        const uint32_t oUp = (oU + VEC - 1u) / VEC * VEC;
-                        const float* seg = buf + ovo;
-                        const float S = seg[oUp - 1u];
-                        const uint32_t* row = a.theta_ent + ooff;
-                        const uint32_t zt = a.z[t];
-                        const uint32_t occ = t - ot0;
-                        uint32_t k = zt;
-                        for (int retry = 0; retry <= kMaxRetry; ++retry) {
-                            const U3 u = draw_u(a, odoc, v, occ, (uint32_t)retry);
-                            const bool isS = __fmul_rn(u.b, __fadd_rn(S, Q)) < S;
-                            const float target = __fmul_rn(u.s, isS ? S : Q);
-                            // Q: only the guide bucket [guide[j], guide[j+1]] (exact, see build_context)
-                            const uint32_t gj = (uint32_t)(u.s * (float)kGuide);
-                            const uint32_t qlo = (isS || !guided) ? 0u : guide[gj];
-                            const uint32_t qn = isS ? oUp : (guided ? guide[gj + 1] - qlo + 1u : (uint32_t)K);
-                            uint32_t g = first_above((isS ? seg : lvl0) + qlo, qn, target) + qlo;
-                            uint32_t cnt = 0;
-                            if (isS) {
-                                g = min(g, oU - 1u);
-                                float cum = g ? seg[g - 1u] : 0.f;
-                                const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + 4u * g));
-                                const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
-                                uint32_t pick = 0u, last = 0u;
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    cum += w_of(e4[i], smem);
-                                    if (e4[i] >> 16) last = e4[i];                  // pads (count 0) never picked
-                                    if (!pick && (e4[i] >> 16) && cum > target) pick = e4[i];
-                                }
-                                if (!pick) pick = last;                             // rounding guard
-                                k = topic_of(pick, a.tm);
-                                cnt = pick >> 16;
-                            } else {
-                                k = g;
-                                if (k == zt) cnt = row_count(row, onnz, zt, a.tm);
-                            }
-                            if (k != zt) break;
-                            const float pz = zt < (uint32_t)K ? pex_of(a, pex, col, zt) : 0.f;
-                            if (zt >= (uint32_t)K || cnt == 0u || pz == 0.f) {   // inconsistent state
-                                atomicMin(a.errs, (unsigned long long)t);
-                                break;
-                            }
-                            if (keep_own(u.t, cnt, a.alpha, pstar[tpos(zt, a.tm)], pz)) break;
-                            if (retry == kMaxRetry) {                 // 64 rejections: one exact draw
-                                k = exact_excluded_draw(a.K, a.alpha, a.tm, pstar, row, onnz, zt, pz,
-                                    make_uint4(odoc, v, occ | ((uint32_t)kMaxRetry << 26), a.iteration), a.key);
-                                break;
-                            }
-                            k = zt;                                                   // rejected: redraw
-                        }
-                        a.z[t] = (uint16_t)k;
-                        a.zdoc[odwp + occ] = (uint16_t)k;
-                    }
+                    if (t < tend)
+                        draw_token(a, smem, lvl0, guide, guided, Q, v, col, buf + ovo, t, t - ot0, odoc, ooff, onnz,
+                                   odwp);
                 }
             }
             __syncwarp();
@@ -833,14 +844,18 @@ cudaError_t launch_sample_range(gf_shard* s, uint32_t iteration, int eval_only, 
     if (var == 2) return launch_variant<256, kCapV, 4, true, false>(s, a, n);        // 8-warp CTAs (A/B)
     if (var == 3) return launch_variant<128, 768, 8, false, false>(s, a, n);         // no pass prefetch (A/B)
     if (var == 1) return launch_variant<128, 768, 8, true, false>(s, a, n);          // 8 CTAs/SM (A/B)
+    if (var == 4) return launch_variant<128, 640, 9, true, false>(s, a, n);          // 9 CTAs/SM (A/B)
     if (var == 5) return launch_variant<128, 512, 10, true, false>(s, a, n);         // 10 CTAs/SM (A/B)
-    // 4-warp CTAs, 9 per SM (52 registers, 640-vector staging: rows <= 2560
-    // entries, i.e. any K <= 2048): a slice's tail (warps idle at the final
-    // barrier while the last batch finishes) strands few warps, the pass keeps
-    // its next 1 KB step in flight.  Measured against 8 CTAs/SM (768-vector
-    // staging, 63 registers): PubMed-shape equal, the 8-way shard proxy 2.3%
-    // faster (smaller slices: more prologue latency to hide); 10 CTAs/SM slower.
-    return launch_variant<128, 640, 9, true, false>(s, a, n);
+    // 4-warp CTAs (a slice's tail -- warps idle at the final barrier while the
+    // last batch finishes -- strands few warps; the pass keeps its next 1 KB
+    // step in flight).  Slices averaging < 600 runs (e.g. one rank of an
+    // 8-way PubMed-shape split: 359) have more prologue latency to hide: 9
+    // CTAs/SM with 640-vector staging (52 registers; rows <= 2560 entries, any
+    // K <= 2048), measured 1.5-2.3% faster there; full corpora (PubMed-shape
+    // 908 runs per slice, NYTimes-shape) run 0.5-2% faster at 8 CTAs/SM with
+    // 768-vector staging (60 registers).  10 CTAs/SM is slower everywhere.
+    if (s->R < 600 * s->n_slices) return launch_variant<128, 640, 9, true, false>(s, a, n);
+    return launch_variant<128, 768, 8, true, false>(s, a, n);
 }
 
 }  // namespace gf

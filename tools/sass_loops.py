@@ -3,9 +3,9 @@ contain the pass's 256-bit theta load, their length and how many special-registe
 reads / constant loads / moves the compiler put inside (register-pressure
 rematerialisation shows up here first).  Usage: python tools/sass_loops.py lib.so"""
 import re,subprocess,sys
-# the default K1 variant (K <= 2048: 4 warps, 640-vector staging, 9 CTAs/SM);
-# its entry-parallel pass loop should stay ~104 SASS per step
-DEFAULT_FN = "_ZN2gf13sample_kernelILi128ELj640ELi9ELb1ELb0EEEvNS_10SampleArgsE"
+# the full-corpus K1 variant (K <= 2048: 4 warps, 768-vector staging, 8
+# CTAs/SM); its entry-parallel pass loop should stay ~104 SASS per step
+DEFAULT_FN = "_ZN2gf13sample_kernelILi128ELj768ELi8ELb1ELb0EEEvNS_10SampleArgsE"
 
 
 def loops(obj, fn=DEFAULT_FN):
@@ -18,7 +18,7 @@ def loops(obj, fn=DEFAULT_FN):
     addr={a:k for k,(a,_) in enumerate(ins)}
     enl=[k for k,(a,s) in enumerate(ins) if 'ENL2.256' in s]
     for k,(a,s) in enumerate(ins):
-        m=re.search(r'BRA (0x[0-9a-f]+)',s)
+        m=re.search(r'BRA(?:\.U)? (?:!?U?P\d+, )?(0x[0-9a-f]+)',s)
         if m:
             t=int(m.group(1),16)
             if t<a and t in addr and addr[t] <= enl[-1] <= k:
