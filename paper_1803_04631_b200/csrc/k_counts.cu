@@ -377,7 +377,7 @@ cudaError_t launch_prepare(gf_shard* s) {
 // topic << 2) (the topic pre-scaled to a byte offset into K1's shared p*
 // table), ascending topic, in the fixed-capacity row; nnz into meta.y.
 __host__ __device__ inline int k3_words(int K) { return (K + 31) >> 5; }
-__host__ __device__ inline int k3_warp_u32(int K) { return K + 2 * k3_words(K); }   // bins | bitmap | word ranks
+__host__ __device__ inline int k3_warp_u32(int K) { return K + 2 * k3_words(K) + 32; }   // bins | bitmap | word ranks | 32 dummies
 
 template <int MINB>
 __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const uint32_t* __restrict__ dw_ptr,
@@ -403,6 +403,7 @@ __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const u
     __syncwarp();
     // 32-bit shared addresses of the warp's bins / bitmap / word ranks (sh_*)
     const uint32_t s_bins = smem_addr(bins), s_bmp = smem_addr(bmp), s_wpre = smem_addr(wpre);
+    const uint32_t s_dum = smem_addr(wpre + NW + lane);           // this lane's dummy word
     (void)wpre;
     const unsigned lt = (1u << lane) - 1u;
     // The warp takes GROUPS of gsz <= 32 consecutive documents (group g, then
@@ -466,21 +467,27 @@ __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const u
                 // inside the word; one token per topic wins atomicExch(bin, 0) (it
                 // gets the count and clears the bin) and writes the entry.
                 const uint32_t ncol = (L + 31u) >> 5;
+                const uint16_t* zl = zdoc + (b + (uint32_t)lane);           // column j at zl[32 j]
                 uint32_t kk[4] = {zf, 0xffffu, 0xffffu, 0xffffu};
 #pragma unroll
                 for (uint32_t j = 1; j < 4; ++j)
-                    if (j < ncol && lane + 32u * j < L) kk[j] = zdoc[b + lane + 32u * j];
+                    if (j < ncol && lane + 32u * j < L) kk[j] = zl[32u * j];
+                // count: branch-free -- a token outside [0, K) (past the document
+                // in its column, or an invalid topic) updates the lane's own dummy
+                // word instead; an invalid topic is reported once per document
+                bool bad = false;
 #pragma unroll
                 for (uint32_t j = 0; j < 4; ++j) {
-                    const uint32_t k = kk[j];
-                    if (j < ncol && k < (uint32_t)K) {
-                        sh_red_add(s_bins + 4u * k, 1u);
-                        sh_red_or(s_bmp + ((k >> 3) & ~3u), 1u << (k & 31u));
-                    } else if (j < ncol && k != 0xffffu) {
-                        atomicMin(errs + 2, (unsigned long long)d);
-                        kk[j] = 0xffffu;
+                    if (j < ncol) {
+                        const uint32_t k = kk[j];
+                        const bool ok = k < (uint32_t)K;
+                        bad |= !ok && k != 0xffffu;
+                        sh_red_add(ok ? s_bins + 4u * k : s_dum, 1u);
+                        sh_red_or(ok ? s_bmp + ((k >> 3) & ~3u) : s_dum, 1u << (k & 31u));
+                        if (!ok) kk[j] = 0xffffu;
                     }
                 }
+                if (__any_sync(kFull, bad) && bad) atomicMin(errs + 2, (unsigned long long)d);
                 __syncwarp();
                 if (NW <= 32) {
                     // K <= 1024: lane w holds bitmap word w and the distinct topics
@@ -496,15 +503,24 @@ __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const u
                     }
                     nnz = __shfl_sync(kFull, incl, 31);
                     const uint32_t pre = incl - pc;
+                    // every column's exchange first (their latencies overlap; the
+                    // dummy word absorbs the lanes without a topic), then each
+                    // winner's store -- the only predicated instruction
+                    uint32_t cc[4];
+#pragma unroll
+                    for (uint32_t j = 0; j < 4; ++j) {
+                        const bool ok = kk[j] < (uint32_t)K;
+                        const uint32_t c = j < ncol ? sh_exch(ok ? s_bins + 4u * kk[j] : s_dum, 0u) : 0u;
+                        cc[j] = ok ? c : 0u;
+                    }
 #pragma unroll
                     for (uint32_t j = 0; j < 4; ++j) {
                         if (j < ncol) {
-                            const uint32_t k = kk[j], w = (k >> 5) & 31u;
+                            const uint32_t k = kk[j] < (uint32_t)K ? kk[j] : 0u, w = k >> 5;
                             const uint32_t ww = __shfl_sync(kFull, word, w), pw = __shfl_sync(kFull, pre, w);
-                            const uint32_t c = k < (uint32_t)K ? sh_exch(s_bins + 4u * k, 0u) : 0u;
-                            if (c)
-                                theta_ent[off + pw + __popc(ww & ((1u << (k & 31u)) - 1u))] =
-                                    sh_ld(s_tpo + 4u * k) | (c << 16);               // <= 128: no overflow
+                            const uint32_t e = sh_ld(s_tpo + 4u * k) | (cc[j] << 16);   // <= 128: no overflow
+                            const uint32_t at = off + pw + __popc(ww & ((1u << (k & 31u)) - 1u));
+                            if (cc[j]) theta_ent[at] = e;
                         }
                     }
                 } else {
@@ -540,23 +556,23 @@ __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const u
                 }
                 __syncwarp();
             } else {
+                // branch-free count as above (L > 128: the first four columns are full)
+                bool bad = false;
                 auto count = [&](uint32_t k) {
-                    if (k < (uint32_t)K) {
-                        sh_red_add(s_bins + 4u * k, 1u);
-                        sh_red_or(s_bmp + ((k >> 3) & ~3u), 1u << (k & 31u));
-                    } else {
-                        atomicMin(errs + 2, (unsigned long long)d);
-                    }
+                    const bool ok = k < (uint32_t)K;
+                    bad |= !ok;
+                    sh_red_add(ok ? s_bins + 4u * k : s_dum, 1u);
+                    sh_red_or(ok ? s_bmp + ((k >> 3) & ~3u) : s_dum, 1u << (k & 31u));
                 };
                 // the next 96 topics load together (independent), then count
-                const uint32_t i1 = lane + 32u, i2 = lane + 64u, i3 = lane + 96u;
-                const uint32_t k1 = i1 < L ? zdoc[b + i1] : 0u, k2 = i2 < L ? zdoc[b + i2] : 0u,
-                               k3 = i3 < L ? zdoc[b + i3] : 0u;
-                count(zf);                                          // L > 32: every lane has one
-                if (i1 < L) count(k1);
-                if (i2 < L) count(k2);
-                if (i3 < L) count(k3);
+                const uint16_t* zl = zdoc + (b + (uint32_t)lane);
+                const uint32_t k1 = zl[32], k2 = zl[64], k3 = zl[96];
+                count(zf);
+                count(k1);
+                count(k2);
+                count(k3);
                 for (uint32_t i = lane + 128u; i < L; i += 32) count(zdoc[b + i]);
+                if (__any_sync(kFull, bad) && bad) atomicMin(errs + 2, (unsigned long long)d);
                 __syncwarp();
                 uint32_t base = 0, mx = 0;
                 for (int c = 0; c < NW; c += 32) {
