@@ -19,6 +19,7 @@ for w in ["pm", "ref", "shard0of8", "shard7of8", "nyt", "z4", "k128", "k256", "k
 summ = os.path.join(P, "ncu_summary.py")
 for rep, out, top in [(f"{tag}_k1_nyt.ncu-rep", f"{tag}_nyt_sample_kernel_ncu.txt", "30"),
                       (f"{tag}_pm.ncu-rep", f"{tag}_pubmed_k1_k2_k3_ncu.txt", "25"),
+                      (f"{tag}_k3_pm.ncu-rep", f"{tag}_pubmed_k3_ncu.txt", "20"),
                       (f"{tag}_k5_pm.ncu-rep", f"{tag}_pubmed_k5_ncu.txt", "15")]:
     if os.path.exists(os.path.join(O, rep)):
         with open(os.path.join(P, out), "w") as fh:

@@ -47,6 +47,11 @@ echo "launch list rc=$?"
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"sample_kernel|theta_rebuild|phi_rebuild" -s 20 -c 3 \
   -o $o/${tag}_pm python bench.py --steps 2 --warmup 5 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 echo "pubmed capture rc=$?"
+# K3 alone (in the combined capture above, K3 -- launched on the side stream
+# beside K2 -- comes back with most metric passes NaN)
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"theta_rebuild" -s 6 -c 1 \
+  -o $o/${tag}_k3_pm python bench.py --steps 2 --warmup 5 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+echo "k3 capture rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k5_" -c 6 \
   -o $o/${tag}_k5_pm python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 echo "k5 capture rc=$?"
