@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(256, MINB) theta_rebuild_kernel(int D, const u
                     if (j < ncol) {
                         const uint32_t k = kk[j];
                         const bool ok = k < (uint32_t)K;
-                        bad |= !ok && k != 0xffffu;
+                        bad |= !ok && (j == 0 || lane + 32u * j < L);      // a token, not a pad
                         sh_red_add(ok ? s_bins + 4u * k : s_dum, 1u);
                         sh_red_or(ok ? s_bmp + ((k >> 3) & ~3u) : s_dum, 1u << (k & 31u));
                         if (!ok) kk[j] = 0xffffu;

@@ -361,6 +361,33 @@ def test_consistency_error_when_topic_absent():
             sh.check_errors()
 
 
+@pytest.mark.parametrize("bad_docs", [(0,), (1,), (2,), (3, 1), (2, 3)])
+def test_theta_rebuild_reports_out_of_range_topic(bad_docs):
+    """K3 flags a topic >= K (an import the host does not range-check) as a
+    ConsistencyError naming the first such document, on each of its paths:
+    documents of 20 (warp sort), 100 (register columns) and 300 tokens
+    (histogram loop); a clean state raises nothing."""
+    K, V = 16, 40
+    r = np.random.default_rng(len(bad_docs) * 10 + bad_docs[0])
+    lens = [20, 100, 300, 100]
+    docs = np.repeat(np.arange(len(lens)), lens)
+    ch = build_chunk(docs, r.integers(0, V, docs.size), r.integers(0, K, docs.size))
+    with DeviceShard(K, V, 0.5, 0.1) as sh:
+        sh.load(ch)
+        z = sh.get_assignments()
+        np.testing.assert_array_equal(z, ch.assignments)
+        sh.rebuild_theta()
+        sh.check_errors()
+        for d in bad_docs:
+            pos = np.flatnonzero(ch.doc_ids == d)
+            z[r.choice(pos, size=2, replace=False)] = [K + 3, 0xFFFF]
+        sh.set_assignments(z)
+        sh.rebuild_theta()
+        with pytest.raises(errors.ConsistencyError, match=f"document {min(bad_docs)}: a token's topic is outside"):
+            sh.check_errors()
+        sh.check_errors()                       # reported once, then cleared
+
+
 def _chunk_state(corp, K, seed):
     ch = cp.partition(corp, 1, K, seed)[0]
     rp, ids, cn = oracle_theta(ch, K)
