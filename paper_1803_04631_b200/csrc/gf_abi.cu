@@ -297,6 +297,9 @@ int gf_shard_destroy(gf_shard* s) {
     if (s->aux) { cudaStreamSynchronize(s->aux); cudaStreamDestroy(s->aux); }
     if (s->fork) cudaEventDestroy(s->fork);
     if (s->join) cudaEventDestroy(s->join);
+    if (s->alt) { cudaStreamSynchronize(s->alt); cudaStreamDestroy(s->alt); }
+    for (auto& ev : s->phase_ev)
+        if (ev) cudaEventDestroy(ev);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
     return GF_OK;
@@ -539,19 +542,47 @@ int gf_shard_sample_export(gf_shard* s, uint32_t iteration, uint16_t* out) {
         CU(gf::xfer_d2h(out, s->d.z, s->T * 2, s->stream), "sample_export");
         return GF_OK;
     }
+    // Phases alternate between the caller's stream and `alt` (they are
+    // independent: each reads the iteration-start counts and writes its own
+    // tokens), so a phase's tail CTAs overlap the next phase's first ones; the
+    // loglik reduction waits for both.  Phase p's tokens go out on `aux` as
+    // soon as phase p is done.
+    if (!s->alt) CU(cudaStreamCreateWithFlags(&s->alt, cudaStreamNonBlocking), "sample_export");
+    while ((int)s->phase_ev.size() < P) {
+        cudaEvent_t e;
+        CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "sample_export");
+        s->phase_ev.push_back(e);
+    }
+    cudaStream_t const main = s->stream;
+    struct Restore {                           // s->stream back to the caller's on every exit
+        gf_shard* s;
+        cudaStream_t st;
+        ~Restore() { s->stream = st; }
+    } restore{s, main};
+    CU(cudaEventRecord(s->fork, main), "sample_export");
+    CU(cudaStreamWaitEvent(s->alt, s->fork, 0), "sample_export");
     for (int p = 0; p < P; ++p) {
         const int64_t a = s->phase_slice0[p], b = s->phase_slice0[p + 1];
+        s->stream = (p & 1) ? s->alt : main;
         CU(gf::launch_sample_range(s, iteration, 0, a, b - a), "sample");
-        if (p == P - 1) CU(gf::launch_ll_reduce(s), "loglik");
+        CU(cudaEventRecord(s->phase_ev[p], s->stream), "sample_export");
+        if (p == P - 1) {                      // P > 1: phase P-2 ran on the other stream
+            CU(cudaStreamWaitEvent(s->stream, s->phase_ev[P - 2], 0), "sample_export");
+            CU(gf::launch_ll_reduce(s), "loglik");
+            if (s->stream != main) {
+                CU(cudaEventRecord(s->join, s->stream), "sample_export");
+                CU(cudaStreamWaitEvent(main, s->join, 0), "sample_export");
+            }
+        }
         const int64_t t0 = s->phase_tok0[p], t1 = s->phase_tok0[p + 1];
         if (t1 > t0) {
             // phase p alone writes z[t0, t1): copy it out behind the later phases
-            CU(cudaEventRecord(s->fork, s->stream), "sample_export");
-            CU(cudaStreamWaitEvent(s->aux, s->fork, 0), "sample_export");
+            CU(cudaStreamWaitEvent(s->aux, s->phase_ev[p], 0), "sample_export");
             CU(cudaMemcpyAsync(out + t0, s->d.z + t0, (size_t)(t1 - t0) * 2, cudaMemcpyDeviceToHost, s->aux),
                "sample_export");
         }
     }
+    s->stream = main;
     s->stat_sample_launches++;
     CU(cudaStreamSynchronize(s->aux), "sample_export");
     CU(cudaStreamSynchronize(s->stream), "sample_export");

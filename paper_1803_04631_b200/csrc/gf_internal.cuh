@@ -132,6 +132,8 @@ struct gf_shard {
     cudaEvent_t ev[6] = {};
     cudaStream_t aux = nullptr;              // gf_shard_iterate: K3 beside K2 + prepare
     cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t alt = nullptr;              // gf_shard_sample_export: every other phase
+    std::vector<cudaEvent_t> phase_ev;       // ... and each phase's completion
     float last_ms[4] = {0, 0, 0, 0};
     gf::PeerGroup peer;                      // open: gf_shard_iterate reduces phi over peer memory
     bool timing = true;
